@@ -1,0 +1,250 @@
+"""Generate golden vectors by running the REFERENCE (emtrace) itself.
+
+Run in the build container, where /root/reference exists:
+
+    python tests/golden/make_golden.py
+
+Each case writes ``tests/golden/<case>.npz`` holding the scene (as the
+reference's JSON schema, so nothing here depends on /root/reference at test
+time) and the reference's outputs.  The GPU box never runs this script; it
+only reads the committed .npz files.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import emtrace as E  # noqa: E402  (the reference)
+from emtrace import bvh as accel  # noqa: E402
+from emtrace.autodiff import Tape  # noqa: E402
+from emtrace.channel import GridSpec  # noqa: E402
+from emtrace.scene import load_scene, bundled_scene, scene_from_dict  # noqa: E402
+
+from paper_2303_11103_b200 import scenes as S  # noqa: E402
+from paper_2303_11103_b200.scene import (AntennaArray, RadioDevice, RadioMaterial,  # noqa: E402
+                                         Scene, SceneObject, scene_to_dict)
+
+
+def to_ref(scene):
+    return scene_from_dict(scene_to_dict(scene))
+
+
+def scene_json(ref_scene):
+    return json.dumps(scene_to_dict(ref_scene))
+
+
+def pack_paths(paths, max_len):
+    n = len(paths)
+    names = sorted({p.tx for p in paths} | {p.rx for p in paths})
+    seq = np.full((n, max_len), -1, dtype=np.int32)
+    verts = np.zeros((n, max_len + 2, 3))
+    nrm = np.zeros((n, max_len, 3))
+    cos = np.zeros((n, max_len))
+    out = dict(
+        p_tx=np.array([p.tx for p in paths], dtype="U32"),
+        p_rx=np.array([p.rx for p in paths], dtype="U32"),
+        p_kind=np.array([0 if p.kind == "los" else 1 for p in paths], dtype=np.int8),
+        p_order=np.array([p.order for p in paths], dtype=np.int8),
+        p_length=np.array([p.length_m for p in paths]),
+        p_delay=np.array([p.delay_s for p in paths]),
+        p_kdep=np.array([p.k_dep for p in paths]).reshape(n, 3),
+        p_karr=np.array([p.k_arr for p in paths]).reshape(n, 3),
+    )
+    for i, p in enumerate(paths):
+        k = p.order
+        seq[i, :k] = p.seq
+        verts[i, :k + 2] = p.vertices
+        if k:
+            nrm[i, :k] = p.normals
+            cos[i, :k] = p.cos_incidence
+    out.update(p_seq=seq, p_verts=verts, p_normals=nrm, p_cos=cos)
+    del names
+    return out
+
+
+def cands_array(cands, max_len):
+    cl = sorted(cands, key=lambda s: (len(s), s))
+    arr = np.full((len(cl), max_len), -1, dtype=np.int32)
+    for i, s in enumerate(cl):
+        arr[i, :len(s)] = s
+    return arr
+
+
+def paths_case(name, ref_scene, max_depth, method="exhaustive", num_rays=4096, extra=None,
+               launch=None, coverage=None, launch_max_len=None):
+    t0 = time.time()
+    tree = accel.build(ref_scene)
+    ps = E.compute_paths(ref_scene, tree, max_depth, method=method, num_rays=num_rays)
+    gains = E.compute_gains(ref_scene, tree, ps)
+    cir = E.build_cir(gains)
+    out = dict(scene=np.array(scene_json(ref_scene)), max_depth=max_depth,
+               method=np.array(method), num_rays=num_rays)
+    out.update(pack_paths(ps.paths, max(max_depth, 1)))
+    out["gains_a"] = (np.stack([e.a for e in gains.entries]) if gains.entries
+                      else np.zeros((0, 1, 1, 1), dtype=complex))
+    out["cir_a"] = cir.a
+    out["cir_tau"] = cir.tau
+    for tx in ref_scene.transmitters:
+        for depth, n in (launch or []):
+            c = E.launch_candidates(ref_scene, tree, tx.position, depth, n)
+            out[f"launch_{tx.name}_{depth}_{n}"] = cands_array(c, depth)
+    if coverage:
+        for i, (grid, depth, meth, nr, mode) in enumerate(coverage):
+            cm = E.coverage_map(ref_scene, tree, grid, depth, method=meth, num_rays=nr,
+                                tx_mode=mode)
+            out[f"cov{i}_gains"] = cm.gains
+            out[f"cov{i}_spec"] = np.array([grid.origin[0], grid.origin[1], grid.cell_size,
+                                            grid.nx, grid.ny, grid.height, depth, nr])
+            out[f"cov{i}_method"] = np.array(meth)
+            out[f"cov{i}_mode"] = np.array(mode)
+    if extra:
+        out.update(extra)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: {len(ps.paths)} paths, {time.time() - t0:.1f}s", flush=True)
+
+
+def soup_case():
+    sc = to_ref(S.random_soup(2000, seed=2))
+    tree = accel.build(sc)
+    rng = np.random.RandomState(102)
+    o = rng.uniform(-60, 60, (1500, 3))
+    d = rng.randn(1500, 3)
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    t = np.full(1500, np.inf)
+    prim = np.full(1500, -1, dtype=np.int64)
+    normal = np.zeros((1500, 3))
+    point = np.zeros((1500, 3))
+    for i in range(1500):
+        h = tree.intersect(o[i], d[i])
+        if h is not None:
+            t[i], prim[i], normal[i], point[i] = h.t, h.prim, h.normal, h.point
+    rng = np.random.RandomState(9)
+    p = rng.uniform(-60, 60, (600, 3))
+    q = rng.uniform(-60, 60, (600, 3))
+    occ = np.array([tree.occluded(a, b) for a, b in zip(p, q)])
+    np.savez_compressed(os.path.join(HERE, "soup.npz"), scene=np.array(scene_json(sc)),
+                        o=o, d=d, t=t, prim=prim, normal=normal, point=point,
+                        occ_p=p, occ_q=q, occ=occ, normals=tree.normals,
+                        plane_offset=tree.plane_offset)
+    print("soup: done", flush=True)
+
+
+def corner_scene():
+    def q(name, c):
+        v, t = S.quad(c)
+        return SceneObject(name, "metal", v, t)
+    return Scene(1e9, [q("wall_a", [(0, 0, 0), (0, 10, 0), (0, 10, 10), (0, 0, 10)]),
+                       q("wall_b", [(0, 0, 0), (10, 0, 0), (10, 0, 10), (0, 0, 10)])],
+                 {"metal": RadioMaterial("metal", "constant", 1.0, 1e7)},
+                 AntennaArray(), AntennaArray(),
+                 [RadioDevice("tx", "tx", np.array([4.0, 3.0, 5.0])),
+                  RadioDevice("rx", "rx", np.array([3.0, 4.0, 5.0]))])
+
+
+def ground_scene(tx=(0, 0, 10), rx=(100, 0, 10), L=10000.0, pol="H"):
+    v, t = S.quad([(-L, -L, 0), (L, -L, 0), (L, L, 0), (-L, L, 0)])
+    arr = AntennaArray(pattern="iso", polarization=pol)
+    return Scene(1e9, [SceneObject("ground", "ground", v, t)],
+                 {"ground": RadioMaterial("ground", "constant", 15.0, 0.015)}, arr, arr,
+                 [RadioDevice("tx", "tx", np.array(tx, dtype=float)),
+                  RadioDevice("rx", "rx", np.array(rx, dtype=float))])
+
+
+def calib_case():
+    """C4 gradient golden: NMSE frequency-response loss (optim.py:305-372) at the
+    initial guess, differentiated by the reference Tape w.r.t. all 8 leaves."""
+    from emtrace.optim import _central_gains, _projected_sq_error, generate_dataset
+    from emtrace.channel import probe_receiver, subcarrier_frequencies
+    from emtrace.tracer import compute_paths_between
+    from emtrace.em import EvalContext
+    truth = to_ref(S.calib_scene(n_rx=16, truth=True))
+    init = to_ref(S.calib_scene(n_rx=16, truth=False))
+    tree = accel.build(truth)
+    ds = generate_dataset(truth, num_subcarriers=64, subcarrier_spacing_hz=30e3,
+                          max_depth=2, bvh=tree)
+    # receivers with no propagation path at all have a zero target (the
+    # reference refuses those records, optim.py:347-348): drop them
+    ds.records = [r for r in ds.records if float(np.vdot(r.h, r.h).real) > 0.0]
+    f = subcarrier_frequencies(64, 30e3)
+    tx = init.transmitters[0]
+    names = sorted(n for n, m in init.materials.items() if m.trainable)
+    tape = Tape()
+    leaves = {}
+    for n in names:
+        leaves[n] = (tape.leaf(init.materials[n].eps_r, f"{n}:eps_r"),
+                     tape.leaf(init.materials[n].sigma, f"{n}:sigma"))
+    ctx = EvalContext(init, material_values=leaves)
+    total = 0.0
+    for rec in ds.records:
+        probe = probe_receiver(rec.position)
+        paths = compute_paths_between(init, tree, tx, probe, 2, "exhaustive", 4096)
+        basis = np.exp(-2j * np.pi * f[:, None] * np.array([p.delay_s for p in paths])[None, :])
+        g = _central_gains(init, tree, ctx, tx, probe, paths)
+        norm2 = float(np.vdot(rec.h, rec.h).real)
+        total = total + _projected_sq_error(tape, g, basis, rec.h) / norm2
+    loss = total / len(ds.records)
+    grads = tape.gradient(loss)
+    np.savez_compressed(
+        os.path.join(HERE, "calib.npz"), scene_truth=np.array(scene_json(truth)),
+        scene_init=np.array(scene_json(init)),
+        positions=np.array([r.position for r in ds.records]),
+        h=np.array([r.h for r in ds.records]), loss=loss.value,
+        grad_names=np.array(sorted(grads)), grads=np.array([grads[k] for k in sorted(grads)]),
+        num_subcarriers=64, spacing=30e3, max_depth=2)
+    print("calib: loss", loss.value, flush=True)
+
+
+def main(which=None):
+    cases = {
+        "soup": soup_case,
+        "box": lambda: paths_case(
+            "box", load_scene(bundled_scene("box")), 3,
+            launch=[(2, 4096), (3, 16384)],
+            coverage=[(GridSpec((0.5, 0.5), 1.0, 8, 6, 1.5), 2, "exhaustive", 4096, "central")]),
+        "two_ray": lambda: paths_case(
+            "two_ray", load_scene(bundled_scene("two_ray")), 1,
+            coverage=[(GridSpec((20.0, -30.0), 10.0, 6, 6, 1.5), 1, "exhaustive", 4096,
+                       "central")]),
+        "c1": lambda: paths_case(
+            "c1", to_ref(S.ground_box_scene()), 1, method="fibonacci", num_rays=4096,
+            launch=[(1, 4096), (2, 4096)],
+            coverage=[(GridSpec((-20.0, -40.0), 5.0, 16, 16, 1.5), 1, "exhaustive", 4096,
+                       "central"),
+                      (GridSpec((0.0, -20.0), 8.0, 8, 6, 1.5), 2, "fibonacci", 3000, "array")]),
+        "corner": lambda: paths_case("corner", to_ref(corner_scene()), 2),
+        "merge": lambda: paths_case("merge", to_ref(ground_scene(rx=(20, 20, 10))), 1),
+        "canyon": lambda: paths_case(
+            "canyon", to_ref(_canyon_small()), 3, method="fibonacci", num_rays=20000,
+            launch=[(3, 20000)],
+            coverage=[(GridSpec((-40.0, -8.0), 10.0, 8, 4, 1.5), 2, "fibonacci", 2000,
+                       "central")]),
+        "calib": calib_case,
+    }
+    for k, fn in cases.items():
+        if which and k not in which:
+            continue
+        fn()
+
+
+def _canyon_small():
+    sc = S.street_canyon(n_per_row=10, n_rx=(4, 2),
+                         tx_array=AntennaArray(2, 2, 0.5, 0.5, "tr38901", "VH"))
+    sc.rx_array = AntennaArray(1, 1, 0.5, 0.5, "dipole", "cross")
+    sc.devices[0].orientation = (0.3, 0.1, 0.0)
+    sc.devices[2].orientation = (1.0, -0.2, 0.4)
+    return sc
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or None)
