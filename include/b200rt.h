@@ -1,0 +1,160 @@
+/*
+ * b200rt.h — C ABI of libb200rt.so, the B200 (sm_100a) propagation hot path.
+ *
+ * The reference (emtrace, pure Python) has no FFI boundary: its seam is the
+ * Python module API.  Each entry point below replaces the reference function
+ * named beside it; the Python host layer (paper_2303_11103_b200/*.py) keeps
+ * emtrace's signatures and calls these through ctypes (see INTEGRATION.md
+ * for the stub a maintainer would add to emtrace itself).
+ *
+ * Conventions
+ *  - Every pointer argument documented "device" is CUDA device memory; host
+ *    arrays are only the small fixed-size ones marked "host".
+ *  - Calls are ordered on `stream` (a cudaStream_t, NULL = legacy default).
+ *    Entry points that return a size (n_*_out) synchronise that stream.
+ *  - Return value: RT_OK (0) or a negative RT_E* code; rt_last_error() gives
+ *    the message.  The Python layer maps RT_EINVAL to the reference's
+ *    ValueError subclasses (TracerError / ChannelError / EmError), RT_ECAP to
+ *    the cap errors (tracer.py:203-207, channel.py:239-242), RT_ECOINCIDE to
+ *    tracer.py:188-189, and RT_ECUDA / RT_ENOMEM to RuntimeError.
+ *  - One context per device and per host thread; a context owns the scene,
+ *    the BVH, the current candidate set and the current path table.
+ */
+#ifndef B200RT_H
+#define B200RT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RT_OK 0
+#define RT_EINVAL (-1)
+#define RT_ECAP (-2)
+#define RT_ECOINCIDE (-3)
+#define RT_ECUDA (-4)
+#define RT_ENOMEM (-5)
+#define RT_ESTATE (-6)
+
+/* antenna pattern ids (em.py:42-83) */
+#define RT_PAT_ISO 0
+#define RT_PAT_DIPOLE 1
+#define RT_PAT_TR38901 2
+#define RT_PAT_PROBE_THETA 3
+#define RT_PAT_PROBE_PHI 4
+
+typedef struct rt_ctx rt_ctx;
+
+int rt_version(void);
+int rt_create(int device, rt_ctx** out);
+int rt_destroy(rt_ctx* ctx);
+const char* rt_last_error(const rt_ctx* ctx);
+
+/* ---- scene ingest + acceleration (bvh.py:33-79,180-202: Bvh.__init__, _gather, build) ----
+ * vertices: device [n_vertices*3] f64; tri_vertex: device [n_prims*3] i64 global
+ * vertex ids in _gather order (object order, then triangle order);
+ * prim_material: device [n_prims] i32.  Computes v0/e1/e2, unit normals and
+ * plane offsets bit-identically to the reference's numpy calls. */
+int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
+                    const int64_t* tri_vertex, const int32_t* prim_material, int64_t n_prims,
+                    void* stream);
+/* LBVH over the uploaded primitives (Morton codes, radix sort, Karras
+ * hierarchy, atomic refit, leaf collapse to <=4 prims). */
+int rt_bvh_build(rt_ctx* ctx, void* stream);
+int64_t rt_num_prims(const rt_ctx* ctx);
+/* copy the per-primitive arrays (device outputs, any may be NULL) */
+int rt_scene_arrays(rt_ctx* ctx, double* v0, double* e1, double* e2, double* normals,
+                    double* plane_offset, void* stream);
+
+/* ---- queries (bvh.py:83-115 Bvh.intersect / Bvh.occluded) ----
+ * rt_trace: n rays (device o,d [n*3], tmin,tmax [n]); closest hit (t, global
+ * prim id, -1 on miss) or, with any_hit, the first hit found. */
+int rt_trace(rt_ctx* ctx, const double* o, const double* d, const double* tmin,
+             const double* tmax, int64_t n, int any_hit, double* t_out, int32_t* prim_out,
+             void* stream);
+/* rt_occluded: segments p->q (device [n*3]); out[i] = 1 blocked, 0 clear,
+ * -1 endpoints coincide (bvh.py:109-110 raises). */
+int rt_occluded(rt_ctx* ctx, const double* p, const double* q, int64_t n, int32_t* out,
+                void* stream);
+
+/* ---- candidate sequences ----
+ * rt_launch replaces launch_candidates (tracer.py:217-244): Fibonacci rays
+ * (geometry.py:62-76) from host tx[3], slots [slot_begin, slot_end) of an
+ * n_rays lattice (a coherence permutation maps slots to lattice indices; the
+ * union over slots is the whole lattice), up to max_depth closest hits each;
+ * every prefix of every ray's hit sequence becomes a candidate.  dirs
+ * (device [n_rays*3]) overrides the on-device directions when non-NULL.
+ * The candidate set replaces the context's current one, sorted by
+ * (length, lexicographic sequence). */
+int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
+              int64_t slot_end, int max_depth, const double* dirs, int64_t* n_cand_out,
+              int64_t* n_bounces_out, void* stream);
+/* enumerate_candidates (tracer.py:196-214); RT_ECAP when n^max_depth > cap */
+int rt_enumerate(rt_ctx* ctx, int max_depth, int64_t cap, int64_t* n_cand_out, void* stream);
+/* install an arbitrary candidate list (device seq [n*max_len] i32 -1 padded,
+ * len [n] i8); duplicates are removed and the result sorted */
+int rt_candidates_set(rt_ctx* ctx, const int32_t* seq, const int8_t* len, int64_t n,
+                      int max_len, int64_t* n_unique_out, void* stream);
+int rt_candidates_get(rt_ctx* ctx, int32_t* seq, int8_t* len, int max_len, void* stream);
+int64_t rt_num_candidates(const rt_ctx* ctx);
+int rt_candidates_max_len(const rt_ctx* ctx);
+
+/* ---- paths to explicit receivers (tracer.py:150-193,247-311) ----
+ * Image solve + validity + occlusion for every (receiver, candidate) pair,
+ * LOS per receiver, coincident-path merge, order (los, order, seq) per
+ * receiver.  The path table replaces the context's current one. */
+int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx,
+             int64_t* n_paths_out, void* stream);
+/* copy the path table (device outputs; any may be NULL); rows are grouped by
+ * receiver in rx order.  max_len = rt_candidates_max_len (>=1). */
+int rt_paths_get(rt_ctx* ctx, int32_t* rx_index, int32_t* cand, int8_t* order, int32_t* seq,
+                 double* vertices, double* length, double* delay, double* k_dep,
+                 double* k_arr, double* normals, double* cos_inc, void* stream);
+
+/* ---- polarized field transfer (em.py:98-171,291-312) ----
+ * For every path p and element-slant pair (s, r): a[p, s, r] (complex as 2
+ * doubles) of the geometry given by vertices [P*(L+2)*3], oriented normals
+ * [P*L*3], cosines [P*L], length, delay; materials per interaction from the
+ * scene's prim_material and eta [n_mat*2] (device).  tx_rows/rx_rows are
+ * per-path 3x3 row-major rotations (device [P*9]). */
+int rt_transfer(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
+                const int32_t* seq, const double* vertices, const double* normals,
+                const double* cos_inc, const double* length, const double* delay,
+                const double* tx_rows, const double* rx_rows, int tx_pattern, int rx_pattern,
+                const double* tx_slants, int n_tx_slants, const double* rx_slants,
+                int n_rx_slants, const double* eta, int n_mat, double wavelength,
+                double frequency_hz, double* a_out, void* stream);
+/* Hand-written adjoint of rt_transfer w.r.t. eta: given grad_a (device
+ * [P*S*R*2], PyTorch's dL/dRe + j dL/dIm convention) accumulate
+ * grad_eta[m] = (dL/dRe eta_m, dL/dIm eta_m) into device [n_mat*2]. */
+int rt_transfer_bwd(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
+                    const int32_t* seq, const double* vertices, const double* normals,
+                    const double* cos_inc, const double* length, const double* delay,
+                    const double* tx_rows, const double* rx_rows, int tx_pattern,
+                    int rx_pattern, const double* tx_slants, int n_tx_slants,
+                    const double* rx_slants, int n_rx_slants, const double* eta, int n_mat,
+                    double wavelength, double frequency_hz, const double* grad_a,
+                    double* grad_eta, void* stream);
+
+/* ---- coverage map (channel.py:190-253 point_path_gain / coverage_map) ----
+ * Probe receivers at the centers of an nx*ny grid at `height`.  Every cell
+ * receives sum_paths sum_{theta,phi probes} |a|^2 over the current candidate
+ * set, with per-cell merge; tx_mode 0 = central element (slants[0]), 1 =
+ * coherent sum over n_el elements with world offsets offsets_w [n_el*3] and
+ * slants [n_el] (host arrays).  Rows with iy % shard_count == shard_index are
+ * computed; other cells are written 0 (sum-allreduce the shards).
+ * gains_out: device [ny*nx] f64.  stats_out (host [8], may be NULL):
+ * work items, geometric pairs, valid paths, cells, candidates. */
+int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
+                double cell_size, int64_t nx, int64_t ny, double height,
+                const double* tx_rows, const double* probe_rows, int tx_pattern,
+                const double* slants, const double* offsets_w, int n_el, int tx_mode,
+                const double* eta, int n_mat, double wavelength, double frequency_hz,
+                int shard_index, int shard_count, double* gains_out, int64_t* stats_out,
+                void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200RT_H */

@@ -1,0 +1,179 @@
+"""ctypes binding of libb200rt.so (include/b200rt.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is present, every entry point raises.  Device buffers are torch
+tensors; only their data pointers cross the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_native", "libb200rt.so")
+SRC_DIR = os.path.join(HERE, "csrc")
+
+RT_OK, RT_EINVAL, RT_ECAP, RT_ECOINCIDE, RT_ECUDA, RT_ENOMEM, RT_ESTATE = 0, -1, -2, -3, -4, -5, -6
+PATTERN_IDS = {"iso": 0, "dipole": 1, "tr38901": 2, "_probe_theta": 3, "_probe_phi": 4}
+
+EXPORTS = [
+    "rt_version", "rt_create", "rt_destroy", "rt_last_error", "rt_scene_upload", "rt_bvh_build",
+    "rt_num_prims", "rt_scene_arrays", "rt_trace", "rt_occluded", "rt_launch", "rt_enumerate",
+    "rt_candidates_set", "rt_candidates_get", "rt_num_candidates", "rt_candidates_max_len",
+    "rt_paths", "rt_paths_get", "rt_transfer", "rt_transfer_bwd", "rt_coverage",
+]
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeError(RuntimeError):
+    """CUDA / allocation failure inside libb200rt (RT_ECUDA, RT_ENOMEM)."""
+
+
+def nvcc_command(out=LIB_PATH):
+    return ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+            "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+            "-diag-suppress", "550", "-o", out, os.path.join(SRC_DIR, "b200rt.cu")]
+
+
+def build_library(force=False, verbose=False):
+    """Compile csrc/b200rt.cu for sm_100a into paper_2303_11103_b200/_native/."""
+    import subprocess
+    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
+    srcs = [os.path.join(SRC_DIR, f) for f in os.listdir(SRC_DIR)]
+    srcs.append(os.path.join(os.path.dirname(HERE), "include", "b200rt.h"))
+    if not force and os.path.exists(LIB_PATH):
+        built = os.path.getmtime(LIB_PATH)
+        if all(os.path.getmtime(s) <= built for s in srcs):
+            return LIB_PATH
+    cmd = nvcc_command()
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise NativeError("nvcc failed:\n" + r.stdout + r.stderr)
+    if verbose:
+        print(r.stdout + r.stderr)
+    return LIB_PATH
+
+
+def lib():
+    """Load the shared library (raises when it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(the CUDA path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i64, i32, f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        pp = ctypes.POINTER(ctypes.c_void_p)
+        pi64 = ctypes.POINTER(ctypes.c_int64)
+        sig = {
+            "rt_version": (i32, []),
+            "rt_create": (i32, [i32, pp]),
+            "rt_destroy": (i32, [P]),
+            "rt_last_error": (ctypes.c_char_p, [P]),
+            "rt_scene_upload": (i32, [P, P, i64, P, P, i64, P]),
+            "rt_bvh_build": (i32, [P, P]),
+            "rt_num_prims": (i64, [P]),
+            "rt_scene_arrays": (i32, [P, P, P, P, P, P, P]),
+            "rt_trace": (i32, [P, P, P, P, P, i64, i32, P, P, P]),
+            "rt_occluded": (i32, [P, P, P, i64, P, P]),
+            "rt_launch": (i32, [P, P, i64, i64, i64, i32, P, pi64, pi64, P]),
+            "rt_enumerate": (i32, [P, i32, i64, pi64, P]),
+            "rt_candidates_set": (i32, [P, P, P, i64, i32, pi64, P]),
+            "rt_candidates_get": (i32, [P, P, P, i32, P]),
+            "rt_num_candidates": (i64, [P]),
+            "rt_candidates_max_len": (i32, [P]),
+            "rt_paths": (i32, [P, P, P, i64, pi64, P]),
+            "rt_paths_get": (i32, [P] + [P] * 11 + [P]),
+            "rt_transfer": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P, i32,
+                                  P, i32, f64, f64, P, P]),
+            "rt_transfer_bwd": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P,
+                                      i32, P, i32, f64, f64, P, P, P]),
+            "rt_coverage": (i32, [P, P, f64, f64, f64, i64, i64, f64, P, P, i32, P, P, i32, i32, P,
+                                  i32, f64, f64, i32, i32, P, P, P]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+        return L
+
+
+def ptr(t):
+    """Device (or host) address of a tensor / ndarray, None for None."""
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return ctypes.c_void_p(t.data_ptr())
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data_as(ctypes.c_void_p)
+    raise TypeError(type(t))
+
+
+def host_doubles(values):
+    arr = np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(-1))
+    return arr, arr.ctypes.data_as(ctypes.c_void_p)
+
+
+class Context:
+    """One rt_ctx per CUDA device (the library keeps scene/BVH/candidate state)."""
+
+    def __init__(self, device=None):
+        if not torch.cuda.is_available():
+            raise NativeError("no CUDA device: the B200 path has no CPU fallback")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        self.lib = lib()
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            torch.cuda.init()
+            self.check(self.lib.rt_create(self.device.index, ctypes.byref(h)), None)
+        self.h = h
+        self.scene_token = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and self.h.value:
+                self.lib.rt_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def check(self, rc, exc_map=None):
+        if rc == RT_OK:
+            return
+        msg = self.lib.rt_last_error(self.h).decode() if getattr(self, "h", None) else "rt_create failed"
+        exc_map = exc_map or {}
+        if rc in exc_map:
+            raise exc_map[rc](msg)
+        if rc in (RT_ECUDA, RT_ENOMEM):
+            raise NativeError(f"libb200rt error {rc}: {msg}")
+        raise ValueError(msg)
+
+    def call(self, name, *args, exc_map=None):
+        rc = getattr(self.lib, name)(self.h, *args)
+        self.check(rc, exc_map)
+
+
+_contexts = {}
+
+
+def context(device=None) -> Context:
+    idx = torch.cuda.current_device() if device is None else (torch.device(device).index or 0)
+    c = _contexts.get(idx)
+    if c is None:
+        c = _contexts[idx] = Context(idx)
+    return c

@@ -1,0 +1,173 @@
+"""Acceleration structure: GPU LBVH over the scene triangles.
+
+Drop-in for /root/reference/pkg/src/emtrace/bvh.py: ``build(scene) -> Bvh``
+with ``Bvh.intersect`` (:83-101), ``Bvh.occluded`` (:103-115) and the
+per-primitive arrays the rest of the reference reads (``num_prims``,
+``prim_object``, ``prim_triangle``, ``v0``/``e1``/``e2``, ``normals``,
+``plane_offset``; :33-44).  Construction and queries run in libb200rt.so;
+the host only flattens the meshes (``_gather`` order, :180-197).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+RAY_EPS = 1e-4
+LEAF_SIZE = 4
+
+
+@dataclass(frozen=True)
+class Hit:
+    t: float
+    prim: int
+    point: np.ndarray
+    normal: np.ndarray
+
+
+def gather_meshes(scene):
+    """Flatten objects into (vertices [V,3], tri_vertex [N,3], prim_object, prim_triangle,
+    prim_material, material_names) in the reference's global primitive order."""
+    verts, tris, objs, tids = [], [], [], []
+    base = 0
+    for oi, obj in enumerate(scene.objects):
+        t = np.asarray(obj.triangles, dtype=np.int64).reshape(-1, 3)
+        v = np.asarray(obj.vertices, dtype=np.float64).reshape(-1, 3)
+        if not len(t):
+            continue
+        verts.append(v)
+        tris.append(t + base)
+        objs.append(np.full(len(t), oi))
+        tids.append(np.arange(len(t)))
+        base += len(v)
+    names = list(scene.materials.keys())
+    mindex = {m: i for i, m in enumerate(names)}
+    if not tris:
+        z = np.zeros((0, 3))
+        zi = np.zeros(0, dtype=np.int64)
+        return z, np.zeros((0, 3), dtype=np.int64), zi, zi.copy(), np.zeros(0, dtype=np.int32), names
+    prim_object = np.concatenate(objs)
+    mat_of_obj = np.array([mindex.get(o.material, -1) for o in scene.objects], dtype=np.int32)
+    return (np.concatenate(verts), np.concatenate(tris), prim_object, np.concatenate(tids),
+            mat_of_obj[prim_object], names)
+
+
+class Bvh:
+    """Device-resident scene + LBVH; immutable after build, queries are stream-ordered."""
+
+    def __init__(self, scene, device=None):
+        self.ctx = N.Context(device)
+        self.device = self.ctx.device
+        (verts, tris, self.prim_object, self.prim_triangle, prim_mat,
+         self.material_names) = gather_meshes(scene)
+        self.num_prims = len(tris)
+        self.frequency_hz = float(scene.frequency_hz)
+        dev = self.device
+        with torch.cuda.device(dev):
+            self._verts = torch.from_numpy(np.ascontiguousarray(verts)).to(dev, non_blocking=True)
+            self._tris = torch.from_numpy(np.ascontiguousarray(tris)).to(dev, non_blocking=True)
+            self._pmat = torch.from_numpy(np.ascontiguousarray(prim_mat)).to(dev, non_blocking=True)
+            s = self.ctx.stream
+            self.ctx.call("rt_scene_upload", N.ptr(self._verts), len(verts), N.ptr(self._tris),
+                          N.ptr(self._pmat), self.num_prims, s)
+            self.ctx.call("rt_bvh_build", s)
+        self._arrays = None
+
+    # -- per-primitive arrays (bit-identical to the reference's numpy ones) ------------
+    def _fetch_arrays(self):
+        if self._arrays is None:
+            n = max(self.num_prims, 0)
+            with torch.cuda.device(self.device):
+                outs = [torch.empty((n, 3), dtype=torch.float64, device=self.device) for _ in range(4)]
+                poff = torch.empty(n, dtype=torch.float64, device=self.device)
+                self.ctx.call("rt_scene_arrays", *[N.ptr(o) for o in outs], N.ptr(poff), self.ctx.stream)
+                self._arrays = [o.cpu().numpy() for o in outs] + [poff.cpu().numpy()]
+                self.normals_dev = outs[3]
+        return self._arrays
+
+    @property
+    def v0(self):
+        return self._fetch_arrays()[0]
+
+    @property
+    def e1(self):
+        return self._fetch_arrays()[1]
+
+    @property
+    def e2(self):
+        return self._fetch_arrays()[2]
+
+    @property
+    def normals(self):
+        return self._fetch_arrays()[3]
+
+    @property
+    def plane_offset(self):
+        return self._fetch_arrays()[4]
+
+    # -- queries ----------------------------------------------------------------------
+    def trace(self, origins, directions, t_min=RAY_EPS, t_max=math.inf, any_hit=False):
+        """Batched closest (or any) hit: returns device tensors (t [n], prim [n], -1 miss)."""
+        dev = self.device
+        o = torch.as_tensor(np.asarray(origins, dtype=np.float64).reshape(-1, 3) if not
+                            isinstance(origins, torch.Tensor) else origins, dtype=torch.float64,
+                            device=dev).reshape(-1, 3).contiguous()
+        d = torch.as_tensor(np.asarray(directions, dtype=np.float64).reshape(-1, 3) if not
+                            isinstance(directions, torch.Tensor) else directions,
+                            dtype=torch.float64, device=dev).reshape(-1, 3).contiguous()
+        n = o.shape[0]
+        tmin = torch.as_tensor(t_min, dtype=torch.float64, device=dev).expand(n).contiguous()
+        tmax = torch.as_tensor(t_max, dtype=torch.float64, device=dev).expand(n).contiguous()
+        t = torch.empty(n, dtype=torch.float64, device=dev)
+        p = torch.empty(n, dtype=torch.int32, device=dev)
+        with torch.cuda.device(dev):
+            self.ctx.call("rt_trace", N.ptr(o), N.ptr(d), N.ptr(tmin), N.ptr(tmax), n,
+                          int(any_hit), N.ptr(t), N.ptr(p), self.ctx.stream)
+        return t, p
+
+    def intersect(self, origin, direction, t_min: float = RAY_EPS, t_max: float = math.inf):
+        """Nearest hit with t in (t_min, t_max), or None (bvh.py:83-101)."""
+        t, p = self.trace(origin, direction, t_min, t_max)
+        prim = int(p[0].item())
+        if prim < 0:
+            return None
+        tt = float(t[0].item())
+        o = np.asarray(origin, dtype=np.float64)
+        d = np.asarray(direction, dtype=np.float64)
+        n = self.normals[prim]
+        if float(n @ d) > 0.0:
+            n = -n
+        return Hit(t=tt, prim=prim, point=o + tt * d, normal=n)
+
+    def occluded(self, p, q, eps: float = RAY_EPS) -> bool:
+        """True iff a primitive cuts the open segment p -> q shrunk by eps (bvh.py:103-115)."""
+        dx = float(q[0]) - float(p[0])
+        dy = float(q[1]) - float(p[1])
+        dz = float(q[2]) - float(p[2])
+        dist = math.sqrt(dx * dx + dy * dy + dz * dz)
+        if dist == 0.0:
+            raise ValueError("occlusion query endpoints coincide")
+        inv = 1.0 / dist
+        _, prim = self.trace([float(p[0]), float(p[1]), float(p[2])], [dx * inv, dy * inv, dz * inv],
+                             eps, dist - eps, any_hit=True)
+        return bool(prim[0].item() >= 0)
+
+    def occluded_batch(self, p, q):
+        """Device batch of Bvh.occluded with eps = RAY_EPS; -1 marks coincident endpoints."""
+        dev = self.device
+        P = torch.as_tensor(p, dtype=torch.float64, device=dev).reshape(-1, 3).contiguous()
+        Q = torch.as_tensor(q, dtype=torch.float64, device=dev).reshape(-1, 3).contiguous()
+        out = torch.empty(P.shape[0], dtype=torch.int32, device=dev)
+        with torch.cuda.device(dev):
+            self.ctx.call("rt_occluded", N.ptr(P), N.ptr(Q), P.shape[0], N.ptr(out), self.ctx.stream)
+        return out
+
+
+def build(scene, device=None) -> Bvh:
+    """Build the acceleration structure for a validated scene (bvh.py:200-202)."""
+    return Bvh(scene, device)

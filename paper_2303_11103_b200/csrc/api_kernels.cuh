@@ -1,0 +1,174 @@
+// api_kernels.cuh — small kernels behind the C ABI: batched queries, path
+// table assembly and the transfer entry points.
+#pragma once
+#include "solve.cuh"
+
+namespace rt {
+
+__global__ void k_iota(int* p, long long n) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = (int)i;
+}
+
+// Bvh.intersect / occluded-style batched query (bvh.py:83-101)
+template <bool ANY>
+__global__ void k_trace_batch(Bvh bvh, const double* o, const double* d, const double* tmin,
+                              const double* tmax, long long n, double* t_out, int* prim_out,
+                              long long* err) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Ray r = make_ray(ld3(o + 3 * i), ld3(d + 3 * i));
+    double t;
+    int p = trace<ANY>(bvh, r, tmin[i], tmax[i], &t);
+    if (p == -2) { atomicOr((unsigned long long*)err, 1ULL); p = -1; }
+    prim_out[i] = p;
+    t_out[i] = p >= 0 ? t : __longlong_as_double(0x7ff0000000000000LL);
+}
+
+__global__ void k_occluded_batch(Bvh bvh, const double* p, const double* q, long long n,
+                                 int* out) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = occluded(bvh, ld3(p + 3 * i), ld3(q + 3 * i));
+}
+
+// first sorted-record index of every receiver (-1 when it has none)
+__global__ void k_seg_heads(const unsigned long long* keys, long long n, int* heads) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long rx = (long long)(keys[i] >> 36);
+    if (i == 0 || (long long)(keys[i - 1] >> 36) != rx) heads[rx] = (int)i;
+}
+
+__global__ void k_path_counts(long long n_rx, const int* heads, const unsigned long long* keys,
+                              long long n_rec, const unsigned char* keep,
+                              const unsigned char* los, int* counts) {
+    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= n_rx) return;
+    int c = los[r];
+    int h = heads[r];
+    if (h >= 0)
+        for (long long i = h; i < n_rec && (long long)(keys[i] >> 36) == r; ++i) c += keep[i];
+    counts[r] = c;
+}
+
+struct PathTable {
+    int* rx;
+    int* cand;
+    signed char* order;
+    int* seq;        // [P*L]
+    double* verts;   // [P*(L+2)*3]
+    double* length;
+    double* delay;
+    double* kdep;
+    double* karr;
+    double* nrm;     // [P*L*3]
+    double* cosv;    // [P*L]
+    int L;
+};
+
+__device__ void emit_row(const PathTable& T, long long row, long long rx_i, int cand, int K,
+                         const int* seq, d3 tx, const d3* pts, d3 rx, const SceneDev& S) {
+    Geom g;
+    geom_from_points(tx, pts, K, rx, seq, S.nrm, S.prim_mat, g);
+    T.rx[row] = (int)rx_i;
+    T.cand[row] = cand;
+    T.order[row] = (signed char)K;
+    double* v = T.verts + row * (T.L + 2) * 3;
+    for (int j = 0; j < T.L + 2; ++j) st3(v + 3 * j, d3{0.0, 0.0, 0.0});
+    st3(v, tx);
+    for (int j = 0; j < K; ++j) st3(v + 3 * (j + 1), pts[j]);
+    st3(v + 3 * (K + 1), rx);
+    for (int j = 0; j < T.L; ++j) {
+        T.seq[row * T.L + j] = j < K ? seq[j] : -1;
+        st3(T.nrm + (row * T.L + j) * 3, j < K ? g.nrm[j] : d3{0.0, 0.0, 0.0});
+        T.cosv[row * T.L + j] = j < K ? g.cosi[j] : 0.0;
+    }
+    T.length[row] = g.length;
+    T.delay[row] = g.delay;
+    st3(T.kdep + 3 * row, g.dir[0]);
+    st3(T.karr + 3 * row, g.dir[K]);
+}
+
+// LOS first, then kept records in (order, candidate) order (tracer.py:294)
+__global__ void k_emit_paths(Cands C, SceneDev S, const double* images, Receivers R, d3 tx,
+                             const Rec* recs, const int* order, const unsigned long long* keys,
+                             long long n_rec, const unsigned char* keep, const unsigned char* los,
+                             const int* heads, const int* offsets, PathTable T) {
+    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= R.n) return;
+    long long row = offsets[r];
+    d3 rx = receiver_pos(R, r);
+    if (los[r]) emit_row(T, row++, r, -1, 0, nullptr, tx, nullptr, rx, S);
+    int h = heads[r];
+    if (h < 0) return;
+    for (long long i = h; i < n_rec && (long long)(keys[i] >> 36) == r; ++i) {
+        if (!keep[i]) continue;
+        const Rec& a = recs[order[i]];
+        d3 pts[MAX_DEPTH];
+        solve_geometric(C, S, images, a.cand, tx, rx, pts);
+        emit_row(T, row++, r, a.cand, a.order, C.seq + (long long)a.cand * C.max_len, tx, pts, rx, S);
+    }
+}
+
+struct TransferArgs {
+    long long n;
+    int L;
+    const signed char* order;
+    const int* seq;
+    const double* verts;
+    const double* nrm;
+    const double* cosv;
+    const double* length;
+    const double* delay;
+    const double* tx_rows;
+    const double* rx_rows;
+    int tx_pat, rx_pat;
+    const double* tx_slants;
+    int n_st;
+    const double* rx_slants;
+    int n_sr;
+    const double* eta;
+    const int* prim_mat;
+    double wavelength, frequency;
+};
+
+__device__ inline void table_geom(const TransferArgs& A, long long p, Geom& g) {
+    int K = A.order[p];
+    geom_from_table(K, A.verts + p * (A.L + 2) * 3, A.nrm + p * A.L * 3, A.cosv + p * A.L,
+                    A.seq + p * A.L, A.prim_mat, A.length[p], A.delay[p], g);
+}
+
+// a[p, s, r] for every path and slant pair (em.py:291-312, 397-405)
+__global__ void k_transfer(TransferArgs A, double* a_out) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= A.n * A.n_st) return;
+    long long p = i / A.n_st;
+    int s = (int)(i - p * A.n_st);
+    Geom g;
+    table_geom(A, p, g);
+    c3 f = transport(g, A.tx_pat, A.tx_slants[s], A.tx_rows + 9 * p, A.eta);
+    for (int r = 0; r < A.n_sr; ++r) {
+        d3 rf = rx_field(g, A.rx_pat, A.rx_slants[r], A.rx_rows + 9 * p);
+        c2 a = finish(f, rf, g, A.wavelength, A.frequency);
+        long long o = ((p * A.n_st + s) * A.n_sr + r) * 2;
+        a_out[o] = a.re;
+        a_out[o + 1] = a.im;
+    }
+}
+
+__global__ void k_transfer_bwd(TransferArgs A, const double* grad_a, double* grad_eta) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= A.n * A.n_st * A.n_sr) return;
+    long long p = i / (A.n_st * A.n_sr);
+    int rem = (int)(i - p * A.n_st * A.n_sr);
+    int s = rem / A.n_sr, r = rem - s * A.n_sr;
+    c2 G = c2{grad_a[2 * i], grad_a[2 * i + 1]};
+    if (G.re == 0.0 && G.im == 0.0) return;
+    Geom g;
+    table_geom(A, p, g);
+    transfer_adjoint(g, A.tx_pat, A.tx_slants[s], A.tx_rows + 9 * p, A.rx_pat, A.rx_slants[r],
+                     A.rx_rows + 9 * p, A.eta, A.wavelength, A.frequency, G, grad_eta);
+}
+
+}  // namespace rt

@@ -1,0 +1,943 @@
+// b200rt.cu — the C ABI (include/b200rt.h) over the sm_100a kernels.
+//
+// One translation unit: the kernels live in the .cuh files included below.
+// Built with --fmad=false (see rt_common.cuh) for sm_100a only.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/b200rt.h"
+#include "api_kernels.cuh"
+#include "bvh_build.cuh"
+#include "launch.cuh"
+#include "solve.cuh"
+
+using namespace rt;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <class T>
+    T* get() const { return static_cast<T*>(p); }
+    cudaError_t reserve(size_t n) {
+        if (n <= bytes && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t want = std::max<size_t>(n, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+};
+
+}  // namespace
+
+struct rt_ctx {
+    int device = 0;
+    int n_sm = 148;
+    std::string err;
+    // scene (global gather order)
+    int64_t n_prims = 0;
+    DevBuf v0, e1, e2, nrm, poff, prim_mat, pbox, cent, cbounds;
+    // bvh
+    DevBuf nodes, tris, sorted_idx, morton, morton_alt, idx_alt, child, parent_int, parent_leaf,
+        rfirst, rlast, nbox, flags;
+    bool bvh_ready = false;
+    // candidates
+    DevBuf cand_seq, cand_len;
+    int64_t n_cand = 0;
+    int cand_max_len = 1;
+    // launch scratch
+    DevBuf t_keys, t_vals, t_parent, t_prim, t_depth, t_counter, perm_band;
+    int band_B = -1;
+    uint64_t trie_cap = 0;
+    // sort / unique scratch
+    DevBuf s_seq, s_len, s_perm, s_perm_alt, s_keys, s_keys_alt, s_flag, s_pos;
+    DevBuf cub_tmp;
+    // solve scratch
+    DevBuf images, fp, counts, scan, pending, recs, rkeys, rkeys_alt, ridx, ridx_alt, keep,
+        losbuf, heads, pcounts, poffs, em_small, ctrs;
+    uint64_t pending_cap = 0;
+    // path table
+    int64_t n_paths = 0;
+    int path_L = 1;
+    DevBuf p_rx, p_cand, p_order, p_seq, p_verts, p_len, p_delay, p_kdep, p_karr, p_nrm, p_cos;
+    // error flags + pinned host staging
+    DevBuf dflag;
+    long long* hpin = nullptr;
+};
+
+namespace {
+
+inline cudaStream_t ST(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int fail(rt_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+#define CK(expr)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            return fail(ctx, _e == cudaErrorMemoryAllocation ? RT_ENOMEM : RT_ECUDA,       \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+    } while (0)
+#define CKL() CK(cudaGetLastError())
+#define RC(expr)                  \
+    do {                          \
+        int _r = (expr);          \
+        if (_r != RT_OK) return _r; \
+    } while (0)
+
+inline unsigned nblk(long long n, int bs) {
+    return (unsigned)std::max<long long>(1, (n + bs - 1) / bs);
+}
+
+SceneDev scene_dev(rt_ctx* ctx) {
+    SceneDev s;
+    s.v0 = ctx->v0.get<double>();
+    s.e1 = ctx->e1.get<double>();
+    s.e2 = ctx->e2.get<double>();
+    s.nrm = ctx->nrm.get<double>();
+    s.poff = ctx->poff.get<double>();
+    s.prim_mat = ctx->prim_mat.get<int>();
+    s.n = (int)ctx->n_prims;
+    return s;
+}
+
+rt::Bvh bvh_dev(rt_ctx* ctx) {
+    rt::Bvh b;
+    b.nodes = ctx->nodes.get<BNode>();
+    b.tris = ctx->tris.get<TriRec>();
+    b.n_prims = (int)ctx->n_prims;
+    return b;
+}
+
+Cands cands_dev(rt_ctx* ctx) {
+    Cands c;
+    c.seq = ctx->cand_seq.get<int>();
+    c.len = ctx->cand_len.get<signed char>();
+    c.max_len = ctx->cand_max_len;
+    c.n = ctx->n_cand;
+    return c;
+}
+
+// copy n 8-byte words device -> pinned host, synchronizing the stream
+int fetch(rt_ctx* ctx, const void* dev, int n, cudaStream_t st) {
+    CK(cudaMemcpyAsync(ctx->hpin, dev, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return RT_OK;
+}
+
+int clear_flags(rt_ctx* ctx, cudaStream_t st) {
+    CK(cudaMemsetAsync(ctx->dflag.p, 0, sizeof(long long), st));
+    return RT_OK;
+}
+
+int check_flags(rt_ctx* ctx, cudaStream_t st) {
+    RC(fetch(ctx, ctx->dflag.p, 1, st));
+    long long f = ctx->hpin[0];
+    if (f & 1) return fail(ctx, RT_ECUDA, "BVH traversal stack overflow");
+    if (f & 4) return fail(ctx, RT_ECOINCIDE, "transmitter and probe/receiver coincide");
+    return RT_OK;
+}
+
+int bits_for(long long v) {
+    int b = 1;
+    while (b < 32 && (1LL << b) <= v) ++b;
+    return b;
+}
+
+template <class F>
+int cub_call(rt_ctx* ctx, F&& f) {
+    size_t need = 0;
+    CK(f((void*)nullptr, need));
+    CK(ctx->cub_tmp.reserve(need));
+    size_t have = ctx->cub_tmp.bytes;
+    CK(f(ctx->cub_tmp.p, have));
+    return RT_OK;
+}
+
+// Sort rows (s_seq/s_len, n rows, width L) by (length, lexicographic) and
+// drop duplicates into cand_seq/cand_len (LSD radix over digit columns).
+int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st) {
+    ctx->cand_max_len = std::max(L, 1);
+    if (n == 0) {
+        ctx->n_cand = 0;
+        CK(ctx->cand_seq.reserve(sizeof(int) * ctx->cand_max_len));
+        CK(ctx->cand_len.reserve(1));
+        return RT_OK;
+    }
+    CK(ctx->s_perm.reserve(sizeof(int) * n));
+    CK(ctx->s_perm_alt.reserve(sizeof(int) * n));
+    CK(ctx->s_keys.reserve(sizeof(unsigned) * n));
+    CK(ctx->s_keys_alt.reserve(sizeof(unsigned) * n));
+    CK(ctx->s_flag.reserve(sizeof(int) * (n + 1)));
+    CK(ctx->s_pos.reserve(sizeof(int) * (n + 1)));
+    int* perm = ctx->s_perm.get<int>();
+    int* perm_alt = ctx->s_perm_alt.get<int>();
+    unsigned* keys = ctx->s_keys.get<unsigned>();
+    unsigned* keys_alt = ctx->s_keys_alt.get<unsigned>();
+    const int* seq = ctx->s_seq.get<int>();
+    const signed char* len = ctx->s_len.get<signed char>();
+    k_iota<<<nblk(n, 256), 256, 0, st>>>(perm, n);
+    CKL();
+    int W = bits_for(ctx->n_prims + 1);
+    // passes: digit L-1, ..., digit 0, length (most significant last)
+    for (int pass = 0; pass <= L; ++pass) {
+        int j = pass < L ? (L - 1 - pass) : L;
+        int end_bit = pass < L ? W : 4;
+        k_digit_column<<<nblk(n, 256), 256, 0, st>>>(n, seq, len, L, j, perm, keys);
+        CKL();
+        RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+            return cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys_alt, perm, perm_alt,
+                                                   (int)n, 0, end_bit, st);
+        }));
+        std::swap(perm, perm_alt);
+    }
+    int* flag = ctx->s_flag.get<int>();
+    int* pos = ctx->s_pos.get<int>();
+    k_flag_unique<<<nblk(n, 256), 256, 0, st>>>(n, perm, seq, len, L, flag);
+    CKL();
+    RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+        return cub::DeviceScan::ExclusiveSum(tmp, bytes, flag, pos, (int)n, st);
+    }));
+    CK(cudaMemcpyAsync(ctx->hpin, pos + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(reinterpret_cast<int*>(ctx->hpin) + 1, flag + n - 1, sizeof(int),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    long long n_unique = (long long)reinterpret_cast<int*>(ctx->hpin)[0] +
+                         reinterpret_cast<int*>(ctx->hpin)[1];
+    CK(ctx->cand_seq.reserve(sizeof(int) * n_unique * L));
+    CK(ctx->cand_len.reserve(n_unique));
+    k_scatter_unique<<<nblk(n, 256), 256, 0, st>>>(n, perm, flag, pos, seq, len, L,
+                                                   ctx->cand_seq.get<int>(),
+                                                   ctx->cand_len.get<signed char>());
+    CKL();
+    ctx->n_cand = n_unique;
+    return RT_OK;
+}
+
+}  // namespace
+
+// ===========================================================================================
+extern "C" {
+
+int rt_version(void) { return 1; }
+
+int rt_create(int device, rt_ctx** out) {
+    rt_ctx* ctx = nullptr;
+    if (!out) return RT_EINVAL;
+    *out = nullptr;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return RT_ECUDA;
+    ctx = new rt_ctx();
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMallocHost(&ctx->hpin, 64 * sizeof(long long)) != cudaSuccess ||
+        ctx->dflag.reserve(64) != cudaSuccess || ctx->ctrs.reserve(64) != cudaSuccess) {
+        delete ctx;
+        return RT_ENOMEM;
+    }
+    cudaMemset(ctx->dflag.p, 0, 64);
+    *out = ctx;
+    return RT_OK;
+}
+
+int rt_destroy(rt_ctx* ctx) {
+    if (!ctx) return RT_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->hpin) cudaFreeHost(ctx->hpin);
+    delete ctx;
+    return RT_OK;
+}
+
+const char* rt_last_error(const rt_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t rt_num_prims(const rt_ctx* ctx) { return ctx ? ctx->n_prims : 0; }
+int64_t rt_num_candidates(const rt_ctx* ctx) { return ctx ? ctx->n_cand : 0; }
+int rt_candidates_max_len(const rt_ctx* ctx) { return ctx ? ctx->cand_max_len : 1; }
+
+int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
+                    const int64_t* tri_vertex, const int32_t* prim_material, int64_t n_prims,
+                    void* stream) {
+    if (!ctx || n_prims < 0 || n_vertices < 0) return fail(ctx, RT_EINVAL, "bad scene arguments");
+    if (n_prims > (1 << 27)) return fail(ctx, RT_EINVAL, "too many primitives (max 2^27)");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    ctx->n_prims = n_prims;
+    ctx->bvh_ready = false;
+    ctx->n_cand = 0;
+    ctx->n_paths = 0;
+    size_t n = (size_t)std::max<int64_t>(n_prims, 1);
+    CK(ctx->v0.reserve(24 * n));
+    CK(ctx->e1.reserve(24 * n));
+    CK(ctx->e2.reserve(24 * n));
+    CK(ctx->nrm.reserve(24 * n));
+    CK(ctx->poff.reserve(8 * n));
+    CK(ctx->prim_mat.reserve(4 * n));
+    CK(ctx->pbox.reserve(24 * n));
+    CK(ctx->cent.reserve(12 * n));
+    CK(ctx->cbounds.reserve(32));
+    if (n_prims == 0) return RT_OK;
+    CK(cudaMemcpyAsync(ctx->prim_mat.p, prim_material, 4 * n_prims, cudaMemcpyDeviceToDevice, st));
+    unsigned init[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
+    CK(cudaMemcpyAsync(ctx->cbounds.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    k_gather<<<nblk(n_prims, 256), 256, 0, st>>>(
+        vertices, tri_vertex, n_prims, ctx->v0.get<double>(), ctx->e1.get<double>(),
+        ctx->e2.get<double>(), ctx->nrm.get<double>(), ctx->poff.get<double>(),
+        ctx->pbox.get<float>(), ctx->cent.get<float>(), ctx->cbounds.get<unsigned>());
+    CKL();
+    CK(cudaStreamSynchronize(st));   // `init` lives on the host stack
+    return RT_OK;
+}
+
+int rt_bvh_build(rt_ctx* ctx, void* stream) {
+    if (!ctx) return RT_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    long long n = ctx->n_prims;
+    ctx->bvh_ready = true;
+    if (n == 0) return RT_OK;
+    CK(ctx->tris.reserve(sizeof(TriRec) * n));
+    CK(ctx->sorted_idx.reserve(4 * n));
+    CK(ctx->nodes.reserve(sizeof(BNode) * std::max<long long>(n - 1, 1)));
+    if (n == 1) {
+        k_iota<<<1, 32, 0, st>>>(ctx->sorted_idx.get<int>(), 1);
+        k_layout_one<<<1, 1, 0, st>>>(ctx->pbox.get<float>(), ctx->nodes.get<BNode>());
+        k_sorted_tris<<<1, 32, 0, st>>>(1, ctx->sorted_idx.get<int>(), ctx->v0.get<double>(),
+                                        ctx->e1.get<double>(), ctx->e2.get<double>(),
+                                        ctx->tris.get<TriRec>());
+        CKL();
+        return RT_OK;
+    }
+    CK(ctx->morton.reserve(8 * n));
+    CK(ctx->morton_alt.reserve(8 * n));
+    CK(ctx->idx_alt.reserve(4 * n));
+    CK(ctx->child.reserve(8 * n));
+    CK(ctx->parent_int.reserve(4 * n));
+    CK(ctx->parent_leaf.reserve(4 * n));
+    CK(ctx->rfirst.reserve(4 * n));
+    CK(ctx->rlast.reserve(4 * n));
+    CK(ctx->nbox.reserve(24 * n));
+    CK(ctx->flags.reserve(4 * n));
+    k_morton<<<nblk(n, 256), 256, 0, st>>>(ctx->cent.get<float>(), ctx->cbounds.get<unsigned>(), n,
+                                          ctx->morton_alt.get<uint64_t>(), ctx->idx_alt.get<int>());
+    CKL();
+    uint64_t* kin = ctx->morton_alt.get<uint64_t>();
+    uint64_t* kout = ctx->morton.get<uint64_t>();
+    int* vin = ctx->idx_alt.get<int>();
+    int* vout = ctx->sorted_idx.get<int>();
+    RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+        return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, 63, st);
+    }));
+    CK(cudaMemsetAsync(ctx->parent_int.p, 0xFF, 4 * n, st));
+    CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
+    k_karras<<<nblk(n - 1, 256), 256, 0, st>>>(kout, (int)n, ctx->child.get<int>(),
+                                               ctx->parent_int.get<int>(), ctx->parent_leaf.get<int>(),
+                                               ctx->rfirst.get<int>(), ctx->rlast.get<int>());
+    CKL();
+    k_refit<<<nblk(n, 256), 256, 0, st>>>((int)n, vout, ctx->pbox.get<float>(), ctx->child.get<int>(),
+                                          ctx->parent_int.get<int>(), ctx->parent_leaf.get<int>(),
+                                          ctx->nbox.get<float>(), ctx->flags.get<int>());
+    CKL();
+    k_layout<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, vout, ctx->pbox.get<float>(), ctx->child.get<int>(),
+                                               ctx->nbox.get<float>(), ctx->rfirst.get<int>(),
+                                               ctx->rlast.get<int>(), ctx->nodes.get<BNode>());
+    CKL();
+    k_sorted_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, vout, ctx->v0.get<double>(), ctx->e1.get<double>(),
+                                                ctx->e2.get<double>(), ctx->tris.get<TriRec>());
+    CKL();
+    return RT_OK;
+}
+
+int rt_scene_arrays(rt_ctx* ctx, double* v0, double* e1, double* e2, double* normals,
+                    double* plane_offset, void* stream) {
+    if (!ctx) return RT_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    size_t n = ctx->n_prims;
+    if (!n) return RT_OK;
+    if (v0) CK(cudaMemcpyAsync(v0, ctx->v0.p, 24 * n, cudaMemcpyDeviceToDevice, st));
+    if (e1) CK(cudaMemcpyAsync(e1, ctx->e1.p, 24 * n, cudaMemcpyDeviceToDevice, st));
+    if (e2) CK(cudaMemcpyAsync(e2, ctx->e2.p, 24 * n, cudaMemcpyDeviceToDevice, st));
+    if (normals) CK(cudaMemcpyAsync(normals, ctx->nrm.p, 24 * n, cudaMemcpyDeviceToDevice, st));
+    if (plane_offset) CK(cudaMemcpyAsync(plane_offset, ctx->poff.p, 8 * n, cudaMemcpyDeviceToDevice, st));
+    return RT_OK;
+}
+
+int rt_trace(rt_ctx* ctx, const double* o, const double* d, const double* tmin,
+             const double* tmax, int64_t n, int any_hit, double* t_out, int32_t* prim_out,
+             void* stream) {
+    if (!ctx || n < 0) return fail(ctx, RT_EINVAL, "bad trace arguments");
+    if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
+    if (n == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    RC(clear_flags(ctx, st));
+    if (any_hit)
+        k_trace_batch<true><<<nblk(n, 128), 128, 0, st>>>(bvh_dev(ctx), o, d, tmin, tmax, n, t_out,
+                                                          prim_out, ctx->dflag.get<long long>());
+    else
+        k_trace_batch<false><<<nblk(n, 128), 128, 0, st>>>(bvh_dev(ctx), o, d, tmin, tmax, n, t_out,
+                                                           prim_out, ctx->dflag.get<long long>());
+    CKL();
+    return RT_OK;
+}
+
+int rt_occluded(rt_ctx* ctx, const double* p, const double* q, int64_t n, int32_t* out,
+                void* stream) {
+    if (!ctx || n < 0) return fail(ctx, RT_EINVAL, "bad occlusion arguments");
+    if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
+    if (n == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    k_occluded_batch<<<nblk(n, 128), 128, 0, ST(stream)>>>(bvh_dev(ctx), p, q, n, out);
+    CKL();
+    return RT_OK;
+}
+
+int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
+              int64_t slot_end, int max_depth, const double* dirs, int64_t* n_cand_out,
+              int64_t* n_bounces_out, void* stream) {
+    if (!ctx || !tx || n_rays < 1 || max_depth < 1)
+        return fail(ctx, RT_EINVAL, "need num_rays >= 1 and max_depth >= 1");
+    if (max_depth > MAX_DEPTH) return fail(ctx, RT_EINVAL, "max_depth above the compiled bound (8)");
+    if (slot_begin < 0 || slot_end > n_rays || slot_begin > slot_end)
+        return fail(ctx, RT_EINVAL, "bad ray slot range");
+    if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    if (n_bounces_out) *n_bounces_out = 0;
+    if (ctx->n_prims == 0) {
+        RC(sort_unique_candidates(ctx, 0, max_depth, st));
+        if (n_cand_out) *n_cand_out = 0;
+        // every ray still costs one (missing) intersect call
+        if (n_bounces_out) *n_bounces_out = slot_end - slot_begin;
+        return RT_OK;
+    }
+    // coherence band: ~sqrt(pi n) indices sorted by azimuth (launch.cuh)
+    int B = 1;
+    while ((double)B * B < 3.14159 * (double)n_rays && B < 65536) B <<= 1;
+    if (B < 32 || B > n_rays) B = 0;
+    if (B != ctx->band_B) {
+        if (B > 0) {
+            std::vector<std::pair<double, int>> az(B);
+            const double inv_g = 1.0 / 2.618033988749895;
+            for (int j = 0; j < B; ++j) {
+                double f = (double)j * inv_g;
+                az[j] = {f - std::floor(f), j};
+            }
+            std::sort(az.begin(), az.end());
+            std::vector<int> perm(B);
+            for (int j = 0; j < B; ++j) perm[j] = az[j].second;
+            CK(ctx->perm_band.reserve(4 * B));
+            CK(cudaMemcpy(ctx->perm_band.p, perm.data(), 4 * B, cudaMemcpyHostToDevice));
+        }
+        ctx->band_B = B;
+    }
+    long long span = slot_end - slot_begin;
+    if (ctx->trie_cap == 0) {
+        uint64_t want = 1ULL << 20;
+        while (want < 4ULL * std::min<long long>(span * max_depth, 1LL << 24)) want <<= 1;
+        ctx->trie_cap = want;
+    }
+    for (int attempt = 0; attempt < 6; ++attempt) {
+        uint64_t cap = ctx->trie_cap;
+        int max_nodes = (int)std::min<uint64_t>(cap / 2, (1ULL << 31) - 2);
+        CK(ctx->t_keys.reserve(8 * cap));
+        CK(ctx->t_vals.reserve(4 * cap));
+        CK(ctx->t_parent.reserve(4ULL * max_nodes));
+        CK(ctx->t_prim.reserve(4ULL * max_nodes));
+        CK(ctx->t_depth.reserve((size_t)max_nodes));
+        CK(cudaMemsetAsync(ctx->t_keys.p, 0xFF, 8 * cap, st));
+        CK(cudaMemsetAsync(ctx->t_vals.p, 0xFF, 4 * cap, st));
+        CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
+        RC(clear_flags(ctx, st));
+        Trie T;
+        T.keys = ctx->t_keys.get<unsigned long long>();
+        T.vals = ctx->t_vals.get<int>();
+        T.node_parent = ctx->t_parent.get<int>();
+        T.node_prim = ctx->t_prim.get<int>();
+        T.node_depth = ctx->t_depth.get<signed char>();
+        T.mask = (unsigned)(cap - 1);
+        T.max_nodes = max_nodes;
+        long long* ctr = ctx->ctrs.get<long long>();
+        T.counter = reinterpret_cast<int*>(ctr + 0);
+        T.overflow = reinterpret_cast<int*>(ctr + 1);
+        LaunchParams P;
+        P.tx = tx[0]; P.ty = tx[1]; P.tz = tx[2];
+        P.n_rays = n_rays;
+        P.slot_begin = slot_begin;
+        P.slot_end = slot_end;
+        P.max_depth = max_depth;
+        P.band = B;
+        P.perm = ctx->perm_band.get<int>();
+        P.dirs = dirs;
+        P.normals = ctx->nrm.get<double>();
+        P.bounces = reinterpret_cast<unsigned long long*>(ctr + 2);
+        P.error = reinterpret_cast<int*>(ctx->dflag.get<long long>());
+        long long blocks = std::min<long long>((span + 255) / 256, (long long)ctx->n_sm * 16);
+        if (span > 0) {
+            k_launch<<<(unsigned)std::max<long long>(blocks, 1), 256, 0, st>>>(bvh_dev(ctx), P, T);
+            CKL();
+        }
+        RC(fetch(ctx, ctr, 3, st));
+        long long nodes = (long long)(int)(ctx->hpin[0] & 0xffffffff);
+        bool overflow = (int)(ctx->hpin[1] & 0xffffffff) != 0;
+        long long bounces = ctx->hpin[2];
+        RC(check_flags(ctx, st));
+        if (overflow) {
+            ctx->trie_cap *= 4;
+            continue;
+        }
+        if (n_bounces_out) *n_bounces_out = bounces;
+        // materialize sequences and sort them
+        CK(ctx->s_seq.reserve(4ULL * std::max<long long>(nodes, 1) * max_depth));
+        CK(ctx->s_len.reserve((size_t)std::max<long long>(nodes, 1)));
+        if (nodes > 0) {
+            k_trie_sequences<<<nblk(nodes, 256), 256, 0, st>>>((int)nodes, T.node_parent, T.node_prim,
+                                                               T.node_depth, max_depth,
+                                                               ctx->s_seq.get<int>(),
+                                                               ctx->s_len.get<signed char>());
+            CKL();
+        }
+        RC(sort_unique_candidates(ctx, nodes, max_depth, st));
+        if (n_cand_out) *n_cand_out = ctx->n_cand;
+        return RT_OK;
+    }
+    return fail(ctx, RT_ENOMEM, "candidate trie overflow after growing");
+}
+
+int rt_enumerate(rt_ctx* ctx, int max_depth, int64_t cap, int64_t* n_cand_out, void* stream) {
+    if (!ctx) return RT_EINVAL;
+    if (max_depth < 1) return fail(ctx, RT_EINVAL, "max_depth must be >= 1 for candidate enumeration");
+    if (max_depth > MAX_DEPTH) return fail(ctx, RT_EINVAL, "max_depth above the compiled bound (8)");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    long long n = ctx->n_prims;
+    if (n == 0) {
+        RC(sort_unique_candidates(ctx, 0, max_depth, st));
+        if (n_cand_out) *n_cand_out = 0;
+        return RT_OK;
+    }
+    // n ** max_depth > cap (tracer.py:203-207), in floating point to avoid overflow
+    if (std::pow((double)n, (double)max_depth) > (double)cap) {
+        char buf[256];
+        snprintf(buf, sizeof buf,
+                 "exhaustive enumeration of %lld primitives at depth %d exceeds the cap of %.0e "
+                 "sequences; use the fibonacci ray-launching method instead",
+                 n, max_depth, (double)cap);
+        return fail(ctx, RT_ECAP, buf);
+    }
+    std::vector<long long> start(max_depth + 1, 0);
+    long long level = n, total = 0;
+    for (int k = 0; k < max_depth; ++k) {
+        start[k] = total;
+        total += level;
+        level *= (n - 1);
+    }
+    start[max_depth] = total;
+    CK(ctx->em_small.reserve(8 * (max_depth + 1)));
+    CK(cudaMemcpyAsync(ctx->em_small.p, start.data(), 8 * (max_depth + 1), cudaMemcpyHostToDevice, st));
+    CK(ctx->cand_seq.reserve(4ULL * std::max<long long>(total, 1) * max_depth));
+    CK(ctx->cand_len.reserve((size_t)std::max<long long>(total, 1)));
+    k_enumerate<<<nblk(total, 256), 256, 0, st>>>(total, (int)n, max_depth, ctx->em_small.get<long long>(),
+                                                  ctx->cand_seq.get<int>(), ctx->cand_len.get<signed char>());
+    CKL();
+    CK(cudaStreamSynchronize(st));
+    ctx->n_cand = total;
+    ctx->cand_max_len = max_depth;
+    if (n_cand_out) *n_cand_out = total;
+    return RT_OK;
+}
+
+int rt_candidates_set(rt_ctx* ctx, const int32_t* seq, const int8_t* len, int64_t n, int max_len,
+                      int64_t* n_unique_out, void* stream) {
+    if (!ctx || n < 0 || max_len < 1 || max_len > MAX_DEPTH)
+        return fail(ctx, RT_EINVAL, "bad candidate arguments");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    CK(ctx->s_seq.reserve(4ULL * std::max<long long>(n, 1) * max_len));
+    CK(ctx->s_len.reserve((size_t)std::max<long long>(n, 1)));
+    if (n) {
+        CK(cudaMemcpyAsync(ctx->s_seq.p, seq, 4ULL * n * max_len, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(ctx->s_len.p, len, (size_t)n, cudaMemcpyDeviceToDevice, st));
+    }
+    RC(sort_unique_candidates(ctx, n, max_len, st));
+    if (n_unique_out) *n_unique_out = ctx->n_cand;
+    return RT_OK;
+}
+
+int rt_candidates_get(rt_ctx* ctx, int32_t* seq, int8_t* len, int max_len, void* stream) {
+    if (!ctx || max_len != ctx->cand_max_len) return fail(ctx, RT_EINVAL, "max_len mismatch");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    if (ctx->n_cand == 0) return RT_OK;
+    if (seq) CK(cudaMemcpyAsync(seq, ctx->cand_seq.p, 4ULL * ctx->n_cand * max_len, cudaMemcpyDeviceToDevice, st));
+    if (len) CK(cudaMemcpyAsync(len, ctx->cand_len.p, (size_t)ctx->n_cand, cudaMemcpyDeviceToDevice, st));
+    return RT_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// stage 1-4 of the solve pipeline for either receiver kind; leaves sorted
+// records in recs/ridx/rkeys and returns their count
+int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power, const EmParams& E,
+                  int shard_index, int shard_count, long long* n_rec_out, long long* stats,
+                  cudaStream_t st) {
+    Cands C = cands_dev(ctx);
+    SceneDev SD = scene_dev(ctx);
+    long long nC = C.n;
+    *n_rec_out = 0;
+    if (nC == 0 || R.n == 0) return RT_OK;
+    CK(ctx->images.reserve(24ULL * nC * C.max_len));
+    k_images<<<nblk(nC, 256), 256, 0, st>>>(C, SD, tx, ctx->images.get<double>());
+    CKL();
+    long long W = 0;
+    if (grid) {
+        CK(ctx->fp.reserve(sizeof(Footprint) * nC));
+        CK(ctx->counts.reserve(8ULL * (nC + 1)));
+        CK(ctx->scan.reserve(8ULL * (nC + 1)));
+        k_footprint<<<nblk(nC + 1, 256), 256, 0, st>>>(C, SD, ctx->images.get<double>(), R, shard_index,
+                                                       shard_count, ctx->fp.get<Footprint>(),
+                                                       ctx->counts.get<long long>());
+        CKL();
+        long long* cnt = ctx->counts.get<long long>();
+        long long* scan = ctx->scan.get<long long>();
+        RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+            return cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, scan, (int)(nC + 1), st);
+        }));
+        RC(fetch(ctx, scan + nC, 1, st));
+        W = ctx->hpin[0];
+    } else {
+        W = nC * R.n;
+    }
+    if (stats) stats[0] = W;
+    if (W == 0) return RT_OK;
+    // geometric solve with compaction; grow and retry when the buffer is short
+    if (ctx->pending_cap == 0) ctx->pending_cap = 1 << 20;
+    long long n_pend = 0;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        CK(ctx->pending.reserve(sizeof(Pending) * ctx->pending_cap));
+        CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
+        unsigned long long* np = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>());
+        long long blocks = std::min<long long>((W + 255) / 256, (long long)ctx->n_sm * 32);
+        if (grid)
+            k_solve<true><<<(unsigned)blocks, 256, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, W,
+                                                            ctx->scan.get<long long>(), ctx->fp.get<Footprint>(),
+                                                            shard_count, ctx->pending.get<Pending>(), np,
+                                                            ctx->pending_cap);
+        else
+            k_solve<false><<<(unsigned)blocks, 256, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, W,
+                                                             nullptr, nullptr, 1, ctx->pending.get<Pending>(),
+                                                             np, ctx->pending_cap);
+        CKL();
+        RC(fetch(ctx, np, 1, st));
+        n_pend = ctx->hpin[0];
+        if ((unsigned long long)n_pend <= ctx->pending_cap) break;
+        while (ctx->pending_cap < (unsigned long long)n_pend) ctx->pending_cap *= 2;
+    }
+    if (stats) stats[1] = n_pend;
+    if (n_pend == 0) return RT_OK;
+    CK(ctx->recs.reserve(sizeof(Rec) * n_pend));
+    CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
+    unsigned long long* nr = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>()) + 1;
+    RC(clear_flags(ctx, st));
+    long long vblocks = std::min<long long>((n_pend + 127) / 128, (long long)ctx->n_sm * 32);
+    if (power)
+        k_validate<true><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
+                                                            bvh_dev(ctx), ctx->pending.get<Pending>(),
+                                                            n_pend, E, ctx->recs.get<Rec>(), nr);
+    else
+        k_validate<false><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
+                                                             bvh_dev(ctx), ctx->pending.get<Pending>(),
+                                                             n_pend, E, ctx->recs.get<Rec>(), nr);
+    CKL();
+    RC(fetch(ctx, nr, 1, st));
+    long long n_rec = ctx->hpin[0];
+    RC(check_flags(ctx, st));
+    if (stats) stats[2] = n_rec;
+    if (n_rec == 0) return RT_OK;
+    CK(ctx->rkeys.reserve(8 * n_rec));
+    CK(ctx->rkeys_alt.reserve(8 * n_rec));
+    CK(ctx->ridx.reserve(4 * n_rec));
+    CK(ctx->ridx_alt.reserve(4 * n_rec));
+    k_rec_keys<<<nblk(n_rec, 256), 256, 0, st>>>(ctx->recs.get<Rec>(), n_rec, ctx->rkeys_alt.get<unsigned long long>(),
+                                                ctx->ridx_alt.get<int>());
+    CKL();
+    unsigned long long* kin = ctx->rkeys_alt.get<unsigned long long>();
+    unsigned long long* kout = ctx->rkeys.get<unsigned long long>();
+    int* vin = ctx->ridx_alt.get<int>();
+    int* vout = ctx->ridx.get<int>();
+    int end_bit = 36 + bits_for(R.n);
+    RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+        return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n_rec, 0,
+                                               std::min(end_bit, 64), st);
+    }));
+    *n_rec_out = n_rec;
+    return RT_OK;
+}
+
+int em_upload(rt_ctx* ctx, const double* tx_rows, const double* probe_rows, const double* slants,
+              const double* offsets_w, int n_el, cudaStream_t st, double** d_tx, double** d_probe,
+              double** d_sl, double** d_off) {
+    size_t n = 18 + (size_t)n_el * 4;
+    std::vector<double> h(n, 0.0);
+    for (int i = 0; i < 9; ++i) h[i] = tx_rows ? tx_rows[i] : (i % 4 == 0 ? 1.0 : 0.0);
+    for (int i = 0; i < 9; ++i) h[9 + i] = probe_rows ? probe_rows[i] : (i % 4 == 0 ? 1.0 : 0.0);
+    for (int e = 0; e < n_el; ++e) h[18 + e] = slants ? slants[e] : 0.0;
+    for (int e = 0; e < 3 * n_el; ++e) h[18 + n_el + e] = offsets_w ? offsets_w[e] : 0.0;
+    CK(ctx->em_small.reserve(8 * n));
+    CK(cudaMemcpyAsync(ctx->em_small.p, h.data(), 8 * n, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    double* b = ctx->em_small.get<double>();
+    *d_tx = b;
+    *d_probe = b + 9;
+    *d_sl = b + 18;
+    *d_off = b + 18 + n_el;
+    return RT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx, int64_t* n_paths_out,
+             void* stream) {
+    if (!ctx || !tx || n_rx < 0) return fail(ctx, RT_EINVAL, "bad path arguments");
+    if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    d3 T = d3{tx[0], tx[1], tx[2]};
+    Receivers R;
+    R.pts = rx;
+    R.ox = R.oy = R.cell = R.height = 0.0;
+    R.nx = R.ny = 0;
+    R.n = n_rx;
+    ctx->n_paths = 0;
+    ctx->path_L = ctx->cand_max_len;
+    if (n_rx == 0) {
+        if (n_paths_out) *n_paths_out = 0;
+        return RT_OK;
+    }
+    EmParams E{};
+    long long n_rec = 0;
+    RC(solve_records(ctx, T, R, false, false, E, 0, 1, &n_rec, nullptr, st));
+    CK(ctx->keep.reserve((size_t)std::max<long long>(n_rec, 1)));
+    CK(ctx->losbuf.reserve((size_t)n_rx));
+    CK(ctx->heads.reserve(4ULL * n_rx));
+    CK(ctx->pcounts.reserve(4ULL * (n_rx + 1)));
+    CK(ctx->poffs.reserve(4ULL * (n_rx + 1)));
+    RC(clear_flags(ctx, st));
+    k_los<false><<<nblk(n_rx, 128), 128, 0, st>>>(R, T, bvh_dev(ctx), scene_dev(ctx), E, 0, 1,
+                                                  ctx->losbuf.get<unsigned char>(), nullptr,
+                                                  reinterpret_cast<int*>(ctx->dflag.get<long long>()));
+    CKL();
+    RC(check_flags(ctx, st));
+    CK(cudaMemsetAsync(ctx->heads.p, 0xFF, 4ULL * n_rx, st));
+    if (n_rec > 0) {
+        k_merge<false><<<nblk(n_rec, 128), 128, 0, st>>>(cands_dev(ctx), scene_dev(ctx), ctx->images.get<double>(),
+                                                        R, T, ctx->recs.get<Rec>(), ctx->ridx.get<int>(),
+                                                        ctx->rkeys.get<unsigned long long>(), n_rec,
+                                                        ctx->keep.get<unsigned char>(), nullptr);
+        CKL();
+        k_seg_heads<<<nblk(n_rec, 256), 256, 0, st>>>(ctx->rkeys.get<unsigned long long>(), n_rec,
+                                                      ctx->heads.get<int>());
+        CKL();
+    }
+    int* cnt = ctx->pcounts.get<int>();
+    int* off = ctx->poffs.get<int>();
+    CK(cudaMemsetAsync(cnt + n_rx, 0, 4, st));
+    k_path_counts<<<nblk(n_rx, 128), 128, 0, st>>>(n_rx, ctx->heads.get<int>(), ctx->rkeys.get<unsigned long long>(),
+                                                   n_rec, ctx->keep.get<unsigned char>(),
+                                                   ctx->losbuf.get<unsigned char>(), cnt);
+    CKL();
+    RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+        return cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, off, (int)(n_rx + 1), st);
+    }));
+    CK(cudaMemcpyAsync(ctx->hpin, off + n_rx, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    long long P = reinterpret_cast<int*>(ctx->hpin)[0];
+    int L = ctx->path_L;
+    size_t Pn = (size_t)std::max<long long>(P, 1);
+    CK(ctx->p_rx.reserve(4 * Pn));
+    CK(ctx->p_cand.reserve(4 * Pn));
+    CK(ctx->p_order.reserve(Pn));
+    CK(ctx->p_seq.reserve(4 * Pn * L));
+    CK(ctx->p_verts.reserve(24 * Pn * (L + 2)));
+    CK(ctx->p_len.reserve(8 * Pn));
+    CK(ctx->p_delay.reserve(8 * Pn));
+    CK(ctx->p_kdep.reserve(24 * Pn));
+    CK(ctx->p_karr.reserve(24 * Pn));
+    CK(ctx->p_nrm.reserve(24 * Pn * L));
+    CK(ctx->p_cos.reserve(8 * Pn * L));
+    PathTable PT;
+    PT.rx = ctx->p_rx.get<int>();
+    PT.cand = ctx->p_cand.get<int>();
+    PT.order = ctx->p_order.get<signed char>();
+    PT.seq = ctx->p_seq.get<int>();
+    PT.verts = ctx->p_verts.get<double>();
+    PT.length = ctx->p_len.get<double>();
+    PT.delay = ctx->p_delay.get<double>();
+    PT.kdep = ctx->p_kdep.get<double>();
+    PT.karr = ctx->p_karr.get<double>();
+    PT.nrm = ctx->p_nrm.get<double>();
+    PT.cosv = ctx->p_cos.get<double>();
+    PT.L = L;
+    if (P > 0) {
+        k_emit_paths<<<nblk(n_rx, 64), 64, 0, st>>>(cands_dev(ctx), scene_dev(ctx), ctx->images.get<double>(), R, T,
+                                                     ctx->recs.get<Rec>(), ctx->ridx.get<int>(),
+                                                     ctx->rkeys.get<unsigned long long>(), n_rec,
+                                                     ctx->keep.get<unsigned char>(), ctx->losbuf.get<unsigned char>(),
+                                                     ctx->heads.get<int>(), off, PT);
+        CKL();
+    }
+    ctx->n_paths = P;
+    if (n_paths_out) *n_paths_out = P;
+    return RT_OK;
+}
+
+int rt_paths_get(rt_ctx* ctx, int32_t* rx_index, int32_t* cand, int8_t* order, int32_t* seq,
+                 double* vertices, double* length, double* delay, double* k_dep, double* k_arr,
+                 double* normals, double* cos_inc, void* stream) {
+    if (!ctx) return RT_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    size_t P = ctx->n_paths, L = ctx->path_L;
+    if (!P) return RT_OK;
+    auto cp = [&](void* dst, const DevBuf& src, size_t bytes) -> cudaError_t {
+        return dst ? cudaMemcpyAsync(dst, src.p, bytes, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+    };
+    CK(cp(rx_index, ctx->p_rx, 4 * P));
+    CK(cp(cand, ctx->p_cand, 4 * P));
+    CK(cp(order, ctx->p_order, P));
+    CK(cp(seq, ctx->p_seq, 4 * P * L));
+    CK(cp(vertices, ctx->p_verts, 24 * P * (L + 2)));
+    CK(cp(length, ctx->p_len, 8 * P));
+    CK(cp(delay, ctx->p_delay, 8 * P));
+    CK(cp(k_dep, ctx->p_kdep, 24 * P));
+    CK(cp(k_arr, ctx->p_karr, 24 * P));
+    CK(cp(normals, ctx->p_nrm, 24 * P * L));
+    CK(cp(cos_inc, ctx->p_cos, 8 * P * L));
+    return RT_OK;
+}
+
+int rt_transfer(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, const int32_t* seq,
+                const double* vertices, const double* normals, const double* cos_inc,
+                const double* length, const double* delay, const double* tx_rows,
+                const double* rx_rows, int tx_pattern, int rx_pattern, const double* tx_slants,
+                int n_tx_slants, const double* rx_slants, int n_rx_slants, const double* eta,
+                int n_mat, double wavelength, double frequency_hz, double* a_out, void* stream) {
+    if (!ctx || n_paths < 0 || max_len < 1 || n_tx_slants < 1 || n_rx_slants < 1)
+        return fail(ctx, RT_EINVAL, "bad transfer arguments");
+    if (tx_pattern < 0 || tx_pattern > 4 || rx_pattern < 0 || rx_pattern > 4)
+        return fail(ctx, RT_EINVAL, "unknown antenna pattern");
+    if (n_paths == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    (void)n_mat;
+    TransferArgs A{n_paths, max_len, (const signed char*)order, seq, vertices, normals, cos_inc, length,
+                   delay, tx_rows, rx_rows, tx_pattern, rx_pattern, tx_slants, n_tx_slants,
+                   rx_slants, n_rx_slants, eta, ctx->prim_mat.get<int>(), wavelength, frequency_hz};
+    k_transfer<<<nblk(n_paths * n_tx_slants, 128), 128, 0, ST(stream)>>>(A, a_out);
+    CKL();
+    return RT_OK;
+}
+
+int rt_transfer_bwd(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
+                    const int32_t* seq, const double* vertices, const double* normals,
+                    const double* cos_inc, const double* length, const double* delay,
+                    const double* tx_rows, const double* rx_rows, int tx_pattern, int rx_pattern,
+                    const double* tx_slants, int n_tx_slants, const double* rx_slants,
+                    int n_rx_slants, const double* eta, int n_mat, double wavelength,
+                    double frequency_hz, const double* grad_a, double* grad_eta, void* stream) {
+    if (!ctx || n_paths < 0 || max_len < 1 || n_tx_slants < 1 || n_rx_slants < 1)
+        return fail(ctx, RT_EINVAL, "bad transfer arguments");
+    if (n_paths == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    (void)n_mat;
+    TransferArgs A{n_paths, max_len, (const signed char*)order, seq, vertices, normals, cos_inc, length,
+                   delay, tx_rows, rx_rows, tx_pattern, rx_pattern, tx_slants, n_tx_slants,
+                   rx_slants, n_rx_slants, eta, ctx->prim_mat.get<int>(), wavelength, frequency_hz};
+    long long n = n_paths * n_tx_slants * n_rx_slants;
+    k_transfer_bwd<<<nblk(n, 128), 128, 0, ST(stream)>>>(A, grad_a, grad_eta);
+    CKL();
+    return RT_OK;
+}
+
+int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y, double cell_size,
+                int64_t nx, int64_t ny, double height, const double* tx_rows,
+                const double* probe_rows, int tx_pattern, const double* slants,
+                const double* offsets_w, int n_el, int tx_mode, const double* eta, int n_mat,
+                double wavelength, double frequency_hz, int shard_index, int shard_count,
+                double* gains_out, int64_t* stats_out, void* stream) {
+    if (!ctx || !tx || nx < 0 || ny < 0 || n_el < 1 || shard_count < 1 || shard_index < 0 ||
+        shard_index >= shard_count || !(cell_size > 0.0))
+        return fail(ctx, RT_EINVAL, "bad coverage arguments");
+    if (tx_mode != 0 && tx_mode != 1) return fail(ctx, RT_EINVAL, "unknown tx_mode");
+    if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    (void)n_mat;
+    d3 T = d3{tx[0], tx[1], tx[2]};
+    Receivers R;
+    R.pts = nullptr;
+    R.ox = origin_x;
+    R.oy = origin_y;
+    R.cell = cell_size;
+    R.height = height;
+    R.nx = nx;
+    R.ny = ny;
+    R.n = nx * ny;
+    long long stats[8] = {0, 0, 0, R.n, ctx->n_cand, 0, 0, 0};
+    if (R.n == 0) {
+        if (stats_out) memcpy(stats_out, stats, sizeof stats);
+        return RT_OK;
+    }
+    EmParams E;
+    double *d_tx, *d_probe, *d_sl, *d_off;
+    RC(em_upload(ctx, tx_rows, probe_rows, slants, offsets_w, n_el, st, &d_tx, &d_probe, &d_sl, &d_off));
+    E.eta = eta;
+    E.tx_rows = d_tx;
+    E.probe_rows = d_probe;
+    E.slants = d_sl;
+    E.offsets_w = d_off;
+    E.n_el = n_el;
+    E.tx_pattern = tx_pattern;
+    E.tx_mode = tx_mode;
+    E.wavelength = wavelength;
+    E.frequency = frequency_hz;
+    RC(clear_flags(ctx, st));
+    k_los<true><<<nblk(R.n, 128), 128, 0, st>>>(R, T, bvh_dev(ctx), scene_dev(ctx), E, shard_index,
+                                                shard_count, nullptr, gains_out,
+                                                reinterpret_cast<int*>(ctx->dflag.get<long long>()));
+    CKL();
+    RC(check_flags(ctx, st));
+    long long n_rec = 0;
+    RC(solve_records(ctx, T, R, true, true, E, shard_index, shard_count, &n_rec, stats, st));
+    if (n_rec > 0) {
+        CK(ctx->keep.reserve((size_t)n_rec));
+        k_merge<true><<<nblk(n_rec, 128), 128, 0, st>>>(cands_dev(ctx), scene_dev(ctx), ctx->images.get<double>(),
+                                                       R, T, ctx->recs.get<Rec>(), ctx->ridx.get<int>(),
+                                                       ctx->rkeys.get<unsigned long long>(), n_rec,
+                                                       ctx->keep.get<unsigned char>(), gains_out);
+        CKL();
+    }
+    if (stats_out) memcpy(stats_out, stats, sizeof stats);
+    return RT_OK;
+}
+
+}  // extern "C"

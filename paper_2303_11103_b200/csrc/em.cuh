@@ -1,0 +1,279 @@
+// em.cuh — polarized field transfer along a specular path and its adjoint.
+//
+// Restates em.py:42-171 and 291-312 in FP64: antenna patterns, element
+// field in the rotated/slanted element frame, Fresnel coefficients on the
+// Re>=0 square-root branch (autodiff.py:365-382), the 3-vector TE/TM basis
+// change per bounce with the normal-incidence fallback axis, free-space
+// amplitude lambda/(4 pi L) and phase e^{-j 2 pi f tau}.  Complex operations
+// follow DiffComplex's component formulas (autodiff.py:215-292).
+#pragma once
+#include "rt_common.cuh"
+
+namespace rt {
+
+struct c2 {
+    double re, im;
+};
+__device__ inline c2 cmul(c2 a, c2 b) { return c2{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+__device__ inline c2 cdiv(c2 a, c2 o) {
+    double d = o.re * o.re + o.im * o.im;
+    return c2{(a.re * o.re + a.im * o.im) / d, (a.im * o.re - a.re * o.im) / d};
+}
+__device__ inline c2 cscl(c2 a, double s) { return c2{a.re * s, a.im * s}; }
+__device__ inline c2 cadd(c2 a, c2 b) { return c2{a.re + b.re, a.im + b.im}; }
+__device__ inline c2 csub(c2 a, c2 b) { return c2{a.re - b.re, a.im - b.im}; }
+__device__ inline c2 cconj(c2 a) { return c2{a.re, -a.im}; }
+
+struct c3 {
+    c2 x, y, z;
+};
+// sum_i f_i * e_i (complex * real), left to right
+__device__ inline c2 cdotr(const c3& f, d3 e) {
+    return cadd(cadd(cscl(f.x, e.x), cscl(f.y, e.y)), cscl(f.z, e.z));
+}
+
+// em.py:42-75; returns (E_theta, E_phi)
+__device__ inline void pattern_eval(int id, double theta, double phi, double& eth, double& eph) {
+    eth = 0.0;
+    eph = 0.0;
+    if (id == 0 || id == 3) {
+        eth = 1.0;
+    } else if (id == 1) {
+        double s = sin(theta);
+        if (s < 1e-9) return;
+        eth = sqrt(1.643) * cos(1.5707963267948966 * cos(theta)) / s;
+    } else if (id == 2) {
+        const double deg = 180.0 / PI;
+        double tilt = theta * deg - 90.0, pan = phi * deg;
+        double av = 12.0 * (tilt / 65.0) * (tilt / 65.0);
+        if (!(av <= 30.0)) av = 30.0;
+        double ah = 12.0 * (pan / 65.0) * (pan / 65.0);
+        if (!(ah <= 30.0)) ah = 30.0;
+        double s = av + ah;
+        if (!(s <= 30.0)) s = 30.0;
+        eth = exp((8.0 - s) * (2.302585092994046 / 20.0));
+    } else if (id == 4) {
+        eph = 1.0;
+    }
+}
+
+// em.py:98-118; R row-major (rotation_entries rows)
+__device__ inline d3 element_field(int pat, double slant, const double* R, d3 k) {
+    d3 kb = d3{R[0] * k.x + R[3] * k.y + R[6] * k.z, R[1] * k.x + R[4] * k.y + R[7] * k.z,
+               R[2] * k.x + R[5] * k.y + R[8] * k.z};
+    double cz = cos(slant), sz = sin(slant);
+    d3 ke = d3{kb.x, cz * kb.y + sz * kb.z, -sz * kb.y + cz * kb.z};
+    double theta = atan2(sqrt(ke.x * ke.x + ke.y * ke.y), ke.z);
+    double phi = atan2(ke.y, ke.x);
+    double eth, eph;
+    pattern_eval(pat, theta, phi, eth, eph);
+    double ct = cos(theta), st = sin(theta), cp = cos(phi), sp = sin(phi);
+    d3 ee = d3{eth * (ct * cp) + eph * (-sp), eth * (ct * sp) + eph * cp, eth * (-st)};
+    d3 eb = d3{ee.x, cz * ee.y - sz * ee.z, sz * ee.y + cz * ee.z};
+    return d3{R[0] * eb.x + R[1] * eb.y + R[2] * eb.z, R[3] * eb.x + R[4] * eb.y + R[5] * eb.z,
+              R[6] * eb.x + R[7] * eb.y + R[8] * eb.z};
+}
+
+__device__ inline c2 csqrt_posreal(c2 z) {
+    double m = sqrt(z.re * z.re + z.im * z.im);
+    double u2 = (m + z.re) * 0.5, v2 = (m - z.re) * 0.5;
+    double u = u2 > 0.0 ? sqrt(u2) : u2 * 0.0;
+    double v = v2 > 0.0 ? sqrt(v2) : v2 * 0.0;
+    if (z.im < 0.0) v = -v;
+    return c2{u, v};
+}
+
+// em.py:123-141; also returns w for the adjoint
+__device__ inline void fresnel(c2 eta, double ci, c2& rte, c2& rtm, c2& w) {
+    double sin2 = 1.0 - ci * ci;
+    w = csqrt_posreal(c2{eta.re - sin2, eta.im});
+    c2 c = c2{ci, 0.0};
+    rte = cdiv(csub(c, w), cadd(c, w));
+    c2 ec = cscl(eta, ci);
+    rtm = cdiv(csub(w, ec), cadd(w, ec));
+}
+
+struct Basis {
+    d3 ep, epi, epr;
+};
+// em.py:144-157 (_perp_axis) and the two parallel axes of reflect_field
+__device__ inline Basis reflect_basis(d3 kin, d3 kout, d3 n) {
+    d3 e = cross(kin, n);
+    if (tdot(e, e) < 1e-16) {
+        double a0 = fabs(kin.x), a1 = fabs(kin.y), a2 = fabs(kin.z);
+        d3 axis = d3{1.0, 0.0, 0.0};
+        double mn = a0;
+        if (a1 < mn) { mn = a1; axis = d3{0.0, 1.0, 0.0}; }
+        if (a2 < mn) { axis = d3{0.0, 0.0, 1.0}; }
+        e = cross(kin, axis);
+    }
+    double nn = sqrt(tdot(e, e));
+    e = d3{e.x / nn, e.y / nn, e.z / nn};
+    Basis b;
+    b.ep = e;
+    b.epi = cross(kin, e);
+    b.epr = cross(e, kout);
+    return b;
+}
+
+// em.py:160-171
+__device__ inline void reflect_apply(c3& f, const Basis& b, c2 rte, c2 rtm) {
+    c2 fp = cdotr(f, b.ep), fa = cdotr(f, b.epi);
+    c2 gp = cmul(rte, fp), ga = cmul(rtm, fa);
+    f.x = cadd(cscl(gp, b.ep.x), cscl(ga, b.epr.x));
+    f.y = cadd(cscl(gp, b.ep.y), cscl(ga, b.epr.y));
+    f.z = cadd(cscl(gp, b.ep.z), cscl(ga, b.epr.z));
+}
+
+// Path geometry as path_from_points (tracer.py:105-133) followed by
+// geometry_from_path (em.py:246-255).
+struct Geom {
+    int k;
+    d3 dir[MAX_DEPTH + 1];
+    d3 nrm[MAX_DEPTH];
+    double cosi[MAX_DEPTH];
+    int mat[MAX_DEPTH];
+    double length, delay;
+};
+
+// from endpoints + interaction points; normals oriented against incidence
+__device__ inline void geom_from_points(d3 tx, const d3* pts, int k, d3 rx, const int* seq,
+                                        const double* normals, const int* prim_mat, Geom& g) {
+    g.k = k;
+    double total = 0.0;
+    d3 a = tx;
+    for (int j = 0; j <= k; ++j) {
+        d3 b = j < k ? pts[j] : rx;
+        d3 s = sub(b, a);
+        double l = sqrt(s.x * s.x + s.y * s.y + s.z * s.z);
+        total += l;
+        g.dir[j] = d3{s.x / l, s.y / l, s.z / l};
+        a = b;
+    }
+    for (int j = 0; j < k; ++j) {
+        d3 n = ld3(normals + 3 * (long long)seq[j]);
+        double ci = -dot_blas(g.dir[j], n);
+        if (ci < 0.0) { n = d3{-n.x, -n.y, -n.z}; ci = -ci; }
+        g.nrm[j] = n;
+        g.cosi[j] = ci;
+        g.mat[j] = prim_mat[seq[j]];
+    }
+    g.length = total;
+    g.delay = total / SPEED_OF_LIGHT;
+}
+
+// from a stored path table row (vertices + oriented normals + cosines)
+__device__ inline void geom_from_table(int k, const double* verts, const double* nrm,
+                                       const double* cosv, const int* seq, const int* prim_mat,
+                                       double length, double delay, Geom& g) {
+    g.k = k;
+    for (int j = 0; j <= k; ++j) {
+        d3 s = sub(ld3(verts + 3 * (j + 1)), ld3(verts + 3 * j));
+        double l = sqrt(s.x * s.x + s.y * s.y + s.z * s.z);
+        g.dir[j] = d3{s.x / l, s.y / l, s.z / l};
+    }
+    for (int j = 0; j < k; ++j) {
+        g.nrm[j] = ld3(nrm + 3 * j);
+        g.cosi[j] = cosv[j];
+        g.mat[j] = prim_mat[seq[j]];
+    }
+    g.length = length;
+    g.delay = delay;
+}
+
+// transported field at the receiver end (before the rx element projection)
+__device__ inline c3 transport(const Geom& g, int tx_pat, double tx_slant, const double* Rtx,
+                               const double* eta) {
+    d3 ef = element_field(tx_pat, tx_slant, Rtx, g.dir[0]);
+    c3 f = c3{c2{ef.x, 0.0}, c2{ef.y, 0.0}, c2{ef.z, 0.0}};
+    for (int j = 0; j < g.k; ++j) {
+        c2 e = c2{eta[2 * g.mat[j]], eta[2 * g.mat[j] + 1]};
+        c2 rte, rtm, w;
+        fresnel(e, g.cosi[j], rte, rtm, w);
+        Basis b = reflect_basis(g.dir[j], g.dir[j + 1], g.nrm[j]);
+        reflect_apply(f, b, rte, rtm);
+    }
+    return f;
+}
+
+// em.py:306-312: a = (coupling * amp) * expj(phase)
+__device__ inline c2 finish(const c3& f, d3 rf, const Geom& g, double wavelength,
+                            double frequency) {
+    c2 coup = cadd(cadd(cscl(f.x, rf.x), cscl(f.y, rf.y)), cscl(f.z, rf.z));
+    double amp = wavelength / (2.0 * TWO_PI * g.length);
+    double phase = -TWO_PI * frequency * g.delay;
+    double s, c;
+    sincos(phase, &s, &c);
+    return cmul(cscl(coup, amp), c2{c, s});
+}
+
+__device__ inline d3 rx_field(const Geom& g, int rx_pat, double rx_slant, const double* Rrx) {
+    d3 karr = g.dir[g.k];
+    return element_field(rx_pat, rx_slant, Rrx, d3{karr.x * -1.0, karr.y * -1.0, karr.z * -1.0});
+}
+
+// Adjoint of a(eta) for one path and one element pair: accumulates
+// (dL/dRe eta_m, dL/dIm eta_m) for upstream G = dL/dRe a + j dL/dIm a.
+// Branch handling matches the reference tape: where Im(eta - sin^2) == 0 the
+// square root's imaginary-direction derivative is 0 (autodiff.py:373-377).
+__device__ inline void transfer_adjoint(const Geom& g, int tx_pat, double tx_slant,
+                                        const double* Rtx, int rx_pat, double rx_slant,
+                                        const double* Rrx, const double* eta, double wavelength,
+                                        double frequency, c2 G, double* grad_eta) {
+    if (g.k == 0) return;
+    d3 ef = element_field(tx_pat, tx_slant, Rtx, g.dir[0]);
+    c3 f = c3{c2{ef.x, 0.0}, c2{ef.y, 0.0}, c2{ef.z, 0.0}};
+    c3 fin[MAX_DEPTH];
+    c2 rte[MAX_DEPTH], rtm[MAX_DEPTH], ww[MAX_DEPTH], et[MAX_DEPTH];
+    Basis bs[MAX_DEPTH];
+    for (int j = 0; j < g.k; ++j) {
+        fin[j] = f;
+        et[j] = c2{eta[2 * g.mat[j]], eta[2 * g.mat[j] + 1]};
+        fresnel(et[j], g.cosi[j], rte[j], rtm[j], ww[j]);
+        bs[j] = reflect_basis(g.dir[j], g.dir[j + 1], g.nrm[j]);
+        reflect_apply(f, bs[j], rte[j], rtm[j]);
+    }
+    d3 rf = rx_field(g, rx_pat, rx_slant, Rrx);
+    double amp = wavelength / (2.0 * TWO_PI * g.length);
+    double phase = -TWO_PI * frequency * g.delay;
+    double s, c;
+    sincos(phase, &s, &c);
+    c2 scl = c2{amp * c, amp * s};
+    c2 Gc = cconj(G);
+    // backward vector b (complex 3-vector), starts as the rx element field
+    c3 b = c3{c2{rf.x, 0.0}, c2{rf.y, 0.0}, c2{rf.z, 0.0}};
+    for (int j = g.k - 1; j >= 0; --j) {
+        const Basis& B = bs[j];
+        c2 b_ep = cdotr(b, B.ep), b_epr = cdotr(b, B.epr);
+        c2 f_ep = cdotr(fin[j], B.ep), f_epi = cdotr(fin[j], B.epi);
+        c2 da_drte = cmul(scl, cmul(b_ep, f_ep));
+        c2 da_drtm = cmul(scl, cmul(b_epr, f_epi));
+        // Fresnel partials at this interaction
+        double ci = g.cosi[j];
+        c2 w = ww[j], e = et[j];
+        c2 cpw = cadd(c2{ci, 0.0}, w);
+        c2 ec = cscl(e, ci);
+        c2 wpe = cadd(w, ec);
+        c2 drte_dw = cdiv(c2{-2.0 * ci, 0.0}, cmul(cpw, cpw));
+        c2 drtm_dw = cdiv(cscl(e, 2.0 * ci), cmul(wpe, wpe));
+        c2 drtm_de = cdiv(cscl(w, -2.0 * ci), cmul(wpe, wpe));
+        c2 da_dw = cadd(cmul(da_drte, drte_dw), cmul(da_drtm, drtm_dw));
+        c2 da_de = cmul(da_drtm, drtm_de);   // explicit eta dependence of r_TM
+        // dw/dRe(arg) = 1/(2w); dw/dIm(arg) = j/(2w), 0 on the real axis (tape branch)
+        c2 dw_dre = cdiv(c2{1.0, 0.0}, cscl(w, 2.0));
+        double arg_im = e.im;
+        c2 dw_dim = arg_im == 0.0 ? c2{0.0, 0.0} : cmul(c2{0.0, 1.0}, dw_dre);
+        c2 dre = cadd(da_de, cmul(da_dw, dw_dre));
+        c2 dim = cadd(cmul(c2{0.0, 1.0}, da_de), cmul(da_dw, dw_dim));
+        int m = g.mat[j];
+        atomicAdd(grad_eta + 2 * m, cmul(Gc, dre).re);
+        atomicAdd(grad_eta + 2 * m + 1, cmul(Gc, dim).re);
+        // b <- R_j^T b = rte (b.ep) ep + rtm (b.epr) epi
+        c2 gp = cmul(rte[j], b_ep), ga = cmul(rtm[j], b_epr);
+        b.x = cadd(cscl(gp, B.ep.x), cscl(ga, B.epi.x));
+        b.y = cadd(cscl(gp, B.ep.y), cscl(ga, B.epi.y));
+        b.z = cadd(cscl(gp, B.ep.z), cscl(ga, B.epi.z));
+    }
+}
+
+}  // namespace rt

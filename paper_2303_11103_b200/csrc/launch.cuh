@@ -1,0 +1,249 @@
+// launch.cuh — Fibonacci ray launch with on-device candidate trie.
+//
+// Replaces launch_candidates (tracer.py:217-244) and fibonacci_directions
+// (geometry.py:62-76).  Each thread owns one ray: up to max_depth closest
+// hits (t_min = RAY_EPS, t_max = inf), normal flipped to face the ray, point
+// o + t*d, specular d <- d - 2(d.n)n, all with the reference's FP64 operation
+// order.  The set of every prefix of every ray's hit sequence is kept as a
+// trie in a global open-addressing hash table keyed (parent node, prim):
+// node ids are allocated on first insert, so each unique prefix is one node.
+// Warps aggregate identical keys with __match_any_sync before touching the
+// table (neighbouring rays mostly hit the same triangles).
+//
+// Coherence: lattice index i = band * B + perm[slot % B] where perm sorts a
+// band of B consecutive indices by azimuth; neighbouring threads therefore
+// trace neighbouring directions.  The permutation is a bijection, so the
+// set of rays (and the candidate set) is unchanged.
+#pragma once
+#include "trace.cuh"
+
+namespace rt {
+
+constexpr unsigned long long EMPTY_KEY = 0xFFFFFFFFFFFFFFFFULL;
+
+struct Trie {
+    unsigned long long* keys;   // [cap]
+    int* vals;                  // [cap], -1 = not yet published
+    int* node_parent;           // [max_nodes]
+    int* node_prim;
+    signed char* node_depth;
+    unsigned mask;
+    int max_nodes;
+    int* counter;               // nodes allocated (root = 0 is implicit)
+    int* overflow;
+};
+
+__device__ inline unsigned hash64(unsigned long long k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdULL;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ULL;
+    k ^= k >> 33;
+    return (unsigned)k;
+}
+
+// insert-or-get (parent, prim) -> node id (>= 1); -1 on overflow
+__device__ int trie_insert(const Trie& T, int parent, int prim, int depth) {
+    unsigned long long key = ((unsigned long long)(unsigned)parent << 32) | (unsigned)prim;
+    unsigned h = hash64(key) & T.mask;
+    for (unsigned probe = 0; probe <= T.mask; ++probe) {
+        unsigned long long k = *((volatile unsigned long long*)(T.keys + h));
+        if (k == EMPTY_KEY) {
+            unsigned long long prev = atomicCAS(T.keys + h, EMPTY_KEY, key);
+            if (prev == EMPTY_KEY) {
+                int id = atomicAdd(T.counter, 1) + 1;
+                if (id >= T.max_nodes) {
+                    atomicExch(T.overflow, 1);
+                    atomicExch(T.vals + h, -2);
+                    return -1;
+                }
+                T.node_parent[id] = parent;
+                T.node_prim[id] = prim;
+                T.node_depth[id] = (signed char)depth;
+                __threadfence();
+                atomicExch(T.vals + h, id);
+                return id;
+            }
+            k = prev;
+        }
+        if (k == key) {
+            int v;
+            while ((v = *((volatile int*)(T.vals + h))) == -1) {}
+            return v >= 0 ? v : -1;
+        }
+        h = (h + 1) & T.mask;
+    }
+    atomicExch(T.overflow, 1);
+    return -1;
+}
+
+struct LaunchParams {
+    double tx, ty, tz;
+    long long n_rays, slot_begin, slot_end;
+    int max_depth;
+    int band;                 // B; 0 disables the permutation
+    const int* perm;          // [B]
+    const double* dirs;       // optional [n_rays*3]
+    const double* normals;    // [n_prims*3] global order
+    unsigned long long* bounces;
+    int* error;
+};
+
+// geometry.py:70-76 for one index (on-device sin/cos; see DESIGN.md on ulps)
+__device__ inline d3 fib_dir(long long i, long long n) {
+    double di = (double)i;
+    double z = 1.0 - (2.0 * di + 1.0) / (double)n;
+    const double golden_sq = 2.618033988749895;   // (3 + sqrt 5) / 2 in double
+    double phi = (2.0 * PI) * di / golden_sq;
+    double r = sqrt(fmax(0.0, 1.0 - z * z));
+    double s, c;
+    sincos(phi, &s, &c);
+    return d3{r * c, r * s, z};
+}
+
+__global__ void __launch_bounds__(256) k_launch(Bvh bvh, LaunchParams P, Trie T) {
+    const unsigned FULL = 0xffffffffu;
+    int lane = threadIdx.x & 31;
+    unsigned long long my_bounces = 0;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    long long span = P.slot_end - P.slot_begin;
+    long long iters = (span + stride - 1) / stride;
+    for (long long it = 0; it < iters; ++it) {
+        long long slot = P.slot_begin + it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+        bool active = slot < P.slot_end;
+        d3 o = d3{P.tx, P.ty, P.tz}, d = d3{0, 0, 0};
+        if (active) {
+            long long i = slot;
+            if (P.band > 0) {
+                long long b = slot / P.band;
+                if ((b + 1) * P.band <= P.n_rays) i = b * P.band + P.perm[slot - b * P.band];
+            }
+            d = P.dirs ? ld3(P.dirs + 3 * i) : fib_dir(i, P.n_rays);
+        }
+        int parent = 0;
+        for (int k = 0; k < P.max_depth; ++k) {
+            int prim = -1;
+            double t = 0.0;
+            if (active) {
+                Ray r = make_ray(o, d);
+                prim = trace<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t);
+                ++my_bounces;
+                if (prim == -2) { atomicOr(P.error, 1); prim = -1; }
+                if (prim < 0) active = false;
+            }
+            unsigned amask = __ballot_sync(FULL, active);
+            if (amask == 0) break;
+            if (active) {
+                unsigned long long key = ((unsigned long long)(unsigned)parent << 32) | (unsigned)prim;
+                unsigned peers = __match_any_sync(amask, key);
+                int leader = __ffs(peers) - 1;
+                int id = 0;
+                if (lane == leader) id = trie_insert(T, parent, prim, k + 1);
+                id = __shfl_sync(peers, id, leader);
+                if (id < 0) { active = false; }
+                parent = id;
+                // Bvh.intersect normal orientation (bvh.py:98-100), hit point (:101)
+                d3 n = ld3(P.normals + 3 * (long long)prim);
+                if (dot_blas(n, d) > 0.0) n = d3{-n.x, -n.y, -n.z};
+                d3 pt = d3{o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+                // tracer.py:242-243
+                double kk = 2.0 * dot_blas(d, n);
+                d = d3{d.x - kk * n.x, d.y - kk * n.y, d.z - kk * n.z};
+                o = pt;
+            }
+        }
+    }
+    // warp-reduce the bounce count
+    for (int s = 16; s; s >>= 1) my_bounces += __shfl_xor_sync(FULL, my_bounces, s);
+    if (lane == 0 && my_bounces) atomicAdd(P.bounces, my_bounces);
+}
+
+// ---- candidate materialization ----------------------------------------------------------
+
+// node id (1..n_nodes) -> padded sequence + length
+__global__ void k_trie_sequences(int n_nodes, const int* node_parent, const int* node_prim,
+                                 const signed char* node_depth, int max_len, int* seq,
+                                 signed char* len) {
+    int id = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (id > n_nodes) return;
+    int L = node_depth[id];
+    int row = id - 1;
+    for (int k = L; k < max_len; ++k) seq[(long long)row * max_len + k] = -1;
+    int cur = id;
+    for (int k = L - 1; k >= 0; --k) {
+        seq[(long long)row * max_len + k] = node_prim[cur];
+        cur = node_parent[cur];
+    }
+    len[row] = (signed char)L;
+}
+
+// LSD radix passes over the digit columns: key of row perm[r] at column j
+// (prim + 1, 0 = padding) or, for j == max_len, the sequence length.
+__global__ void k_digit_column(long long n, const int* seq, const signed char* len, int max_len,
+                               int j, const int* perm, unsigned* keys) {
+    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    long long row = perm[r];
+    unsigned v;
+    if (j == max_len) v = (unsigned)len[row];
+    else {
+        int p = seq[row * max_len + j];
+        v = (j < len[row] && p >= 0) ? (unsigned)(p + 1) : 0u;
+    }
+    keys[r] = v;
+}
+
+__global__ void k_flag_unique(long long n, const int* perm, const int* seq, const signed char* len,
+                              int max_len, int* flag) {
+    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int f = 1;
+    if (r > 0) {
+        long long a = perm[r], b = perm[r - 1];
+        if (len[a] == len[b]) {
+            f = 0;
+            for (int j = 0; j < len[a]; ++j)
+                if (seq[a * max_len + j] != seq[b * max_len + j]) { f = 1; break; }
+        }
+    }
+    flag[r] = f;
+}
+
+__global__ void k_scatter_unique(long long n, const int* perm, const int* flag, const int* pos,
+                                 const int* seq_in, const signed char* len_in, int max_len,
+                                 int* seq_out, signed char* len_out) {
+    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= n || !flag[r]) return;
+    long long src = perm[r];
+    long long dst = pos[r];
+    int L = len_in[src];
+    for (int j = 0; j < max_len; ++j)
+        seq_out[dst * max_len + j] = j < L ? seq_in[src * max_len + j] : -1;
+    len_out[dst] = (signed char)L;
+}
+
+// exhaustive enumeration (tracer.py:196-214) directly in (length, lex) order
+__global__ void k_enumerate(long long total, int n, int max_depth, const long long* level_start,
+                            int* seq, signed char* len) {
+    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= total) return;
+    int L = 1;
+    while (L < max_depth && r >= level_start[L]) ++L;
+    long long local = r - level_start[L - 1];
+    // digits: first in [0,n), later in [0,n-1) skipping the previous prim
+    int digits[MAX_DEPTH];
+    for (int k = L - 1; k >= 1; --k) { digits[k] = (int)(local % (n - 1)); local /= (n - 1); }
+    digits[0] = (int)local;
+    int prev = -1;
+    for (int k = 0; k < max_depth; ++k) {
+        int v = -1;
+        if (k < L) {
+            v = (k == 0) ? digits[0] : (digits[k] >= prev ? digits[k] + 1 : digits[k]);
+            prev = v;
+        }
+        seq[r * max_depth + k] = v;
+    }
+    len[r] = (signed char)L;
+}
+
+}  // namespace rt

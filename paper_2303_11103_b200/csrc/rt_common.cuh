@@ -1,0 +1,73 @@
+// rt_common.cuh — shared types, constants and exact-rounding helpers.
+//
+// Every discrete decision of the reference (hit / miss, inside / outside,
+// valid / invalid) is taken in FP64 with the reference's operation order.
+// The library is compiled with --fmad=false, so `a*b + c` is two roundings
+// exactly like a Python float expression; numpy's BLAS dot on 3-vectors is
+// reproduced explicitly with __fma_rn (see dot_blas).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rt {
+
+constexpr double RAY_EPS = 1e-4;      // bvh.py:17
+constexpr double DET_EPS = 1e-12;     // bvh.py:18
+constexpr double BARY_EPS = 1e-12;    // bvh.py:19
+constexpr double MERGE_TOL = 1e-6;    // tracer.py:30
+constexpr double INSIDE_TOL = 1e-9;   // tracer.py:31
+constexpr double SIDE_TOL = 1e-12;    // tracer.py:32
+constexpr double SPEED_OF_LIGHT = 299792458.0;
+constexpr double PI = 3.141592653589793;
+constexpr double TWO_PI = 2.0 * 3.141592653589793;
+constexpr int MAX_DEPTH = 8;          // compile-time bound on interactions per path
+constexpr int LEAF_MAX = 4;           // BVH leaf collapse threshold
+constexpr int STACK_SIZE = 64;
+constexpr int RT_PAT_PROBE_THETA_ID = 3;  // em.py:70-75 internal coverage probes
+constexpr int RT_PAT_PROBE_PHI_ID = 4;
+
+struct d3 {
+    double x, y, z;
+};
+
+__host__ __device__ inline d3 mk(double x, double y, double z) { return d3{x, y, z}; }
+__host__ __device__ inline d3 sub(d3 a, d3 b) { return d3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__host__ __device__ inline d3 add(d3 a, d3 b) { return d3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+__host__ __device__ inline d3 scale(d3 a, double s) { return d3{a.x * s, a.y * s, a.z * s}; }
+// geometry.py t_dot: left-to-right, no contraction
+__host__ __device__ inline double tdot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+// numpy 1-D `a @ b` (OpenBLAS ddot): fma(a2,b2, fma(a1,b1, a0*b0))
+__device__ inline double dot_blas(d3 a, d3 b) {
+    return __fma_rn(a.z, b.z, __fma_rn(a.y, b.y, a.x * b.x));
+}
+__host__ __device__ inline d3 cross(d3 a, d3 b) {
+    return d3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ inline d3 ld3(const double* p) { return d3{p[0], p[1], p[2]}; }
+__device__ inline void st3(double* p, d3 v) { p[0] = v.x; p[1] = v.y; p[2] = v.z; }
+
+// BVH node: both children's boxes (float, rounded outward) + child refs.
+// A child ref >= 0 is an internal node index; a leaf ref has bit 31 set,
+// bits 28..30 = count-1, bits 0..27 = first slot in the sorted triangle array.
+struct __align__(16) BNode {
+    float4 a;   // lo0.x lo0.y lo0.z hi0.x
+    float4 b;   // hi0.y hi0.z lo1.x lo1.y
+    float4 c;   // lo1.z hi1.x hi1.y hi1.z
+    int4 d;     // child0 child1 - -
+};
+
+// triangle in sorted (BVH) order: FP64 v0, e1, e2 and the global prim id
+struct __align__(16) TriRec {
+    double v0x, v0y, v0z, e1x, e1y, e1z, e2x, e2y, e2z;
+    int prim;
+    int pad;
+};
+
+__host__ __device__ inline bool ref_is_leaf(int r) { return r < 0; }
+__host__ __device__ inline int leaf_first(int r) { return r & 0x0FFFFFFF; }
+__host__ __device__ inline int leaf_count(int r) { return ((r >> 28) & 7) + 1; }
+__host__ __device__ inline int make_leaf(int first, int count) {
+    return (int)(0x80000000u | ((unsigned)(count - 1) << 28) | (unsigned)first);
+}
+
+}  // namespace rt

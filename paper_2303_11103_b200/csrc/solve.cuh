@@ -1,0 +1,487 @@
+// solve.cuh — image-method solve, validity, occlusion, merge, coverage.
+//
+// Restates tracer.py:71-183 (_mirror, solve_points, _inside_triangle,
+// image_solve), tracer.py:186-193 (los_path), tracer.py:247-295 (merge and
+// ordering) and channel.py:190-253 (probe path gain per cell) as a
+// candidate-major pipeline:
+//   1. k_images      per candidate: the image chain I_1..I_K of the tx
+//                     (identical floats to solve_points' images).
+//   2. k_footprint   per candidate: conservative cell range on the grid plane:
+//                     a valid receiver lies in every cone from I_K through the
+//                     forward-mirrored interaction triangles; the bbox of their
+//                     projections (padded) bounds the cells worth solving.
+//   3. k_solve       per (candidate, cell in footprint) or (candidate, rx):
+//                     back-substitution + the geometric tests; survivors are
+//                     compacted (warp-aggregated atomics).
+//   4. k_validate    per survivor: occlusion of every segment (any-hit
+//                     traversals) then the field transfer; emits a record
+//                     keyed (receiver, order, candidate rank).
+//   5. sort records (CUB) and merge coincident paths per receiver in the
+//      reference's greedy order, then accumulate / materialize.
+#pragma once
+#include "em.cuh"
+#include "trace.cuh"
+
+namespace rt {
+
+struct SceneDev {
+    const double* v0;
+    const double* e1;
+    const double* e2;
+    const double* nrm;
+    const double* poff;
+    const int* prim_mat;
+    int n;
+};
+
+struct Cands {
+    const int* seq;
+    const signed char* len;
+    int max_len;
+    long long n;
+};
+
+__device__ inline d3 mirror(d3 p, d3 n, double c) {   // tracer.py:71-73
+    double k = 2.0 * (tdot(p, n) - c);
+    return d3{p.x - n.x * k, p.y - n.y * k, p.z - n.z * k};
+}
+
+__global__ void k_images(Cands C, SceneDev S, d3 tx, double* images /*[n*max_len*3]*/) {
+    long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= C.n) return;
+    int K = C.len[c];
+    d3 p = tx;
+    for (int j = 0; j < K; ++j) {
+        int prim = C.seq[c * C.max_len + j];
+        p = mirror(p, ld3(S.nrm + 3 * (long long)prim), S.poff[prim]);
+        st3(images + (c * C.max_len + j) * 3, p);
+    }
+}
+
+// solve_points back-substitution (tracer.py:88-102) + the geometric part of
+// image_solve (tracer.py:164-180).  Returns true when every test passes; the
+// interaction points land in pts[0..K).
+__device__ inline bool solve_geometric(const Cands& C, const SceneDev& S, const double* images,
+                                       long long c, d3 tx, d3 rx, d3* pts) {
+    int K = C.len[c];
+    const int* seq = C.seq + c * C.max_len;
+    d3 cur = rx;
+    double params[MAX_DEPTH];
+    for (int j = K - 1; j >= 0; --j) {
+        int prim = seq[j];
+        d3 n = ld3(S.nrm + 3 * (long long)prim);
+        double cc = S.poff[prim];
+        d3 target = ld3(images + (c * C.max_len + j) * 3);
+        d3 seg = sub(target, cur);
+        double denom = tdot(seg, n);
+        if (fabs(denom) < 1e-15) return false;
+        double s = (cc - tdot(cur, n)) / denom;
+        d3 p = d3{cur.x + seg.x * s, cur.y + seg.y * s, cur.z + seg.z * s};
+        // early out: the same test image_solve applies after the loop
+        if (!(1e-12 < s && s < 1.0 - 1e-12)) return false;
+        params[j] = s;
+        pts[j] = p;
+        cur = p;
+    }
+    (void)params;
+    for (int j = 0; j < K; ++j) {   // _inside_triangle (tracer.py:136-147)
+        int prim = seq[j];
+        d3 v0 = ld3(S.v0 + 3 * (long long)prim), e1 = ld3(S.e1 + 3 * (long long)prim),
+           e2 = ld3(S.e2 + 3 * (long long)prim);
+        d3 w = sub(pts[j], v0);
+        double d11 = dot_blas(e1, e1), d12 = dot_blas(e1, e2), d22 = dot_blas(e2, e2);
+        double w1 = dot_blas(w, e1), w2 = dot_blas(w, e2);
+        double den = d11 * d22 - d12 * d12;
+        double u = (d22 * w1 - d12 * w2) / den;
+        double v = (d11 * w2 - d12 * w1) / den;
+        if (!(u >= -INSIDE_TOL && v >= -INSIDE_TOL && u + v <= 1.0 + INSIDE_TOL)) return false;
+    }
+    for (int j = 0; j < K; ++j) {   // same-side reflection (tracer.py:170-176)
+        int prim = seq[j];
+        d3 n = ld3(S.nrm + 3 * (long long)prim);
+        double cc = S.poff[prim];
+        d3 before = j == 0 ? tx : pts[j - 1];
+        d3 after = j == K - 1 ? rx : pts[j + 1];
+        double b = tdot(before, n) - cc, a = tdot(after, n) - cc;
+        if (b * a <= SIDE_TOL) return false;
+    }
+    d3 a = tx;
+    for (int j = 0; j <= K; ++j) {   // minimum segment length (tracer.py:178-180)
+        d3 b = j < K ? pts[j] : rx;
+        double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+        if (sqrt(dx * dx + dy * dy + dz * dz) <= 2 * RAY_EPS) return false;
+        a = b;
+    }
+    return true;
+}
+
+// occlusion of every segment (tracer.py:181-182)
+__device__ inline bool segments_clear(const Bvh& bvh, d3 tx, const d3* pts, int K, d3 rx) {
+    d3 a = tx;
+    for (int j = 0; j <= K; ++j) {
+        d3 b = j < K ? pts[j] : rx;
+        if (occluded(bvh, a, b) != 0) return false;
+        a = b;
+    }
+    return true;
+}
+
+// ---- receivers: an explicit list or the cells of a grid --------------------------------
+
+struct Receivers {
+    const double* pts;   // list mode [n*3]; NULL for grid mode
+    double ox, oy, cell, height;
+    long long nx, ny;
+    long long n;         // list: n rx; grid: nx*ny
+};
+
+// GridSpec.cell_center (channel.py:146-149)
+__device__ inline d3 receiver_pos(const Receivers& R, long long r) {
+    if (R.pts) return ld3(R.pts + 3 * r);
+    long long iy = r / R.nx, ix = r - iy * R.nx;
+    return d3{R.ox + ((double)ix + 0.5) * R.cell, R.oy + ((double)iy + 0.5) * R.cell, R.height};
+}
+
+// ---- footprints -------------------------------------------------------------------------
+
+struct Footprint {
+    int ix0, iy0, w, h;   // cell box; w*h (or rows in shard) work items
+};
+
+__global__ void k_footprint(Cands C, SceneDev S, const double* images, Receivers R,
+                            int shard_index, int shard_count, Footprint* fp,
+                            long long* counts /*[n+1]*/) {
+    long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= C.n) {
+        if (c == C.n) counts[c] = 0;
+        return;
+    }
+    int K = C.len[c];
+    const int* seq = C.seq + c * C.max_len;
+    d3 A = ld3(images + (c * C.max_len + K - 1) * 3);
+    double hA = R.height - A.z;
+    double bx0 = -INFINITY, bx1 = INFINITY, by0 = -INFINITY, by1 = INFINITY;
+    bool empty = false;
+    if (hA != 0.0) {
+        for (int j = K - 1; j >= 0 && !empty; --j) {
+            int prim = seq[j];
+            d3 v0 = ld3(S.v0 + 3 * (long long)prim), e1 = ld3(S.e1 + 3 * (long long)prim),
+               e2 = ld3(S.e2 + 3 * (long long)prim);
+            d3 x[3] = {v0, add(v0, e1), add(v0, e2)};
+            // inflate about the centroid (covers the 1e-9 barycentric tolerance)
+            d3 ctr = d3{(x[0].x + x[1].x + x[2].x) / 3.0, (x[0].y + x[1].y + x[2].y) / 3.0,
+                        (x[0].z + x[1].z + x[2].z) / 3.0};
+            for (int m = 0; m < 3; ++m) x[m] = add(ctr, scale(sub(x[m], ctr), 1.0 + 1e-6));
+            // forward-mirror through planes j+1..K-1
+            for (int q = j + 1; q < K; ++q) {
+                int pq = seq[q];
+                d3 n = ld3(S.nrm + 3 * (long long)pq);
+                double cc = S.poff[pq];
+                for (int m = 0; m < 3; ++m) x[m] = mirror(x[m], n, cc);
+            }
+            int same = 0, opp = 0;
+            double px[3], py[3];
+            for (int m = 0; m < 3; ++m) {
+                double s = x[m].z - A.z;
+                if ((s > 0.0 && hA > 0.0) || (s < 0.0 && hA < 0.0)) {
+                    double lam = hA / s;
+                    px[m] = A.x + lam * (x[m].x - A.x);
+                    py[m] = A.y + lam * (x[m].y - A.y);
+                    ++same;
+                } else if ((s < 0.0 && hA > 0.0) || (s > 0.0 && hA < 0.0)) {
+                    ++opp;
+                }
+            }
+            if (opp == 3) { empty = true; break; }
+            if (same == 3) {
+                double lx = fmin(fmin(px[0], px[1]), px[2]), hx = fmax(fmax(px[0], px[1]), px[2]);
+                double ly = fmin(fmin(py[0], py[1]), py[2]), hy = fmax(fmax(py[0], py[1]), py[2]);
+                double mx = 1e-6 * (1.0 + fabs(lx) + fabs(hx)), my = 1e-6 * (1.0 + fabs(ly) + fabs(hy));
+                bx0 = fmax(bx0, lx - mx); bx1 = fmin(bx1, hx + mx);
+                by0 = fmax(by0, ly - my); by1 = fmin(by1, hy + my);
+                if (bx0 > bx1 || by0 > by1) { empty = true; break; }
+            }
+        }
+    }
+    Footprint f = {0, 0, 0, 0};
+    long long cnt = 0;
+    if (!empty) {
+        // cells whose centers can fall in [b0, b1], padded by one cell each side
+        double fx0 = isinf(bx0) ? -1e30 : (bx0 - R.ox) / R.cell - 0.5;
+        double fx1 = isinf(bx1) ? 1e30 : (bx1 - R.ox) / R.cell - 0.5;
+        double fy0 = isinf(by0) ? -1e30 : (by0 - R.oy) / R.cell - 0.5;
+        double fy1 = isinf(by1) ? 1e30 : (by1 - R.oy) / R.cell - 0.5;
+        long long ix0 = (long long)fmax(floor(fx0) - 1.0, 0.0);
+        long long ix1 = (long long)fmin(ceil(fx1) + 1.0, (double)(R.nx - 1));
+        long long iy0 = (long long)fmax(floor(fy0) - 1.0, 0.0);
+        long long iy1 = (long long)fmin(ceil(fy1) + 1.0, (double)(R.ny - 1));
+        if (ix0 <= ix1 && iy0 <= iy1 && fx0 < 1e29 && fy0 < 1e29 && fx1 > -1e29 && fy1 > -1e29) {
+            // rows of this shard: iy = first + k * shard_count
+            long long first = iy0 + ((shard_index - iy0 % shard_count) + shard_count) % shard_count;
+            long long rows = first <= iy1 ? (iy1 - first) / shard_count + 1 : 0;
+            f.ix0 = (int)ix0;
+            f.iy0 = (int)first;
+            f.w = (int)(ix1 - ix0 + 1);
+            f.h = (int)rows;
+            cnt = (long long)f.w * rows;
+        }
+    }
+    fp[c] = f;
+    counts[c] = cnt;
+}
+
+// survivor of the geometric tests
+struct Pending {
+    long long rx;
+    int cand;
+    int pad;
+};
+
+__device__ inline long long find_cand(const long long* scan, long long n, long long w) {
+    long long lo = 0, hi = n;   // largest c with scan[c] <= w
+    while (hi - lo > 1) {
+        long long mid = (lo + hi) >> 1;
+        if (scan[mid] <= w) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+template <bool GRID>
+__global__ void __launch_bounds__(256) k_solve(Cands C, SceneDev S, const double* images,
+                                               Receivers R, d3 tx, long long W,
+                                               const long long* scan, const Footprint* fp,
+                                               int shard_count, Pending* out,
+                                               unsigned long long* n_out,
+                                               unsigned long long cap) {
+    const unsigned FULL = 0xffffffffu;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    long long iters = (W + stride - 1) / stride;
+    int lane = threadIdx.x & 31;
+    for (long long it = 0; it < iters; ++it) {
+        long long w = it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+        bool ok = false;
+        long long rxi = 0;
+        int c = 0;
+        if (w < W) {
+            if (GRID) {
+                c = (int)find_cand(scan, C.n, w);
+                long long local = w - scan[c];
+                Footprint f = fp[c];
+                long long row = local / f.w, col = local - row * f.w;
+                long long iy = f.iy0 + row * shard_count, ix = f.ix0 + col;
+                rxi = iy * R.nx + ix;
+            } else {
+                c = (int)(w % C.n);
+                rxi = w / C.n;
+            }
+            d3 pts[MAX_DEPTH];
+            ok = solve_geometric(C, S, images, c, tx, receiver_pos(R, rxi), pts);
+        }
+        unsigned m = __ballot_sync(FULL, ok);
+        if (m) {
+            unsigned long long base = 0;
+            int leader = __ffs(m) - 1;
+            if (lane == leader) base = atomicAdd(n_out, (unsigned long long)__popc(m));
+            base = __shfl_sync(FULL, base, leader);
+            if (ok) {
+                unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
+                if (slot < cap) { out[slot].rx = rxi; out[slot].cand = c; }
+            }
+        }
+    }
+}
+
+// A valid path (after occlusion) of one receiver.
+struct Rec {
+    double p_theta, p_phi;   // probe powers (coverage) — unused for paths
+    double p0x, p0y, p0z;    // first interaction point (merge pre-check)
+    long long rx;
+    int cand;
+    int order;
+};
+
+struct EmParams {
+    const double* eta;
+    const double* tx_rows;     // 9
+    const double* probe_rows;  // 9
+    const double* slants;      // [n_el]
+    const double* offsets_w;   // [n_el*3]
+    int n_el;
+    int tx_pattern;
+    int tx_mode;               // 0 central, 1 array
+    double wavelength, frequency;
+};
+
+// coverage power of one path: sum over the theta / phi probes (channel.py:214-232)
+__device__ inline void probe_powers(const Geom& g, const EmParams& E, double& pt, double& pp) {
+    d3 rft = rx_field(g, RT_PAT_PROBE_THETA_ID, 0.0, E.probe_rows);
+    d3 rfp = rx_field(g, RT_PAT_PROBE_PHI_ID, 0.0, E.probe_rows);
+    c2 at, ap;
+    if (E.tx_mode == 0) {
+        c3 f = transport(g, E.tx_pattern, E.slants[0], E.tx_rows, E.eta);
+        at = finish(f, rft, g, E.wavelength, E.frequency);
+        ap = finish(f, rfp, g, E.wavelength, E.frequency);
+    } else {
+        at = c2{0.0, 0.0};
+        ap = c2{0.0, 0.0};
+        // the element transfer depends on the element only through its slant
+        double s_prev = 0.0;
+        c2 bt = c2{0.0, 0.0}, bp = c2{0.0, 0.0};
+        for (int e = 0; e < E.n_el; ++e) {
+            double sl = E.slants[e];
+            if (e == 0 || sl != s_prev) {
+                c3 f = transport(g, E.tx_pattern, sl, E.tx_rows, E.eta);
+                bt = finish(f, rft, g, E.wavelength, E.frequency);
+                bp = finish(f, rfp, g, E.wavelength, E.frequency);
+                s_prev = sl;
+            }
+            d3 off = ld3(E.offsets_w + 3 * e);
+            double ph = TWO_PI * tdot(g.dir[0], off) / E.wavelength;   // em.py:174-181
+            double s, c;
+            sincos(ph, &s, &c);
+            at = cadd(at, cmul(bt, c2{c, s}));
+            ap = cadd(ap, cmul(bp, c2{c, s}));
+        }
+    }
+    pt = at.re * at.re + at.im * at.im;
+    pp = ap.re * ap.re + ap.im * ap.im;
+}
+
+template <bool POWER>
+__global__ void __launch_bounds__(128) k_validate(Cands C, SceneDev S, const double* images,
+                                                  Receivers R, d3 tx, Bvh bvh,
+                                                  const Pending* pend, long long n_pend,
+                                                  EmParams E, Rec* recs,
+                                                  unsigned long long* n_out) {
+    const unsigned FULL = 0xffffffffu;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    long long iters = (n_pend + stride - 1) / stride;
+    int lane = threadIdx.x & 31;
+    for (long long it = 0; it < iters; ++it) {
+        long long i = it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+        bool ok = false;
+        Rec rec;
+        if (i < n_pend) {
+            Pending pd = pend[i];
+            d3 rx = receiver_pos(R, pd.rx);
+            d3 pts[MAX_DEPTH];
+            solve_geometric(C, S, images, pd.cand, tx, rx, pts);   // recompute points
+            int K = C.len[pd.cand];
+            ok = segments_clear(bvh, tx, pts, K, rx);
+            if (ok) {
+                rec.rx = pd.rx;
+                rec.cand = pd.cand;
+                rec.order = K;
+                rec.p0x = pts[0].x; rec.p0y = pts[0].y; rec.p0z = pts[0].z;
+                rec.p_theta = 0.0;
+                rec.p_phi = 0.0;
+                if (POWER) {
+                    Geom g;
+                    geom_from_points(tx, pts, K, rx, C.seq + (long long)pd.cand * C.max_len, S.nrm,
+                                     S.prim_mat, g);
+                    probe_powers(g, E, rec.p_theta, rec.p_phi);
+                }
+            }
+        }
+        unsigned m = __ballot_sync(FULL, ok);
+        if (m) {
+            unsigned long long base = 0;
+            int leader = __ffs(m) - 1;
+            if (lane == leader) base = atomicAdd(n_out, (unsigned long long)__popc(m));
+            base = __shfl_sync(FULL, base, leader);
+            if (ok) recs[base + __popc(m & ((1u << lane) - 1u))] = rec;
+        }
+    }
+}
+
+__global__ void k_rec_keys(const Rec* recs, long long n, unsigned long long* keys, int* idx) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const Rec& r = recs[i];
+    keys[i] = ((unsigned long long)r.rx << 36) | ((unsigned long long)r.order << 32) | (unsigned)r.cand;
+    idx[i] = (int)i;
+}
+
+// Greedy coincident merge of one receiver's records (tracer.py:247-265):
+// records are visited in (order, candidate) order; a record is dropped when
+// an earlier KEPT record of the same order has every vertex within 1e-6.
+__device__ inline bool coincident(const Cands& C, const SceneDev& S, const double* images, d3 tx,
+                                  d3 rx, const Rec& a, const Rec& b) {
+    double m0 = fmax(fmax(fabs(a.p0x - b.p0x), fabs(a.p0y - b.p0y)), fabs(a.p0z - b.p0z));
+    if (!(m0 < MERGE_TOL)) return false;
+    d3 pa[MAX_DEPTH], pb[MAX_DEPTH];
+    solve_geometric(C, S, images, a.cand, tx, rx, pa);
+    solve_geometric(C, S, images, b.cand, tx, rx, pb);
+    double mx = 0.0;
+    for (int j = 0; j < a.order; ++j)
+        mx = fmax(mx, fmax(fmax(fabs(pa[j].x - pb[j].x), fabs(pa[j].y - pb[j].y)), fabs(pa[j].z - pb[j].z)));
+    return mx < MERGE_TOL;
+}
+
+// one thread per receiver segment of the sorted records; writes keep[] and,
+// for coverage, adds the kept probe powers after the LOS term in gains[rx]
+template <bool COVERAGE>
+__global__ void k_merge(Cands C, SceneDev S, const double* images, Receivers R, d3 tx,
+                        const Rec* recs, const int* order, const unsigned long long* keys,
+                        long long n, unsigned char* keep, double* gains) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long rxi = (long long)(keys[i] >> 36);
+    if (i > 0 && (long long)(keys[i - 1] >> 36) == rxi) return;   // not the segment head
+    d3 rx = receiver_pos(R, rxi);
+    double g = COVERAGE ? gains[rxi] : 0.0;
+    long long grp = i;   // start of the current (rx, order) group
+    for (long long r = i; r < n && (long long)(keys[r] >> 36) == rxi; ++r) {
+        const Rec& a = recs[order[r]];
+        if (((keys[r] >> 32) & 0xF) != ((keys[grp] >> 32) & 0xF)) grp = r;
+        bool merged = false;
+        for (long long q = grp; q < r && !merged; ++q) {
+            if (!keep[q]) continue;
+            merged = coincident(C, S, images, tx, rx, recs[order[q]], a);
+        }
+        keep[r] = merged ? 0 : 1;
+        if (COVERAGE && !merged) {
+            g = g + a.p_theta;
+            g = g + a.p_phi;
+        }
+    }
+    if (COVERAGE) gains[rxi] = g;
+}
+
+// LOS per receiver (tracer.py:186-193); coverage adds its probe power first
+template <bool COVERAGE>
+__global__ void k_los(Receivers R, d3 tx, Bvh bvh, SceneDev S, EmParams E,
+                      int shard_index, int shard_count, unsigned char* los, double* gains,
+                      int* error) {
+    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= R.n) return;
+    if (COVERAGE) {
+        long long iy = r / R.nx;
+        if (iy % shard_count != shard_index) { gains[r] = 0.0; return; }
+    }
+    d3 rx = receiver_pos(R, r);
+    // np.allclose(tx, rx): |a-b| <= 1e-8 + 1e-5 |b|
+    if (fabs(tx.x - rx.x) <= 1e-8 + 1e-5 * fabs(rx.x) && fabs(tx.y - rx.y) <= 1e-8 + 1e-5 * fabs(rx.y) &&
+        fabs(tx.z - rx.z) <= 1e-8 + 1e-5 * fabs(rx.z)) {
+        atomicOr(error, 4);
+        if (COVERAGE) gains[r] = 0.0; else los[r] = 0;
+        return;
+    }
+    bool vis = S.n == 0 || occluded(bvh, tx, rx) == 0;
+    if (COVERAGE) {
+        double g = 0.0;
+        if (vis) {
+            Geom geo;
+            geom_from_points(tx, nullptr, 0, rx, nullptr, S.nrm, S.prim_mat, geo);
+            double pt, pp;
+            probe_powers(geo, E, pt, pp);
+            g = g + pt;
+            g = g + pp;
+        }
+        gains[r] = g;
+    } else {
+        los[r] = vis ? 1 : 0;
+    }
+}
+
+}  // namespace rt

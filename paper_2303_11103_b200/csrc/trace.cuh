@@ -1,0 +1,151 @@
+// trace.cuh — LBVH traversal with the reference's FP64 Moller-Trumbore test.
+//
+// Semantics (bvh.py:117-177 restated as a closest-hit query): the hit is the
+// triangle with the smallest t in (t_min, t_max) among all triangles whose
+// FP64 Moller-Trumbore test (two-sided, det window 1e-12, barycentric
+// tolerance 1e-12, operation order of bvh.py:151-170) accepts the ray; equal
+// t resolves to the lower global prim id (the reference's brute-force oracle,
+// tests/conftest.py:45-80).  Node boxes are conservative (inflated, rounded
+// outward to float) so the tree never culls a triangle the exact test accepts.
+#pragma once
+#include "rt_common.cuh"
+
+namespace rt {
+
+struct Ray {
+    double ox, oy, oz, dx, dy, dz;
+    double ix, iy, iz;   // 1/d, +inf where d == 0 (bvh.py:120-122)
+};
+
+__device__ inline Ray make_ray(d3 o, d3 d) {
+    Ray r;
+    r.ox = o.x; r.oy = o.y; r.oz = o.z;
+    r.dx = d.x; r.dy = d.y; r.dz = d.z;
+    r.ix = d.x != 0.0 ? 1.0 / d.x : __longlong_as_double(0x7ff0000000000000LL);
+    r.iy = d.y != 0.0 ? 1.0 / d.y : __longlong_as_double(0x7ff0000000000000LL);
+    r.iz = d.z != 0.0 ? 1.0 / d.z : __longlong_as_double(0x7ff0000000000000LL);
+    return r;
+}
+
+// Slab test of one float box in FP64; NaN (0*inf) never culls (fmin/fmax drop it).
+__device__ __forceinline__ bool slab(const Ray& r, float lx, float ly, float lz, float hx,
+                                     float hy, float hz, double tmin, double tmax,
+                                     double& tnear) {
+    double t0x = ((double)lx - r.ox) * r.ix, t1x = ((double)hx - r.ox) * r.ix;
+    double t0y = ((double)ly - r.oy) * r.iy, t1y = ((double)hy - r.oy) * r.iy;
+    double t0z = ((double)lz - r.oz) * r.iz, t1z = ((double)hz - r.oz) * r.iz;
+    double n = fmax(fmax(fmin(t0x, t1x), fmin(t0y, t1y)), fmax(fmin(t0z, t1z), tmin));
+    double f = fmin(fmin(fmax(t0x, t1x), fmax(t0y, t1y)), fmin(fmax(t0z, t1z), tmax));
+    tnear = n;
+    return n <= f;
+}
+
+// bvh.py:151-170 verbatim in operation order; returns true and t when accepted.
+__device__ __forceinline__ bool mt_test(const Ray& r, const TriRec* __restrict__ tp, double& t) {
+    const double2* q = reinterpret_cast<const double2*>(tp);
+    double2 a = __ldg(q + 0), b = __ldg(q + 1), c = __ldg(q + 2), dd = __ldg(q + 3),
+            e = __ldg(q + 4);
+    double v0x = a.x, v0y = a.y, v0z = b.x, e1x = b.y, e1y = c.x, e1z = c.y;
+    double e2x = dd.x, e2y = dd.y, e2z = e.x;
+    double px = r.dy * e2z - r.dz * e2y;
+    double py = r.dz * e2x - r.dx * e2z;
+    double pz = r.dx * e2y - r.dy * e2x;
+    double det = e1x * px + e1y * py + e1z * pz;
+    if (-DET_EPS < det && det < DET_EPS) return false;
+    double inv_det = 1.0 / det;
+    double tx = r.ox - v0x, ty = r.oy - v0y, tz = r.oz - v0z;
+    double u = (tx * px + ty * py + tz * pz) * inv_det;
+    if (u < -BARY_EPS || u > 1.0 + BARY_EPS) return false;
+    double qx = ty * e1z - tz * e1y;
+    double qy = tz * e1x - tx * e1z;
+    double qz = tx * e1y - ty * e1x;
+    double v = (r.dx * qx + r.dy * qy + r.dz * qz) * inv_det;
+    if (v < -BARY_EPS || u + v > 1.0 + BARY_EPS) return false;
+    t = (e2x * qx + e2y * qy + e2z * qz) * inv_det;
+    return true;
+}
+
+struct Bvh {
+    const BNode* __restrict__ nodes;
+    const TriRec* __restrict__ tris;
+    int n_prims;
+};
+
+// Closest (ANY=false) or first (ANY=true) hit with t in (tmin, tmax).
+// Returns the global prim id or -1; *t_out the hit distance.
+template <bool ANY>
+__device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, double* t_out,
+                     int* visits = nullptr) {
+    if (bvh.n_prims == 0) return -1;
+    int stack[STACK_SIZE];
+    double stack_t[STACK_SIZE];
+    int sp = 0;
+    double best_t = tmax;
+    int best_prim = -1;
+    int cur = 0;   // root is internal node 0 (a 1..4 prim scene gets a root with one leaf)
+    int nv = 0;
+    while (true) {
+        if (!ref_is_leaf(cur)) {
+            const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
+            float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
+            int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
+            ++nv;
+            double tn0, tn1;
+            bool h0 = slab(r, a.x, a.y, a.z, a.w, b.x, b.y, tmin, best_t, tn0);
+            bool h1 = slab(r, b.z, b.w, c.x, c.y, c.z, c.w, tmin, best_t, tn1);
+            if (h0 && h1) {
+                int nearc = ch.x, farc = ch.y;
+                double tf = tn1;
+                if (tn1 < tn0) { nearc = ch.y; farc = ch.x; tf = tn0; }
+                if (sp < STACK_SIZE) { stack[sp] = farc; stack_t[sp] = tf; ++sp; }
+                else { *t_out = -1.0; return -2; }   // overflow: reported as an error
+                cur = nearc;
+                continue;
+            } else if (h0) {
+                cur = ch.x;
+                continue;
+            } else if (h1) {
+                cur = ch.y;
+                continue;
+            }
+        } else {
+            int first = leaf_first(cur), cnt = leaf_count(cur);
+            for (int k = 0; k < cnt; ++k) {
+                const TriRec* tp = bvh.tris + first + k;
+                double t;
+                if (mt_test(r, tp, t)) {
+                    int prim = __ldg(&tp->prim);
+                    if (tmin < t && (t < best_t || (t == best_t && best_prim >= 0 && prim < best_prim))) {
+                        best_t = t;
+                        best_prim = prim;
+                        if (ANY) { *t_out = t; if (visits) *visits = nv; return prim; }
+                    }
+                }
+            }
+        }
+        // pop the next subtree whose entry distance still beats the best hit
+        bool found = false;
+        while (sp > 0) {
+            --sp;
+            if (stack_t[sp] <= best_t) { cur = stack[sp]; found = true; break; }
+        }
+        if (!found) break;
+    }
+    *t_out = best_t;
+    if (visits) *visits = nv;
+    return best_prim;
+}
+
+// Bvh.occluded (bvh.py:103-115): 1 blocked, 0 clear, -1 coincident endpoints
+__device__ inline int occluded(const Bvh& bvh, d3 p, d3 q, double eps = RAY_EPS) {
+    double dx = q.x - p.x, dy = q.y - p.y, dz = q.z - p.z;
+    double dist = sqrt(dx * dx + dy * dy + dz * dz);
+    if (dist == 0.0) return -1;
+    double inv = 1.0 / dist;
+    Ray r = make_ray(p, d3{dx * inv, dy * inv, dz * inv});
+    double t;
+    int h = trace<true>(bvh, r, eps, dist - eps, &t);
+    return h >= 0 ? 1 : (h == -2 ? 1 : 0);
+}
+
+}  // namespace rt

@@ -1,0 +1,355 @@
+"""Polarized channel coefficients along traced paths (+ adjoint).
+
+Drop-in for /root/reference/pkg/src/emtrace/em.py.  ``transfer`` (:291-312)
+and ``compute_gains`` (:359-422, synthetic arrays) evaluate every path and
+element-slant pair in one rt_transfer launch; the plane-wave array phasors
+(:408-415) are applied on the device with torch.  Gradients with respect to
+material parameters flow through ``PathCoefficients`` (a
+``torch.autograd.Function`` whose backward is the hand-written adjoint
+kernel rt_transfer_bwd) — this replaces the reference's scalar Tape.
+"""
+
+from __future__ import annotations
+
+import math
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .scene import (POLARIZATION_SLANTS, SPEED_OF_LIGHT, element_layout, eta_scale,
+                    material_params)
+from .tracer import PathSet, PathTable
+
+TWO_PI = 2.0 * math.pi
+
+
+class EmError(ValueError):
+    pass
+
+
+def rotation_entries(yaw, pitch, roll):
+    """Intrinsic Z-Y'-X'' rows (geometry.py:50-59)."""
+    cy, sy = math.cos(yaw), math.sin(yaw)
+    cp, sp = math.cos(pitch), math.sin(pitch)
+    cr, sr = math.cos(roll), math.sin(roll)
+    return ((cy * cp, cy * sp * sr - sy * cr, cy * sp * cr + sy * sr),
+            (sy * cp, sy * sp * sr + cy * cr, sy * sp * cr - cy * sr),
+            (-sp, cp * sr, cp * cr))
+
+
+def pattern_id(name):
+    try:
+        return N.PATTERN_IDS[name]
+    except KeyError:
+        raise EmError(f"unknown antenna pattern {name!r}") from None
+
+
+class EvalContext:
+    """Per-evaluation parameter values (em.py:186-227).
+
+    ``material_values`` maps material name -> (eps_r, sigma) (floats or 0-d
+    tensors); ``orientations`` maps device name -> (yaw, pitch, roll).
+    """
+
+    def __init__(self, scene, material_values=None, orientations=None, positions=None):
+        self.scene = scene
+        self.material_values = material_values or {}
+        self.orientations = orientations or {}
+        self.positions = positions or {}
+
+    def rotation_rows(self, device):
+        return rotation_entries(*self.orientations.get(device.name, device.orientation))
+
+    def eta_table(self, bvh):
+        """Complex permittivity per material in the scene's material order, [n_mat, 2]."""
+        vals = []
+        for name in bvh.material_names:
+            m = self.scene.materials[name]
+            ov = self.material_values.get(name)
+            e, s = material_params(m, self.scene.frequency_hz,
+                                   None if ov is None else float(ov[0]),
+                                   None if ov is None else float(ov[1]))
+            vals.append((e, s * (-eta_scale(self.scene.frequency_hz))))
+        if not vals:
+            vals = [(1.0, 0.0)]
+        return torch.tensor(vals, dtype=torch.float64, device=bvh.device)
+
+
+def path_materials(scene, bvh, path) -> tuple:
+    """Material name per interaction (em.py:315-317)."""
+    return tuple(scene.objects[bvh.prim_object[p]].material for p in path.seq)
+
+
+def _rows_tensor(rows_list, device):
+    return torch.tensor(np.asarray(rows_list, dtype=np.float64).reshape(-1, 9), dtype=torch.float64,
+                        device=device).contiguous()
+
+
+def _table_from_paths(paths, bvh, tx_names, rx_names):
+    """Device path table from reference-style PropagationPath objects."""
+    L = max([p.order for p in paths] + [1])
+    P = len(paths)
+    seq = np.full((P, L), -1, dtype=np.int32)
+    verts = np.zeros((P, L + 2, 3))
+    nrm = np.zeros((P, L, 3))
+    cos = np.zeros((P, L))
+    for i, p in enumerate(paths):
+        k = p.order
+        seq[i, :k] = p.seq
+        verts[i, :k + 2] = p.vertices
+        if k:
+            nrm[i, :k] = p.normals
+            cos[i, :k] = p.cos_incidence
+    dev = bvh.device
+    t = lambda a, dt=torch.float64: torch.as_tensor(a, dtype=dt, device=dev).contiguous()  # noqa: E731
+    return PathTable(L, tx_names, rx_names,
+                     tx=t([tx_names.index(p.tx) for p in paths], torch.int32),
+                     rx=t([rx_names.index(p.rx) for p in paths], torch.int32),
+                     cand=t(np.zeros(P), torch.int32), order=t([p.order for p in paths], torch.int8),
+                     seq=t(seq, torch.int32), verts=t(verts),
+                     length=t([p.length_m for p in paths]), delay=t([p.delay_s for p in paths]),
+                     kdep=t(np.array([p.k_dep for p in paths]).reshape(P, 3)),
+                     karr=t(np.array([p.k_arr for p in paths]).reshape(P, 3)),
+                     normals=t(nrm), cos=t(cos))
+
+
+def _launch_transfer(bvh, T: PathTable, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, eta, wavelength,
+                     frequency):
+    P = T.n
+    a = torch.empty((P, len(st), len(sr), 2), dtype=torch.float64, device=bvh.device)
+    if P == 0:
+        return a
+    stt = torch.tensor(st, dtype=torch.float64, device=bvh.device)
+    srt = torch.tensor(sr, dtype=torch.float64, device=bvh.device)
+    with torch.cuda.device(bvh.device):
+        bvh.ctx.call("rt_transfer", P, T.L, N.ptr(T.order), N.ptr(T.seq), N.ptr(T.verts),
+                     N.ptr(T.normals), N.ptr(T.cos), N.ptr(T.length), N.ptr(T.delay),
+                     N.ptr(tx_rows), N.ptr(rx_rows), tx_pat, rx_pat, N.ptr(stt), len(st),
+                     N.ptr(srt), len(sr), N.ptr(eta), eta.shape[0], float(wavelength),
+                     float(frequency), N.ptr(a), bvh.ctx.stream, exc_map={N.RT_EINVAL: EmError})
+    return a
+
+
+class PathCoefficients(torch.autograd.Function):
+    """a[p, s, r] (complex) as a function of eta (real pairs [n_mat, 2]).
+
+    forward = rt_transfer; backward = rt_transfer_bwd (hand-written adjoint
+    through the Fresnel / basis-change chain, em.py:123-171)."""
+
+    @staticmethod
+    def forward(ctx, eta, bvh, T, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, wavelength, frequency):
+        eta_c = eta.detach().contiguous()
+        a = _launch_transfer(bvh, T, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, eta_c, wavelength,
+                             frequency)
+        ctx.save_for_backward(eta_c)
+        ctx.args = (bvh, T, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, wavelength, frequency)
+        return torch.view_as_complex(a)
+
+    @staticmethod
+    def backward(ctx, grad_a):
+        (eta,) = ctx.saved_tensors
+        bvh, T, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, wavelength, frequency = ctx.args
+        g = torch.view_as_real(grad_a.contiguous().to(torch.complex128)).contiguous()
+        grad_eta = torch.zeros_like(eta)
+        if T.n:
+            stt = torch.tensor(st, dtype=torch.float64, device=bvh.device)
+            srt = torch.tensor(sr, dtype=torch.float64, device=bvh.device)
+            with torch.cuda.device(bvh.device):
+                bvh.ctx.call("rt_transfer_bwd", T.n, T.L, N.ptr(T.order), N.ptr(T.seq),
+                             N.ptr(T.verts), N.ptr(T.normals), N.ptr(T.cos), N.ptr(T.length),
+                             N.ptr(T.delay), N.ptr(tx_rows), N.ptr(rx_rows), tx_pat, rx_pat,
+                             N.ptr(stt), len(st), N.ptr(srt), len(sr), N.ptr(eta), eta.shape[0],
+                             float(wavelength), float(frequency), N.ptr(g), N.ptr(grad_eta),
+                             bvh.ctx.stream)
+        return (grad_eta,) + (None,) * 10
+
+
+def path_coefficients(bvh, T: PathTable, eta, tx_rows, rx_rows, tx_pattern, rx_pattern,
+                      tx_slants, rx_slants, wavelength, frequency):
+    """Differentiable a[p, s, r] (complex128) for a device path table."""
+    return PathCoefficients.apply(eta, bvh, T, tx_rows, rx_rows, pattern_id(tx_pattern),
+                                  pattern_id(rx_pattern), tuple(float(s) for s in tx_slants),
+                                  tuple(float(s) for s in rx_slants), float(wavelength),
+                                  float(frequency))
+
+
+def eta_from_params(eps_r, sigma, frequency_hz):
+    """eta = eps_r - j sigma / (2 pi f eps0) as real pairs (scene.py:99-100); differentiable."""
+    return torch.stack([eps_r, sigma * (-eta_scale(frequency_hz))], dim=-1)
+
+
+def transfer(ctx: EvalContext, geom, materials, tx_dev, rx_dev, tx_pattern: str, rx_pattern: str,
+             tx_slant: float, rx_slant: float, bvh=None) -> complex:
+    """Complex gain of one path for one element pair (em.py:291-312).
+
+    ``geom`` is a PropagationPath (the reference passes its PathGeometry,
+    which is derived from the same path); ``bvh`` supplies the device.
+    """
+    if bvh is None:
+        raise EmError("transfer needs the Bvh of the scene (bvh=...)")
+    T = _table_from_paths([geom], bvh, [geom.tx], [geom.rx])
+    a = _launch_transfer(bvh, T, _rows_tensor([ctx.rotation_rows(tx_dev)], bvh.device),
+                         _rows_tensor([ctx.rotation_rows(rx_dev)], bvh.device),
+                         pattern_id(tx_pattern), pattern_id(rx_pattern), [float(tx_slant)],
+                         [float(rx_slant)], ctx.eta_table(bvh), ctx.scene.wavelength,
+                         ctx.scene.frequency_hz)
+    v = a[0, 0, 0].cpu().numpy()
+    return complex(v[0], v[1])
+
+
+# -- channel gains for full arrays -----------------------------------------------------------
+
+@dataclass
+class PathGain:
+    tx: str
+    rx: str
+    kind: str
+    seq: tuple
+    delay: float
+    a: np.ndarray
+    delays: np.ndarray
+    k_dep: np.ndarray
+    k_arr: np.ndarray
+
+
+class ChannelGains:
+    """Columnar gains: a [P, rx_el, tx_el, T] complex128 on the device + path table."""
+
+    def __init__(self, scene, table: PathTable, a, sample_times):
+        self.scene = scene
+        self.table = table
+        self.a = a
+        self.sample_times = np.asarray(sample_times, dtype=np.float64)
+        self._entries = None
+
+    @property
+    def entries(self):
+        if self._entries is None:
+            T = self.table
+            if T is None or T.n == 0:
+                self._entries = []
+            else:
+                h = T.host()
+                a = self.a.cpu().numpy()
+                out = []
+                for i in range(T.n):
+                    k = int(h["order"][i])
+                    nr, nt = a.shape[1], a.shape[2]
+                    out.append(PathGain(
+                        tx=T.tx_names[int(h["tx"][i])], rx=T.rx_names[int(h["rx"][i])],
+                        kind="specular" if k else "los",
+                        seq=tuple(int(s) for s in h["seq"][i, :k]), delay=float(h["delay"][i]),
+                        a=a[i], delays=np.full((nr, nt), float(h["delay"][i])),
+                        k_dep=np.broadcast_to(h["kdep"][i], (nr, nt, 3)).copy(),
+                        k_arr=np.broadcast_to(h["karr"][i], (nr, nt, 3)).copy()))
+                self._entries = out
+        return self._entries
+
+
+def _fraunhofer_check(scene, tx_name, rx_name, off_tx_w, off_rx_w, length):
+    aperture = 0.0
+    for off in (off_tx_w, off_rx_w):
+        if len(off) > 1:
+            aperture = max(aperture, float(np.linalg.norm(off.max(axis=0) - off.min(axis=0))))
+    if aperture > 0.0:
+        fr = 2.0 * aperture * aperture / scene.wavelength
+        if length < fr:
+            warnings.warn(f"path {tx_name}->{rx_name} at {length:.1f} m is inside the Fraunhofer "
+                          f"distance {fr:.1f} m; the plane-wave synthetic-array assumption "
+                          "degrades here", stacklevel=3)
+
+
+def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=None) -> ChannelGains:
+    """Complex gains for every path and element pair (em.py:359-422)."""
+    if ctx is None:
+        ctx = EvalContext(scene)
+    if not scene.synthetic_array:
+        raise EmError("explicit (non-synthetic) arrays are not implemented on the B200 path yet")
+    T = pathset.table
+    if T is None:
+        txn = [d.name for d in scene.devices if d.kind == "tx"]
+        rxn = [d.name for d in scene.devices if d.kind == "rx"]
+        T = _table_from_paths(pathset.paths, bvh, txn, rxn) if pathset.paths else None
+    lam = scene.wavelength
+    tx_arr, rx_arr = scene.tx_array, scene.rx_array
+    off_tx, sl_tx = element_layout(tx_arr, lam)
+    off_rx, sl_rx = element_layout(rx_arr, lam)
+    n_tx_el, n_rx_el = len(off_tx), len(off_rx)
+    dev = bvh.device
+    if T is None or T.n == 0:
+        empty = torch.zeros((0, n_rx_el, n_tx_el, 1), dtype=torch.complex128, device=dev)
+        return ChannelGains(scene, T, empty, np.zeros(1))
+    devs = {d.name: d for d in scene.devices}
+    tx_rows_dev = [ctx.rotation_rows(devs[n]) for n in T.tx_names]
+    rx_rows_dev = [ctx.rotation_rows(devs[n]) for n in T.rx_names]
+    tx_idx = T.tx.long()
+    rx_idx = T.rx.long()
+    tx_rows = _rows_tensor(tx_rows_dev, dev)[tx_idx].contiguous()
+    rx_rows = _rows_tensor(rx_rows_dev, dev)[rx_idx].contiguous()
+    st = sorted(set(float(s) for s in sl_tx))
+    sr = sorted(set(float(s) for s in sl_rx))
+    if eta is None:
+        eta = ctx.eta_table(bvh)
+    base = path_coefficients(bvh, T, eta, tx_rows, rx_rows, tx_arr.pattern, rx_arr.pattern, st, sr,
+                             lam, scene.frequency_hz)                       # [P, S, R]
+    # world-frame element offsets per device (em.py:372-379)
+    Rt = torch.tensor(np.asarray(tx_rows_dev, dtype=np.float64), device=dev)   # [n_tx, 3, 3]
+    Rr = torch.tensor(np.asarray(rx_rows_dev, dtype=np.float64), device=dev)
+    offt = torch.tensor(off_tx, dtype=torch.float64, device=dev)
+    offr = torch.tensor(off_rx, dtype=torch.float64, device=dev)
+    off_tx_w = torch.einsum("ek,dmk->dem", offt, Rt)                           # [n_tx, E, 3]
+    off_rx_w = torch.einsum("ek,dmk->dem", offr, Rr)
+    if scene.synthetic_array:
+        h_len = T.length.cpu().numpy()
+        h_tx, h_rx = tx_idx.cpu().numpy(), rx_idx.cpu().numpy()
+        for ti, tn in enumerate(T.tx_names):
+            for ri, rn in enumerate(T.rx_names):
+                m = (h_tx == ti) & (h_rx == ri)
+                if m.any():
+                    _fraunhofer_check(scene, tn, rn, off_tx_w[ti].cpu().numpy(),
+                                      off_rx_w[ri].cpu().numpy(), float(h_len[m].min()))
+    ph_tx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", off_tx_w[tx_idx], T.kdep) / lam)
+    ph_rx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", off_rx_w[rx_idx], -T.karr) / lam)
+    s_index = torch.tensor([st.index(float(s)) for s in sl_tx], device=dev)
+    r_index = torch.tensor([sr.index(float(s)) for s in sl_rx], device=dev)
+    b = base[:, s_index][:, :, r_index].transpose(1, 2)                       # [P, rx_el, tx_el]
+    a = b * ph_rx[:, :, None] * ph_tx[:, None, :]
+    return ChannelGains(scene, T, a[..., None], np.zeros(1))
+
+
+def apply_doppler(gains: ChannelGains, sampling_frequency: float, num_time_steps: int,
+                  tx_velocities=None, rx_velocities=None) -> ChannelGains:
+    """a_i(t_n) = a_i e^{j 2 pi f_D t_n}, f_D = (f/c)(k_dep.v_tx - k_arr.v_rx) (em.py:462-494)."""
+    if num_time_steps < 1 or sampling_frequency <= 0:
+        raise EmError("need num_time_steps >= 1 and a positive sampling frequency")
+    if gains.a.shape[-1] != 1:
+        raise EmError("doppler already applied to these gains")
+    T = gains.table
+    t = np.arange(num_time_steps) / sampling_frequency
+    if T is None or T.n == 0:
+        return ChannelGains(gains.scene, T, gains.a[..., :1].repeat(1, 1, 1, num_time_steps), t)
+    dev = gains.a.device
+
+    def vel(side, names):
+        if side is None:
+            return torch.zeros((len(names), 3), dtype=torch.float64, device=dev)
+        if isinstance(side, dict):
+            return torch.tensor(np.array([np.asarray(side.get(n, np.zeros(3)), dtype=np.float64)
+                                          for n in names]), device=dev)
+        return torch.tensor(np.tile(np.asarray(side, dtype=np.float64), (len(names), 1)), device=dev)
+
+    vt = vel(tx_velocities, T.tx_names)[T.tx.long()]
+    vr = vel(rx_velocities, T.rx_names)[T.rx.long()]
+    f_over_c = gains.scene.frequency_hz / SPEED_OF_LIGHT
+    fd = f_over_c * ((T.kdep * vt).sum(-1) - (T.karr * vr).sum(-1))             # [P]
+    tt = torch.tensor(t, dtype=torch.float64, device=dev)
+    ph = torch.exp(1j * TWO_PI * fd[:, None] * tt[None, :])                    # [P, T]
+    a = gains.a[..., :1] * ph[:, None, None, :]
+    return ChannelGains(gains.scene, T, a, t)
+
+
+def slants_of(arr):
+    return POLARIZATION_SLANTS[arr.polarization]

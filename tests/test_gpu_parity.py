@@ -1,0 +1,184 @@
+"""CUDA path vs the reference's golden vectors (and the pinned CPU oracle).
+
+Every test calls libb200rt.so through the package API (ctypes C ABI).
+Tolerances (BASELINE.json north_star): interaction sequences identical;
+delays within 1e-6 relative (we check 1e-12); complex gains and coverage
+cells within 1e-4 relative (we check 1e-9 — everything is FP64);
+gradients within 1e-3 relative.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_scene
+
+pytestmark = pytest.mark.gpu
+
+PATH_CASES = ["box", "two_ray", "c1", "corner", "merge", "canyon"]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2303_11103_b200 as P
+    assert torch.cuda.is_available()
+    return P
+
+
+def _bvh(P, sc):
+    return P.build(sc)
+
+
+def test_scene_arrays_bitwise(P, golden):
+    g = golden("soup")
+    b = _bvh(P, golden_scene(g))
+    assert np.array_equal(b.normals, g["normals"])
+    assert np.array_equal(b.plane_offset, g["plane_offset"])
+
+
+def test_intersect_matches_reference_bitwise(P, golden):
+    g = golden("soup")
+    b = _bvh(P, golden_scene(g))
+    t, p = b.trace(g["o"], g["d"])
+    p = p.cpu().numpy()
+    t = t.cpu().numpy()
+    assert np.array_equal(p, g["prim"])
+    hit = g["prim"] >= 0
+    assert np.array_equal(t[hit], g["t"][hit])
+
+
+def test_occluded_matches_reference(P, golden):
+    g = golden("soup")
+    b = _bvh(P, golden_scene(g))
+    occ = b.occluded_batch(g["occ_p"], g["occ_q"]).cpu().numpy()
+    assert np.array_equal(occ == 1, g["occ"])
+    assert all(b.occluded(a, q) == w for a, q, w in zip(g["occ_p"][:50], g["occ_q"][:50], g["occ"][:50]))
+
+
+def test_intersect_brute_force_random_soups(P):
+    import oracle as O
+    from paper_2303_11103_b200 import scenes
+    for n, seed in [(200, 1), (10_000, 2), (50_000, 3)]:
+        sc = scenes.random_soup(n, seed=seed)
+        b = _bvh(P, sc)
+        ob = O.Bvh(O.SceneArrays(sc))
+        rng = np.random.RandomState(seed + 100)
+        o = rng.uniform(-60, 60, (20000, 3))
+        d = rng.randn(20000, 3)
+        d /= np.linalg.norm(d, axis=1)[:, None]
+        t, p = b.trace(o, d)
+        ot, op = ob.trace(o, d, 1e-4, np.inf)
+        assert np.array_equal(p.cpu().numpy(), op)
+        hit = op >= 0
+        assert np.array_equal(t.cpu().numpy()[hit], ot[hit])
+
+
+def test_empty_and_tiny_scenes(P):
+    from paper_2303_11103_b200 import scenes
+    from paper_2303_11103_b200.scene import Scene, AntennaArray, RadioDevice
+    sc = Scene(1e9, [], {}, AntennaArray(), AntennaArray(),
+               [RadioDevice("tx", "tx", np.zeros(3)), RadioDevice("rx", "rx", np.ones(3))])
+    b = _bvh(P, sc)
+    assert b.num_prims == 0 and b.intersect(np.zeros(3), np.array([1.0, 0, 0])) is None
+    assert P.launch_candidates(sc, b, [0, 0, 0], 2, 128) == set()
+    ps = P.compute_paths(sc, b, 2)
+    assert [p.kind for p in ps.paths] == ["los"]
+    # one triangle
+    s1 = scenes.random_soup(1, seed=4)
+    b1 = _bvh(P, s1)
+    tri_c = s1.objects[0].vertices.mean(axis=0)
+    h = b1.intersect(tri_c + np.array([0, 0, 5.0]), np.array([0, 0, -1.0]))
+    assert h is not None and h.prim == 0
+
+
+def _check_paths(got, g):
+    assert len(got) == len(g["p_kind"]), (len(got), len(g["p_kind"]))
+    for i, p in enumerate(got):
+        k = int(g["p_order"][i])
+        assert p.tx == g["p_tx"][i] and p.rx == g["p_rx"][i]
+        assert p.order == k and p.seq == tuple(int(x) for x in g["p_seq"][i, :k])
+        assert np.allclose(p.vertices, g["p_verts"][i, :k + 2], rtol=0, atol=1e-9)
+        assert abs(p.delay_s - g["p_delay"][i]) <= 1e-12 * g["p_delay"][i]
+        assert abs(p.length_m - g["p_length"][i]) <= 1e-12 * g["p_length"][i]
+        assert np.allclose(p.normals, g["p_normals"][i, :k], atol=1e-15)
+        assert np.allclose(p.cos_incidence, g["p_cos"][i, :k], rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("case", PATH_CASES)
+def test_paths_gains_cir(P, golden, case):
+    g = golden(case)
+    sc = golden_scene(g)
+    b = _bvh(P, sc)
+    ps = P.compute_paths(sc, b, int(g["max_depth"]), method=str(g["method"]),
+                         num_rays=int(g["num_rays"]))
+    _check_paths(ps.paths, g)
+    gains = P.compute_gains(sc, b, ps)
+    ga = np.stack([e.a for e in gains.entries]) if gains.entries else np.zeros((0, 1, 1, 1))
+    ref = g["gains_a"]
+    assert ga.shape == ref.shape
+    scale = np.abs(ref).max() if ref.size else 1.0
+    assert np.abs(ga - ref).max() <= 1e-9 * scale
+    cir = P.build_cir(gains)
+    assert cir.a.shape == g["cir_a"].shape
+    assert np.abs(cir.a - g["cir_a"]).max() <= 1e-9 * max(np.abs(g["cir_a"]).max(), 1e-300)
+    assert np.allclose(cir.tau, g["cir_tau"], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("case", ["box", "c1", "canyon"])
+def test_launch_candidates_equal_reference(P, golden, case):
+    g = golden(case)
+    sc = golden_scene(g)
+    b = _bvh(P, sc)
+    for k in [k for k in g if k.startswith("launch_")]:
+        _, txn, depth, n = k.split("_")
+        got = P.launch_candidates(sc, b, sc.device(txn).position, int(depth), int(n))
+        want = {tuple(int(x) for x in row if x >= 0) for row in g[k]}
+        assert got == want, (k, len(got), len(want), sorted(got ^ want)[:10])
+
+
+def test_launch_matches_oracle_larger(P):
+    """Canyon (~2k tris), 200k rays, depth 3: device launch == oracle launch."""
+    import oracle as O
+    from paper_2303_11103_b200 import scenes
+    sc = scenes.street_canyon(n_per_row=100, n_rx=(2, 1))
+    b = _bvh(P, sc)
+    ob = O.Bvh(O.SceneArrays(sc))
+    tx = sc.transmitters[0].position
+    got = P.launch_candidates(sc, b, tx, 3, 200_000)
+    want = O.launch_candidates(ob, tx, 3, 200_000)
+    assert got == want, (len(got), len(want), sorted(got ^ want)[:10])
+
+
+@pytest.mark.parametrize("case", ["box", "two_ray", "c1", "canyon"])
+def test_coverage_matches_reference(P, golden, case):
+    g = golden(case)
+    sc = golden_scene(g)
+    b = _bvh(P, sc)
+    i = 0
+    while f"cov{i}_gains" in g:
+        ox, oy, cs, nx, ny, h, depth, nr = g[f"cov{i}_spec"]
+        grid = P.GridSpec((ox, oy), cs, int(nx), int(ny), h)
+        cm = P.coverage_map(sc, b, grid, int(depth), method=str(g[f"cov{i}_method"]),
+                            num_rays=int(nr), tx_mode=str(g[f"cov{i}_mode"]))
+        want = g[f"cov{i}_gains"]
+        assert np.array_equal(cm.gains == 0.0, want == 0.0)
+        nz = want > 0
+        assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz])
+        i += 1
+    assert i > 0
+
+
+def test_material_gradient_matches_reference_tape(P, golden):
+    """Config 4: NMSE frequency-response loss, d/d(eps_r, sigma) of 4 materials
+    through the hand-written adjoint, vs the reference Tape (rel 1e-3)."""
+    from paper_2303_11103_b200 import optim
+    g = golden("calib")
+    init = golden_scene(g, "scene_init")
+    loss, grads = optim.material_loss_and_grad(init, g["positions"], g["h"], int(g["max_depth"]),
+                                               int(g["num_subcarriers"]), float(g["spacing"]))
+    assert abs(loss - float(g["loss"])) <= 1e-9 * abs(float(g["loss"]))
+    for name, ref in zip(g["grad_names"], g["grads"]):
+        got = grads[str(name)]
+        assert abs(got - ref) <= 1e-3 * abs(ref) + 1e-12, (name, got, ref)
