@@ -154,6 +154,20 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
                 int shard_index, int shard_count, double* gains_out, int64_t* stats_out,
                 void* stream);
 
+/* ---- measurement ----
+ * flags bit 0: record CUDA events around each stage on the caller's stream;
+ * bit 1: run the instrumented launch kernel (per-traversal node and
+ * triangle counters, for the roofline's algorithmic bytes).
+ * rt_get_profile (host out [16] each): ms per stage of the last call
+ * (-1 = not run): 0 launch kernel, 1 candidate sort+unique, 2 images +
+ * footprints + scan, 3 geometric solve, 4 occlusion+transfer, 5 record sort,
+ * 6 merge/accumulate, 7 LOS, 8 trie -> sequences; counters: 0 ray-bounces,
+ * 1 node visits, 2 triangle tests, 3 candidates, 4 work items, 5 geometric
+ * pairs, 6 valid paths, 15 kernel launches issued by the library
+ * (cumulative; a CUB device-wide primitive counts once). */
+int rt_set_profiling(rt_ctx* ctx, int flags);
+int rt_get_profile(rt_ctx* ctx, double* ms_out, int64_t* counters_out);
+
 #ifdef __cplusplus
 }
 #endif

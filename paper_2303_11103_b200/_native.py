@@ -26,6 +26,7 @@ EXPORTS = [
     "rt_num_prims", "rt_scene_arrays", "rt_trace", "rt_occluded", "rt_launch", "rt_enumerate",
     "rt_candidates_set", "rt_candidates_get", "rt_num_candidates", "rt_candidates_max_len",
     "rt_paths", "rt_paths_get", "rt_transfer", "rt_transfer_bwd", "rt_coverage",
+    "rt_set_profiling", "rt_get_profile",
 ]
 
 _lib = None
@@ -99,6 +100,8 @@ def lib():
                                       i32, P, i32, f64, f64, P, P, P]),
             "rt_coverage": (i32, [P, P, f64, f64, f64, i64, i64, f64, P, P, i32, P, P, i32, i32, P,
                                   i32, f64, f64, i32, i32, P, P, P]),
+            "rt_set_profiling": (i32, [P, i32]),
+            "rt_get_profile": (i32, [P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

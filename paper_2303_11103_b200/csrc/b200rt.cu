@@ -19,6 +19,11 @@
 
 using namespace rt;
 
+// profiling stages (rt_get_profile)
+enum { ST_LAUNCH = 0, ST_CAND_SORT, ST_FOOTPRINT, ST_SOLVE, ST_VALIDATE, ST_REC_SORT, ST_MERGE,
+       ST_LOS, ST_TRIE_SEQ, RT_NSTAGE_USED };
+#define RT_NSTAGE 16
+
 namespace {
 
 struct DevBuf {
@@ -76,6 +81,11 @@ struct rt_ctx {
     // error flags + pinned host staging
     DevBuf dflag;
     long long* hpin = nullptr;
+    // profiling: per-stage CUDA events on the caller's stream + counters
+    int prof = 0;
+    cudaEvent_t ev[RT_NSTAGE][2] = {};
+    bool ev_used[RT_NSTAGE] = {};
+    long long counters[RT_NSTAGE] = {};
 };
 
 namespace {
@@ -94,7 +104,11 @@ int fail(rt_ctx* c, int code, const std::string& msg) {
             return fail(ctx, _e == cudaErrorMemoryAllocation ? RT_ENOMEM : RT_ECUDA,       \
                         std::string(#expr) + ": " + cudaGetErrorString(_e));              \
     } while (0)
-#define CKL() CK(cudaGetLastError())
+#define CKL()                  \
+    do {                       \
+        ++ctx->counters[15];   \
+        CK(cudaGetLastError()); \
+    } while (0)
 #define RC(expr)                  \
     do {                          \
         int _r = (expr);          \
@@ -154,6 +168,15 @@ int check_flags(rt_ctx* ctx, cudaStream_t st) {
     return RT_OK;
 }
 
+void prof_mark(rt_ctx* ctx, int stage, int end, cudaStream_t st) {
+    if (!(ctx->prof & 1)) return;
+    if (!ctx->ev[stage][end]) cudaEventCreate(&ctx->ev[stage][end]);
+    cudaEventRecord(ctx->ev[stage][end], st);
+    if (end) ctx->ev_used[stage] = true;
+}
+#define PROF_BEGIN(i) prof_mark(ctx, (i), 0, st)
+#define PROF_END(i) prof_mark(ctx, (i), 1, st)
+
 int bits_for(long long v) {
     int b = 1;
     while (b < 32 && (1LL << b) <= v) ++b;
@@ -167,6 +190,7 @@ int cub_call(rt_ctx* ctx, F&& f) {
     CK(ctx->cub_tmp.reserve(need));
     size_t have = ctx->cub_tmp.bytes;
     CK(f(ctx->cub_tmp.p, have));
+    ++ctx->counters[15];   // one device-wide CUB primitive
     return RT_OK;
 }
 
@@ -489,11 +513,19 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         P.bounces = reinterpret_cast<unsigned long long*>(ctr + 2);
         P.error = reinterpret_cast<int*>(ctx->dflag.get<long long>());
         long long blocks = std::min<long long>((span + 255) / 256, (long long)ctx->n_sm * 16);
+        P.node_visits = reinterpret_cast<unsigned long long*>(ctr + 3);
+        P.tri_tests = reinterpret_cast<unsigned long long*>(ctr + 4);
+        PROF_BEGIN(ST_LAUNCH);
         if (span > 0) {
-            k_launch<<<(unsigned)std::max<long long>(blocks, 1), 256, 0, st>>>(bvh_dev(ctx), P, T);
+            unsigned g = (unsigned)std::max<long long>(blocks, 1);
+            if (ctx->prof & 2) k_launch<true><<<g, 256, 0, st>>>(bvh_dev(ctx), P, T);
+            else k_launch<false><<<g, 256, 0, st>>>(bvh_dev(ctx), P, T);
             CKL();
         }
-        RC(fetch(ctx, ctr, 3, st));
+        PROF_END(ST_LAUNCH);
+        RC(fetch(ctx, ctr, 5, st));
+        ctx->counters[1] = ctx->hpin[3];
+        ctx->counters[2] = ctx->hpin[4];
         long long nodes = (long long)(int)(ctx->hpin[0] & 0xffffffff);
         bool overflow = (int)(ctx->hpin[1] & 0xffffffff) != 0;
         long long bounces = ctx->hpin[2];
@@ -503,9 +535,11 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
             continue;
         }
         if (n_bounces_out) *n_bounces_out = bounces;
+        ctx->counters[0] = bounces;
         // materialize sequences and sort them
         CK(ctx->s_seq.reserve(4ULL * std::max<long long>(nodes, 1) * max_depth));
         CK(ctx->s_len.reserve((size_t)std::max<long long>(nodes, 1)));
+        PROF_BEGIN(ST_TRIE_SEQ);
         if (nodes > 0) {
             k_trie_sequences<<<nblk(nodes, 256), 256, 0, st>>>((int)nodes, T.node_parent, T.node_prim,
                                                                T.node_depth, max_depth,
@@ -513,7 +547,11 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
                                                                ctx->s_len.get<signed char>());
             CKL();
         }
+        PROF_END(ST_TRIE_SEQ);
+        PROF_BEGIN(ST_CAND_SORT);
         RC(sort_unique_candidates(ctx, nodes, max_depth, st));
+        PROF_END(ST_CAND_SORT);
+        ctx->counters[3] = ctx->n_cand;
         if (n_cand_out) *n_cand_out = ctx->n_cand;
         return RT_OK;
     }
@@ -604,6 +642,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     long long nC = C.n;
     *n_rec_out = 0;
     if (nC == 0 || R.n == 0) return RT_OK;
+    PROF_BEGIN(ST_FOOTPRINT);
     CK(ctx->images.reserve(24ULL * nC * C.max_len));
     k_images<<<nblk(nC, 256), 256, 0, st>>>(C, SD, tx, ctx->images.get<double>());
     CKL();
@@ -626,6 +665,8 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     } else {
         W = nC * R.n;
     }
+    PROF_END(ST_FOOTPRINT);
+    ctx->counters[4] = W;
     if (stats) stats[0] = W;
     if (W == 0) return RT_OK;
     // geometric solve with compaction; grow and retry when the buffer is short
@@ -636,6 +677,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
         unsigned long long* np = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>());
         long long blocks = std::min<long long>((W + 255) / 256, (long long)ctx->n_sm * 32);
+        PROF_BEGIN(ST_SOLVE);
         if (grid)
             k_solve<true><<<(unsigned)blocks, 256, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, W,
                                                             ctx->scan.get<long long>(), ctx->fp.get<Footprint>(),
@@ -646,18 +688,21 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
                                                              nullptr, nullptr, 1, ctx->pending.get<Pending>(),
                                                              np, ctx->pending_cap);
         CKL();
+        PROF_END(ST_SOLVE);
         RC(fetch(ctx, np, 1, st));
         n_pend = ctx->hpin[0];
         if ((unsigned long long)n_pend <= ctx->pending_cap) break;
         while (ctx->pending_cap < (unsigned long long)n_pend) ctx->pending_cap *= 2;
     }
     if (stats) stats[1] = n_pend;
+    ctx->counters[5] = n_pend;
     if (n_pend == 0) return RT_OK;
     CK(ctx->recs.reserve(sizeof(Rec) * n_pend));
     CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
     unsigned long long* nr = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>()) + 1;
     RC(clear_flags(ctx, st));
     long long vblocks = std::min<long long>((n_pend + 127) / 128, (long long)ctx->n_sm * 32);
+    PROF_BEGIN(ST_VALIDATE);
     if (power)
         k_validate<true><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
                                                             bvh_dev(ctx), ctx->pending.get<Pending>(),
@@ -667,11 +712,14 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
                                                              bvh_dev(ctx), ctx->pending.get<Pending>(),
                                                              n_pend, E, ctx->recs.get<Rec>(), nr);
     CKL();
+    PROF_END(ST_VALIDATE);
     RC(fetch(ctx, nr, 1, st));
     long long n_rec = ctx->hpin[0];
+    ctx->counters[6] = n_rec;
     RC(check_flags(ctx, st));
     if (stats) stats[2] = n_rec;
     if (n_rec == 0) return RT_OK;
+    PROF_BEGIN(ST_REC_SORT);
     CK(ctx->rkeys.reserve(8 * n_rec));
     CK(ctx->rkeys_alt.reserve(8 * n_rec));
     CK(ctx->ridx.reserve(4 * n_rec));
@@ -688,6 +736,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n_rec, 0,
                                                std::min(end_bit, 64), st);
     }));
+    PROF_END(ST_REC_SORT);
     *n_rec_out = n_rec;
     return RT_OK;
 }
@@ -921,22 +970,50 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
     E.wavelength = wavelength;
     E.frequency = frequency_hz;
     RC(clear_flags(ctx, st));
+    PROF_BEGIN(ST_LOS);
     k_los<true><<<nblk(R.n, 128), 128, 0, st>>>(R, T, bvh_dev(ctx), scene_dev(ctx), E, shard_index,
                                                 shard_count, nullptr, gains_out,
                                                 reinterpret_cast<int*>(ctx->dflag.get<long long>()));
     CKL();
+    PROF_END(ST_LOS);
     RC(check_flags(ctx, st));
     long long n_rec = 0;
     RC(solve_records(ctx, T, R, true, true, E, shard_index, shard_count, &n_rec, stats, st));
     if (n_rec > 0) {
         CK(ctx->keep.reserve((size_t)n_rec));
+        PROF_BEGIN(ST_MERGE);
         k_merge<true><<<nblk(n_rec, 128), 128, 0, st>>>(cands_dev(ctx), scene_dev(ctx), ctx->images.get<double>(),
                                                        R, T, ctx->recs.get<Rec>(), ctx->ridx.get<int>(),
                                                        ctx->rkeys.get<unsigned long long>(), n_rec,
                                                        ctx->keep.get<unsigned char>(), gains_out);
         CKL();
+        PROF_END(ST_MERGE);
     }
     if (stats_out) memcpy(stats_out, stats, sizeof stats);
+    return RT_OK;
+}
+
+int rt_set_profiling(rt_ctx* ctx, int flags) {
+    if (!ctx) return RT_EINVAL;
+    ctx->prof = flags;
+    for (int i = 0; i < RT_NSTAGE; ++i) ctx->ev_used[i] = false;
+    return RT_OK;
+}
+
+int rt_get_profile(rt_ctx* ctx, double* ms_out, int64_t* counters_out) {
+    if (!ctx) return RT_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    for (int i = 0; i < RT_NSTAGE; ++i) {
+        double v = -1.0;
+        if (ctx->ev_used[i] && ctx->ev[i][0] && ctx->ev[i][1]) {
+            float ms = 0.f;
+            CK(cudaEventSynchronize(ctx->ev[i][1]));
+            CK(cudaEventElapsedTime(&ms, ctx->ev[i][0], ctx->ev[i][1]));
+            v = ms;
+        }
+        if (ms_out) ms_out[i] = v;
+        if (counters_out) counters_out[i] = ctx->counters[i];
+    }
     return RT_OK;
 }
 

@@ -86,6 +86,8 @@ struct LaunchParams {
     const double* dirs;       // optional [n_rays*3]
     const double* normals;    // [n_prims*3] global order
     unsigned long long* bounces;
+    unsigned long long* node_visits;   // COUNT builds only
+    unsigned long long* tri_tests;
     int* error;
 };
 
@@ -101,10 +103,11 @@ __device__ inline d3 fib_dir(long long i, long long n) {
     return d3{r * c, r * s, z};
 }
 
+template <bool COUNT>
 __global__ void __launch_bounds__(256) k_launch(Bvh bvh, LaunchParams P, Trie T) {
     const unsigned FULL = 0xffffffffu;
     int lane = threadIdx.x & 31;
-    unsigned long long my_bounces = 0;
+    unsigned long long my_bounces = 0, my_nodes = 0, my_tris = 0;
     long long stride = (long long)gridDim.x * blockDim.x;
     long long span = P.slot_end - P.slot_begin;
     long long iters = (span + stride - 1) / stride;
@@ -126,7 +129,15 @@ __global__ void __launch_bounds__(256) k_launch(Bvh bvh, LaunchParams P, Trie T)
             double t = 0.0;
             if (active) {
                 Ray r = make_ray(o, d);
-                prim = trace<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t);
+                if (COUNT) {
+                    int nv = 0, nt = 0;
+                    prim = trace<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t,
+                                        &nv, &nt);
+                    my_nodes += nv;
+                    my_tris += nt;
+                } else {
+                    prim = trace<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t);
+                }
                 ++my_bounces;
                 if (prim == -2) { atomicOr(P.error, 1); prim = -1; }
                 if (prim < 0) active = false;
@@ -156,6 +167,16 @@ __global__ void __launch_bounds__(256) k_launch(Bvh bvh, LaunchParams P, Trie T)
     // warp-reduce the bounce count
     for (int s = 16; s; s >>= 1) my_bounces += __shfl_xor_sync(FULL, my_bounces, s);
     if (lane == 0 && my_bounces) atomicAdd(P.bounces, my_bounces);
+    if (COUNT) {
+        for (int s = 16; s; s >>= 1) {
+            my_nodes += __shfl_xor_sync(FULL, my_nodes, s);
+            my_tris += __shfl_xor_sync(FULL, my_tris, s);
+        }
+        if (lane == 0) {
+            atomicAdd(P.node_visits, my_nodes);
+            atomicAdd(P.tri_tests, my_tris);
+        }
+    }
 }
 
 // ---- candidate materialization ----------------------------------------------------------

@@ -75,7 +75,7 @@ struct Bvh {
 // Returns the global prim id or -1; *t_out the hit distance.
 template <bool ANY>
 __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, double* t_out,
-                     int* visits = nullptr) {
+                     int* visits = nullptr, int* tests = nullptr) {
     if (bvh.n_prims == 0) return -1;
     int stack[STACK_SIZE];
     double stack_t[STACK_SIZE];
@@ -83,7 +83,7 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
     double best_t = tmax;
     int best_prim = -1;
     int cur = 0;   // root is internal node 0 (a 1..4 prim scene gets a root with one leaf)
-    int nv = 0;
+    int nv = 0, nt = 0;
     while (true) {
         if (!ref_is_leaf(cur)) {
             const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
@@ -110,6 +110,7 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
             }
         } else {
             int first = leaf_first(cur), cnt = leaf_count(cur);
+            nt += cnt;
             for (int k = 0; k < cnt; ++k) {
                 const TriRec* tp = bvh.tris + first + k;
                 double t;
@@ -118,7 +119,12 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
                     if (tmin < t && (t < best_t || (t == best_t && best_prim >= 0 && prim < best_prim))) {
                         best_t = t;
                         best_prim = prim;
-                        if (ANY) { *t_out = t; if (visits) *visits = nv; return prim; }
+                        if (ANY) {
+                            *t_out = t;
+                            if (visits) *visits = nv;
+                            if (tests) *tests = nt;
+                            return prim;
+                        }
                     }
                 }
             }
@@ -133,6 +139,7 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
     }
     *t_out = best_t;
     if (visits) *visits = nv;
+    if (tests) *tests = nt;
     return best_prim;
 }
 
