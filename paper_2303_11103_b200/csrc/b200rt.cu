@@ -71,6 +71,7 @@ struct rt_ctx {
     DevBuf s_seq, s_len, s_perm, s_perm_alt, s_keys, s_keys_alt, s_flag, s_pos;
     DevBuf cub_tmp;
     // solve scratch
+    DevBuf hps, nhp, row0, seg_cand, seg_iy, seg_ix0, seg_cnt, item_off;
     DevBuf images, fp, counts, scan, pending, recs, rkeys, rkeys_alt, ridx, ridx_alt, keep,
         losbuf, heads, pcounts, poffs, em_small, ctrs;
     uint64_t pending_cap = 0;
@@ -647,21 +648,44 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     k_images<<<nblk(nC, 256), 256, 0, st>>>(C, SD, tx, ctx->images.get<double>());
     CKL();
     long long W = 0;
+    Segs G{nullptr, nullptr, nullptr, nullptr, 0};
     if (grid) {
-        CK(ctx->fp.reserve(sizeof(Footprint) * nC));
+        CK(ctx->hps.reserve(sizeof(double) * 3 * HP_MAX * nC));
+        CK(ctx->nhp.reserve(4ULL * nC));
+        CK(ctx->row0.reserve(4ULL * nC));
         CK(ctx->counts.reserve(8ULL * (nC + 1)));
         CK(ctx->scan.reserve(8ULL * (nC + 1)));
-        k_footprint<<<nblk(nC + 1, 256), 256, 0, st>>>(C, SD, ctx->images.get<double>(), R, shard_index,
-                                                       shard_count, ctx->fp.get<Footprint>(),
-                                                       ctx->counts.get<long long>());
+        k_halfplanes<<<nblk(nC + 1, 128), 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, shard_index,
+                                                        shard_count, ctx->hps.get<double>(), ctx->nhp.get<int>(),
+                                                        ctx->row0.get<int>(), ctx->counts.get<long long>());
         CKL();
         long long* cnt = ctx->counts.get<long long>();
-        long long* scan = ctx->scan.get<long long>();
+        long long* seg_off = ctx->scan.get<long long>();
         RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
-            return cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, scan, (int)(nC + 1), st);
+            return cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, seg_off, (int)(nC + 1), st);
         }));
-        RC(fetch(ctx, scan + nC, 1, st));
+        RC(fetch(ctx, seg_off + nC, 1, st));
+        long long nS = ctx->hpin[0];
+        CK(ctx->seg_cand.reserve(4ULL * std::max<long long>(nS, 1)));
+        CK(ctx->seg_iy.reserve(4ULL * std::max<long long>(nS, 1)));
+        CK(ctx->seg_ix0.reserve(4ULL * std::max<long long>(nS, 1)));
+        CK(ctx->seg_cnt.reserve(8ULL * (nS + 1)));
+        CK(ctx->item_off.reserve(8ULL * (nS + 1)));
+        CK(cudaMemsetAsync(ctx->seg_cnt.get<long long>() + nS, 0, 8, st));
+        k_segments<<<nblk(nC, 128), 128, 0, st>>>(nC, ctx->hps.get<double>(), ctx->nhp.get<int>(),
+                                                  ctx->row0.get<int>(), seg_off, R, shard_count,
+                                                  ctx->seg_cand.get<int>(), ctx->seg_iy.get<int>(),
+                                                  ctx->seg_ix0.get<int>(), ctx->seg_cnt.get<long long>());
+        CKL();
+        long long* sc = ctx->seg_cnt.get<long long>();
+        long long* io = ctx->item_off.get<long long>();
+        RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+            return cub::DeviceScan::ExclusiveSum(tmp, bytes, sc, io, (int)(nS + 1), st);
+        }));
+        RC(fetch(ctx, io + nS, 1, st));
         W = ctx->hpin[0];
+        G = Segs{io, ctx->seg_cand.get<int>(), ctx->seg_iy.get<int>(), ctx->seg_ix0.get<int>(), nS};
+        ctx->counters[7] = nS;
     } else {
         W = nC * R.n;
     }
@@ -679,14 +703,11 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         long long blocks = std::min<long long>((W + 255) / 256, (long long)ctx->n_sm * 32);
         PROF_BEGIN(ST_SOLVE);
         if (grid)
-            k_solve<true><<<(unsigned)blocks, 256, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, W,
-                                                            ctx->scan.get<long long>(), ctx->fp.get<Footprint>(),
-                                                            shard_count, ctx->pending.get<Pending>(), np,
-                                                            ctx->pending_cap);
+            k_solve<true><<<(unsigned)blocks, 256, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, W, G,
+                                                            ctx->pending.get<Pending>(), np, ctx->pending_cap);
         else
-            k_solve<false><<<(unsigned)blocks, 256, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, W,
-                                                             nullptr, nullptr, 1, ctx->pending.get<Pending>(),
-                                                             np, ctx->pending_cap);
+            k_solve<false><<<(unsigned)blocks, 256, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, W, G,
+                                                             ctx->pending.get<Pending>(), np, ctx->pending_cap);
         CKL();
         PROF_END(ST_SOLVE);
         RC(fetch(ctx, np, 1, st));

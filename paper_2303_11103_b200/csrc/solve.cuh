@@ -66,7 +66,6 @@ __device__ inline bool solve_geometric(const Cands& C, const SceneDev& S, const 
     int K = C.len[c];
     const int* seq = C.seq + c * C.max_len;
     d3 cur = rx;
-    double params[MAX_DEPTH];
     for (int j = K - 1; j >= 0; --j) {
         int prim = seq[j];
         d3 n = ld3(S.nrm + 3 * (long long)prim);
@@ -77,24 +76,22 @@ __device__ inline bool solve_geometric(const Cands& C, const SceneDev& S, const 
         if (fabs(denom) < 1e-15) return false;
         double s = (cc - tdot(cur, n)) / denom;
         d3 p = d3{cur.x + seg.x * s, cur.y + seg.y * s, cur.z + seg.z * s};
-        // early out: the same test image_solve applies after the loop
+        // early outs: image_solve applies the same tests after the loop
+        // (tracer.py:164-169); the conjunction does not depend on the order
         if (!(1e-12 < s && s < 1.0 - 1e-12)) return false;
-        params[j] = s;
+        {   // _inside_triangle (tracer.py:136-147)
+            d3 v0 = ld3(S.v0 + 3 * (long long)prim), e1 = ld3(S.e1 + 3 * (long long)prim),
+               e2 = ld3(S.e2 + 3 * (long long)prim);
+            d3 w = sub(p, v0);
+            double d11 = dot_blas(e1, e1), d12 = dot_blas(e1, e2), d22 = dot_blas(e2, e2);
+            double w1 = dot_blas(w, e1), w2 = dot_blas(w, e2);
+            double den = d11 * d22 - d12 * d12;
+            double u = (d22 * w1 - d12 * w2) / den;
+            double v = (d11 * w2 - d12 * w1) / den;
+            if (!(u >= -INSIDE_TOL && v >= -INSIDE_TOL && u + v <= 1.0 + INSIDE_TOL)) return false;
+        }
         pts[j] = p;
         cur = p;
-    }
-    (void)params;
-    for (int j = 0; j < K; ++j) {   // _inside_triangle (tracer.py:136-147)
-        int prim = seq[j];
-        d3 v0 = ld3(S.v0 + 3 * (long long)prim), e1 = ld3(S.e1 + 3 * (long long)prim),
-           e2 = ld3(S.e2 + 3 * (long long)prim);
-        d3 w = sub(pts[j], v0);
-        double d11 = dot_blas(e1, e1), d12 = dot_blas(e1, e2), d22 = dot_blas(e2, e2);
-        double w1 = dot_blas(w, e1), w2 = dot_blas(w, e2);
-        double den = d11 * d22 - d12 * d12;
-        double u = (d22 * w1 - d12 * w2) / den;
-        double v = (d11 * w2 - d12 * w1) / den;
-        if (!(u >= -INSIDE_TOL && v >= -INSIDE_TOL && u + v <= 1.0 + INSIDE_TOL)) return false;
     }
     for (int j = 0; j < K; ++j) {   // same-side reflection (tracer.py:170-176)
         int prim = seq[j];
@@ -115,13 +112,13 @@ __device__ inline bool solve_geometric(const Cands& C, const SceneDev& S, const 
     return true;
 }
 
-// occlusion of every segment (tracer.py:181-182)
+// occlusion of every segment (tracer.py:181-182); the conjunction is order-free,
+// so the receiver-side segment (most often blocked near the ground) goes first
 __device__ inline bool segments_clear(const Bvh& bvh, d3 tx, const d3* pts, int K, d3 rx) {
-    d3 a = tx;
-    for (int j = 0; j <= K; ++j) {
-        d3 b = j < K ? pts[j] : rx;
+    for (int j = K; j >= 0; --j) {
+        d3 a = j == 0 ? tx : pts[j - 1];
+        d3 b = j == K ? rx : pts[j];
         if (occluded(bvh, a, b) != 0) return false;
-        a = b;
     }
     return true;
 }
@@ -142,92 +139,154 @@ __device__ inline d3 receiver_pos(const Receivers& R, long long r) {
     return d3{R.ox + ((double)ix + 0.5) * R.cell, R.oy + ((double)iy + 0.5) * R.cell, R.height};
 }
 
-// ---- footprints -------------------------------------------------------------------------
+// ---- footprints ---------------------------------------------------------------------------
+//
+// A receiver R is reachable by candidate (t_0..t_{K-1}) only if R lies in every
+// cone {A + mu (x - A) : x in T'_j, mu > 0} with apex A = I_K (the last
+// image) through the forward-mirrored interaction triangles T'_j =
+// M_{K-1}...M_{j+1}(T_j), and beyond each T'_j's plane (segment fractions in
+// (0,1), tracer.py:164-166).  Each cone is 3 half-spaces, each "beyond" one
+// more; on the grid plane z = height they are half-planes.  Triangles are
+// inflated by 1e-6 about their centroid first (the reference accepts
+// barycentric -1e-9), so the half-planes are conservative.  Cells are then
+// enumerated row by row inside the clipped polygon, padded by one cell.
 
-struct Footprint {
-    int ix0, iy0, w, h;   // cell box; w*h (or rows in shard) work items
-};
+constexpr int HP_PER_TRI = 4;
+constexpr int HP_MAX = HP_PER_TRI * MAX_DEPTH;
+constexpr int POLY_MAX = 4 + HP_MAX;
 
-__global__ void k_footprint(Cands C, SceneDev S, const double* images, Receivers R,
-                            int shard_index, int shard_count, Footprint* fp,
-                            long long* counts /*[n+1]*/) {
+__device__ inline void add_hp(double* hp, int& m, double a, double b, double c) {
+    hp[3 * m] = a;
+    hp[3 * m + 1] = b;
+    hp[3 * m + 2] = c + 1e-9 * (fabs(a) + fabs(b) + fabs(c));   // rounding margin
+    ++m;
+}
+
+// clip a convex polygon by a x + b y + c >= 0 (Sutherland-Hodgman)
+__device__ inline int clip_poly(const double* px, const double* py, int n, double a, double b,
+                                double c, double* qx, double* qy) {
+    int m = 0;
+    for (int i = 0; i < n; ++i) {
+        int j = (i + 1) % n;
+        double fi = a * px[i] + b * py[i] + c, fj = a * px[j] + b * py[j] + c;
+        if (fi >= 0.0) { qx[m] = px[i]; qy[m] = py[i]; ++m; }
+        if ((fi >= 0.0) != (fj >= 0.0)) {
+            double t = fi / (fi - fj);
+            qx[m] = px[i] + t * (px[j] - px[i]);
+            qy[m] = py[i] + t * (py[j] - py[i]);
+            ++m;
+        }
+    }
+    return m;
+}
+
+__global__ void k_halfplanes(Cands C, SceneDev S, const double* images, Receivers R,
+                             int shard_index, int shard_count, double* hps /*[n*HP_MAX*3]*/,
+                             int* nhp, int* row0, long long* seg_counts /*[n+1]*/) {
     long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (c >= C.n) {
-        if (c == C.n) counts[c] = 0;
+        if (c == C.n) seg_counts[c] = 0;
         return;
     }
     int K = C.len[c];
     const int* seq = C.seq + c * C.max_len;
     d3 A = ld3(images + (c * C.max_len + K - 1) * 3);
     double hA = R.height - A.z;
-    double bx0 = -INFINITY, bx1 = INFINITY, by0 = -INFINITY, by1 = INFINITY;
-    bool empty = false;
-    if (hA != 0.0) {
-        for (int j = K - 1; j >= 0 && !empty; --j) {
-            int prim = seq[j];
-            d3 v0 = ld3(S.v0 + 3 * (long long)prim), e1 = ld3(S.e1 + 3 * (long long)prim),
-               e2 = ld3(S.e2 + 3 * (long long)prim);
-            d3 x[3] = {v0, add(v0, e1), add(v0, e2)};
-            // inflate about the centroid (covers the 1e-9 barycentric tolerance)
-            d3 ctr = d3{(x[0].x + x[1].x + x[2].x) / 3.0, (x[0].y + x[1].y + x[2].y) / 3.0,
-                        (x[0].z + x[1].z + x[2].z) / 3.0};
-            for (int m = 0; m < 3; ++m) x[m] = add(ctr, scale(sub(x[m], ctr), 1.0 + 1e-6));
-            // forward-mirror through planes j+1..K-1
-            for (int q = j + 1; q < K; ++q) {
-                int pq = seq[q];
-                d3 n = ld3(S.nrm + 3 * (long long)pq);
-                double cc = S.poff[pq];
-                for (int m = 0; m < 3; ++m) x[m] = mirror(x[m], n, cc);
-            }
-            int same = 0, opp = 0;
-            double px[3], py[3];
-            for (int m = 0; m < 3; ++m) {
-                double s = x[m].z - A.z;
-                if ((s > 0.0 && hA > 0.0) || (s < 0.0 && hA < 0.0)) {
-                    double lam = hA / s;
-                    px[m] = A.x + lam * (x[m].x - A.x);
-                    py[m] = A.y + lam * (x[m].y - A.y);
-                    ++same;
-                } else if ((s < 0.0 && hA > 0.0) || (s > 0.0 && hA < 0.0)) {
-                    ++opp;
-                }
-            }
-            if (opp == 3) { empty = true; break; }
-            if (same == 3) {
-                double lx = fmin(fmin(px[0], px[1]), px[2]), hx = fmax(fmax(px[0], px[1]), px[2]);
-                double ly = fmin(fmin(py[0], py[1]), py[2]), hy = fmax(fmax(py[0], py[1]), py[2]);
-                double mx = 1e-6 * (1.0 + fabs(lx) + fabs(hx)), my = 1e-6 * (1.0 + fabs(ly) + fabs(hy));
-                bx0 = fmax(bx0, lx - mx); bx1 = fmin(bx1, hx + mx);
-                by0 = fmax(by0, ly - my); by1 = fmin(by1, hy + my);
-                if (bx0 > bx1 || by0 > by1) { empty = true; break; }
-            }
+    double* hp = hps + c * HP_MAX * 3;
+    int m = 0;
+    for (int j = 0; j < K; ++j) {
+        int prim = seq[j];
+        d3 v0 = ld3(S.v0 + 3 * (long long)prim), e1 = ld3(S.e1 + 3 * (long long)prim),
+           e2 = ld3(S.e2 + 3 * (long long)prim);
+        d3 x[3] = {v0, add(v0, e1), add(v0, e2)};
+        d3 ctr = d3{(x[0].x + x[1].x + x[2].x) / 3.0, (x[0].y + x[1].y + x[2].y) / 3.0,
+                    (x[0].z + x[1].z + x[2].z) / 3.0};
+        for (int q = 0; q < 3; ++q) x[q] = add(ctr, scale(sub(x[q], ctr), 1.0 + 1e-6));
+        for (int q = j + 1; q < K; ++q) {
+            int pq = seq[q];
+            d3 n = ld3(S.nrm + 3 * (long long)pq);
+            double cc = S.poff[pq];
+            for (int u = 0; u < 3; ++u) x[u] = mirror(x[u], n, cc);
+        }
+        // three side half-spaces of the cone through A
+        for (int e = 0; e < 3; ++e) {
+            d3 va = sub(x[e], A), vb = sub(x[(e + 1) % 3], A), vc = sub(x[(e + 2) % 3], A);
+            d3 n = cross(va, vb);
+            double sgn = tdot(n, vc);
+            if (sgn == 0.0) continue;   // degenerate cone: no constraint
+            if (sgn < 0.0) n = d3{-n.x, -n.y, -n.z};
+            add_hp(hp, m, n.x, n.y, n.z * hA - n.x * A.x - n.y * A.y);
+        }
+        // beyond the (mirrored) triangle's plane, on the side away from A
+        d3 nt = cross(sub(x[1], x[0]), sub(x[2], x[0]));
+        double sA = tdot(nt, sub(A, x[0]));
+        if (sA != 0.0) {
+            double s = sA > 0.0 ? -1.0 : 1.0;
+            add_hp(hp, m, s * nt.x, s * nt.y, s * (nt.z * R.height - tdot(nt, x[0])));
         }
     }
-    Footprint f = {0, 0, 0, 0};
-    long long cnt = 0;
-    if (!empty) {
-        // cells whose centers can fall in [b0, b1], padded by one cell each side
-        double fx0 = isinf(bx0) ? -1e30 : (bx0 - R.ox) / R.cell - 0.5;
-        double fx1 = isinf(bx1) ? 1e30 : (bx1 - R.ox) / R.cell - 0.5;
-        double fy0 = isinf(by0) ? -1e30 : (by0 - R.oy) / R.cell - 0.5;
-        double fy1 = isinf(by1) ? 1e30 : (by1 - R.oy) / R.cell - 0.5;
-        long long ix0 = (long long)fmax(floor(fx0) - 1.0, 0.0);
-        long long ix1 = (long long)fmin(ceil(fx1) + 1.0, (double)(R.nx - 1));
-        long long iy0 = (long long)fmax(floor(fy0) - 1.0, 0.0);
-        long long iy1 = (long long)fmin(ceil(fy1) + 1.0, (double)(R.ny - 1));
-        if (ix0 <= ix1 && iy0 <= iy1 && fx0 < 1e29 && fy0 < 1e29 && fx1 > -1e29 && fy1 > -1e29) {
-            // rows of this shard: iy = first + k * shard_count
-            long long first = iy0 + ((shard_index - iy0 % shard_count) + shard_count) % shard_count;
-            long long rows = first <= iy1 ? (iy1 - first) / shard_count + 1 : 0;
-            f.ix0 = (int)ix0;
-            f.iy0 = (int)first;
-            f.w = (int)(ix1 - ix0 + 1);
-            f.h = (int)rows;
-            cnt = (long long)f.w * rows;
+    nhp[c] = m;
+    // clip the (padded) grid rectangle
+    double px[POLY_MAX], py[POLY_MAX], qx[POLY_MAX], qy[POLY_MAX];
+    double x0 = R.ox - R.cell, x1 = R.ox + (R.nx + 1) * R.cell;
+    double y0 = R.oy - R.cell, y1 = R.oy + (R.ny + 1) * R.cell;
+    px[0] = x0; py[0] = y0; px[1] = x1; py[1] = y0; px[2] = x1; py[2] = y1; px[3] = x0; py[3] = y1;
+    int n = 4;
+    for (int i = 0; i < m && n > 0; ++i) {
+        n = clip_poly(px, py, n, hp[3 * i], hp[3 * i + 1], hp[3 * i + 2], qx, qy);
+        for (int k = 0; k < n; ++k) { px[k] = qx[k]; py[k] = qy[k]; }
+    }
+    long long rows = 0, first = 0;
+    if (n > 0) {
+        double ylo = py[0], yhi = py[0];
+        for (int k = 1; k < n; ++k) { ylo = fmin(ylo, py[k]); yhi = fmax(yhi, py[k]); }
+        long long iy0 = (long long)fmax(floor((ylo - R.oy) / R.cell - 0.5) - 1.0, 0.0);
+        long long iy1 = (long long)fmin(ceil((yhi - R.oy) / R.cell - 0.5) + 1.0, (double)(R.ny - 1));
+        if (iy0 <= iy1) {
+            first = iy0 + ((shard_index - iy0 % shard_count) + shard_count) % shard_count;
+            rows = first <= iy1 ? (iy1 - first) / shard_count + 1 : 0;
         }
     }
-    fp[c] = f;
-    counts[c] = cnt;
+    row0[c] = (int)first;
+    seg_counts[c] = rows;
+}
+
+// x-interval of cell centers inside every half-plane on row iy (padded one cell)
+__device__ inline void row_interval(const double* hp, int m, const Receivers& R, long long iy,
+                                    long long& ix0, long long& ix1) {
+    double y = R.oy + ((double)iy + 0.5) * R.cell;
+    double lo = -INFINITY, hi = INFINITY;
+    for (int i = 0; i < m; ++i) {
+        double a = hp[3 * i], r = hp[3 * i + 1] * y + hp[3 * i + 2];
+        if (a > 0.0) lo = fmax(lo, -r / a);
+        else if (a < 0.0) hi = fmin(hi, -r / a);
+        else if (r < 0.0) { lo = INFINITY; hi = -INFINITY; }
+    }
+    if (!(lo <= hi)) { ix0 = 0; ix1 = -1; return; }
+    double flo = isinf(lo) ? -1.0 : fmax(ceil((lo - R.ox) / R.cell - 0.5) - 1.0, 0.0);
+    double fhi = isinf(hi) ? (double)(R.nx - 1) : fmin(floor((hi - R.ox) / R.cell - 0.5) + 1.0, (double)(R.nx - 1));
+    ix0 = (long long)fmax(flo, 0.0);
+    ix1 = fhi < 0.0 ? -1 : (long long)fhi;
+}
+
+// one thread per candidate: fill its row segments (cand, iy, ix0, count)
+__global__ void k_segments(long long n_cand, const double* hps, const int* nhp, const int* row0,
+                           const long long* seg_off, Receivers R, int shard_count, int* seg_cand,
+                           int* seg_iy, int* seg_ix0, long long* seg_cnt) {
+    long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= n_cand) return;
+    long long s0 = seg_off[c], s1 = seg_off[c + 1];
+    const double* hp = hps + c * HP_MAX * 3;
+    int m = nhp[c];
+    for (long long s = s0; s < s1; ++s) {
+        long long iy = row0[c] + (s - s0) * shard_count;
+        long long ix0, ix1;
+        row_interval(hp, m, R, iy, ix0, ix1);
+        seg_cand[s] = (int)c;
+        seg_iy[s] = (int)iy;
+        seg_ix0[s] = (int)ix0;
+        seg_cnt[s] = ix1 >= ix0 ? ix1 - ix0 + 1 : 0;
+    }
 }
 
 // survivor of the geometric tests
@@ -237,21 +296,28 @@ struct Pending {
     int pad;
 };
 
-__device__ inline long long find_cand(const long long* scan, long long n, long long w) {
-    long long lo = 0, hi = n;   // largest c with scan[c] <= w
+// largest s with off[s] <= w (off nondecreasing, off[0] = 0)
+__device__ inline long long upper_index(const long long* off, long long n, long long w) {
+    long long lo = 0, hi = n;
     while (hi - lo > 1) {
         long long mid = (lo + hi) >> 1;
-        if (scan[mid] <= w) lo = mid; else hi = mid;
+        if (off[mid] <= w) lo = mid; else hi = mid;
     }
     return lo;
 }
 
+struct Segs {
+    const long long* item_off;   // [S+1]
+    const int* cand;
+    const int* iy;
+    const int* ix0;
+    long long n;
+};
+
 template <bool GRID>
 __global__ void __launch_bounds__(256) k_solve(Cands C, SceneDev S, const double* images,
-                                               Receivers R, d3 tx, long long W,
-                                               const long long* scan, const Footprint* fp,
-                                               int shard_count, Pending* out,
-                                               unsigned long long* n_out,
+                                               Receivers R, d3 tx, long long W, Segs G,
+                                               Pending* out, unsigned long long* n_out,
                                                unsigned long long cap) {
     const unsigned FULL = 0xffffffffu;
     long long stride = (long long)gridDim.x * blockDim.x;
@@ -262,18 +328,24 @@ __global__ void __launch_bounds__(256) k_solve(Cands C, SceneDev S, const double
         bool ok = false;
         long long rxi = 0;
         int c = 0;
-        if (w < W) {
-            if (GRID) {
-                c = (int)find_cand(scan, C.n, w);
-                long long local = w - scan[c];
-                Footprint f = fp[c];
-                long long row = local / f.w, col = local - row * f.w;
-                long long iy = f.iy0 + row * shard_count, ix = f.ix0 + col;
+        if (GRID) {
+            // one binary search per warp, then a short walk per lane
+            long long w0 = w - lane;
+            long long s0 = 0;
+            if (lane == 0 && w0 < W) s0 = upper_index(G.item_off, G.n, w0);
+            s0 = __shfl_sync(FULL, s0, 0);
+            if (w < W) {
+                long long s = s0;
+                while (G.item_off[s + 1] <= w) ++s;
+                c = G.cand[s];
+                long long iy = G.iy[s], ix = G.ix0[s] + (w - G.item_off[s]);
                 rxi = iy * R.nx + ix;
-            } else {
-                c = (int)(w % C.n);
-                rxi = w / C.n;
             }
+        } else if (w < W) {
+            c = (int)(w % C.n);
+            rxi = w / C.n;
+        }
+        if (w < W) {
             d3 pts[MAX_DEPTH];
             ok = solve_geometric(C, S, images, c, tx, receiver_pos(R, rxi), pts);
         }
