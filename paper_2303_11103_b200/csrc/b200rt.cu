@@ -59,6 +59,7 @@ struct rt_ctx {
     DevBuf nodes, tris, sorted_idx, morton, morton_alt, idx_alt, child, parent_int, parent_leaf,
         rfirst, rlast, nbox, flags;
     bool bvh_ready = false;
+    double origin_limit = 0.0;
     // candidates
     DevBuf cand_seq, cand_len;
     int64_t n_cand = 0;
@@ -137,6 +138,7 @@ rt::Bvh bvh_dev(rt_ctx* ctx) {
     b.nodes = ctx->nodes.get<BNode>();
     b.tris = ctx->tris.get<TriRec>();
     b.n_prims = (int)ctx->n_prims;
+    b.origin_limit = ctx->origin_limit;
     return b;
 }
 
@@ -316,9 +318,10 @@ int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
     CK(ctx->pbox.reserve(24 * n));
     CK(ctx->cent.reserve(12 * n));
     CK(ctx->cbounds.reserve(32));
+    ctx->origin_limit = 0.0;
     if (n_prims == 0) return RT_OK;
     CK(cudaMemcpyAsync(ctx->prim_mat.p, prim_material, 4 * n_prims, cudaMemcpyDeviceToDevice, st));
-    unsigned init[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
+    unsigned init[7] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, 0u};
     CK(cudaMemcpyAsync(ctx->cbounds.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
     k_gather<<<nblk(n_prims, 256), 256, 0, st>>>(
         vertices, tri_vertex, n_prims, ctx->v0.get<double>(), ctx->e1.get<double>(),
@@ -336,12 +339,22 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     long long n = ctx->n_prims;
     ctx->bvh_ready = true;
     if (n == 0) return RT_OK;
+    {   // scene scale S (ordered float in cbounds[6]) -> FP32 filter origin bound 2S
+        unsigned u = 0;
+        CK(cudaMemcpyAsync(&u, ctx->cbounds.get<unsigned>() + 6, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        unsigned v = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+        float S;
+        memcpy(&S, &v, 4);
+        ctx->origin_limit = 2.0 * std::max((double)S, 1.0);
+    }
     CK(ctx->tris.reserve(sizeof(TriRec) * n));
     CK(ctx->sorted_idx.reserve(4 * n));
     CK(ctx->nodes.reserve(sizeof(BNode) * std::max<long long>(n - 1, 1)));
     if (n == 1) {
         k_iota<<<1, 32, 0, st>>>(ctx->sorted_idx.get<int>(), 1);
-        k_layout_one<<<1, 1, 0, st>>>(ctx->pbox.get<float>(), ctx->nodes.get<BNode>());
+        k_layout_one<<<1, 1, 0, st>>>(ctx->pbox.get<float>(), ctx->cbounds.get<unsigned>(),
+                                      ctx->nodes.get<BNode>());
         k_sorted_tris<<<1, 32, 0, st>>>(1, ctx->sorted_idx.get<int>(), ctx->v0.get<double>(),
                                         ctx->e1.get<double>(), ctx->e2.get<double>(),
                                         ctx->tris.get<TriRec>());
@@ -380,7 +393,8 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     CKL();
     k_layout<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, vout, ctx->pbox.get<float>(), ctx->child.get<int>(),
                                                ctx->nbox.get<float>(), ctx->rfirst.get<int>(),
-                                               ctx->rlast.get<int>(), ctx->nodes.get<BNode>());
+                                               ctx->rlast.get<int>(), ctx->cbounds.get<unsigned>(),
+                                               ctx->nodes.get<BNode>());
     CKL();
     k_sorted_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, vout, ctx->v0.get<double>(), ctx->e1.get<double>(),
                                                 ctx->e2.get<double>(), ctx->tris.get<TriRec>());

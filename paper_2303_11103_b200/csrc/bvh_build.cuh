@@ -55,10 +55,15 @@ __global__ void k_gather(const double* __restrict__ V, const int64_t* __restrict
         cent[3 * i] = cx; cent[3 * i + 1] = cy; cent[3 * i + 2] = cz;
     }
     // block-reduce centroid bounds, one atomic per block and component
-    __shared__ float red[6][32];
-    float v[6] = {ok ? cx : INFINITY, ok ? cy : INFINITY, ok ? cz : INFINITY,
-                  ok ? cx : -INFINITY, ok ? cy : -INFINITY, ok ? cz : -INFINITY};
-    for (int k = 0; k < 6; ++k) {
+    __shared__ float red[7][32];
+    float amax = 0.f;
+    if (ok) {
+        const float* bx = box + 6 * i;
+        for (int m = 0; m < 6; ++m) amax = fmaxf(amax, fabsf(bx[m]));
+    }
+    float v[7] = {ok ? cx : INFINITY, ok ? cy : INFINITY, ok ? cz : INFINITY,
+                  ok ? cx : -INFINITY, ok ? cy : -INFINITY, ok ? cz : -INFINITY, amax};
+    for (int k = 0; k < 7; ++k) {
         float x = v[k];
         for (int o = 16; o; o >>= 1) {
             float y = __shfl_xor_sync(0xffffffffu, x, o);
@@ -67,7 +72,7 @@ __global__ void k_gather(const double* __restrict__ V, const int64_t* __restrict
         if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = x;
     }
     __syncthreads();
-    if (threadIdx.x < 6) {
+    if (threadIdx.x < 7) {
         int k = threadIdx.x;
         float x = red[k][0];
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) x = k < 3 ? fminf(x, red[k][w]) : fmaxf(x, red[k][w]);
@@ -171,10 +176,23 @@ __global__ void k_refit(int n, const int* sorted_idx, const float* pbox, const i
     }
 }
 
+// eps_box = 2^-20 * max(S, 1), S = max |coordinate| (trace.cuh slab32)
+__device__ inline float box_eps(const unsigned* cbounds) {
+    return fmaxf(ordered_to_float(cbounds[6]), 1.0f) * 9.5367431640625e-07f;
+}
+__device__ inline void inflate6(float* b, float e) {
+    for (int m = 0; m < 3; ++m) {
+        b[m] = __fsub_rd(b[m], e);
+        b[3 + m] = __fadd_ru(b[3 + m], e);
+    }
+}
+
 __global__ void k_layout(int n, const int* sorted_idx, const float* pbox, const int* child,
-                         const float* nbox, const int* rfirst, const int* rlast, BNode* out) {
+                         const float* nbox, const int* rfirst, const int* rlast,
+                         const unsigned* cbounds, BNode* out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n - 1) return;
+    float eps = box_eps(cbounds);
     float bx[2][6];
     int ref[2];
     for (int c = 0; c < 2; ++c) {
@@ -189,6 +207,7 @@ __global__ void k_layout(int n, const int* sorted_idx, const float* pbox, const 
             ref[c] = cnt <= LEAF_MAX ? make_leaf(rfirst[ch], cnt) : ch;
         }
         for (int m = 0; m < 6; ++m) bx[c][m] = src[m];
+        inflate6(bx[c], eps);
     }
     BNode nd;
     nd.a = make_float4(bx[0][0], bx[0][1], bx[0][2], bx[0][3]);
@@ -199,8 +218,10 @@ __global__ void k_layout(int n, const int* sorted_idx, const float* pbox, const 
 }
 
 // single-prim scene: root with the one leaf on both sides
-__global__ void k_layout_one(const float* pbox, BNode* out) {
-    const float* s = pbox;
+__global__ void k_layout_one(const float* pbox, const unsigned* cbounds, BNode* out) {
+    float s[6];
+    for (int m = 0; m < 6; ++m) s[m] = pbox[m];
+    inflate6(s, box_eps(cbounds));
     BNode nd;
     nd.a = make_float4(s[0], s[1], s[2], s[3]);
     nd.b = make_float4(s[4], s[5], s[0], s[1]);

@@ -15,6 +15,7 @@ namespace rt {
 struct Ray {
     double ox, oy, oz, dx, dy, dz;
     double ix, iy, iz;   // 1/d, +inf where d == 0 (bvh.py:120-122)
+    float fox, foy, foz, fix, fiy, fiz;   // FP32 copies for the box filter
 };
 
 __device__ inline Ray make_ray(d3 o, d3 d) {
@@ -24,7 +25,24 @@ __device__ inline Ray make_ray(d3 o, d3 d) {
     r.ix = d.x != 0.0 ? 1.0 / d.x : __longlong_as_double(0x7ff0000000000000LL);
     r.iy = d.y != 0.0 ? 1.0 / d.y : __longlong_as_double(0x7ff0000000000000LL);
     r.iz = d.z != 0.0 ? 1.0 / d.z : __longlong_as_double(0x7ff0000000000000LL);
+    r.fox = (float)o.x; r.foy = (float)o.y; r.foz = (float)o.z;
+    r.fix = (float)r.ix; r.fiy = (float)r.iy; r.fiz = (float)r.iz;
     return r;
+}
+
+// FP32 box filter.  Conservative by construction: node boxes are inflated by
+// eps_box = 2^-20 * S (S = max |scene coordinate|), which exceeds the origin
+// rounding (<= 2^-23 S for |o| <= 2S) plus the two roundings of (lo - o) * inv
+// (<= 6 * 2^-24 S); tmin is rounded down and tmax up by the caller.
+__device__ __forceinline__ bool slab32(const Ray& r, float lx, float ly, float lz, float hx,
+                                       float hy, float hz, float tmin, float tmax, float& tnear) {
+    float t0x = (lx - r.fox) * r.fix, t1x = (hx - r.fox) * r.fix;
+    float t0y = (ly - r.foy) * r.fiy, t1y = (hy - r.foy) * r.fiy;
+    float t0z = (lz - r.foz) * r.fiz, t1z = (hz - r.foz) * r.fiz;
+    float n = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), tmin));
+    float f = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fminf(fmaxf(t0z, t1z), tmax));
+    tnear = n;
+    return n <= f;
 }
 
 // Slab test of one float box in FP64; NaN (0*inf) never culls (fmin/fmax drop it).
@@ -69,6 +87,7 @@ struct Bvh {
     const BNode* __restrict__ nodes;
     const TriRec* __restrict__ tris;
     int n_prims;
+    double origin_limit;   // |o_i| bound for the FP32 filter (else the FP64 one)
 };
 
 // Closest (ANY=false) or first (ANY=true) hit with t in (tmin, tmax).
@@ -78,9 +97,12 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
                      int* visits = nullptr, int* tests = nullptr) {
     if (bvh.n_prims == 0) return -1;
     int stack[STACK_SIZE];
-    double stack_t[STACK_SIZE];
+    float stack_t[STACK_SIZE];
     int sp = 0;
     double best_t = tmax;
+    float best_tf = __double2float_ru(tmax);
+    const float tmin_f = __double2float_rd(tmin);
+    const bool fast = fmax(fmax(fabs(r.ox), fabs(r.oy)), fabs(r.oz)) <= bvh.origin_limit;
     int best_prim = -1;
     int cur = 0;   // root is internal node 0 (a 1..4 prim scene gets a root with one leaf)
     int nv = 0, nt = 0;
@@ -90,12 +112,21 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
             float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
             int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
             ++nv;
-            double tn0, tn1;
-            bool h0 = slab(r, a.x, a.y, a.z, a.w, b.x, b.y, tmin, best_t, tn0);
-            bool h1 = slab(r, b.z, b.w, c.x, c.y, c.z, c.w, tmin, best_t, tn1);
+            float tn0, tn1;
+            bool h0, h1;
+            if (fast) {
+                h0 = slab32(r, a.x, a.y, a.z, a.w, b.x, b.y, tmin_f, best_tf, tn0);
+                h1 = slab32(r, b.z, b.w, c.x, c.y, c.z, c.w, tmin_f, best_tf, tn1);
+            } else {
+                double d0, d1;
+                h0 = slab(r, a.x, a.y, a.z, a.w, b.x, b.y, tmin, best_t, d0);
+                h1 = slab(r, b.z, b.w, c.x, c.y, c.z, c.w, tmin, best_t, d1);
+                tn0 = __double2float_rd(d0);
+                tn1 = __double2float_rd(d1);
+            }
             if (h0 && h1) {
                 int nearc = ch.x, farc = ch.y;
-                double tf = tn1;
+                float tf = tn1;
                 if (tn1 < tn0) { nearc = ch.y; farc = ch.x; tf = tn0; }
                 if (sp < STACK_SIZE) { stack[sp] = farc; stack_t[sp] = tf; ++sp; }
                 else { *t_out = -1.0; return -2; }   // overflow: reported as an error
@@ -118,6 +149,7 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
                     int prim = __ldg(&tp->prim);
                     if (tmin < t && (t < best_t || (t == best_t && best_prim >= 0 && prim < best_prim))) {
                         best_t = t;
+                        best_tf = __double2float_ru(t);
                         best_prim = prim;
                         if (ANY) {
                             *t_out = t;
@@ -133,7 +165,7 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
         bool found = false;
         while (sp > 0) {
             --sp;
-            if (stack_t[sp] <= best_t) { cur = stack[sp]; found = true; break; }
+            if (stack_t[sp] <= best_tf) { cur = stack[sp]; found = true; break; }
         }
         if (!found) break;
     }
