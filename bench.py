@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--cell-size", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-rays", type=float, default=2e5)
+    ap.add_argument("--cpu-rays", type=float, default=4e6)
     ap.add_argument("--verbose", action="store_true")
     return ap.parse_args()
 
