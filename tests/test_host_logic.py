@@ -1,0 +1,149 @@
+"""Host-side logic on CPU: scene model, array layout, CIR packing, OFDM response,
+multi-rank sharding (gloo, world_size 2).  No CUDA calls."""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import golden_scene
+
+
+def test_scene_json_roundtrip_and_element_layout(golden):
+    from paper_2303_11103_b200.scene import element_layout, scene_from_dict, scene_to_dict
+    g = golden("canyon")
+    sc = golden_scene(g)
+    sc2 = scene_from_dict(scene_to_dict(sc))
+    assert scene_to_dict(sc2) == scene_to_dict(sc)
+    for arr in (sc.tx_array, sc.rx_array):
+        off, sl = element_layout(arr, sc.wavelength)
+        ooff, osl = O.element_layout(arr, sc.wavelength)
+        assert np.array_equal(off, ooff) and np.array_equal(sl, osl)
+
+
+def test_gather_order_matches_reference_prim_ids(golden):
+    from paper_2303_11103_b200.bvh import gather_meshes
+    g = golden("canyon")
+    sc = golden_scene(g)
+    verts, tris, pobj, ptri, pmat, names = gather_meshes(sc)
+    sa = O.SceneArrays(sc)
+    assert np.array_equal(verts[tris[:, 0]], sa.v0)
+    assert np.array_equal(verts[tris[:, 1]] - verts[tris[:, 0]], sa.e1)
+    assert np.array_equal(pobj, sa.prim_object)
+    assert np.array_equal(pmat, sa.prim_material)
+
+
+def _cpu_gains(sc, case_golden):
+    """A ChannelGains built on CPU tensors from the golden path table + gains."""
+    from paper_2303_11103_b200.em import ChannelGains
+    from paper_2303_11103_b200.tracer import PathTable
+    g = case_golden
+    P = len(g["p_kind"])
+    L = g["p_seq"].shape[1]
+    txn = [d.name for d in sc.devices if d.kind == "tx"]
+    rxn = [d.name for d in sc.devices if d.kind == "rx"]
+    t = lambda a, dt=torch.float64: torch.as_tensor(np.asarray(a), dtype=dt)  # noqa: E731
+    T = PathTable(L, txn, rxn, tx=t([txn.index(x) for x in g["p_tx"]], torch.int32),
+                  rx=t([rxn.index(x) for x in g["p_rx"]], torch.int32),
+                  cand=t(np.zeros(P), torch.int32), order=t(g["p_order"], torch.int8),
+                  seq=t(g["p_seq"], torch.int32), verts=t(g["p_verts"]), length=t(g["p_length"]),
+                  delay=t(g["p_delay"]), kdep=t(g["p_kdep"]), karr=t(g["p_karr"]),
+                  normals=t(g["p_normals"]), cos=t(g["p_cos"]))
+    return ChannelGains(sc, T, torch.as_tensor(g["gains_a"]), np.zeros(1))
+
+
+@pytest.mark.parametrize("case", ["box", "canyon", "two_ray"])
+def test_build_cir_packing_matches_reference(golden, case):
+    from paper_2303_11103_b200.channel import build_cir
+    g = golden(case)
+    sc = golden_scene(g)
+    cir = build_cir(_cpu_gains(sc, g))
+    assert np.array_equal(cir.a, g["cir_a"])
+    assert np.array_equal(cir.tau, g["cir_tau"])
+    los_only = build_cir(_cpu_gains(sc, g), los=True, reflection=False)
+    assert los_only.a.shape[4] <= 1
+
+
+def test_frequency_response_matches_oracle(golden):
+    from paper_2303_11103_b200.channel import build_cir, frequency_response
+    g = golden("canyon")
+    sc = golden_scene(g)
+    cir = build_cir(_cpu_gains(sc, g))
+    fr = frequency_response(cir, 32, 30e3)
+    h, f = O.frequency_response(g["cir_a"], g["cir_tau"], 32, 30e3)
+    assert np.allclose(fr.h, h, rtol=1e-12, atol=1e-20)
+    assert np.array_equal(fr.frequencies, f)
+
+
+def test_shard_ranges_cover_every_slot_and_row():
+    from paper_2303_11103_b200.parallel import rows_of_shard, shard_range
+    for n in (1, 7, 100, 10**8 + 3):
+        for w in (1, 2, 3, 8):
+            rngs = [shard_range(n, r, w) for r in range(w)]
+            assert rngs[0][0] == 0 and rngs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
+    rows = sorted(sum((rows_of_shard(513, r, 8) for r in range(8)), []))
+    assert rows == list(range(513))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2303_11103_b200 import parallel
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.RandomState(rank)
+        n = 5 + 3 * rank
+        seq = torch.full((n, 3), -1, dtype=torch.int32)
+        ln = torch.zeros(n, dtype=torch.int8)
+        for i in range(n):
+            k = rng.randint(1, 4)
+            seq[i, :k] = torch.as_tensor(rng.randint(0, 6, k), dtype=torch.int32)
+            ln[i] = k
+        s, l_ = parallel.gather_candidates(seq, ln, world)
+        g = torch.zeros((4, 3), dtype=torch.float64)
+        for iy in parallel.rows_of_shard(4, rank, world):
+            g[iy] = float(iy + 1)
+        parallel.reduce_grid(g, world)
+        mx = parallel.max_over_ranks(float(rank + 10), world)
+        sm = parallel.sum_over_ranks(float(rank + 1), world)
+        q.put((rank, s.numpy().tolist(), l_.numpy().tolist(), g.numpy().tolist(), mx, sm,
+               seq.numpy().tolist(), ln.numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_candidate_gather_and_grid_reduce():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort()
+    local_rows = [np.array(o[6]) for o in out]
+    want = sum((len(r) for r in local_rows))
+    for rank, s, l_, g, mx, sm, _, _ in out:
+        assert len(s) == want and len(l_) == want
+        # the gathered rows are rank 0's rows then rank 1's rows
+        assert np.array_equal(np.array(s), np.concatenate(local_rows))
+        assert np.array_equal(np.array(g)[:, 0], [1.0, 2.0, 3.0, 4.0])
+        assert mx == 11.0 and sm == 3.0

@@ -1,0 +1,96 @@
+"""Summarise ncu outputs into profiles/ (launch list shares + per-kernel metrics).
+
+usage: python tools/ncu_summary.py launches <launches.csv> <out.md>
+       python tools/ncu_summary.py full <report.ncu-rep> <out.md>
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[start]
+    data = [dict(zip(hdr, r)) for r in rows[start + 1:] if len(r) == len(hdr)]
+    agg = defaultdict(lambda: [0, 0.0])
+    for d in data:
+        if d.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = d["Kernel Name"].split("(")[0]
+        v = float(d["Metric Value"].replace(",", ""))
+        unit = d.get("Metric Unit", "ns")
+        scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0,
+                 "msecond": 1.0}.get(unit, 1e-6)
+        agg[name][0] += 1
+        agg[name][1] += v * scale
+    tot = sum(v[1] for v in agg.values())
+    with open(out, "w") as fh:
+        fh.write(f"# ncu launch list: {path}\n\n`--metrics gpu__time_duration.sum --clock-control none` "
+                 "(cold-cache, serialised per launch: compare shares, not absolutes)\n\n")
+        fh.write("| kernel | launches | total ms | share |\n|---|---|---|---|\n")
+        for k, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            fh.write(f"| `{k[:90]}` | {n} | {ms:.3f} | {100 * ms / tot:.1f}% |\n")
+        fh.write(f"\ntotal kernel time {tot:.2f} ms over {sum(v[0] for v in agg.values())} launches\n")
+
+
+KEYS = ["Duration", "Compute (SM) Throughput", "Memory Throughput", "DRAM Throughput",
+        "L1/TEX Hit Rate", "L2 Hit Rate", "L1/TEX Cache Throughput", "L2 Cache Throughput",
+        "Executed Ipc Active", "Issue Slots Busy", "Registers Per Thread",
+        "Theoretical Occupancy", "Achieved Occupancy", "Avg. Active Threads Per Warp",
+        "Warp Cycles Per Issued Instruction", "Branch Efficiency", "Executed Instructions"]
+
+
+def full(path, out):
+    txt = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr = rows[0]
+    per = defaultdict(dict)
+    for r in rows[1:]:
+        d = dict(zip(hdr, r))
+        k = (d.get("ID"), d.get("Kernel Name", "").split("(")[0])
+        if d.get("Metric Name") in KEYS:
+            per[k][d["Metric Name"]] = f'{d["Metric Value"]} {d["Metric Unit"]}'.strip()
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    rh = rr[0]
+    dram = {}
+    stalls = {}
+    for r in rr[2:]:
+        d = dict(zip(rh, r))
+        k = (d.get("ID"), d.get("Kernel Name", "").split("(")[0])
+        try:
+            dram[k] = float(d["dram__bytes_read.sum"].replace(",", "")) + float(
+                d["dram__bytes_write.sum"].replace(",", ""))
+        except (KeyError, ValueError):
+            pass
+        st = {}
+        for h, v in d.items():
+            if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
+                try:
+                    st[h.replace("smsp__pcsamp_warps_issue_stalled_", "")] = float(v.replace(",", ""))
+                except ValueError:
+                    pass
+        stalls[k] = st
+    with open(out, "w") as fh:
+        fh.write(f"# ncu --set full: {path}\n\n")
+        for k, m in per.items():
+            fh.write(f"## {k[1]} (launch id {k[0]})\n\n")
+            for key in KEYS:
+                if key in m:
+                    fh.write(f"- {key}: {m[key]}\n")
+            if k in dram:
+                fh.write(f"- dram bytes (read+write): {dram[k]:.4g}\n")
+            st = stalls.get(k, {})
+            tot = sum(st.values()) or 1.0
+            top = sorted(st.items(), key=lambda kv: -kv[1])[:6]
+            fh.write("- top stall reasons (share of samples): " +
+                     ", ".join(f"{n} {100 * v / tot:.0f}%" for n, v in top) + "\n\n")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
