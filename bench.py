@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--cell-size", type=float, default=1.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--cpu-rays", type=float, default=4e6)
     ap.add_argument("--verbose", action="store_true")
     return ap.parse_args()
@@ -243,9 +244,38 @@ def run_b200(args):
     }
     if e2e:
         line["e2e"] = e2e
+    if not args.no_c2:
+        line["c2_paths_cir"] = c2_latency(args)
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, sc, tx, grid, samples=1)
     return line
+
+
+def c2_latency(args):
+    """BASELINE metric part 2: compute_paths + CIR latency at C2 (street canyon,
+    2,002 tris, 8x8 tr38901 array, 256 rx, depth 3, 1e6 rays) through the public
+    API, host arrays in, host CIR out (wall clock, device synchronised)."""
+    import torch
+    import paper_2303_11103_b200 as P
+    from paper_2303_11103_b200 import scenes
+    sc = scenes.street_canyon(n_per_row=100)
+    times = []
+    out = None
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bvh = P.build(sc)
+        ps = P.compute_paths(sc, bvh, 3, method="fibonacci", num_rays=1_000_000)
+        cir = P.build_cir(P.compute_gains(sc, bvh, ps))
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            times.append(t1 - t0)
+        out = (ps.table.n, list(cir.a.shape), bvh.num_prims)
+    return {"metric": "compute_paths+CIR latency", "value_ms": 1e3 * float(np.median(times)),
+            "unit": "ms", "higher_is_better": False, "paths": out[0], "cir_a_shape": out[1],
+            "triangles": out[2], "rx": 256, "tx_elements": 64, "num_rays": 1_000_000, "max_depth": 3,
+            "includes": "build(scene) H2D + launch + paths + gains + CIR D2H"}
 
 
 def _profile(bvh):

@@ -738,18 +738,18 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     RC(clear_flags(ctx, st));
     long long vblocks = std::min<long long>((n_pend + 127) / 128, (long long)ctx->n_sm * 32);
     PROF_BEGIN(ST_VALIDATE);
-    if (power)
-        k_validate<true><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
-                                                            bvh_dev(ctx), ctx->pending.get<Pending>(),
-                                                            n_pend, E, ctx->recs.get<Rec>(), nr);
-    else
-        k_validate<false><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
-                                                             bvh_dev(ctx), ctx->pending.get<Pending>(),
-                                                             n_pend, E, ctx->recs.get<Rec>(), nr);
+    k_validate<false><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
+                                                         bvh_dev(ctx), ctx->pending.get<Pending>(),
+                                                         n_pend, E, ctx->recs.get<Rec>(), nr);
     CKL();
-    PROF_END(ST_VALIDATE);
     RC(fetch(ctx, nr, 1, st));
     long long n_rec = ctx->hpin[0];
+    if (power && n_rec > 0) {
+        k_rec_powers<<<nblk(n_rec, 128), 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, E,
+                                                       ctx->recs.get<Rec>(), n_rec);
+        CKL();
+    }
+    PROF_END(ST_VALIDATE);
     ctx->counters[6] = n_rec;
     RC(check_flags(ctx, st));
     if (stats) stats[2] = n_rec;

@@ -466,6 +466,24 @@ __global__ void __launch_bounds__(128) k_validate(Cands C, SceneDev S, const dou
     }
 }
 
+// probe powers of the surviving records (split from k_validate so the
+// occlusion kernel stays light on registers)
+__global__ void __launch_bounds__(128) k_rec_powers(Cands C, SceneDev S, const double* images,
+                                                    Receivers R, d3 tx, EmParams E, Rec* recs,
+                                                    long long n) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Rec r = recs[i];
+    d3 rx = receiver_pos(R, r.rx);
+    d3 pts[MAX_DEPTH];
+    solve_geometric(C, S, images, r.cand, tx, rx, pts);
+    Geom g;
+    geom_from_points(tx, pts, r.order, rx, C.seq + (long long)r.cand * C.max_len, S.nrm, S.prim_mat, g);
+    probe_powers(g, E, r.p_theta, r.p_phi);
+    recs[i].p_theta = r.p_theta;
+    recs[i].p_phi = r.p_phi;
+}
+
 __global__ void k_rec_keys(const Rec* recs, long long n, unsigned long long* keys, int* idx) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;

@@ -182,3 +182,41 @@ def test_material_gradient_matches_reference_tape(P, golden):
     for name, ref in zip(g["grad_names"], g["grads"]):
         got = grads[str(name)]
         assert abs(got - ref) <= 1e-3 * abs(ref) + 1e-12, (name, got, ref)
+
+
+def test_c2_paths_and_cir_match_oracle(P):
+    """C2 shape (2,002-tri canyon, 8x8 tr38901 array, 256 rx, depth 3) at 1e5 rays:
+    path sets identical to the oracle, CIR within 1e-9 rel."""
+    import oracle as O
+    from paper_2303_11103_b200 import scenes
+    sc = scenes.street_canyon(n_per_row=100)
+    b = _bvh(P, sc)
+    ps = P.compute_paths(sc, b, 3, method="fibonacci", num_rays=100_000)
+    ob = O.Bvh(O.SceneArrays(sc))
+    want = O.compute_paths(sc, ob, 3, method="fibonacci", num_rays=100_000)
+    got = ps.paths
+    assert [(p.rx, p.kind, p.seq) for p in got] == [(p.rx, p.kind, p.seq) for p in want]
+    for a, w in zip(got, want):
+        assert abs(a.delay_s - w.delay_s) <= 1e-12 * w.delay_s
+    cir = P.build_cir(P.compute_gains(sc, b, ps))
+    oa, otau = O.build_cir(sc, O.compute_gains(sc, ob, want))
+    assert cir.a.shape == oa.shape
+    assert np.abs(cir.a - oa).max() <= 1e-9 * np.abs(oa).max()
+    assert np.allclose(cir.tau, otau, rtol=1e-12, atol=0)
+
+
+def test_coverage_matches_oracle_city_subset(P):
+    """C3-like city (6x6 blocks), depth 3, 20k rays, 24x24 cells: every cell vs oracle."""
+    import oracle as O
+    from paper_2303_11103_b200 import scenes
+    sc = scenes.city(n_side=6, seed=1)
+    b = _bvh(P, sc)
+    tx = sc.devices[0]
+    grid = P.GridSpec((float(tx.position[0]) - 60.0, float(tx.position[1]) - 60.0), 5.0, 24, 24, 1.5)
+    cm = P.coverage_map(sc, b, grid, 3, method="fibonacci", num_rays=20_000)
+    ob = O.Bvh(O.SceneArrays(sc))
+    want = O.coverage_map(sc, ob, grid.origin, grid.cell_size, grid.nx, grid.ny, grid.height, 3,
+                          method="fibonacci", num_rays=20_000)
+    assert np.array_equal(cm.gains == 0.0, want == 0.0)
+    nz = want > 0
+    assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz])
