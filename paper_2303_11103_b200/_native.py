@@ -171,12 +171,21 @@ class Context:
         self.check(rc, exc_map)
 
 
-_contexts = {}
+_pool = {}
+_pool_lock = threading.Lock()
 
 
-def context(device=None) -> Context:
+def acquire_context(device=None) -> Context:
+    """An idle library context for ``device`` (reused so its device buffers —
+    trie, scratch, path tables — persist across scenes), or a new one."""
     idx = torch.cuda.current_device() if device is None else (torch.device(device).index or 0)
-    c = _contexts.get(idx)
-    if c is None:
-        c = _contexts[idx] = Context(idx)
-    return c
+    with _pool_lock:
+        free = _pool.setdefault(idx, [])
+        if free:
+            return free.pop()
+    return Context(idx)
+
+
+def release_context(ctx: Context):
+    with _pool_lock:
+        _pool.setdefault(ctx.device.index, []).append(ctx)

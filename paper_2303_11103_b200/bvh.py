@@ -61,7 +61,7 @@ class Bvh:
     """Device-resident scene + LBVH; immutable after build, queries are stream-ordered."""
 
     def __init__(self, scene, device=None):
-        self.ctx = N.Context(device)
+        self.ctx = N.acquire_context(device)
         self.device = self.ctx.device
         (verts, tris, self.prim_object, self.prim_triangle, prim_mat,
          self.material_names) = gather_meshes(scene)
@@ -77,6 +77,12 @@ class Bvh:
                           N.ptr(self._pmat), self.num_prims, s)
             self.ctx.call("rt_bvh_build", s)
         self._arrays = None
+
+    def __del__(self):
+        ctx = getattr(self, "ctx", None)
+        if ctx is not None:
+            self.ctx = None
+            N.release_context(ctx)
 
     # -- per-primitive arrays (bit-identical to the reference's numpy ones) ------------
     def _fetch_arrays(self):

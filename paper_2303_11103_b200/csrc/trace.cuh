@@ -58,8 +58,17 @@ __device__ __forceinline__ bool slab(const Ray& r, float lx, float ly, float lz,
     return n <= f;
 }
 
-// bvh.py:151-170 verbatim in operation order; returns true and t when accepted.
-__device__ __forceinline__ bool mt_test(const Ray& r, const TriRec* __restrict__ tp, double& t) {
+// bvh.py:151-170 in operation order; returns true and t when accepted.
+//
+// The reference divides once (inv_det = 1/det) and multiplies: u = u_num *
+// inv_det etc.  The computed u is within 2^-52 relative of the exact quotient
+// u_num/det, so a test whose outcome is already certain from the exact
+// numerator (rejected with a 1e-6 relative margin) skips the division; every
+// other case runs the reference's arithmetic verbatim.  Decisions are
+// therefore identical to the reference's, and the FP64 divide only runs for
+// near-hits.  `tmax` is the current closest hit for the t-window quick reject.
+__device__ __forceinline__ bool mt_test(const Ray& r, const TriRec* __restrict__ tp, double tmin,
+                                        double tmax, double& t) {
     const double2* q = reinterpret_cast<const double2*>(tp);
     double2 a = __ldg(q + 0), b = __ldg(q + 1), c = __ldg(q + 2), dd = __ldg(q + 3),
             e = __ldg(q + 4);
@@ -70,16 +79,26 @@ __device__ __forceinline__ bool mt_test(const Ray& r, const TriRec* __restrict__
     double pz = r.dx * e2y - r.dy * e2x;
     double det = e1x * px + e1y * py + e1z * pz;
     if (-DET_EPS < det && det < DET_EPS) return false;
-    double inv_det = 1.0 / det;
+    double s = det > 0.0 ? 1.0 : -1.0, ad = fabs(det);
     double tx = r.ox - v0x, ty = r.oy - v0y, tz = r.oz - v0z;
-    double u = (tx * px + ty * py + tz * pz) * inv_det;
-    if (u < -BARY_EPS || u > 1.0 + BARY_EPS) return false;
+    double un = tx * px + ty * py + tz * pz;
+    double us = un * s;   // sign(u) * |u| * |det|, exact
+    if (us < -1.000001e-12 * ad || us > (1.0 + 2e-6) * ad) return false;   // certain u reject
     double qx = ty * e1z - tz * e1y;
     double qy = tz * e1x - tx * e1z;
     double qz = tx * e1y - ty * e1x;
-    double v = (r.dx * qx + r.dy * qy + r.dz * qz) * inv_det;
+    double vn = r.dx * qx + r.dy * qy + r.dz * qz;
+    double vs = vn * s;
+    if (vs < -1.000001e-12 * ad || us + vs > (1.0 + 2e-6) * ad) return false;   // certain v reject
+    double tn = e2x * qx + e2y * qy + e2z * qz;
+    double ts = tn * s;
+    if (ts < tmin * ad * (1.0 - 1e-6) || ts > tmax * ad * (1.0 + 1e-6)) return false;   // certain t reject
+    double inv_det = 1.0 / det;   // the reference's arithmetic from here on
+    double u = un * inv_det;
+    if (u < -BARY_EPS || u > 1.0 + BARY_EPS) return false;
+    double v = vn * inv_det;
     if (v < -BARY_EPS || u + v > 1.0 + BARY_EPS) return false;
-    t = (e2x * qx + e2y * qy + e2z * qz) * inv_det;
+    t = tn * inv_det;
     return true;
 }
 
@@ -145,7 +164,7 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
             for (int k = 0; k < cnt; ++k) {
                 const TriRec* tp = bvh.tris + first + k;
                 double t;
-                if (mt_test(r, tp, t)) {
+                if (mt_test(r, tp, tmin, best_t, t)) {
                     int prim = __ldg(&tp->prim);
                     if (tmin < t && (t < best_t || (t == best_t && best_prim >= 0 && prim < best_prim))) {
                         best_t = t;

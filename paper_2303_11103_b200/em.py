@@ -249,17 +249,32 @@ class ChannelGains:
         return self._entries
 
 
-def _fraunhofer_check(scene, tx_name, rx_name, off_tx_w, off_rx_w, length):
-    aperture = 0.0
-    for off in (off_tx_w, off_rx_w):
-        if len(off) > 1:
-            aperture = max(aperture, float(np.linalg.norm(off.max(axis=0) - off.min(axis=0))))
-    if aperture > 0.0:
+def _aperture(off, rows):
+    if len(off) <= 1:
+        return 0.0
+    w = off @ np.asarray(rows, dtype=np.float64).T
+    return float(np.linalg.norm(w.max(axis=0) - w.min(axis=0)))
+
+
+def _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows, rx_rows):
+    """em.py:344-356 for every (tx, rx) pair, vectorized over the path table."""
+    ap_t = [_aperture(off_tx, r) for r in tx_rows]
+    ap_r = [_aperture(off_rx, r) for r in rx_rows]
+    if max(ap_t + ap_r + [0.0]) == 0.0:
+        return
+    n_rx = len(T.rx_names)
+    pair = (T.tx.long() * n_rx + T.rx.long()).cpu().numpy()
+    length = T.length.cpu().numpy()
+    mins = np.full(len(T.tx_names) * n_rx, np.inf)
+    np.minimum.at(mins, pair, length)
+    for k in np.flatnonzero(np.isfinite(mins)):
+        ti, ri = divmod(int(k), n_rx)
+        aperture = max(ap_t[ti], ap_r[ri])
         fr = 2.0 * aperture * aperture / scene.wavelength
-        if length < fr:
-            warnings.warn(f"path {tx_name}->{rx_name} at {length:.1f} m is inside the Fraunhofer "
-                          f"distance {fr:.1f} m; the plane-wave synthetic-array assumption "
-                          "degrades here", stacklevel=3)
+        if aperture > 0.0 and mins[k] < fr:
+            warnings.warn(f"path {T.tx_names[ti]}->{T.rx_names[ri]} at {mins[k]:.1f} m is inside "
+                          f"the Fraunhofer distance {fr:.1f} m; the plane-wave synthetic-array "
+                          "assumption degrades here", stacklevel=3)
 
 
 def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=None) -> ChannelGains:
@@ -303,14 +318,7 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
     off_tx_w = torch.einsum("ek,dmk->dem", offt, Rt)                           # [n_tx, E, 3]
     off_rx_w = torch.einsum("ek,dmk->dem", offr, Rr)
     if scene.synthetic_array:
-        h_len = T.length.cpu().numpy()
-        h_tx, h_rx = tx_idx.cpu().numpy(), rx_idx.cpu().numpy()
-        for ti, tn in enumerate(T.tx_names):
-            for ri, rn in enumerate(T.rx_names):
-                m = (h_tx == ti) & (h_rx == ri)
-                if m.any():
-                    _fraunhofer_check(scene, tn, rn, off_tx_w[ti].cpu().numpy(),
-                                      off_rx_w[ri].cpu().numpy(), float(h_len[m].min()))
+        _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows_dev, rx_rows_dev)
     ph_tx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", off_tx_w[tx_idx], T.kdep) / lam)
     ph_rx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", off_rx_w[rx_idx], -T.karr) / lam)
     s_index = torch.tensor([st.index(float(s)) for s in sl_tx], device=dev)
