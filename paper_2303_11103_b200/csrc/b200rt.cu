@@ -56,7 +56,7 @@ struct rt_ctx {
     int64_t n_prims = 0;
     DevBuf v0, e1, e2, nrm, poff, prim_mat, pbox, cent, cbounds;
     // bvh
-    DevBuf nodes, tris, sorted_idx, morton, morton_alt, idx_alt, child, parent_int, parent_leaf,
+    DevBuf nodes4, frontier, frontier2, map4, nodes, tris, sorted_idx, morton, morton_alt, idx_alt, child, parent_int, parent_leaf,
         rfirst, rlast, nbox, flags;
     bool bvh_ready = false;
     double origin_limit = 0.0;
@@ -135,7 +135,7 @@ SceneDev scene_dev(rt_ctx* ctx) {
 
 rt::Bvh bvh_dev(rt_ctx* ctx) {
     rt::Bvh b;
-    b.nodes = ctx->nodes.get<BNode>();
+    b.nodes = ctx->nodes4.get<BNode4>();
     b.tris = ctx->tris.get<TriRec>();
     b.n_prims = (int)ctx->n_prims;
     b.origin_limit = ctx->origin_limit;
@@ -257,6 +257,41 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st) {
     return RT_OK;
 }
 
+// binary child-pair nodes (n_bin of them, root 0) -> 4-wide nodes
+int collapse4(rt_ctx* ctx, long long n_bin, cudaStream_t st) {
+    long long cap = std::max<long long>(n_bin, 1);
+    CK(ctx->nodes4.reserve(sizeof(BNode4) * cap));
+    CK(ctx->frontier.reserve(4 * cap));
+    CK(ctx->frontier2.reserve(4 * cap));
+    CK(ctx->map4.reserve(4 * cap));
+    int* cnt = reinterpret_cast<int*>(ctx->ctrs.get<long long>());   // [0] out nodes, [2] next size
+    CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
+    int zero = 0;
+    CK(cudaMemcpyAsync(ctx->frontier.p, &zero, 4, cudaMemcpyHostToDevice, st));
+    int* f = ctx->frontier.get<int>();
+    int* g = ctx->frontier2.get<int>();
+    long long nf = 1;
+    while (nf > 0) {
+        CK(cudaMemsetAsync(cnt + 2, 0, 4, st));
+        k_collapse<<<nblk(nf, 128), 128, 0, st>>>(ctx->nodes.get<BNode>(), f, (int)nf,
+                                                  ctx->nodes4.get<BNode4>(), cnt, ctx->map4.get<int>(),
+                                                  g, cnt + 2);
+        CKL();
+        int nxt = 0;
+        CK(cudaMemcpyAsync(&nxt, cnt + 2, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        nf = nxt;
+        std::swap(f, g);
+    }
+    int n4 = 0;
+    CK(cudaMemcpyAsync(&n4, cnt, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    k_fix_refs<<<nblk(n4, 128), 128, 0, st>>>(ctx->nodes4.get<BNode4>(), n4, ctx->map4.get<int>());
+    CKL();
+    ctx->counters[8] = n4;
+    return RT_OK;
+}
+
 }  // namespace
 
 // ===========================================================================================
@@ -359,7 +394,7 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
                                         ctx->e1.get<double>(), ctx->e2.get<double>(),
                                         ctx->tris.get<TriRec>());
         CKL();
-        return RT_OK;
+        return collapse4(ctx, 1, st);
     }
     CK(ctx->morton.reserve(8 * n));
     CK(ctx->morton_alt.reserve(8 * n));
@@ -399,7 +434,7 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     k_sorted_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, vout, ctx->v0.get<double>(), ctx->e1.get<double>(),
                                                 ctx->e2.get<double>(), ctx->tris.get<TriRec>());
     CKL();
-    return RT_OK;
+    return collapse4(ctx, n - 1, st);
 }
 
 int rt_scene_arrays(rt_ctx* ctx, double* v0, double* e1, double* e2, double* normals,

@@ -230,6 +230,86 @@ __global__ void k_layout_one(const float* pbox, const unsigned* cbounds, BNode* 
     out[0] = nd;
 }
 
+// ---- 4-wide collapse (level-synchronous, top-down) ---------------------------------------
+// BVH4 node = binary node X; its children = X's two children with the internal
+// child of largest surface area repeatedly replaced by its own two children
+// until there are four (or only leaves remain).
+
+__device__ inline float box_area(const float* b) {
+    float dx = fmaxf(b[3] - b[0], 0.f), dy = fmaxf(b[4] - b[1], 0.f), dz = fmaxf(b[5] - b[2], 0.f);
+    return dx * dy + dy * dz + dz * dx;
+}
+
+__device__ inline void bin_child(const BNode& nd, int c, int& ref, float* b) {
+    if (c == 0) {
+        b[0] = nd.a.x; b[1] = nd.a.y; b[2] = nd.a.z; b[3] = nd.a.w; b[4] = nd.b.x; b[5] = nd.b.y;
+        ref = nd.d.x;
+    } else {
+        b[0] = nd.b.z; b[1] = nd.b.w; b[2] = nd.c.x; b[3] = nd.c.y; b[4] = nd.c.z; b[5] = nd.c.w;
+        ref = nd.d.y;
+    }
+}
+
+__global__ void k_collapse(const BNode* bin, const int* frontier, int nf, BNode4* out, int* out_count,
+                           int* map, int* next, int* next_count) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nf) return;
+    int X = frontier[i];
+    int q = atomicAdd(out_count, 1);
+    map[X] = q;
+    int ref[4];
+    float bx[4][6];
+    BNode nd = bin[X];
+    bin_child(nd, 0, ref[0], bx[0]);
+    bin_child(nd, 1, ref[1], bx[1]);
+    int n = 2;
+    while (n < 4) {
+        int best = -1;
+        float bestA = -1.f;
+        for (int k = 0; k < n; ++k)
+            if (!ref_is_leaf(ref[k])) {
+                float A = box_area(bx[k]);
+                if (A > bestA) { bestA = A; best = k; }
+            }
+        if (best < 0) break;
+        BNode y = bin[ref[best]];
+        bin_child(y, 0, ref[best], bx[best]);
+        bin_child(y, 1, ref[n], bx[n]);
+        ++n;
+    }
+    BNode4 o;
+    float lo[3][4], hi[3][4];
+    int ch[4];
+    for (int k = 0; k < 4; ++k) {
+        for (int m = 0; m < 3; ++m) {
+            lo[m][k] = k < n ? bx[k][m] : INFINITY;
+            hi[m][k] = k < n ? bx[k][3 + m] : -INFINITY;
+        }
+        ch[k] = k < n ? ref[k] : EMPTY_REF;
+        if (k < n && !ref_is_leaf(ref[k])) next[atomicAdd(next_count, 1)] = ref[k];
+    }
+    o.lox = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+    o.loy = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+    o.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+    o.hix = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+    o.hiy = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+    o.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+    o.child = make_int4(ch[0], ch[1], ch[2], ch[3]);
+    o.pad = make_int4(0, 0, 0, 0);
+    out[q] = o;
+}
+
+// binary internal indices -> BVH4 indices
+__global__ void k_fix_refs(BNode4* out, int n4, const int* map) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n4) return;
+    int4 c = out[i].child;
+    int v[4] = {c.x, c.y, c.z, c.w};
+    for (int k = 0; k < 4; ++k)
+        if (v[k] != EMPTY_REF && !ref_is_leaf(v[k])) v[k] = map[v[k]];
+    out[i].child = make_int4(v[0], v[1], v[2], v[3]);
+}
+
 __global__ void k_sorted_tris(int n, const int* sorted_idx, const double* v0, const double* e1,
                               const double* e2, TriRec* tris) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;

@@ -22,7 +22,7 @@ constexpr double PI = 3.141592653589793;
 constexpr double TWO_PI = 2.0 * 3.141592653589793;
 constexpr int MAX_DEPTH = 8;          // compile-time bound on interactions per path
 constexpr int LEAF_MAX = 4;           // BVH leaf collapse threshold
-constexpr int STACK_SIZE = 64;
+constexpr int STACK_SIZE = 128;
 constexpr int RT_PAT_PROBE_THETA_ID = 3;  // em.py:70-75 internal coverage probes
 constexpr int RT_PAT_PROBE_PHI_ID = 4;
 
@@ -55,6 +55,15 @@ struct __align__(16) BNode {
     float4 c;   // lo1.z hi1.x hi1.y hi1.z
     int4 d;     // child0 child1 - -
 };
+
+// 4-wide node (collapsed from the binary LBVH): per-axis float4 of the four
+// children's bounds + refs; unused slots hold EMPTY_REF.
+struct __align__(16) BNode4 {
+    float4 lox, loy, loz, hix, hiy, hiz;
+    int4 child;
+    int4 pad;
+};
+constexpr int EMPTY_REF = 0x7fffffff;
 
 // triangle in sorted (BVH) order: FP64 v0, e1, e2 and the global prim id
 struct __align__(16) TriRec {

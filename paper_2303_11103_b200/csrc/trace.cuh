@@ -103,14 +103,23 @@ __device__ __forceinline__ bool mt_test(const Ray& r, const TriRec* __restrict__
 }
 
 struct Bvh {
-    const BNode* __restrict__ nodes;
+    const BNode4* __restrict__ nodes;
     const TriRec* __restrict__ tris;
     int n_prims;
     double origin_limit;   // |o_i| bound for the FP32 filter (else the FP64 one)
 };
 
-// Closest (ANY=false) or first (ANY=true) hit with t in (tmin, tmax).
-// Returns the global prim id or -1; *t_out the hit distance.
+// compare-exchange on (t, ref) pairs, ascending t
+__device__ __forceinline__ void cx(float& ta, int& ra, float& tb, int& rb) {
+    if (tb < ta) {
+        float t = ta; ta = tb; tb = t;
+        int r = ra; ra = rb; rb = r;
+    }
+}
+
+// Closest (ANY=false) or first (ANY=true) hit with t in (tmin, tmax) over the
+// 4-wide BVH.  Returns the global prim id, -1 on a miss, -2 on stack overflow;
+// *t_out the hit distance.  Children are visited nearest-first.
 template <bool ANY>
 __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, double* t_out,
                      int* visits = nullptr, int* tests = nullptr) {
@@ -123,39 +132,50 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
     const float tmin_f = __double2float_rd(tmin);
     const bool fast = fmax(fmax(fabs(r.ox), fabs(r.oy)), fabs(r.oz)) <= bvh.origin_limit;
     int best_prim = -1;
-    int cur = 0;   // root is internal node 0 (a 1..4 prim scene gets a root with one leaf)
+    int cur = 0;   // root: BVH4 node 0
     int nv = 0, nt = 0;
     while (true) {
         if (!ref_is_leaf(cur)) {
             const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
-            float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
-            int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
+            float4 lx = __ldg(np), ly = __ldg(np + 1), lz = __ldg(np + 2);
+            float4 hx = __ldg(np + 3), hy = __ldg(np + 4), hz = __ldg(np + 5);
+            int4 ch = __ldg(reinterpret_cast<const int4*>(np + 6));
             ++nv;
-            float tn0, tn1;
-            bool h0, h1;
+            float t0, t1, t2, t3;
+            bool h0, h1, h2, h3;
             if (fast) {
-                h0 = slab32(r, a.x, a.y, a.z, a.w, b.x, b.y, tmin_f, best_tf, tn0);
-                h1 = slab32(r, b.z, b.w, c.x, c.y, c.z, c.w, tmin_f, best_tf, tn1);
+                h0 = slab32(r, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, tmin_f, best_tf, t0);
+                h1 = slab32(r, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, tmin_f, best_tf, t1);
+                h2 = slab32(r, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, tmin_f, best_tf, t2);
+                h3 = slab32(r, lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, tmin_f, best_tf, t3);
             } else {
-                double d0, d1;
-                h0 = slab(r, a.x, a.y, a.z, a.w, b.x, b.y, tmin, best_t, d0);
-                h1 = slab(r, b.z, b.w, c.x, c.y, c.z, c.w, tmin, best_t, d1);
-                tn0 = __double2float_rd(d0);
-                tn1 = __double2float_rd(d1);
+                double d0, d1, d2, d3;
+                h0 = slab(r, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, tmin, best_t, d0);
+                h1 = slab(r, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, tmin, best_t, d1);
+                h2 = slab(r, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, tmin, best_t, d2);
+                h3 = slab(r, lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, tmin, best_t, d3);
+                t0 = __double2float_rd(d0); t1 = __double2float_rd(d1);
+                t2 = __double2float_rd(d2); t3 = __double2float_rd(d3);
             }
-            if (h0 && h1) {
-                int nearc = ch.x, farc = ch.y;
-                float tf = tn1;
-                if (tn1 < tn0) { nearc = ch.y; farc = ch.x; tf = tn0; }
-                if (sp < STACK_SIZE) { stack[sp] = farc; stack_t[sp] = tf; ++sp; }
-                else { *t_out = -1.0; return -2; }   // overflow: reported as an error
-                cur = nearc;
-                continue;
-            } else if (h0) {
-                cur = ch.x;
-                continue;
-            } else if (h1) {
-                cur = ch.y;
+            const float INF = __int_as_float(0x7f800000);
+            int r0 = ch.x, r1 = ch.y, r2 = ch.z, r3 = ch.w;
+            if (!h0 || r0 == EMPTY_REF) t0 = INF;
+            if (!h1 || r1 == EMPTY_REF) t1 = INF;
+            if (!h2 || r2 == EMPTY_REF) t2 = INF;
+            if (!h3 || r3 == EMPTY_REF) t3 = INF;
+            int nh = (t0 != INF) + (t1 != INF) + (t2 != INF) + (t3 != INF);
+            if (nh > 0) {
+                // 5-comparator sorting network, nearest first
+                cx(t0, r0, t1, r1);
+                cx(t2, r2, t3, r3);
+                cx(t0, r0, t2, r2);
+                cx(t1, r1, t3, r3);
+                cx(t1, r1, t2, r2);
+                if (sp + 3 > STACK_SIZE) { *t_out = -1.0; return -2; }   // reported as an error
+                if (nh > 3) { stack[sp] = r3; stack_t[sp] = t3; ++sp; }
+                if (nh > 2) { stack[sp] = r2; stack_t[sp] = t2; ++sp; }
+                if (nh > 1) { stack[sp] = r1; stack_t[sp] = t1; ++sp; }
+                cur = r0;
                 continue;
             }
         } else {
