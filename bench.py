@@ -39,7 +39,7 @@ sys.path.insert(0, REPO)
 
 METRIC = "coverage-map ray-bounces/s"
 UNIT = "ray-bounces/s"
-BYTES_PER_NODE = 64    # BNode: two float child boxes + refs (rt_common.cuh)
+BYTES_PER_NODE = 128   # BNode4: four float child boxes + refs (rt_common.cuh)
 BYTES_PER_TRI = 80     # TriRec: FP64 v0/e1/e2 + prim id
 
 

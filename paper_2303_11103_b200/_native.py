@@ -16,6 +16,10 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_native", "libb200rt.so")
+# experiment hook: load an alternative build of the same ABI (e.g. a variant
+# compiled with other -D flags into _native/); the default is the product build
+if os.environ.get("B200RT_LIB"):
+    LIB_PATH = os.path.join(HERE, "_native", os.path.basename(os.environ["B200RT_LIB"]))
 SRC_DIR = os.path.join(HERE, "csrc")
 
 RT_OK, RT_EINVAL, RT_ECAP, RT_ECOINCIDE, RT_ECUDA, RT_ENOMEM, RT_ESTATE = 0, -1, -2, -3, -4, -5, -6

@@ -82,7 +82,10 @@ class Bvh:
         ctx = getattr(self, "ctx", None)
         if ctx is not None:
             self.ctx = None
-            N.release_context(ctx)
+            try:
+                N.release_context(ctx)
+            except Exception:   # interpreter shutdown
+                pass
 
     # -- per-primitive arrays (bit-identical to the reference's numpy ones) ------------
     def _fetch_arrays(self):

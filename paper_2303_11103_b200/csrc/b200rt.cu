@@ -135,7 +135,11 @@ SceneDev scene_dev(rt_ctx* ctx) {
 
 rt::Bvh bvh_dev(rt_ctx* ctx) {
     rt::Bvh b;
+#if RT_WIDE
     b.nodes = ctx->nodes4.get<BNode4>();
+#else
+    b.nodes = ctx->nodes.get<BNode>();
+#endif
     b.tris = ctx->tris.get<TriRec>();
     b.n_prims = (int)ctx->n_prims;
     b.origin_limit = ctx->origin_limit;
@@ -394,7 +398,7 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
                                         ctx->e1.get<double>(), ctx->e2.get<double>(),
                                         ctx->tris.get<TriRec>());
         CKL();
-        return collapse4(ctx, 1, st);
+        return RT_WIDE ? collapse4(ctx, 1, st) : RT_OK;
     }
     CK(ctx->morton.reserve(8 * n));
     CK(ctx->morton_alt.reserve(8 * n));
@@ -434,7 +438,7 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     k_sorted_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, vout, ctx->v0.get<double>(), ctx->e1.get<double>(),
                                                 ctx->e2.get<double>(), ctx->tris.get<TriRec>());
     CKL();
-    return collapse4(ctx, n - 1, st);
+    return RT_WIDE ? collapse4(ctx, n - 1, st) : RT_OK;
 }
 
 int rt_scene_arrays(rt_ctx* ctx, double* v0, double* e1, double* e2, double* normals,

@@ -7,55 +7,84 @@
 // t resolves to the lower global prim id (the reference's brute-force oracle,
 // tests/conftest.py:45-80).  Node boxes are conservative (inflated, rounded
 // outward to float) so the tree never culls a triangle the exact test accepts.
+//
+// RT_WIDE selects the node format walked: 0 = binary child-pair nodes (BNode),
+// 1 = 4-wide nodes (BNode4) collapsed from the same LBVH.
 #pragma once
 #include "rt_common.cuh"
+
+#ifndef RT_WIDE
+#define RT_WIDE 0
+#endif
 
 namespace rt {
 
 struct Ray {
     double ox, oy, oz, dx, dy, dz;
-    double ix, iy, iz;   // 1/d, +inf where d == 0 (bvh.py:120-122)
-    float fox, foy, foz, fix, fiy, fiz;   // FP32 copies for the box filter
+    float fix, fiy, fiz;      // FP32 1/d for the box filter
+    float oix, oiy, oiz;      // FP32 o * (1/d): slab planes are fma(bound, inv, -oi)
 };
+
+// 1/d, +inf where d == 0 (bvh.py:120-122)
+__device__ __forceinline__ double inv_dir(double d) {
+    return d != 0.0 ? 1.0 / d : __longlong_as_double(0x7ff0000000000000LL);
+}
 
 __device__ inline Ray make_ray(d3 o, d3 d) {
     Ray r;
     r.ox = o.x; r.oy = o.y; r.oz = o.z;
     r.dx = d.x; r.dy = d.y; r.dz = d.z;
-    r.ix = d.x != 0.0 ? 1.0 / d.x : __longlong_as_double(0x7ff0000000000000LL);
-    r.iy = d.y != 0.0 ? 1.0 / d.y : __longlong_as_double(0x7ff0000000000000LL);
-    r.iz = d.z != 0.0 ? 1.0 / d.z : __longlong_as_double(0x7ff0000000000000LL);
-    r.fox = (float)o.x; r.foy = (float)o.y; r.foz = (float)o.z;
-    r.fix = (float)r.ix; r.fiy = (float)r.iy; r.fiz = (float)r.iz;
+    // clamp 1/d to +-1e30: with an infinite inverse the fma form yields
+    // inf - inf = NaN on one plane and +-inf on the other, which mis-culls a
+    // slab the ray lies inside; a 1e-30 direction component moves the ray by
+    // < 1e-25 m over any scene, far inside eps_box.
+    r.fix = (float)fmin(fmax(inv_dir(d.x), -1e30), 1e30);
+    r.fiy = (float)fmin(fmax(inv_dir(d.y), -1e30), 1e30);
+    r.fiz = (float)fmin(fmax(inv_dir(d.z), -1e30), 1e30);
+    r.oix = (float)o.x * r.fix; r.oiy = (float)o.y * r.fiy; r.oiz = (float)o.z * r.fiz;
     return r;
 }
 
-// FP32 box filter.  Conservative by construction: node boxes are inflated by
-// eps_box = 2^-20 * S (S = max |scene coordinate|), which exceeds the origin
-// rounding (<= 2^-23 S for |o| <= 2S) plus the two roundings of (lo - o) * inv
-// (<= 6 * 2^-24 S); tmin is rounded down and tmax up by the caller.
+// FP32 box filter, one FFMA per slab plane: t = bound * inv - o * inv.
+// Conservative by construction: node boxes are inflated by eps_box = 2^-20 S
+// (S = max |scene coordinate|).  For |o| <= 2S the spatial error of a plane
+// distance is <= 2^-24 (|o| [origin rounding] + |o| [o*inv rounding] +
+// |bound - o| [1/d rounding] + |t d| [fma rounding]) <= 10 * 2^-24 S < eps_box.
+// tmin is rounded down and tmax up by the caller; 1/d is clamped (make_ray)
+// so no plane distance is NaN.
 __device__ __forceinline__ bool slab32(const Ray& r, float lx, float ly, float lz, float hx,
                                        float hy, float hz, float tmin, float tmax, float& tnear) {
-    float t0x = (lx - r.fox) * r.fix, t1x = (hx - r.fox) * r.fix;
-    float t0y = (ly - r.foy) * r.fiy, t1y = (hy - r.foy) * r.fiy;
-    float t0z = (lz - r.foz) * r.fiz, t1z = (hz - r.foz) * r.fiz;
+    float t0x = __fmaf_rn(lx, r.fix, -r.oix), t1x = __fmaf_rn(hx, r.fix, -r.oix);
+    float t0y = __fmaf_rn(ly, r.fiy, -r.oiy), t1y = __fmaf_rn(hy, r.fiy, -r.oiy);
+    float t0z = __fmaf_rn(lz, r.fiz, -r.oiz), t1z = __fmaf_rn(hz, r.fiz, -r.oiz);
     float n = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), tmin));
     float f = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fminf(fmaxf(t0z, t1z), tmax));
     tnear = n;
     return n <= f;
 }
 
-// Slab test of one float box in FP64; NaN (0*inf) never culls (fmin/fmax drop it).
+// FP64 slab test (origins beyond the FP32 filter's range); NaN never culls.
 __device__ __forceinline__ bool slab(const Ray& r, float lx, float ly, float lz, float hx,
                                      float hy, float hz, double tmin, double tmax,
                                      double& tnear) {
-    double t0x = ((double)lx - r.ox) * r.ix, t1x = ((double)hx - r.ox) * r.ix;
-    double t0y = ((double)ly - r.oy) * r.iy, t1y = ((double)hy - r.oy) * r.iy;
-    double t0z = ((double)lz - r.oz) * r.iz, t1z = ((double)hz - r.oz) * r.iz;
+    double ix = inv_dir(r.dx), iy = inv_dir(r.dy), iz = inv_dir(r.dz);
+    double t0x = ((double)lx - r.ox) * ix, t1x = ((double)hx - r.ox) * ix;
+    double t0y = ((double)ly - r.oy) * iy, t1y = ((double)hy - r.oy) * iy;
+    double t0z = ((double)lz - r.oz) * iz, t1z = ((double)hz - r.oz) * iz;
     double n = fmax(fmax(fmin(t0x, t1x), fmin(t0y, t1y)), fmax(fmin(t0z, t1z), tmin));
     double f = fmin(fmin(fmax(t0x, t1x), fmax(t0y, t1y)), fmin(fmax(t0z, t1z), tmax));
     tnear = n;
     return n <= f;
+}
+
+__device__ __forceinline__ bool box_hit(const Ray& r, bool fast, float lx, float ly, float lz,
+                                        float hx, float hy, float hz, double tmin, double tmax,
+                                        float tmin_f, float tmax_f, float& tn) {
+    if (fast) return slab32(r, lx, ly, lz, hx, hy, hz, tmin_f, tmax_f, tn);
+    double d;
+    bool h = slab(r, lx, ly, lz, hx, hy, hz, tmin, tmax, d);
+    tn = __double2float_rd(d);
+    return h;
 }
 
 // bvh.py:151-170 in operation order; returns true and t when accepted.
@@ -103,7 +132,11 @@ __device__ __forceinline__ bool mt_test(const Ray& r, const TriRec* __restrict__
 }
 
 struct Bvh {
+#if RT_WIDE
     const BNode4* __restrict__ nodes;
+#else
+    const BNode* __restrict__ nodes;
+#endif
     const TriRec* __restrict__ tris;
     int n_prims;
     double origin_limit;   // |o_i| bound for the FP32 filter (else the FP64 one)
@@ -117,9 +150,9 @@ __device__ __forceinline__ void cx(float& ta, int& ra, float& tb, int& rb) {
     }
 }
 
-// Closest (ANY=false) or first (ANY=true) hit with t in (tmin, tmax) over the
-// 4-wide BVH.  Returns the global prim id, -1 on a miss, -2 on stack overflow;
-// *t_out the hit distance.  Children are visited nearest-first.
+// Closest (ANY=false) or first (ANY=true) hit with t in (tmin, tmax).
+// Returns the global prim id, -1 on a miss, -2 on stack overflow; *t_out
+// the hit distance.  Children are visited nearest-first.
 template <bool ANY>
 __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, double* t_out,
                      int* visits = nullptr, int* tests = nullptr) {
@@ -132,31 +165,21 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
     const float tmin_f = __double2float_rd(tmin);
     const bool fast = fmax(fmax(fabs(r.ox), fabs(r.oy)), fabs(r.oz)) <= bvh.origin_limit;
     int best_prim = -1;
-    int cur = 0;   // root: BVH4 node 0
+    int cur = 0;   // root node 0
     int nv = 0, nt = 0;
     while (true) {
         if (!ref_is_leaf(cur)) {
+            ++nv;
+#if RT_WIDE
             const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
             float4 lx = __ldg(np), ly = __ldg(np + 1), lz = __ldg(np + 2);
             float4 hx = __ldg(np + 3), hy = __ldg(np + 4), hz = __ldg(np + 5);
             int4 ch = __ldg(reinterpret_cast<const int4*>(np + 6));
-            ++nv;
             float t0, t1, t2, t3;
-            bool h0, h1, h2, h3;
-            if (fast) {
-                h0 = slab32(r, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, tmin_f, best_tf, t0);
-                h1 = slab32(r, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, tmin_f, best_tf, t1);
-                h2 = slab32(r, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, tmin_f, best_tf, t2);
-                h3 = slab32(r, lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, tmin_f, best_tf, t3);
-            } else {
-                double d0, d1, d2, d3;
-                h0 = slab(r, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, tmin, best_t, d0);
-                h1 = slab(r, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, tmin, best_t, d1);
-                h2 = slab(r, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, tmin, best_t, d2);
-                h3 = slab(r, lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, tmin, best_t, d3);
-                t0 = __double2float_rd(d0); t1 = __double2float_rd(d1);
-                t2 = __double2float_rd(d2); t3 = __double2float_rd(d3);
-            }
+            bool h0 = box_hit(r, fast, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, tmin, best_t, tmin_f, best_tf, t0);
+            bool h1 = box_hit(r, fast, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, tmin, best_t, tmin_f, best_tf, t1);
+            bool h2 = box_hit(r, fast, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, tmin, best_t, tmin_f, best_tf, t2);
+            bool h3 = box_hit(r, fast, lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, tmin, best_t, tmin_f, best_tf, t3);
             const float INF = __int_as_float(0x7f800000);
             int r0 = ch.x, r1 = ch.y, r2 = ch.z, r3 = ch.w;
             if (!h0 || r0 == EMPTY_REF) t0 = INF;
@@ -165,8 +188,7 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
             if (!h3 || r3 == EMPTY_REF) t3 = INF;
             int nh = (t0 != INF) + (t1 != INF) + (t2 != INF) + (t3 != INF);
             if (nh > 0) {
-                // 5-comparator sorting network, nearest first
-                cx(t0, r0, t1, r1);
+                cx(t0, r0, t1, r1);   // 5-comparator sorting network, nearest first
                 cx(t2, r2, t3, r3);
                 cx(t0, r0, t2, r2);
                 cx(t1, r1, t3, r3);
@@ -178,6 +200,31 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
                 cur = r0;
                 continue;
             }
+#else
+            const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
+            float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
+            int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
+            float tn0, tn1;
+            bool h0 = box_hit(r, fast, a.x, a.y, a.z, a.w, b.x, b.y, tmin, best_t, tmin_f, best_tf, tn0);
+            bool h1 = box_hit(r, fast, b.z, b.w, c.x, c.y, c.z, c.w, tmin, best_t, tmin_f, best_tf, tn1);
+            if (h0 && h1) {
+                int nearc = ch.x, farc = ch.y;
+                float tf = tn1;
+                if (tn1 < tn0) { nearc = ch.y; farc = ch.x; tf = tn0; }
+                if (sp >= STACK_SIZE) { *t_out = -1.0; return -2; }   // reported as an error
+                stack[sp] = farc;
+                stack_t[sp] = tf;
+                ++sp;
+                cur = nearc;
+                continue;
+            } else if (h0) {
+                cur = ch.x;
+                continue;
+            } else if (h1) {
+                cur = ch.y;
+                continue;
+            }
+#endif
         } else {
             int first = leaf_first(cur), cnt = leaf_count(cur);
             nt += cnt;

@@ -220,3 +220,30 @@ def test_coverage_matches_oracle_city_subset(P):
     assert np.array_equal(cm.gains == 0.0, want == 0.0)
     nz = want > 0
     assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz])
+
+
+def test_axis_parallel_rays_match_oracle(P):
+    """Rays with exactly-zero direction components (d = +-x/y/z and in-plane
+    diagonals) from inside and outside boxes: the FP32 box filter must not cull."""
+    import oracle as O
+    from paper_2303_11103_b200 import scenes
+    sc = scenes.city(n_side=4, seed=3)
+    b = _bvh(P, sc)
+    ob = O.Bvh(O.SceneArrays(sc))
+    rng = np.random.RandomState(7)
+    base = rng.uniform(-60, 60, (4000, 3))
+    base[:, 2] = rng.uniform(0.5, 45, 4000)
+    axes = np.array([[1, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1],
+                     [1, 1, 0], [1, 0, -1], [0, 1, 1]], dtype=float)
+    axes /= np.linalg.norm(axes, axis=1)[:, None]
+    o = np.repeat(base, len(axes), axis=0)
+    d = np.tile(axes, (len(base), 1))
+    t, p = b.trace(o, d)
+    ot, op = ob.trace(o, d, 1e-4, np.inf)
+    assert np.array_equal(p.cpu().numpy(), op)
+    hit = op >= 0
+    assert np.array_equal(t.cpu().numpy()[hit], ot[hit])
+    q = o + d * 30.0
+    occ = b.occluded_batch(o, q).cpu().numpy()
+    want = np.array([ob.occluded(a, c) for a, c in zip(o[:3000], q[:3000])])
+    assert np.array_equal(occ[:3000] == 1, want)
