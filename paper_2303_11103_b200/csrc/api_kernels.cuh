@@ -19,7 +19,7 @@ __global__ void k_trace_batch(Bvh bvh, const double* o, const double* d, const d
     if (i >= n) return;
     Ray r = make_ray(ld3(o + 3 * i), ld3(d + 3 * i));
     double t;
-    int p = trace<ANY>(bvh, r, tmin[i], tmax[i], &t);
+    int p = trace_ray<ANY>(bvh, r, tmin[i], tmax[i], &t);
     if (p == -2) { atomicOr((unsigned long long*)err, 1ULL); p = -1; }
     prim_out[i] = p;
     t_out[i] = p >= 0 ? t : __longlong_as_double(0x7ff0000000000000LL);

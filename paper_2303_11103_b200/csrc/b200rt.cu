@@ -566,14 +566,15 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         P.normals = ctx->nrm.get<double>();
         P.bounces = reinterpret_cast<unsigned long long*>(ctr + 2);
         P.error = reinterpret_cast<int*>(ctx->dflag.get<long long>());
-        long long blocks = std::min<long long>((span + 255) / 256, (long long)ctx->n_sm * 16);
+        const int LB = RT_LAUNCH_BLOCK;
+        long long blocks = std::min<long long>((span + LB - 1) / LB, (long long)ctx->n_sm * (4096 / LB));
         P.node_visits = reinterpret_cast<unsigned long long*>(ctr + 3);
         P.tri_tests = reinterpret_cast<unsigned long long*>(ctr + 4);
         PROF_BEGIN(ST_LAUNCH);
         if (span > 0) {
             unsigned g = (unsigned)std::max<long long>(blocks, 1);
-            if (ctx->prof & 2) k_launch<true><<<g, 256, 0, st>>>(bvh_dev(ctx), P, T);
-            else k_launch<false><<<g, 256, 0, st>>>(bvh_dev(ctx), P, T);
+            if (ctx->prof & 2) k_launch<true><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
+            else k_launch<false><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
             CKL();
         }
         PROF_END(ST_LAUNCH);

@@ -104,7 +104,13 @@ __device__ inline d3 fib_dir(long long i, long long n) {
 }
 
 template <bool COUNT>
-__global__ void __launch_bounds__(256) k_launch(Bvh bvh, LaunchParams P, Trie T) {
+#ifndef RT_LAUNCH_BLOCK
+#define RT_LAUNCH_BLOCK 256
+#endif
+#ifndef RT_LAUNCH_MINB
+#define RT_LAUNCH_MINB 3   // <= 85 registers: 24 resident warps per SM (measured best)
+#endif
+__global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh bvh, LaunchParams P, Trie T) {
     const unsigned FULL = 0xffffffffu;
     int lane = threadIdx.x & 31;
     unsigned long long my_bounces = 0, my_nodes = 0, my_tris = 0;
@@ -131,12 +137,12 @@ __global__ void __launch_bounds__(256) k_launch(Bvh bvh, LaunchParams P, Trie T)
                 Ray r = make_ray(o, d);
                 if (COUNT) {
                     int nv = 0, nt = 0;
-                    prim = trace<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t,
+                    prim = trace_ray<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t,
                                         &nv, &nt);
                     my_nodes += nv;
                     my_tris += nt;
                 } else {
-                    prim = trace<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t);
+                    prim = trace_ray<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t);
                 }
                 ++my_bounces;
                 if (prim == -2) { atomicOr(P.error, 1); prim = -1; }

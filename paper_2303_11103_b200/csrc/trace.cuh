@@ -261,6 +261,112 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
     return best_prim;
 }
 
+#if !RT_WIDE
+// "while-while" form of the binary traversal (Aila & Laine 2009): a lane
+// descends internal nodes until it reaches a leaf, then the warp runs leaf
+// tests together, instead of alternating node and FP64 triangle work per
+// iteration.  Same visit order and results as trace<>.
+template <bool ANY>
+__device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, double* t_out,
+                        int* visits = nullptr, int* tests = nullptr) {
+    if (bvh.n_prims == 0) return -1;
+    int stack[STACK_SIZE];
+    float stack_t[STACK_SIZE];
+    int sp = 0;
+    double best_t = tmax;
+    float best_tf = __double2float_ru(tmax);
+    const float tmin_f = __double2float_rd(tmin);
+    const bool fast = fmax(fmax(fabs(r.ox), fabs(r.oy)), fabs(r.oz)) <= bvh.origin_limit;
+    int best_prim = -1;
+    int cur = 0;
+    int nv = 0, nt = 0;
+    bool alive = true;
+    while (alive) {
+        while (!ref_is_leaf(cur)) {
+            ++nv;
+            const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
+            float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
+            int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
+            float tn0, tn1;
+            bool h0 = box_hit(r, fast, a.x, a.y, a.z, a.w, b.x, b.y, tmin, best_t, tmin_f, best_tf, tn0);
+            bool h1 = box_hit(r, fast, b.z, b.w, c.x, c.y, c.z, c.w, tmin, best_t, tmin_f, best_tf, tn1);
+            if (h0 && h1) {
+                int nearc = ch.x, farc = ch.y;
+                float tf = tn1;
+                if (tn1 < tn0) { nearc = ch.y; farc = ch.x; tf = tn0; }
+                if (sp >= STACK_SIZE) { *t_out = -1.0; return -2; }   // reported as an error
+                stack[sp] = farc;
+                stack_t[sp] = tf;
+                ++sp;
+                cur = nearc;
+            } else if (h0) {
+                cur = ch.x;
+            } else if (h1) {
+                cur = ch.y;
+            } else {
+                bool found = false;
+                while (sp > 0) {
+                    --sp;
+                    if (stack_t[sp] <= best_tf) { cur = stack[sp]; found = true; break; }
+                }
+                if (!found) { alive = false; break; }
+            }
+        }
+        if (!alive) break;
+        int first = leaf_first(cur), cnt = leaf_count(cur);
+        nt += cnt;
+        for (int k = 0; k < cnt; ++k) {
+            const TriRec* tp = bvh.tris + first + k;
+            double t;
+            if (mt_test(r, tp, tmin, best_t, t)) {
+                int prim = __ldg(&tp->prim);
+                if (tmin < t && (t < best_t || (t == best_t && best_prim >= 0 && prim < best_prim))) {
+                    best_t = t;
+                    best_tf = __double2float_ru(t);
+                    best_prim = prim;
+                    if (ANY) {
+                        *t_out = t;
+                        if (visits) *visits = nv;
+                        if (tests) *tests = nt;
+                        return prim;
+                    }
+                }
+            }
+        }
+        bool found = false;
+        while (sp > 0) {
+            --sp;
+            if (stack_t[sp] <= best_tf) { cur = stack[sp]; found = true; break; }
+        }
+        if (!found) break;
+    }
+    *t_out = best_t;
+    if (visits) *visits = nv;
+    if (tests) *tests = nt;
+    return best_prim;
+}
+#endif
+
+// measured on C3: while-while wins for the any-hit occlusion queries
+// (7.4 vs 8.4 ms) and loses slightly for the launch's closest-hit (36.0 vs 35.3 ms)
+#ifndef RT_WW_ANY
+#define RT_WW_ANY 1
+#endif
+#ifndef RT_WW_CLOSEST
+#define RT_WW_CLOSEST 0
+#endif
+
+// the traversal the kernels call
+template <bool ANY>
+__device__ __forceinline__ int trace_ray(const Bvh& bvh, const Ray& r, double tmin, double tmax,
+                                         double* t_out, int* visits = nullptr, int* tests = nullptr) {
+#if !RT_WIDE
+    if ((ANY && RT_WW_ANY) || (!ANY && RT_WW_CLOSEST))
+        return trace_ww<ANY>(bvh, r, tmin, tmax, t_out, visits, tests);
+#endif
+    return trace<ANY>(bvh, r, tmin, tmax, t_out, visits, tests);
+}
+
 // Bvh.occluded (bvh.py:103-115): 1 blocked, 0 clear, -1 coincident endpoints
 __device__ inline int occluded(const Bvh& bvh, d3 p, d3 q, double eps = RAY_EPS) {
     double dx = q.x - p.x, dy = q.y - p.y, dz = q.z - p.z;
@@ -269,7 +375,7 @@ __device__ inline int occluded(const Bvh& bvh, d3 p, d3 q, double eps = RAY_EPS)
     double inv = 1.0 / dist;
     Ray r = make_ray(p, d3{dx * inv, dy * inv, dz * inv});
     double t;
-    int h = trace<true>(bvh, r, eps, dist - eps, &t);
+    int h = trace_ray<true>(bvh, r, eps, dist - eps, &t);
     return h >= 0 ? 1 : (h == -2 ? 1 : 0);
 }
 
