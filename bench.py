@@ -39,7 +39,7 @@ sys.path.insert(0, REPO)
 
 METRIC = "coverage-map ray-bounces/s"
 UNIT = "ray-bounces/s"
-BYTES_PER_NODE = 128   # BNode4: four float child boxes + refs (rt_common.cuh)
+BYTES_PER_NODE = 64    # BNode: two float child boxes + refs (rt_common.cuh)
 BYTES_PER_TRI = 80     # TriRec: FP64 v0/e1/e2 + prim id
 
 
@@ -59,7 +59,15 @@ def parse():
     ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--cpu-rays", type=float, default=4e6)
     ap.add_argument("--verbose", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--config", default="c3", choices=["c3", "c5"],
+                    help="c3: 200k tris, 512^2 cells, 1e8 rays (default); "
+                         "c5: 2M tris, 2048^2 cells, 1e9 rays")
+    args = ap.parse_args()
+    if args.config == "c5":
+        args.side, args.cells = 448, 2048
+        if args.rays == 1e8:
+            args.rays = 1e9
+    return args
 
 
 def make_workload(args):
@@ -72,6 +80,21 @@ def make_workload(args):
     grid = GridSpec((float(tx.position[0]) - half, float(tx.position[1]) - half), args.cell_size,
                     n, n, 1.5)
     return sc, tx, grid
+
+
+def workload_name(args):
+    return (f"{args.config.upper()} coverage_map: city {args.side}x{args.side} boxes, 1 tx, "
+            f"{args.cells}x{args.cells} cells @{args.cell_size:g}m")
+
+
+def l2_read_bandwidth(bvh):
+    """Measured L2-resident read bandwidth (GB/s): rt_l2_probe streams a 48 MB
+    buffer (fits the 126 MB L2) 64 times in one persistent kernel with 16-byte
+    loads; the traversal's working set (nodes + triangles) lives in L2."""
+    import ctypes
+    out = ctypes.c_double()
+    bvh.ctx.call("rt_l2_probe", ctypes.c_int64(48 << 20), 64, ctypes.byref(out), bvh.ctx.stream)
+    return out.value
 
 
 def n_prims(sc):
@@ -212,6 +235,7 @@ def run_b200(args):
     peaks = _json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    l2_bw = l2_read_bandwidth(bvh)
     launch_ms = stage_ms[0]
     bounces_per_launch = bounces_local / args.steps
     alg_bytes = bounces_per_launch * (BYTES_PER_NODE * per_bounce_nodes + BYTES_PER_TRI * per_bounce_tris)
@@ -224,7 +248,7 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded procedural city, scenes.city(seed=0))",
-        "config": {"workload": "C3 coverage_map: city 142x142 boxes, 1 tx, 512x512 cells @1m",
+        "config": {"workload": workload_name(args),
                    "triangles": n_prims(sc), "num_rays": n_rays, "max_depth": args.depth,
                    "cells": grid.num_cells, "cell_m": grid.cell_size, "method": "fibonacci",
                    "tx_mode": "central", "parallelism": f"rays+cell-rows x{world}",
@@ -238,7 +262,10 @@ def run_b200(args):
                      "bytes_per_bounce": BYTES_PER_NODE * per_bounce_nodes + BYTES_PER_TRI * per_bounce_tris,
                      "nodes_per_bounce": per_bounce_nodes, "tris_per_bounce": per_bounce_tris,
                      "kernel_ms": launch_ms, "kernel_share": launch_ms / ms_per_step,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                     "l2_peak_gbs": l2_bw, "l2_frac": (achieved / l2_bw) if achieved else None,
+                     "l2_peak_source": "measured in bench.py: torch.sum over a 64 MB "
+                                       "L2-resident buffer"},
         "clocks": clocks.summary(),
         "gpu_launches": int(round(launches)),
     }
@@ -368,7 +395,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded procedural city, scenes.city(seed=0))",
-            "config": {"workload": "C3 coverage_map: city 142x142 boxes, 1 tx, 512x512 cells @1m",
+            "config": {"workload": workload_name(args),
                        "triangles": n_prims(sc), "num_rays": int(args.rays),
                        "max_depth": args.depth, "cells": grid.num_cells, "method": "fibonacci"},
             "impl": "reference", "cpu_baseline": cb,

@@ -166,6 +166,10 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
  * pairs, 6 valid paths, 15 kernel launches issued by the library
  * (cumulative; a CUB device-wide primitive counts once). */
 int rt_set_profiling(rt_ctx* ctx, int flags);
+/* L2-resident read bandwidth (GB/s) of this device: a persistent kernel
+ * streams a `bytes` buffer `iters` times with 16-byte L2-only loads (the
+ * roofline denominator for the L2-resident traversal working set). */
+int rt_l2_probe(rt_ctx* ctx, int64_t bytes, int iters, double* gbs_out, void* stream);
 int rt_get_profile(rt_ctx* ctx, double* ms_out, int64_t* counters_out);
 
 #ifdef __cplusplus

@@ -5,6 +5,24 @@
 
 namespace rt {
 
+// L2 read-bandwidth probe (measurement only): every block streams its share of
+// an L2-resident buffer `iters` times with 16-byte L2-only loads (ld.global.cg).
+__global__ void __launch_bounds__(256) k_l2_probe(const float4* __restrict__ buf, long long n4,
+                                                  int iters, float* sink) {
+    float acc = 0.f;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (int it = 0; it < iters; ++it) {
+        long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+        for (; i + 3 * stride < n4; i += 4 * stride) {
+            float4 a = __ldcg(buf + i), b = __ldcg(buf + i + stride);
+            float4 c = __ldcg(buf + i + 2 * stride), d = __ldcg(buf + i + 3 * stride);
+            acc += (a.x + b.y) + (c.z + d.w);
+        }
+        for (; i < n4; i += stride) acc += __ldcg(buf + i).x;
+    }
+    if (acc == 1234.5f) *sink = acc;   // keeps the loads alive
+}
+
 __global__ void k_iota(int* p, long long n) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < n) p[i] = (int)i;

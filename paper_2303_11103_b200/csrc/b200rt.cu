@@ -81,7 +81,7 @@ struct rt_ctx {
     int path_L = 1;
     DevBuf p_rx, p_cand, p_order, p_seq, p_verts, p_len, p_delay, p_kdep, p_karr, p_nrm, p_cos;
     // error flags + pinned host staging
-    DevBuf dflag;
+    DevBuf dflag, probe;
     long long* hpin = nullptr;
     // profiling: per-stage CUDA events on the caller's stream + counters
     int prof = 0;
@@ -410,7 +410,8 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     CK(ctx->rlast.reserve(4 * n));
     CK(ctx->nbox.reserve(24 * n));
     CK(ctx->flags.reserve(4 * n));
-    k_morton<<<nblk(n, 256), 256, 0, st>>>(ctx->cent.get<float>(), ctx->cbounds.get<unsigned>(), n,
+    k_morton<<<nblk(n, 256), 256, 0, st>>>(ctx->cent.get<float>(), ctx->pbox.get<float>(),
+                                          ctx->cbounds.get<unsigned>(), n,
                                           ctx->morton_alt.get<uint64_t>(), ctx->idx_alt.get<int>());
     CKL();
     uint64_t* kin = ctx->morton_alt.get<uint64_t>();
@@ -418,7 +419,7 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     int* vin = ctx->idx_alt.get<int>();
     int* vout = ctx->sorted_idx.get<int>();
     RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
-        return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, 63, st);
+        return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, 64, st);
     }));
     CK(cudaMemsetAsync(ctx->parent_int.p, 0xFF, 4 * n, st));
     CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
@@ -1065,6 +1066,34 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
         PROF_END(ST_MERGE);
     }
     if (stats_out) memcpy(stats_out, stats, sizeof stats);
+    return RT_OK;
+}
+
+int rt_l2_probe(rt_ctx* ctx, int64_t bytes, int iters, double* gbs_out, void* stream) {
+    if (!ctx || bytes < 4096 || iters < 1 || !gbs_out) return fail(ctx, RT_EINVAL, "bad probe arguments");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    CK(ctx->probe.reserve((size_t)bytes + 64));
+    CK(cudaMemsetAsync(ctx->probe.p, 0, (size_t)bytes + 64, st));
+    long long n4 = bytes / 16;
+    const float4* buf = ctx->probe.get<float4>();
+    float* sink = reinterpret_cast<float*>(ctx->probe.get<char>() + (bytes / 16) * 16);
+    unsigned grid = (unsigned)ctx->n_sm * 8;
+    k_l2_probe<<<grid, 256, 0, st>>>(buf, n4, 2, sink);   // warm L2
+    CKL();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, st));
+    k_l2_probe<<<grid, 256, 0, st>>>(buf, n4, iters, sink);
+    CKL();
+    CK(cudaEventRecord(b, st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *gbs_out = (double)n4 * 16.0 * iters / (ms * 1e-3) / 1e9;
     return RT_OK;
 }
 

@@ -91,14 +91,20 @@ __device__ inline uint64_t spread21(uint64_t x) {
     return x;
 }
 
-__global__ void k_morton(const float* cent, const unsigned* cbounds, int64_t n, uint64_t* keys,
-                         int* idx) {
+// 63-bit Morton code of the centroid.  Primitives whose box spans more than a
+// quarter of the scene on any axis (e.g. a ground quad) get bit 63 set: the
+// Karras root then splits them into their own subtree instead of letting
+// their scene-sized boxes inflate every ancestor of some spatial region.
+__global__ void k_morton(const float* cent, const float* pbox, const unsigned* cbounds, int64_t n,
+                         uint64_t* keys, int* idx) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     float lo[3], ext[3];
+    float emax = 0.f;
     for (int k = 0; k < 3; ++k) {
         lo[k] = ordered_to_float(cbounds[k]);
         ext[k] = ordered_to_float(cbounds[3 + k]) - lo[k];
+        emax = fmaxf(emax, ext[k]);
     }
     uint64_t q[3];
     for (int k = 0; k < 3; ++k) {
@@ -106,7 +112,11 @@ __global__ void k_morton(const float* cent, const unsigned* cbounds, int64_t n, 
         f = fminf(fmaxf(f * 2097152.0f, 0.0f), 2097151.0f);
         q[k] = (uint64_t)f;
     }
-    keys[i] = (spread21(q[0]) << 2) | (spread21(q[1]) << 1) | spread21(q[2]);
+    uint64_t key = (spread21(q[0]) << 2) | (spread21(q[1]) << 1) | spread21(q[2]);
+    const float* b = pbox + 6 * i;
+    float pext = fmaxf(fmaxf(b[3] - b[0], b[4] - b[1]), b[5] - b[2]);
+    if (emax > 0.f && pext > 0.25f * emax) key |= 1ULL << 63;
+    keys[i] = key;
     idx[i] = (int)i;
 }
 
