@@ -264,8 +264,10 @@ def run_b200(args):
                      "kernel_ms": launch_ms, "kernel_share": launch_ms / ms_per_step,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "l2_peak_gbs": l2_bw, "l2_frac": (achieved / l2_bw) if achieved else None,
-                     "l2_peak_source": "measured in bench.py: torch.sum over a 64 MB "
-                                       "L2-resident buffer"},
+                     "l2_peak_source": "measured in bench.py: rt_l2_probe streams a 48 MB "
+                                       "L2-resident buffer with 16-byte L2-only loads",
+                     "north_star_roofline": "T* = max(bytes/BW_L2, FP32 flops/peak); "
+                                            "frac = T*/T_kernel = l2_frac (L1 hits let it exceed 1)"},
         "clocks": clocks.summary(),
         "gpu_launches": int(round(launches)),
     }

@@ -155,7 +155,11 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
                 unsigned peers = __match_any_sync(amask, key);
                 int leader = __ffs(peers) - 1;
                 int id = 0;
+#ifndef RT_NO_TRIE
                 if (lane == leader) id = trie_insert(T, parent, prim, k + 1);
+#else
+                id = 1;   // timing experiment only: traversal without candidate bookkeeping
+#endif
                 id = __shfl_sync(peers, id, leader);
                 if (id < 0) { active = false; }
                 parent = id;
