@@ -20,6 +20,9 @@
 #ifndef RT_PLOC
 #define RT_PLOC 1   // measured on C3: 30.9 vs 42.2 node visits per bounce (Karras LBVH)
 #endif
+#ifndef RT_DYNAMIC
+#define RT_DYNAMIC 0
+#endif
 #include "solve.cuh"
 
 using namespace rt;
@@ -268,6 +271,8 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st) {
     return RT_OK;
 }
 
+int build_karras(rt_ctx* ctx, long long n, const uint64_t* kout, const int* vout, cudaStream_t st);
+
 // PLOC hierarchy over the Morton-sorted prims (sorted_idx), then the
 // depth-first child-pair layout + triangle records (bvh_ploc.cuh)
 int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
@@ -495,10 +500,15 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
         return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, 64, st);
     }));
-    if (RT_PLOC) {   // default: PLOC hierarchy (LBVH below is kept for A/B builds)
-        RC(build_ploc(ctx, n, st));
-        return RT_WIDE ? collapse4(ctx, n - 1, st) : RT_OK;
-    }
+    RC(RT_PLOC ? build_ploc(ctx, n, st) : build_karras(ctx, n, kout, vout, st));
+    return RT_WIDE ? collapse4(ctx, n - 1, st) : RT_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// Karras (2012) LBVH hierarchy from the sorted Morton keys (A/B alternative to PLOC)
+int build_karras(rt_ctx* ctx, long long n, const uint64_t* kout, const int* vout, cudaStream_t st) {
     CK(cudaMemsetAsync(ctx->parent_int.p, 0xFF, 4 * n, st));
     CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
     k_karras<<<nblk(n - 1, 256), 256, 0, st>>>(kout, (int)n, ctx->child.get<int>(),
@@ -517,8 +527,11 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     k_sorted_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, vout, ctx->v0.get<double>(), ctx->e1.get<double>(),
                                                 ctx->e2.get<double>(), ctx->tris.get<TriRec>());
     CKL();
-    return RT_WIDE ? collapse4(ctx, n - 1, st) : RT_OK;
+    return RT_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int rt_scene_arrays(rt_ctx* ctx, double* v0, double* e1, double* e2, double* normals,
                     double* plane_offset, void* stream) {
@@ -652,8 +665,15 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         PROF_BEGIN(ST_LAUNCH);
         if (span > 0) {
             unsigned g = (unsigned)std::max<long long>(blocks, 1);
-            if (ctx->prof & 2) k_launch<true><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
-            else k_launch<false><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
+            if (RT_DYNAMIC) {   // persistent grid, dynamic ray fetch from ctr[5]
+                unsigned long long* sc = reinterpret_cast<unsigned long long*>(ctr + 5);
+                unsigned gp = (unsigned)std::min<long long>(g, (long long)ctx->n_sm * RT_LAUNCH_MINB);
+                if (ctx->prof & 2) k_launch_dyn<true><<<gp, LB, 0, st>>>(bvh_dev(ctx), P, T, sc);
+                else k_launch_dyn<false><<<gp, LB, 0, st>>>(bvh_dev(ctx), P, T, sc);
+            } else {
+                if (ctx->prof & 2) k_launch<true><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
+                else k_launch<false><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
+            }
             CKL();
         }
         PROF_END(ST_LAUNCH);
