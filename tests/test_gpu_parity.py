@@ -247,3 +247,32 @@ def test_axis_parallel_rays_match_oracle(P):
     occ = b.occluded_batch(o, q).cpu().numpy()
     want = np.array([ob.occluded(a, c) for a, c in zip(o[:3000], q[:3000])])
     assert np.array_equal(occ[:3000] == 1, want)
+
+
+def test_sionna_facade_paths_cir_coverage_vs_oracle(P):
+    """scene.compute_paths / paths.apply_doppler / paths.cir / scene.coverage_map
+    (the PAPER.md listing) against the oracle on the same emtrace scene."""
+    import oracle as O
+    from test_host_logic import _paper_listing_scene
+    sc = _paper_listing_scene()
+    paths = sc.compute_paths(max_depth=3, num_samples=50_000)
+    a, tau = paths.cir()
+    em = sc._em
+    ob = O.Bvh(O.SceneArrays(em))
+    want = O.compute_paths(em, ob, 3, method="fibonacci", num_rays=50_000)
+    assert [(p.kind, p.seq) for p in paths.paths] == [(p.kind, p.seq) for p in want]
+    oa, otau = O.build_cir(em, O.compute_gains(em, ob, want))
+    assert a.shape == oa.shape == (1, 2, 1, 32, len(want), 1)
+    assert np.abs(a - oa).max() <= 1e-9 * np.abs(oa).max()
+    assert np.allclose(tau, otau, rtol=1e-12, atol=0)
+    paths.apply_doppler(sampling_frequency=1e6, num_time_steps=14, tx_velocities=[3, 0, 0])
+    a2, _ = paths.cir()
+    assert a2.shape[-1] == 14 and np.allclose(np.abs(a2[..., 0]), np.abs(a[..., 0]))
+    cm = sc.coverage_map(max_depth=2, num_samples=20_000, cm_cell_size=(4.0, 4.0),
+                         cm_center=[10.0, 0.0], cm_size=[48.0, 40.0])
+    g = cm.grid
+    ocm = O.coverage_map(em, ob, g.origin, g.cell_size, g.nx, g.ny, g.height, 2,
+                         method="fibonacci", num_rays=20_000)
+    assert np.array_equal(cm.gains == 0.0, ocm == 0.0)
+    nz = ocm > 0
+    assert np.all(np.abs(cm.gains[nz] - ocm[nz]) <= 1e-9 * ocm[nz])

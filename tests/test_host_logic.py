@@ -147,3 +147,34 @@ def test_two_rank_gloo_candidate_gather_and_grid_reduce():
         assert np.array_equal(np.array(s), np.concatenate(local_rows))
         assert np.array_equal(np.array(g)[:, 0], [1.0, 2.0, 3.0, 4.0])
         assert mx == 11.0 and sm == 3.0
+
+
+def _paper_listing_scene():
+    """The PAPER.md listing (tx 8x2 tr38901 VH array, rx dipole cross) on a small city."""
+    from paper_2303_11103_b200 import scenes
+    from paper_2303_11103_b200.sionna import (PlanarArray, RadioMaterial, Receiver, Scene,
+                                              SceneObject, Transmitter)
+    city = scenes.city(n_side=3, seed=5)
+    sc = Scene(frequency=3.5e9, synthetic_array=True)
+    for m in city.materials.values():
+        sc.add(RadioMaterial(m.name, m.eps_r, m.sigma))
+    for o in city.objects:
+        sc.add(SceneObject(o.name, o.vertices, o.triangles, o.material))
+    sc.tx_array = PlanarArray(8, 2, 0.7, 0.5, "tr38901", "VH")
+    sc.rx_array = PlanarArray(1, 1, 0.5, 0.5, "dipole", "cross")
+    tx = Transmitter("tx", position=[2.0, 3.0, 27.0])
+    rx = Receiver("rx", position=[21.0, -14.0, 1.5])
+    sc.add(tx)
+    sc.add(rx)
+    tx.look_at(rx)
+    return sc
+
+
+def test_sionna_facade_compiles_to_emtrace_scene():
+    sc = _paper_listing_scene()
+    em = sc._em
+    assert [d.kind for d in em.devices] == ["tx", "rx"]
+    assert em.tx_array.num_elements == 32 and em.rx_array.num_elements == 2
+    tx = em.devices[0]
+    assert abs(tx.orientation[0] - math.atan2(-17.0, 19.0)) < 1e-12
+    assert sum(len(o.triangles) for o in em.objects) == 2 + 9 * 10
