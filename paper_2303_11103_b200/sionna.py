@@ -121,7 +121,7 @@ class Paths:
 
     def _ensure_gains(self):
         if self._gains is None:
-            self._gains = _em.compute_gains(self._scene._em, self._bvh, self._pathset)
+            self._gains = _em.compute_gains(self._scene, self._bvh, self._pathset)
         return self._gains
 
     def apply_doppler(self, sampling_frequency, num_time_steps, tx_velocities=None,
