@@ -137,6 +137,19 @@ int rt_transfer_bwd(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* ord
                     double wavelength, double frequency_hz, const double* grad_a,
                     double* grad_eta, void* stream);
 
+/* Position / orientation derivatives (em.py:258-312 with tracked positions and
+ * orientations): a[p,s,r] re-derived from per-path tx/rx positions and yaw/
+ * pitch/roll (device [P*3] each; geometry re-solved by mirroring across the
+ * planes through the path's vertices, geometry_for_positions) plus its
+ * Jacobian jac_out [P*S*R*12*2] w.r.t. (tx xyz, rx xyz, tx ypr, rx ypr). */
+int rt_transfer_jvp(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
+                    const int32_t* seq, const double* vertices, const double* normals,
+                    const double* tx_pos, const double* rx_pos, const double* tx_ypr,
+                    const double* rx_ypr, int tx_pattern, int rx_pattern, const double* tx_slants,
+                    int n_tx_slants, const double* rx_slants, int n_rx_slants, const double* eta,
+                    int n_mat, double wavelength, double frequency_hz, double* a_out,
+                    double* jac_out, void* stream);
+
 /* ---- coverage map (channel.py:190-253 point_path_gain / coverage_map) ----
  * Probe receivers at the centers of an nx*ny grid at `height`.  Every cell
  * receives sum_paths sum_{theta,phi probes} |a|^2 over the current candidate

@@ -30,7 +30,7 @@ EXPORTS = [
     "rt_num_prims", "rt_scene_arrays", "rt_trace", "rt_occluded", "rt_launch", "rt_enumerate",
     "rt_candidates_set", "rt_candidates_get", "rt_num_candidates", "rt_candidates_max_len",
     "rt_paths", "rt_paths_get", "rt_transfer", "rt_transfer_bwd", "rt_coverage",
-    "rt_set_profiling", "rt_get_profile", "rt_l2_probe",
+    "rt_set_profiling", "rt_get_profile", "rt_l2_probe", "rt_transfer_jvp",
 ]
 
 _lib = None
@@ -107,6 +107,8 @@ def lib():
             "rt_set_profiling": (i32, [P, i32]),
             "rt_get_profile": (i32, [P, P, P]),
             "rt_l2_probe": (i32, [P, i64, i32, ctypes.POINTER(ctypes.c_double), P]),
+            "rt_transfer_jvp": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, i32, i32, P, i32, P, i32,
+                                      P, i32, f64, f64, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -15,6 +15,7 @@
 #include "api_kernels.cuh"
 #include "bvh_build.cuh"
 #include "bvh_ploc.cuh"
+#include "em_jvp.cuh"
 #include "launch.cuh"
 
 #ifndef RT_PLOC
@@ -1164,6 +1165,29 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
         PROF_END(ST_MERGE);
     }
     if (stats_out) memcpy(stats_out, stats, sizeof stats);
+    return RT_OK;
+}
+
+int rt_transfer_jvp(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
+                    const int32_t* seq, const double* vertices, const double* normals,
+                    const double* tx_pos, const double* rx_pos, const double* tx_ypr,
+                    const double* rx_ypr, int tx_pattern, int rx_pattern, const double* tx_slants,
+                    int n_tx_slants, const double* rx_slants, int n_rx_slants, const double* eta,
+                    int n_mat, double wavelength, double frequency_hz, double* a_out,
+                    double* jac_out, void* stream) {
+    if (!ctx || n_paths < 0 || max_len < 1 || n_tx_slants < 1 || n_rx_slants < 1)
+        return fail(ctx, RT_EINVAL, "bad transfer arguments");
+    if (tx_pattern < 0 || tx_pattern > 4 || rx_pattern < 0 || rx_pattern > 4)
+        return fail(ctx, RT_EINVAL, "unknown antenna pattern");
+    if (n_paths == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    (void)n_mat;
+    JvpArgs A{n_paths, max_len, (const signed char*)order, seq, vertices, normals, tx_pos, rx_pos,
+              tx_ypr, rx_ypr, tx_pattern, rx_pattern, tx_slants, n_tx_slants, rx_slants,
+              n_rx_slants, eta, ctx->prim_mat.get<int>(), wavelength, frequency_hz};
+    long long n = n_paths * n_tx_slants * NJ;
+    k_transfer_jvp<<<nblk(n, 64), 64, 0, ST(stream)>>>(A, a_out, jac_out);
+    CKL();
     return RT_OK;
 }
 

@@ -176,6 +176,78 @@ def path_coefficients(bvh, T: PathTable, eta, tx_rows, rx_rows, tx_pattern, rx_p
                                   float(frequency))
 
 
+def rows_from_ypr(ypr):
+    """rotation_entries (geometry.py:50-59) for a [P, 3] tensor -> [P, 9] (no grad)."""
+    y, p, r = ypr.detach()[:, 0], ypr.detach()[:, 1], ypr.detach()[:, 2]
+    cy, sy, cp, sp, cr, sr = torch.cos(y), torch.sin(y), torch.cos(p), torch.sin(p), torch.cos(r), torch.sin(r)
+    return torch.stack([cy * cp, cy * sp * sr - sy * cr, cy * sp * cr + sy * sr,
+                        sy * cp, sy * sp * sr + cy * cr, sy * sp * cr - cy * sr,
+                        -sp, cp * sr, cp * cr], dim=1).contiguous()
+
+
+class PathCoefficientsGeo(torch.autograd.Function):
+    """a[p, s, r] (complex) as a function of per-path tx/rx positions and
+    yaw/pitch/roll ([P, 3] each) and eta ([n_mat, 2]).
+
+    forward = rt_transfer_jvp (geometry re-derived by mirroring through the
+    path's planes, em.py:258-282, and its forward-mode Jacobian w.r.t. the 12
+    device parameters); backward contracts the Jacobian with the upstream
+    gradient, and runs the hand-written eta adjoint (rt_transfer_bwd)."""
+
+    @staticmethod
+    def forward(ctx, tx_pos, rx_pos, tx_ypr, rx_ypr, eta, bvh, T, tx_pat, rx_pat, st, sr,
+                wavelength, frequency):
+        P = T.n
+        dev = bvh.device
+        a = torch.empty((P, len(st), len(sr), 2), dtype=torch.float64, device=dev)
+        jac = torch.empty((P, len(st), len(sr), 12, 2), dtype=torch.float64, device=dev)
+        ins = [t.detach().contiguous().to(torch.float64) for t in (tx_pos, rx_pos, tx_ypr, rx_ypr)]
+        eta_c = eta.detach().contiguous()
+        if P:
+            stt = torch.tensor(st, dtype=torch.float64, device=dev)
+            srt = torch.tensor(sr, dtype=torch.float64, device=dev)
+            with torch.cuda.device(dev):
+                bvh.ctx.call("rt_transfer_jvp", P, T.L, N.ptr(T.order), N.ptr(T.seq), N.ptr(T.verts),
+                             N.ptr(T.normals), *[N.ptr(t) for t in ins], tx_pat, rx_pat, N.ptr(stt),
+                             len(st), N.ptr(srt), len(sr), N.ptr(eta_c), eta_c.shape[0],
+                             float(wavelength), float(frequency), N.ptr(a), N.ptr(jac),
+                             bvh.ctx.stream, exc_map={N.RT_EINVAL: EmError})
+        ctx.save_for_backward(jac, eta_c, ins[2], ins[3])
+        ctx.args = (bvh, T, tx_pat, rx_pat, st, sr, wavelength, frequency)
+        return torch.view_as_complex(a)
+
+    @staticmethod
+    def backward(ctx, grad_a):
+        jac, eta, tx_ypr, rx_ypr = ctx.saved_tensors
+        bvh, T, tx_pat, rx_pat, st, sr, wavelength, frequency = ctx.args
+        g = torch.view_as_real(grad_a.contiguous().to(torch.complex128))      # [P, S, R, 2]
+        gp = (g[:, :, :, None, :] * jac).sum(-1).sum((1, 2))                    # [P, 12]
+        grad_eta = None
+        if ctx.needs_input_grad[4] and T.n:
+            grad_eta = PathCoefficients.backward(
+                _EtaCtx(eta, (bvh, T, rows_from_ypr(tx_ypr), rows_from_ypr(rx_ypr), tx_pat, rx_pat,
+                              st, sr, wavelength, frequency)), grad_a)[0]
+        return (gp[:, 0:3], gp[:, 3:6], gp[:, 6:9], gp[:, 9:12], grad_eta) + (None,) * 8
+
+
+class _EtaCtx:
+    """Minimal stand-in for an autograd ctx to reuse PathCoefficients.backward."""
+
+    def __init__(self, eta, args):
+        self.saved_tensors = (eta,)
+        self.args = args
+
+
+def path_coefficients_geo(bvh, T: PathTable, eta, tx_pos, rx_pos, tx_ypr, rx_ypr, tx_pattern,
+                          rx_pattern, tx_slants, rx_slants, wavelength, frequency):
+    """Differentiable a[p, s, r] w.r.t. per-path positions / orientations ([P, 3]) and eta."""
+    return PathCoefficientsGeo.apply(tx_pos, rx_pos, tx_ypr, rx_ypr, eta, bvh, T,
+                                     pattern_id(tx_pattern), pattern_id(rx_pattern),
+                                     tuple(float(s) for s in tx_slants),
+                                     tuple(float(s) for s in rx_slants), float(wavelength),
+                                     float(frequency))
+
+
 def eta_from_params(eps_r, sigma, frequency_hz):
     """eta = eps_r - j sigma / (2 pi f eps0) as real pairs (scene.py:99-100); differentiable."""
     return torch.stack([eps_r, sigma * (-eta_scale(frequency_hz))], dim=-1)

@@ -205,6 +205,43 @@ def calib_case():
     print("calib: loss", loss.value, flush=True)
 
 
+def geo_grad_case():
+    """Orientation + position gradients: for every specular
+    path of the small canyon, d|a|^2 / d(tx xyz, rx xyz, tx ypr, rx ypr) of the
+    first element pair through the reference Tape, with tracked positions
+    (path_geometry -> geometry_for_positions, em.py:258-288)."""
+    from emtrace.em import EvalContext, path_geometry, path_materials, transfer
+    sc = to_ref(_canyon_small())
+    tree = accel.build(sc)
+    ps = E.compute_paths(sc, tree, 3, method="fibonacci", num_rays=20000)
+    tx, rx = sc.device("tx"), None
+    rows = []
+    for p in ps.paths:
+        rx = sc.device(p.rx)
+        tape = Tape()
+        tp = tuple(tape.leaf(float(v), f"tx_pos{i}") for i, v in enumerate(tx.position))
+        rp = tuple(tape.leaf(float(v), f"rx_pos{i}") for i, v in enumerate(rx.position))
+        to = tuple(tape.leaf(float(v), f"tx_ypr{i}") for i, v in enumerate(tx.orientation))
+        ro = tuple(tape.leaf(float(v), f"rx_ypr{i}") for i, v in enumerate(rx.orientation))
+        ctx = EvalContext(sc, orientations={tx.name: to, rx.name: ro},
+                          positions={tx.name: tp, rx.name: rp})
+        geom = path_geometry(ctx, p, tx, rx)
+        a = transfer(ctx, geom, path_materials(sc, tree, p), tx, rx, sc.tx_array.pattern,
+                     sc.rx_array.pattern, sc.tx_array.slants[0], sc.rx_array.slants[0])
+        loss = a.abs2()
+        g = tape.gradient(loss)
+        names = ([f"tx_pos{i}" for i in range(3)] + [f"rx_pos{i}" for i in range(3)]
+                 + [f"tx_ypr{i}" for i in range(3)] + [f"rx_ypr{i}" for i in range(3)])
+        rows.append((a.to_complex(), loss.value, [g[n] for n in names]))
+    out = dict(scene=np.array(scene_json(sc)), num_rays=20000, max_depth=3)
+    out.update(pack_paths(ps.paths, 3))
+    out["a"] = np.array([r[0] for r in rows])
+    out["loss"] = np.array([r[1] for r in rows])
+    out["grads"] = np.array([r[2] for r in rows])
+    np.savez_compressed(os.path.join(HERE, "geo_grads.npz"), **out)
+    print("geo_grads:", len(rows), "paths", flush=True)
+
+
 def main(which=None):
     cases = {
         "soup": soup_case,
@@ -230,6 +267,7 @@ def main(which=None):
             coverage=[(GridSpec((-40.0, -8.0), 10.0, 8, 4, 1.5), 2, "fibonacci", 2000,
                        "central")]),
         "calib": calib_case,
+        "geo_grads": geo_grad_case,
     }
     for k, fn in cases.items():
         if which and k not in which:

@@ -276,3 +276,37 @@ def test_sionna_facade_paths_cir_coverage_vs_oracle(P):
     assert np.array_equal(cm.gains == 0.0, ocm == 0.0)
     nz = ocm > 0
     assert np.all(np.abs(cm.gains[nz] - ocm[nz]) <= 1e-9 * ocm[nz])
+
+
+def test_position_orientation_gradients_match_reference_tape(P, golden):
+    """d|a|^2 / d(tx xyz, rx xyz, tx ypr, rx ypr) for every path of the canyon
+    fixture (tr38901 VH tx, tilted dipole-cross rx) vs the reference Tape
+    (north_star: gradients within 1e-3 relative)."""
+    from paper_2303_11103_b200 import em
+    from paper_2303_11103_b200.scene import POLARIZATION_SLANTS
+    g = golden("geo_grads")
+    sc = golden_scene(g)
+    b = _bvh(P, sc)
+    ps = P.compute_paths(sc, b, 3, method="fibonacci", num_rays=int(g["num_rays"]))
+    _check_paths(ps.paths, g)
+    T = ps.table
+    dev = b.device
+    devs = {d.name: d for d in sc.devices}
+    txd = [devs[T.tx_names[i]] for i in T.tx.cpu().numpy()]
+    rxd = [devs[T.rx_names[i]] for i in T.rx.cpu().numpy()]
+    mk = lambda v: torch.tensor(np.array(v, dtype=np.float64), device=dev, requires_grad=True)  # noqa: E731
+    tp, rp = mk([d.position for d in txd]), mk([d.position for d in rxd])
+    to, ro = mk([d.orientation for d in txd]), mk([d.orientation for d in rxd])
+    eta = em.EvalContext(sc).eta_table(b)
+    a = em.path_coefficients_geo(b, T, eta, tp, rp, to, ro, sc.tx_array.pattern,
+                                 sc.rx_array.pattern, [POLARIZATION_SLANTS[sc.tx_array.polarization][0]],
+                                 [POLARIZATION_SLANTS[sc.rx_array.polarization][0]],
+                                 sc.wavelength, sc.frequency_hz)[:, 0, 0]
+    loss = (a.abs() ** 2)
+    assert np.allclose(loss.detach().cpu().numpy(), g["loss"], rtol=1e-9, atol=0)
+    loss.sum().backward()
+    got = torch.cat([tp.grad, rp.grad, to.grad, ro.grad], dim=1).cpu().numpy()
+    want = g["grads"]
+    scale = np.abs(want).max(axis=1, keepdims=True)
+    assert np.all(np.abs(got - want) <= 1e-3 * np.abs(want) + 1e-6 * scale), \
+        np.abs(got - want).max()
