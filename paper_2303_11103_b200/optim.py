@@ -37,7 +37,7 @@ class MaterialProblem:
     """Frozen topology (paths per record) + differentiable loss in (eps_r, sigma)."""
 
     def __init__(self, scene, positions, h_targets, max_depth=2, num_subcarriers=128,
-                 spacing=30e3, method="exhaustive", num_rays=4096, bvh=None):
+                 spacing=30e3, method="exhaustive", num_rays=4096, bvh=None, check_targets=True):
         self.scene = scene
         self.bvh = bvh or build(scene)
         dev = self.bvh.device
@@ -51,6 +51,8 @@ class MaterialProblem:
         self.basis = torch.exp(-2j * math.pi * f[None, :] * self.T.delay[:, None])   # [P, N]
         self.h = torch.as_tensor(np.asarray(h_targets), dtype=torch.complex128, device=dev)
         self.norm2 = (self.h.abs() ** 2).sum(-1)                                      # [R]
+        if check_targets and bool((self.norm2 <= 0.0).any()):
+            raise ValueError("dataset record has zero-norm target response")   # optim.py:347-348
         P = self.T.n
         self.tx_rows = torch.tensor(np.tile(np.asarray(rotation_entries(*tx.orientation)).reshape(9),
                                             (P, 1)), dtype=torch.float64, device=dev)
@@ -73,13 +75,25 @@ class MaterialProblem:
             rows.append(eta_from_params(e, s, f))
         return torch.stack(rows)
 
-    def loss(self, values):
+    def default_values(self):
+        """The scene's own (eps_r, sigma) of every trainable material as tensors."""
+        dev = self.bvh.device
+        return {n: (torch.tensor(float(self.scene.materials[n].eps_r), dtype=torch.float64, device=dev),
+                    torch.tensor(float(self.scene.materials[n].sigma), dtype=torch.float64, device=dev))
+                for n in self.names}
+
+    def responses(self, values):
+        """H_r(f_k) = sum over record r's paths of a_i e^{-j 2 pi f_k tau_i}  [R, N]."""
         sc = self.scene
         a = path_coefficients(self.bvh, self.T, self.eta(values), self.tx_rows, self.rx_rows,
                               sc.tx_array.pattern, sc.rx_array.pattern, [self.tx_slant],
                               [self.rx_slant], sc.wavelength, sc.frequency_hz)[:, 0, 0]
-        pred = torch.zeros_like(self.h)
-        pred.index_add_(0, self.T.rx.long(), a[:, None] * self.basis)
+        pred = torch.zeros((self.R, self.basis.shape[1]), dtype=torch.complex128,
+                           device=self.bvh.device)
+        return pred.index_add(0, self.T.rx.long(), a[:, None] * self.basis)
+
+    def loss(self, values):
+        pred = self.responses(values)
         err = ((pred - self.h).abs() ** 2).sum(-1) / self.norm2
         return err.mean()
 
@@ -102,3 +116,306 @@ def material_loss_and_grad(scene, positions, h_targets, max_depth=2, num_subcarr
         grads[_EPS_KEY.format(n)] = float(e.grad) if e.grad is not None else 0.0
         grads[_SIG_KEY.format(n)] = float(s.grad) if s.grad is not None else 0.0
     return float(loss.detach()), grads
+
+
+# ---------------------------------------------------------------------------------------------
+# Drivers (optim.py:32-460): dataset generation, material learning, orientation ascent.
+# The Armijo step logic, projections, topology refresh and convergence test restate
+# the reference; losses and gradients come from the device (adjoint / JVP kernels).
+
+from dataclasses import dataclass  # noqa: E402
+import json  # noqa: E402
+import warnings  # noqa: E402
+
+
+class OptimError(ValueError):
+    pass
+
+
+@dataclass
+class OptimConfig:
+    lr: float = 0.05
+    lr_sigma: float = 0.005
+    lr_angle: float = 0.2
+    iterations: int = 500
+    line_search: bool = True
+    topology_refresh: int = 10
+    rel_tol: float = 1e-6
+    tol_window: int = 10
+    max_depth: int = 2
+    method: str = "exhaustive"
+    num_rays: int = 4096
+
+
+@dataclass
+class DatasetRecord:
+    position: np.ndarray
+    h: np.ndarray
+
+
+@dataclass
+class Dataset:
+    frequency_hz: float
+    num_subcarriers: int
+    subcarrier_spacing_hz: float
+    records: list
+
+    def save(self, path: str):
+        payload = {"frequency_hz": self.frequency_hz, "num_subcarriers": self.num_subcarriers,
+                   "subcarrier_spacing_hz": self.subcarrier_spacing_hz,
+                   "records": [{"position_m": [float(x) for x in r.position],
+                                "h_re": [float(v) for v in r.h.real],
+                                "h_im": [float(v) for v in r.h.imag]} for r in self.records]}
+        with open(path, "w") as fh:
+            json.dump(payload, fh)
+            fh.write("\n")
+
+    @staticmethod
+    def load(path: str) -> "Dataset":
+        with open(path) as fh:
+            d = json.load(fh)
+        recs = [DatasetRecord(np.asarray(r["position_m"], dtype=np.float64),
+                              np.asarray(r["h_re"]) + 1j * np.asarray(r["h_im"])) for r in d["records"]]
+        return Dataset(d["frequency_hz"], d["num_subcarriers"], d["subcarrier_spacing_hz"], recs)
+
+
+class TrainLog:
+    """Per-iteration loss and leaf values; CSV like the reference (optim.py:87-112)."""
+
+    def __init__(self, leaf_names):
+        self.leaf_names = list(leaf_names)
+        self.rows = []
+        self.final_values = {}
+
+    def append(self, iteration, loss, values):
+        self.rows.append((iteration, loss, dict(values)))
+
+    @property
+    def losses(self):
+        return [r[1] for r in self.rows]
+
+    def to_csv(self) -> str:
+        lines = [",".join(["iteration", "loss"] + self.leaf_names)]
+        for it, loss, vals in self.rows:
+            lines.append(",".join([str(it), repr(loss)] + [repr(vals[n]) for n in self.leaf_names]))
+        return "\n".join(lines) + "\n"
+
+    def save(self, path):
+        with open(path, "w") as fh:
+            fh.write(self.to_csv())
+
+
+def nmse_loss(h_pred, h_true):
+    h_true = np.asarray(h_true, dtype=np.complex128)
+    norm2 = float(np.vdot(h_true, h_true).real)
+    if norm2 <= 0.0:
+        raise OptimError("NMSE target has zero norm")
+    err = np.asarray(h_pred, dtype=np.complex128) - h_true
+    return float(np.vdot(err, err).real) / norm2
+
+
+def _lr_for(leaf, config):
+    if leaf.endswith(":sigma"):
+        return config.lr_sigma
+    if leaf.split(":")[-1] in ("yaw", "pitch", "roll"):
+        return config.lr_angle
+    return config.lr
+
+
+def _project_materials(values):
+    for k in values:
+        if k.endswith(":eps_r") and values[k] < 1.0:
+            values[k] = 1.0
+        elif k.endswith(":sigma") and values[k] < 0.0:
+            values[k] = 0.0
+
+
+def _descend(values, loss0, grads, loss_fn, config, sign, scale=1.0):
+    """Armijo-backtracked step (optim.py:203-234); sign -1 descends, +1 ascends."""
+    direction = {k: _lr_for(k, config) * grads.get(k, 0.0) for k in values}
+    slope = sum(direction[k] * grads.get(k, 0.0) for k in values)
+    if slope == 0.0:
+        return dict(values), scale
+
+    def stepped(s):
+        new = {k: values[k] + sign * s * direction[k] for k in values}
+        _project_materials(new)
+        return new
+
+    if not config.line_search:
+        return stepped(1.0), scale
+    first = True
+    while scale > 1e-10:
+        cand = stepped(scale)
+        f = float(loss_fn(cand))
+        if sign * (f - loss0) >= 1e-4 * scale * slope:
+            return cand, min(scale * 2.0, 1e9) if first else scale
+        scale *= 0.5
+        first = False
+    return dict(values), 1.0
+
+
+def _converged(losses, config):
+    w = config.tol_window
+    if len(losses) <= w:
+        return False
+    ref = abs(losses[-w - 1])
+    if ref == 0.0:
+        return abs(losses[-1]) == 0.0
+    return abs(losses[-1] - losses[-w - 1]) / ref < config.rel_tol
+
+
+def generate_dataset(scene, positions=None, num_subcarriers=128, subcarrier_spacing_hz=30e3,
+                     max_depth=2, method="exhaustive", num_rays=4096, bvh=None) -> Dataset:
+    """Frequency responses at probe positions with the scene's materials (optim.py:261-288)."""
+    bvh = bvh or build(scene)
+    txs = [d for d in scene.devices if d.kind == "tx"]
+    if not txs:
+        raise OptimError("scene has no transmitter")
+    if positions is None:
+        positions = [d.position for d in scene.devices if d.kind == "rx"]
+    if not len(positions):
+        raise OptimError("no probe positions to generate data for")
+    pos = np.asarray(positions, dtype=np.float64).reshape(-1, 3)
+    zero = np.zeros((len(pos), num_subcarriers), dtype=np.complex128)
+    prob = MaterialProblem(scene, pos, zero, max_depth, num_subcarriers, subcarrier_spacing_hz,
+                           method, num_rays, bvh, check_targets=False)
+    with torch.no_grad():
+        h = prob.responses(prob.default_values()).cpu().numpy()
+    return Dataset(scene.frequency_hz, num_subcarriers, subcarrier_spacing_hz,
+                   [DatasetRecord(pos[i].copy(), h[i].copy()) for i in range(len(pos))])
+
+
+def learn_materials(scene, dataset: Dataset, config: OptimConfig | None = None,
+                    bvh=None) -> TrainLog:
+    """Projected gradient descent on the dataset NMSE over trainable materials
+    (optim.py:305-380); gradients from the hand-written adjoint."""
+    config = config or OptimConfig()
+    bvh = bvh or build(scene)
+    names = trainable_material_names(scene)
+    if not names:
+        raise OptimError("scene has no trainable materials")
+    if abs(dataset.frequency_hz - scene.frequency_hz) > 1e-6 * scene.frequency_hz:
+        raise OptimError("dataset and scene carrier frequencies differ")
+    values = {}
+    for n in names:
+        values[f"mat:{n}:eps_r"] = float(scene.materials[n].eps_r)
+        values[f"mat:{n}:sigma"] = float(scene.materials[n].sigma)
+    leaf_names = sorted(values)
+    pos = np.array([r.position for r in dataset.records], dtype=np.float64)
+    h = np.array([r.h for r in dataset.records])
+    dev = bvh.device
+    prob = None
+
+    def as_tensors(vals, grad):
+        return {n: (torch.tensor(vals[f"mat:{n}:eps_r"], dtype=torch.float64, device=dev,
+                                 requires_grad=grad),
+                    torch.tensor(vals[f"mat:{n}:sigma"], dtype=torch.float64, device=dev,
+                                 requires_grad=grad)) for n in names}
+
+    def loss_fn(vals):
+        with torch.no_grad():
+            return float(prob.loss(as_tensors(vals, False)))
+
+    log = TrainLog(leaf_names)
+    scale = 1.0
+    for it in range(config.iterations):
+        if it % config.topology_refresh == 0:
+            prob = MaterialProblem(scene, pos, h, config.max_depth, dataset.num_subcarriers,
+                                   dataset.subcarrier_spacing_hz, config.method, config.num_rays, bvh)
+        tv = as_tensors(values, True)
+        loss = prob.loss(tv)
+        loss_val = float(loss.detach())
+        if not math.isfinite(loss_val):
+            raise OptimError(f"loss diverged (non-finite) at iteration {it}: values {values}")
+        loss.backward()
+        grads = {}
+        for n, (e, s) in tv.items():
+            grads[f"mat:{n}:eps_r"] = float(e.grad) if e.grad is not None else 0.0
+            grads[f"mat:{n}:sigma"] = float(s.grad) if s.grad is not None else 0.0
+        log.append(it, loss_val, values)
+        values, scale = _descend(values, loss_val, grads, loss_fn, config, sign=-1.0, scale=scale)
+        if _converged(log.losses, config):
+            break
+    log.final_values = dict(values)
+    return log
+
+
+def optimize_orientation(scene, region, config: OptimConfig | None = None, tx_name=None, bvh=None,
+                         tx_mode="central") -> TrainLog:
+    """Gradient ascent of the mean region path gain over tx yaw/pitch/roll
+    (optim.py:384-460), log-objective with Armijo steps; the orientation
+    gradient comes from the forward-mode kernel (rt_transfer_jvp)."""
+    from .channel import PROBE_NAME
+    from .em import EvalContext, path_coefficients_geo
+    if tx_mode != "central":
+        raise OptimError("orientation optimisation supports tx_mode='central'")
+    config = config or OptimConfig()
+    bvh = bvh or build(scene)
+    txs = [d for d in scene.devices if d.kind == "tx"]
+    tx = next(d for d in txs if d.name == tx_name) if tx_name else txs[0]
+    cells = np.array([region.cell_center(ix, iy) for iy in range(region.ny)
+                      for ix in range(region.nx)], dtype=np.float64)
+    if not len(cells):
+        raise OptimError("empty region")
+    keys = [f"dev:{tx.name}:{k}" for k in ("yaw", "pitch", "roll")]
+    values = dict(zip(keys, (float(a) for a in tx.orientation)))
+    dev = bvh.device
+    slant0 = POLARIZATION_SLANTS[scene.tx_array.polarization][0]
+    eta = EvalContext(scene).eta_table(bvh)
+    state = {}
+
+    def refresh():
+        prepare_candidates(bvh, tx.position, config.max_depth, config.method, config.num_rays)
+        T = paths_to_receivers(bvh, tx.position, cells)
+        T.tx_names, T.rx_names = [tx.name], [PROBE_NAME] * len(cells)
+        state["T"] = T
+        P = T.n
+        state["tp"] = torch.tensor(np.tile(tx.position, (P, 1)), dtype=torch.float64, device=dev)
+        state["rp"] = torch.tensor(cells[T.rx.long().cpu().numpy()], dtype=torch.float64, device=dev)
+        state["ro"] = torch.zeros((P, 3), dtype=torch.float64, device=dev)
+
+    def objective(vals, grad):
+        T = state["T"]
+        ypr = torch.tensor([vals[k] for k in keys], dtype=torch.float64, device=dev,
+                           requires_grad=grad)
+        if T.n == 0:
+            return torch.zeros((), dtype=torch.float64, device=dev), ypr
+        to = ypr[None, :].expand(T.n, 3)
+        tot = 0.0
+        for pat in ("_probe_theta", "_probe_phi"):
+            a = path_coefficients_geo(bvh, T, eta, state["tp"], state["rp"], to, state["ro"],
+                                      scene.tx_array.pattern, pat, [slant0], [0.0],
+                                      scene.wavelength, scene.frequency_hz)[:, 0, 0]
+            tot = tot + (a.abs() ** 2).sum()
+        return tot / len(cells), ypr
+
+    def log_objective(vals):
+        with torch.no_grad():
+            v = float(objective(vals, False)[0])
+        return math.log(v) if v > 0 else -math.inf
+
+    log = TrainLog(keys)
+    refresh()
+    if state["T"].n == 0:
+        warnings.warn("no propagation path reaches the target region; orientation left unchanged")
+        log.append(0, 0.0, values)
+        log.final_values = dict(values)
+        return log
+    scale = 1.0
+    for it in range(config.iterations):
+        if it and it % config.topology_refresh == 0:
+            refresh()
+        obj, ypr = objective(values, True)
+        obj_val = float(obj.detach())
+        if not math.isfinite(obj_val) or obj_val <= 0.0:
+            raise OptimError(f"objective degenerated at iteration {it}")
+        torch.log(obj).backward()
+        grads = dict(zip(keys, (float(g) for g in ypr.grad)))
+        log.append(it, obj_val, values)
+        values, scale = _descend(values, math.log(obj_val), grads, log_objective, config,
+                                 sign=+1.0, scale=scale)
+        if _converged(log.losses, config):
+            break
+    log.final_values = dict(values)
+    return log

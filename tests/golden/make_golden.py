@@ -242,6 +242,34 @@ def geo_grad_case():
     print("geo_grads:", len(rows), "paths", flush=True)
 
 
+def drivers_case():
+    """Acceptance criteria 6 and 7 (test_acceptance.py:178-231): the reference's
+    material-learning and orientation-ascent trajectories."""
+    from emtrace.optim import OptimConfig, generate_dataset, learn_materials, optimize_orientation
+    truth = load_scene(bundled_scene("calib_truth"))
+    init = load_scene(bundled_scene("calib_init"))
+    ds = generate_dataset(truth, num_subcarriers=128, subcarrier_spacing_hz=30e3, max_depth=1)
+    log6 = learn_materials(init, ds, OptimConfig(iterations=300, max_depth=1))
+    sc = load_scene(bundled_scene("orient"))
+    c = 70.71067811865476
+    region = GridSpec(origin=(c - 2.5, 47.5), cell_size=5.0, nx=1, ny=1, height=50.0)
+    log7 = optimize_orientation(sc, region, OptimConfig(iterations=150, max_depth=1))
+    np.savez_compressed(
+        os.path.join(HERE, "drivers.npz"),
+        calib_truth=np.array(scene_json(truth)), calib_init=np.array(scene_json(init)),
+        orient=np.array(scene_json(sc)),
+        ds_positions=np.array([r.position for r in ds.records]),
+        ds_h=np.array([r.h for r in ds.records]),
+        learn_names=np.array(log6.leaf_names), learn_losses=np.array(log6.losses),
+        learn_final=np.array([log6.final_values[k] for k in log6.leaf_names]),
+        learn_values=np.array([[v[k] for k in log6.leaf_names] for _, _, v in log6.rows]),
+        orient_names=np.array(log7.leaf_names), orient_losses=np.array(log7.losses),
+        orient_final=np.array([log7.final_values[k] for k in log7.leaf_names]),
+        region=np.array([region.origin[0], region.origin[1], region.cell_size, region.nx,
+                         region.ny, region.height]))
+    print("drivers:", len(log6.rows), "learn iters,", len(log7.rows), "orient iters", flush=True)
+
+
 def main(which=None):
     cases = {
         "soup": soup_case,
@@ -268,6 +296,7 @@ def main(which=None):
                        "central")]),
         "calib": calib_case,
         "geo_grads": geo_grad_case,
+        "drivers": drivers_case,
     }
     for k, fn in cases.items():
         if which and k not in which:

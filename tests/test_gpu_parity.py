@@ -310,3 +310,40 @@ def test_position_orientation_gradients_match_reference_tape(P, golden):
     scale = np.abs(want).max(axis=1, keepdims=True)
     assert np.all(np.abs(got - want) <= 1e-3 * np.abs(want) + 1e-6 * scale), \
         np.abs(got - want).max()
+
+
+def test_material_learning_driver_matches_reference(P, golden):
+    """Acceptance criterion 6 on the device: dataset generation, then 300 Armijo
+    iterations of projected descent (adjoint gradients) vs the reference run."""
+    from paper_2303_11103_b200 import optim
+    g = golden("drivers")
+    truth, init = golden_scene(g, "calib_truth"), golden_scene(g, "calib_init")
+    ds = optim.generate_dataset(truth, num_subcarriers=128, subcarrier_spacing_hz=30e3, max_depth=1)
+    h = np.array([r.h for r in ds.records])
+    assert np.abs(h - g["ds_h"]).max() <= 1e-9 * np.abs(g["ds_h"]).max()
+    log = optim.learn_materials(init, ds, optim.OptimConfig(iterations=300, max_depth=1))
+    assert log.leaf_names == list(g["learn_names"])
+    assert abs(log.losses[0] - g["learn_losses"][0]) <= 1e-9 * g["learn_losses"][0]
+    n = min(len(log.losses), 40)
+    assert np.allclose(log.losses[:n], g["learn_losses"][:n], rtol=1e-6, atol=0)
+    fv = np.array([log.final_values[k] for k in log.leaf_names])
+    assert np.allclose(fv, g["learn_final"], rtol=1e-3, atol=1e-6)
+    assert log.final_values["mat:buried_mat:eps_r"] == 3.0
+    assert log.final_values["mat:buried_mat:sigma"] == 0.1
+    assert log.losses[-1] < 1e-4
+
+
+def test_orientation_driver_matches_reference(P, golden):
+    """Acceptance criterion 7 on the device: log-objective ascent of the tx
+    orientation (forward-mode orientation gradients) vs the reference run."""
+    from paper_2303_11103_b200 import optim
+    g = golden("drivers")
+    sc = golden_scene(g, "orient")
+    ox, oy, cs, nx, ny, h = g["region"]
+    region = P.GridSpec((ox, oy), cs, int(nx), int(ny), h)
+    log = optim.optimize_orientation(sc, region, optim.OptimConfig(iterations=150, max_depth=1))
+    assert abs(log.losses[0] - g["orient_losses"][0]) <= 1e-9 * g["orient_losses"][0]
+    assert all(b >= a for a, b in zip(log.losses, log.losses[1:]))
+    fv = np.array([log.final_values[k] for k in log.leaf_names])
+    assert np.allclose(fv, g["orient_final"], rtol=0, atol=2e-3)
+    assert abs(log.losses[-1] - g["orient_losses"][-1]) <= 1e-3 * g["orient_losses"][-1]
