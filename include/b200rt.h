@@ -137,6 +137,18 @@ int rt_transfer_bwd(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* ord
                     double wavelength, double frequency_hz, const double* grad_a,
                     double* grad_eta, void* stream);
 
+/* Batched image_solve of independent (tx, rx, sequence) triples (tracer.py:
+ * 150-183; order-0 rows are LOS visibility checks, tracer.py:190) — the
+ * explicit-array gains (em.py:425-459) and single image_solve queries.
+ * Inputs device: tx_pos, rx_pos [n*3], seq [n*max_len] (-1 padded), len [n].
+ * Outputs device: valid [n] (1/0) and, for valid rows, the path geometry in
+ * rt_paths_get's layout (rows aligned with the inputs). */
+int rt_solve_pairs(rt_ctx* ctx, int64_t n, int max_len, const double* tx_pos,
+                   const double* rx_pos, const int32_t* seq, const int8_t* len, uint8_t* valid,
+                   double* vertices, double* length, double* delay, double* k_dep, double* k_arr,
+                   double* normals, double* cos_inc, int32_t* seq_out, int8_t* order_out,
+                   void* stream);
+
 /* Position / orientation derivatives (em.py:258-312 with tracked positions and
  * orientations): a[p,s,r] re-derived from per-path tx/rx positions and yaw/
  * pitch/roll (device [P*3] each; geometry re-solved by mirroring across the

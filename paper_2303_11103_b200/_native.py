@@ -30,7 +30,7 @@ EXPORTS = [
     "rt_num_prims", "rt_scene_arrays", "rt_trace", "rt_occluded", "rt_launch", "rt_enumerate",
     "rt_candidates_set", "rt_candidates_get", "rt_num_candidates", "rt_candidates_max_len",
     "rt_paths", "rt_paths_get", "rt_transfer", "rt_transfer_bwd", "rt_coverage",
-    "rt_set_profiling", "rt_get_profile", "rt_l2_probe", "rt_transfer_jvp",
+    "rt_set_profiling", "rt_get_profile", "rt_l2_probe", "rt_transfer_jvp", "rt_solve_pairs",
 ]
 
 _lib = None
@@ -109,6 +109,7 @@ def lib():
             "rt_l2_probe": (i32, [P, i64, i32, ctypes.POINTER(ctypes.c_double), P]),
             "rt_transfer_jvp": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, i32, i32, P, i32, P, i32,
                                       P, i32, f64, f64, P, P, P]),
+            "rt_solve_pairs": (i32, [P, i64, i32] + [P] * 15),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -67,7 +67,7 @@ def build_cir(gains, los: bool = True, reflection: bool = True,
         rxm = torch.tensor([rx_names.index(n) for n in T.rx_names], device=dev)[T.rx.long()[idx]]
         txm = torch.tensor([tx_names.index(n) for n in T.tx_names], device=dev)[T.tx.long()[idx]]
         pair = rxm * len(tx_names) + txm
-        delay = T.delay[idx]
+        delay = (gains.delay if gains.delay is not None else T.delay)[idx]
         # (pair, delay, kind, seq) lexicographic via stable sorts, least significant first
         order = torch.arange(idx.numel(), device=dev)
         seqrank = _seq_rank(T.seq[idx], T.order[idx])

@@ -129,6 +129,67 @@ __global__ void k_emit_paths(Cands C, SceneDev S, const double* images, Receiver
     }
 }
 
+// image_solve (tracer.py:150-183) of independent (tx, rx, sequence) triples —
+// the explicit-array gains (em.py:425-459) and single image_solve queries.
+// Order 0 rows are LOS checks (tracer.py:190, em.py:437-441).
+__global__ void k_solve_pairs(SceneDev S, Bvh bvh, long long n, int L, const double* txp,
+                              const double* rxp, const int* seq, const signed char* len,
+                              unsigned char* valid, PathTable T) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int K = len[i];
+    const int* sq = seq + i * L;
+    d3 tx = ld3(txp + 3 * i), rx = ld3(rxp + 3 * i);
+    d3 pts[MAX_DEPTH];
+    bool ok = true;
+    if (K > 0) {
+        d3 img[MAX_DEPTH + 1];
+        img[0] = tx;
+        for (int j = 0; j < K; ++j)
+            img[j + 1] = mirror(img[j], ld3(S.nrm + 3 * (long long)sq[j]), S.poff[sq[j]]);
+        d3 cur = rx;
+        for (int j = K - 1; j >= 0 && ok; --j) {   // solve_points + validity (solve_geometric)
+            int prim = sq[j];
+            d3 nn = ld3(S.nrm + 3 * (long long)prim);
+            double cc = S.poff[prim];
+            d3 seg = sub(img[j + 1], cur);
+            double denom = tdot(seg, nn);
+            if (fabs(denom) < 1e-15) { ok = false; break; }
+            double s = (cc - tdot(cur, nn)) / denom;
+            d3 p = d3{cur.x + seg.x * s, cur.y + seg.y * s, cur.z + seg.z * s};
+            if (!(1e-12 < s && s < 1.0 - 1e-12)) { ok = false; break; }
+            d3 v0 = ld3(S.v0 + 3 * (long long)prim), e1 = ld3(S.e1 + 3 * (long long)prim),
+               e2 = ld3(S.e2 + 3 * (long long)prim);
+            d3 w = sub(p, v0);
+            double d11 = dot_blas(e1, e1), d12 = dot_blas(e1, e2), d22 = dot_blas(e2, e2);
+            double w1 = dot_blas(w, e1), w2 = dot_blas(w, e2);
+            double den = d11 * d22 - d12 * d12;
+            double u = (d22 * w1 - d12 * w2) / den, v = (d11 * w2 - d12 * w1) / den;
+            if (!(u >= -INSIDE_TOL && v >= -INSIDE_TOL && u + v <= 1.0 + INSIDE_TOL)) { ok = false; break; }
+            pts[j] = p;
+            cur = p;
+        }
+        for (int j = 0; j < K && ok; ++j) {
+            d3 nn = ld3(S.nrm + 3 * (long long)sq[j]);
+            double cc = S.poff[sq[j]];
+            d3 before = j == 0 ? tx : pts[j - 1], after = j == K - 1 ? rx : pts[j + 1];
+            if ((tdot(before, nn) - cc) * (tdot(after, nn) - cc) <= SIDE_TOL) ok = false;
+        }
+        d3 a = tx;
+        for (int j = 0; j <= K && ok; ++j) {
+            d3 b = j < K ? pts[j] : rx;
+            double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+            if (sqrt(dx * dx + dy * dy + dz * dz) <= 2 * RAY_EPS) ok = false;
+            a = b;
+        }
+        if (ok) ok = segments_clear(bvh, tx, pts, K, rx);
+    } else {
+        ok = S.n == 0 || occluded(bvh, tx, rx) == 0;
+    }
+    valid[i] = ok ? 1 : 0;
+    if (ok) emit_row(T, i, 0, 0, K, sq, tx, pts, rx, S);
+}
+
 struct TransferArgs {
     long long n;
     int L;

@@ -1168,6 +1168,39 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
     return RT_OK;
 }
 
+int rt_solve_pairs(rt_ctx* ctx, int64_t n, int max_len, const double* tx_pos,
+                   const double* rx_pos, const int32_t* seq, const int8_t* len, uint8_t* valid,
+                   double* vertices, double* length, double* delay, double* k_dep, double* k_arr,
+                   double* normals, double* cos_inc, int32_t* seq_out, int8_t* order_out,
+                   void* stream) {
+    if (!ctx || n < 0 || max_len < 1 || max_len > MAX_DEPTH)
+        return fail(ctx, RT_EINVAL, "bad solve arguments");
+    if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
+    if (n == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    CK(ctx->p_rx.reserve(4ULL * n));
+    CK(ctx->p_cand.reserve(4ULL * n));
+    PathTable PT;
+    PT.rx = ctx->p_rx.get<int>();
+    PT.cand = ctx->p_cand.get<int>();
+    PT.order = reinterpret_cast<signed char*>(order_out);
+    PT.seq = seq_out;
+    PT.verts = vertices;
+    PT.length = length;
+    PT.delay = delay;
+    PT.kdep = k_dep;
+    PT.karr = k_arr;
+    PT.nrm = normals;
+    PT.cosv = cos_inc;
+    PT.L = max_len;
+    RC(clear_flags(ctx, st));
+    k_solve_pairs<<<nblk(n, 128), 128, 0, st>>>(scene_dev(ctx), bvh_dev(ctx), n, max_len, tx_pos, rx_pos,
+                                                seq, (const signed char*)len, valid, PT);
+    CKL();
+    return check_flags(ctx, st);
+}
+
 int rt_transfer_jvp(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
                     const int32_t* seq, const double* vertices, const double* normals,
                     const double* tx_pos, const double* rx_pos, const double* tx_ypr,

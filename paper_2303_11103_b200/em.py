@@ -290,11 +290,15 @@ class PathGain:
 class ChannelGains:
     """Columnar gains: a [P, rx_el, tx_el, T] complex128 on the device + path table."""
 
-    def __init__(self, scene, table: PathTable, a, sample_times):
+    def __init__(self, scene, table: PathTable, a, sample_times, delay=None, el_geom=None):
         self.scene = scene
         self.table = table
         self.a = a
         self.sample_times = np.asarray(sample_times, dtype=np.float64)
+        # per-path delay (explicit arrays: mean over valid element pairs, em.py:456)
+        self.delay = delay if delay is not None else (table.delay if table is not None else None)
+        # explicit arrays: per element pair (delays, k_dep, k_arr) [P, rx_el, tx_el(, 3)]
+        self.el_geom = el_geom
         self._entries = None
 
     @property
@@ -306,6 +310,8 @@ class ChannelGains:
             else:
                 h = T.host()
                 a = self.a.cpu().numpy()
+                dl = self.delay.cpu().numpy()
+                eg = [g.cpu().numpy() for g in self.el_geom] if self.el_geom else None
                 out = []
                 for i in range(T.n):
                     k = int(h["order"][i])
@@ -313,10 +319,11 @@ class ChannelGains:
                     out.append(PathGain(
                         tx=T.tx_names[int(h["tx"][i])], rx=T.rx_names[int(h["rx"][i])],
                         kind="specular" if k else "los",
-                        seq=tuple(int(s) for s in h["seq"][i, :k]), delay=float(h["delay"][i]),
-                        a=a[i], delays=np.full((nr, nt), float(h["delay"][i])),
-                        k_dep=np.broadcast_to(h["kdep"][i], (nr, nt, 3)).copy(),
-                        k_arr=np.broadcast_to(h["karr"][i], (nr, nt, 3)).copy()))
+                        seq=tuple(int(s) for s in h["seq"][i, :k]), delay=float(dl[i]),
+                        a=a[i],
+                        delays=eg[0][i] if eg else np.full((nr, nt), float(h["delay"][i])),
+                        k_dep=eg[1][i] if eg else np.broadcast_to(h["kdep"][i], (nr, nt, 3)).copy(),
+                        k_arr=eg[2][i] if eg else np.broadcast_to(h["karr"][i], (nr, nt, 3)).copy()))
                 self._entries = out
         return self._entries
 
@@ -353,8 +360,6 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
     """Complex gains for every path and element pair (em.py:359-422)."""
     if ctx is None:
         ctx = EvalContext(scene)
-    if not scene.synthetic_array:
-        raise EmError("explicit (non-synthetic) arrays are not implemented on the B200 path yet")
     T = pathset.table
     if T is None:
         txn = [d.name for d in scene.devices if d.kind == "tx"]
@@ -372,6 +377,9 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
     devs = {d.name: d for d in scene.devices}
     tx_rows_dev = [ctx.rotation_rows(devs[n]) for n in T.tx_names]
     rx_rows_dev = [ctx.rotation_rows(devs[n]) for n in T.rx_names]
+    if not scene.synthetic_array:
+        return _gains_explicit(scene, bvh, T, ctx, off_tx, sl_tx, off_rx, sl_rx, tx_rows_dev,
+                               rx_rows_dev, devs, eta)
     tx_idx = T.tx.long()
     rx_idx = T.rx.long()
     tx_rows = _rows_tensor(tx_rows_dev, dev)[tx_idx].contiguous()
@@ -400,6 +408,60 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
     return ChannelGains(scene, T, a[..., None], np.zeros(1))
 
 
+def _gains_explicit(scene, bvh, T, ctx, off_tx, sl_tx, off_rx, sl_rx, tx_rows_dev, rx_rows_dev,
+                    devs, eta):
+    """Explicit arrays (em.py:425-459): every (path, rx element, tx element) is
+    re-solved with displaced endpoints (rt_solve_pairs; LOS rows re-check
+    visibility), then transferred with that pair's slants; the path delay is
+    the mean over valid pairs."""
+    from .tracer import solve_pairs
+    dev = bvh.device
+    P, L = T.n, T.L
+    nr, nt = len(off_rx), len(off_tx)
+    h = T.host()
+    off_tx_w = [off_tx @ np.array(r, dtype=np.float64).T for r in tx_rows_dev]
+    off_rx_w = [off_rx @ np.array(r, dtype=np.float64).T for r in rx_rows_dev]
+    tpos = np.array([devs[n].position for n in T.tx_names], dtype=np.float64)
+    rpos = np.array([devs[n].position for n in T.rx_names], dtype=np.float64)
+    ti, ri = h["tx"].astype(np.int64), h["rx"].astype(np.int64)
+    # item (p, i, j): rx element i, tx element j (em.py:433-436)
+    txp = tpos[ti][:, None, None, :] + np.stack(off_tx_w)[ti][:, None, :, :]
+    rxp = rpos[ri][:, None, None, :] + np.stack(off_rx_w)[ri][:, :, None, :]
+    txp = np.broadcast_to(txp, (P, nr, nt, 3)).reshape(-1, 3)
+    rxp = np.broadcast_to(rxp, (P, nr, nt, 3)).reshape(-1, 3)
+    seqs = np.repeat(h["seq"], nr * nt, axis=0)
+    lens = np.repeat(h["order"], nr * nt)
+    valid, Q = solve_pairs(bvh, txp, rxp, seqs, lens)
+    a = torch.zeros((P * nr * nt,), dtype=torch.complex128, device=dev)
+    if eta is None:
+        eta = ctx.eta_table(bvh)
+    tx_rows = _rows_tensor(tx_rows_dev, dev)[torch.as_tensor(np.repeat(ti, nr * nt), device=dev)]
+    rx_rows = _rows_tensor(rx_rows_dev, dev)[torch.as_tensor(np.repeat(ri, nr * nt), device=dev)]
+    st_item = np.tile(np.repeat(np.asarray(sl_tx, dtype=np.float64)[None, :], nr, 0).reshape(-1), P)
+    sr_item = np.tile(np.repeat(np.asarray(sl_rx, dtype=np.float64)[:, None], nt, 1).reshape(-1), P)
+    vh = valid.cpu().numpy()
+    for st in sorted(set(st_item.tolist())):
+        for sr in sorted(set(sr_item.tolist())):
+            sel = np.flatnonzero(vh & (st_item == st) & (sr_item == sr))
+            if not len(sel):
+                continue
+            idx = torch.as_tensor(sel, device=dev)
+            sub = PathTable(L, [], [], **{f: getattr(Q, f)[idx] for f in PathTable.FIELDS})
+            v = _launch_transfer(bvh, sub, tx_rows[idx].contiguous(), rx_rows[idx].contiguous(),
+                                 pattern_id(scene.tx_array.pattern), pattern_id(scene.rx_array.pattern),
+                                 [st], [sr], eta, scene.wavelength, scene.frequency_hz)
+            a[idx] = torch.view_as_complex(v[:, 0, 0].contiguous())
+    vm = valid.reshape(P, nr * nt)
+    dl = torch.where(valid, Q.delay, torch.zeros_like(Q.delay)).reshape(P, nr * nt)
+    cnt = vm.sum(1)
+    mean = torch.where(cnt > 0, dl.sum(1) / cnt.clamp(min=1).to(torch.float64), T.delay)
+    z3 = torch.zeros_like(Q.kdep)
+    el = (torch.where(valid, Q.delay, torch.zeros_like(Q.delay)).reshape(P, nr, nt),
+          torch.where(valid[:, None], Q.kdep, z3).reshape(P, nr, nt, 3),
+          torch.where(valid[:, None], Q.karr, z3).reshape(P, nr, nt, 3))
+    return ChannelGains(scene, T, a.reshape(P, nr, nt, 1), np.zeros(1), delay=mean, el_geom=el)
+
+
 def apply_doppler(gains: ChannelGains, sampling_frequency: float, num_time_steps: int,
                   tx_velocities=None, rx_velocities=None) -> ChannelGains:
     """a_i(t_n) = a_i e^{j 2 pi f_D t_n}, f_D = (f/c)(k_dep.v_tx - k_arr.v_rx) (em.py:462-494)."""
@@ -424,11 +486,17 @@ def apply_doppler(gains: ChannelGains, sampling_frequency: float, num_time_steps
     vt = vel(tx_velocities, T.tx_names)[T.tx.long()]
     vr = vel(rx_velocities, T.rx_names)[T.rx.long()]
     f_over_c = gains.scene.frequency_hz / SPEED_OF_LIGHT
-    fd = f_over_c * ((T.kdep * vt).sum(-1) - (T.karr * vr).sum(-1))             # [P]
     tt = torch.tensor(t, dtype=torch.float64, device=dev)
-    ph = torch.exp(1j * TWO_PI * fd[:, None] * tt[None, :])                    # [P, T]
-    a = gains.a[..., :1] * ph[:, None, None, :]
-    return ChannelGains(gains.scene, T, a, t)
+    if gains.el_geom is not None:   # explicit arrays: per element-pair directions
+        kd, ka = gains.el_geom[1], gains.el_geom[2]                             # [P, r, t, 3]
+        fd = f_over_c * ((kd * vt[:, None, None]).sum(-1) - (ka * vr[:, None, None]).sum(-1))
+        ph = torch.exp(1j * TWO_PI * fd[..., None] * tt)                          # [P, r, t, T]
+        a = gains.a[..., :1] * ph
+    else:
+        fd = f_over_c * ((T.kdep * vt).sum(-1) - (T.karr * vr).sum(-1))         # [P]
+        ph = torch.exp(1j * TWO_PI * fd[:, None] * tt[None, :])                # [P, T]
+        a = gains.a[..., :1] * ph[:, None, None, :]
+    return ChannelGains(gains.scene, T, a, t, delay=gains.delay, el_geom=gains.el_geom)
 
 
 def slants_of(arr):

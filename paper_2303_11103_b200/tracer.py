@@ -312,18 +312,47 @@ def compute_paths(scene, bvh: Bvh, max_depth: int, method: str = "exhaustive",
     return PathSet(scene=scene, max_depth=max_depth, method=method, table=T)
 
 
+def solve_pairs(bvh: Bvh, tx_pos, rx_pos, seqs, lens):
+    """Batched image_solve (tracer.py:150-183) of independent (tx, rx, seq) rows
+    via rt_solve_pairs; order-0 rows are LOS visibility checks.  Returns
+    (valid [n] bool tensor, PathTable with one row per input)."""
+    dev = bvh.device
+    f64 = dict(dtype=torch.float64, device=dev)
+    tx = torch.as_tensor(tx_pos, **f64).reshape(-1, 3).contiguous()
+    rx = torch.as_tensor(rx_pos, **f64).reshape(-1, 3).contiguous()
+    sq = torch.as_tensor(seqs, dtype=torch.int32, device=dev).contiguous()
+    n, L = sq.shape[0], max(sq.shape[1] if sq.dim() == 2 else 1, 1)
+    sq = sq.reshape(n, L)
+    ln = torch.as_tensor(lens, dtype=torch.int8, device=dev).reshape(n).contiguous()
+    valid = torch.zeros(n, dtype=torch.uint8, device=dev)
+    cols = dict(rx=torch.zeros(n, dtype=torch.int32, device=dev),
+                cand=torch.zeros(n, dtype=torch.int32, device=dev),
+                order=torch.zeros(n, dtype=torch.int8, device=dev),
+                seq=torch.full((n, L), -1, dtype=torch.int32, device=dev),
+                verts=torch.zeros((n, L + 2, 3), **f64), length=torch.zeros(n, **f64),
+                delay=torch.zeros(n, **f64), kdep=torch.zeros((n, 3), **f64),
+                karr=torch.zeros((n, 3), **f64), normals=torch.zeros((n, L, 3), **f64),
+                cos=torch.zeros((n, L), **f64), tx=torch.zeros(n, dtype=torch.int32, device=dev))
+    if n:
+        with torch.cuda.device(dev):
+            bvh.ctx.call("rt_solve_pairs", n, L, N.ptr(tx), N.ptr(rx), N.ptr(sq), N.ptr(ln),
+                         N.ptr(valid), N.ptr(cols["verts"]), N.ptr(cols["length"]),
+                         N.ptr(cols["delay"]), N.ptr(cols["kdep"]), N.ptr(cols["karr"]),
+                         N.ptr(cols["normals"]), N.ptr(cols["cos"]), N.ptr(cols["seq"]),
+                         N.ptr(cols["order"]), bvh.ctx.stream, exc_map=_TRACER_ERRORS)
+    return valid.bool(), PathTable(L, [], [], **cols)
+
+
 def image_solve(tx_name, rx_name, tx_pos, rx_pos, seq, bvh: Bvh):
     """Image-method solve of one candidate (tracer.py:150-183); None when invalid."""
     seq = tuple(int(s) for s in seq)
     if not seq:
         raise TracerError("image_solve needs a non-empty sequence")
-    set_candidates(bvh, np.array([seq], dtype=np.int32), np.array([len(seq)], dtype=np.int8), len(seq))
-    T = paths_to_receivers(bvh, tx_pos, [rx_pos])
+    valid, T = solve_pairs(bvh, [_pos3(tx_pos)], [_pos3(rx_pos)], [list(seq)], [len(seq)])
+    if not bool(valid[0]):
+        return None
     T.tx_names, T.rx_names = [tx_name], [rx_name]
-    for p in table_to_paths(T):
-        if p.kind == "specular":
-            return p
-    return None
+    return table_to_paths(T)[0]
 
 
 def los_path(scene, bvh: Bvh, tx_dev, rx_dev):

@@ -242,6 +242,34 @@ def geo_grad_case():
     print("geo_grads:", len(rows), "paths", flush=True)
 
 
+def explicit_case():
+    """Explicit (non-synthetic) arrays (em.py:425-459) + Doppler (em.py:462-494)."""
+    out = {}
+    for name, sc in (("ground", to_ref(ground_scene(rx=(200, 0, 10)))), ("canyon", to_ref(_canyon_small()))):
+        if name == "ground":
+            sc.tx_array = E.AntennaArray(num_rows=8, num_cols=2, vertical_spacing=0.7,
+                                         horizontal_spacing=0.5, pattern="iso", polarization="H")
+        sc.synthetic_array = False
+        tree = accel.build(sc)
+        ps = E.compute_paths(sc, tree, 2 if name == "canyon" else 1,
+                             method="fibonacci" if name == "canyon" else "exhaustive", num_rays=20000)
+        gains = E.compute_gains(sc, tree, ps)
+        dop = E.apply_doppler(gains, 1e6, 4, tx_velocities=[3.0, -1.0, 0.5],
+                              rx_velocities={sc.receivers[0].name: [0.0, 2.0, 0.0]})
+        cir = E.build_cir(gains)
+        out[f"{name}_scene"] = np.array(scene_json(sc))
+        out[f"{name}_a"] = np.stack([e.a for e in gains.entries])
+        out[f"{name}_delay"] = np.array([e.delay for e in gains.entries])
+        out[f"{name}_delays"] = np.stack([e.delays for e in gains.entries])
+        out[f"{name}_kdep"] = np.stack([e.k_dep for e in gains.entries])
+        out[f"{name}_dop_a"] = np.stack([e.a for e in dop.entries])
+        out[f"{name}_cir_a"] = cir.a
+        out[f"{name}_cir_tau"] = cir.tau
+        out[f"{name}_max_depth"] = 2 if name == "canyon" else 1
+    np.savez_compressed(os.path.join(HERE, "explicit.npz"), **out)
+    print("explicit: done", flush=True)
+
+
 def drivers_case():
     """Acceptance criteria 6 and 7 (test_acceptance.py:178-231): the reference's
     material-learning and orientation-ascent trajectories."""
@@ -297,6 +325,7 @@ def main(which=None):
         "calib": calib_case,
         "geo_grads": geo_grad_case,
         "drivers": drivers_case,
+        "explicit": explicit_case,
     }
     for k, fn in cases.items():
         if which and k not in which:

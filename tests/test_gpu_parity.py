@@ -312,6 +312,36 @@ def test_position_orientation_gradients_match_reference_tape(P, golden):
         np.abs(got - want).max()
 
 
+@pytest.mark.parametrize("name", ["ground", "canyon"])
+def test_explicit_arrays_and_doppler_match_reference(P, golden, name):
+    """synthetic_array=False (em.py:425-459): every element pair re-solved with
+    displaced endpoints; mean delays; per-pair Doppler (em.py:462-494); CIR."""
+    g = golden("explicit")
+    sc = golden_scene(g, f"{name}_scene")
+    b = _bvh(P, sc)
+    depth = int(g[f"{name}_max_depth"])
+    ps = P.compute_paths(sc, b, depth, method="fibonacci" if name == "canyon" else "exhaustive",
+                         num_rays=20000)
+    gains = P.compute_gains(sc, b, ps)
+    ref = g[f"{name}_a"]
+    got = np.stack([e.a for e in gains.entries])
+    assert got.shape == ref.shape
+    assert np.abs(got - ref).max() <= 1e-9 * np.abs(ref).max()
+    assert np.allclose([e.delay for e in gains.entries], g[f"{name}_delay"], rtol=1e-12, atol=0)
+    assert np.allclose(np.stack([e.delays for e in gains.entries]), g[f"{name}_delays"],
+                       rtol=1e-12, atol=0)
+    assert np.allclose(np.stack([e.k_dep for e in gains.entries]), g[f"{name}_kdep"], atol=1e-12)
+    rxn = [d.name for d in sc.devices if d.kind == "rx"][0]
+    dop = P.apply_doppler(gains, 1e6, 4, tx_velocities=[3.0, -1.0, 0.5],
+                          rx_velocities={rxn: [0.0, 2.0, 0.0]})
+    da = np.stack([e.a for e in dop.entries])
+    assert np.abs(da - g[f"{name}_dop_a"]).max() <= 1e-9 * np.abs(ref).max()
+    cir = P.build_cir(gains)
+    assert cir.a.shape == g[f"{name}_cir_a"].shape
+    assert np.abs(cir.a - g[f"{name}_cir_a"]).max() <= 1e-9 * np.abs(ref).max()
+    assert np.allclose(cir.tau, g[f"{name}_cir_tau"], rtol=1e-12, atol=0)
+
+
 def test_material_learning_driver_matches_reference(P, golden):
     """Acceptance criterion 6 on the device: dataset generation, then 300 Armijo
     iterations of projected descent (adjoint gradients) vs the reference run."""
