@@ -427,8 +427,8 @@ def _gains_explicit(scene, bvh, T, ctx, off_tx, sl_tx, off_rx, sl_rx, tx_rows_de
     # item (p, i, j): rx element i, tx element j (em.py:433-436)
     txp = tpos[ti][:, None, None, :] + np.stack(off_tx_w)[ti][:, None, :, :]
     rxp = rpos[ri][:, None, None, :] + np.stack(off_rx_w)[ri][:, :, None, :]
-    txp = np.broadcast_to(txp, (P, nr, nt, 3)).reshape(-1, 3)
-    rxp = np.broadcast_to(rxp, (P, nr, nt, 3)).reshape(-1, 3)
+    txp = np.array(np.broadcast_to(txp, (P, nr, nt, 3)).reshape(-1, 3))
+    rxp = np.array(np.broadcast_to(rxp, (P, nr, nt, 3)).reshape(-1, 3))
     seqs = np.repeat(h["seq"], nr * nt, axis=0)
     lens = np.repeat(h["order"], nr * nt)
     valid, Q = solve_pairs(bvh, txp, rxp, seqs, lens)
