@@ -318,6 +318,10 @@ def solve_pairs(bvh: Bvh, tx_pos, rx_pos, seqs, lens):
     (valid [n] bool tensor, PathTable with one row per input)."""
     dev = bvh.device
     f64 = dict(dtype=torch.float64, device=dev)
+    if isinstance(tx_pos, np.ndarray) and not tx_pos.flags.writeable:
+        tx_pos = np.array(tx_pos)
+    if isinstance(rx_pos, np.ndarray) and not rx_pos.flags.writeable:
+        rx_pos = np.array(rx_pos)
     tx = torch.as_tensor(tx_pos, **f64).reshape(-1, 3).contiguous()
     rx = torch.as_tensor(rx_pos, **f64).reshape(-1, 3).contiguous()
     sq = torch.as_tensor(seqs, dtype=torch.int32, device=dev).contiguous()
