@@ -619,9 +619,13 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         ctx->band_B = B;
     }
     long long span = slot_end - slot_begin;
+    // The trie holds one node per unique hit prefix, far fewer than rays x depth
+    // (C3: 124k prefixes for 244M bounces).  Start small enough to stay
+    // L2-resident and cheap to clear; an overflow grows it 4x and relaunches,
+    // and the context keeps the grown capacity for later calls.
     if (ctx->trie_cap == 0) {
-        uint64_t want = 1ULL << 20;
-        while (want < 4ULL * std::min<long long>(span * max_depth, 1LL << 24)) want <<= 1;
+        uint64_t want = 1ULL << 16;
+        while (want < 4ULL * std::min<long long>(span * max_depth, 1LL << 18)) want <<= 1;
         ctx->trie_cap = want;
     }
     for (int attempt = 0; attempt < 6; ++attempt) {
@@ -826,7 +830,8 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         CK(ctx->seg_cnt.reserve(8ULL * (nS + 1)));
         CK(ctx->item_off.reserve(8ULL * (nS + 1)));
         CK(cudaMemsetAsync(ctx->seg_cnt.get<long long>() + nS, 0, 8, st));
-        k_segments<<<nblk(nC, 128), 128, 0, st>>>(nC, ctx->hps.get<double>(), ctx->nhp.get<int>(),
+        if (nS > 0)
+            k_segments<<<nblk(nS, 256), 256, 0, st>>>(nC, nS, ctx->hps.get<double>(), ctx->nhp.get<int>(),
                                                   ctx->row0.get<int>(), seg_off, R, shard_count,
                                                   ctx->seg_cand.get<int>(), ctx->seg_iy.get<int>(),
                                                   ctx->seg_ix0.get<int>(), ctx->seg_cnt.get<long long>());

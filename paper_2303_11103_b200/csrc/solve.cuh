@@ -269,33 +269,6 @@ __device__ inline void row_interval(const double* hp, int m, const Receivers& R,
     ix1 = fhi < 0.0 ? -1 : (long long)fhi;
 }
 
-// one thread per candidate: fill its row segments (cand, iy, ix0, count)
-__global__ void k_segments(long long n_cand, const double* hps, const int* nhp, const int* row0,
-                           const long long* seg_off, Receivers R, int shard_count, int* seg_cand,
-                           int* seg_iy, int* seg_ix0, long long* seg_cnt) {
-    long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (c >= n_cand) return;
-    long long s0 = seg_off[c], s1 = seg_off[c + 1];
-    const double* hp = hps + c * HP_MAX * 3;
-    int m = nhp[c];
-    for (long long s = s0; s < s1; ++s) {
-        long long iy = row0[c] + (s - s0) * shard_count;
-        long long ix0, ix1;
-        row_interval(hp, m, R, iy, ix0, ix1);
-        seg_cand[s] = (int)c;
-        seg_iy[s] = (int)iy;
-        seg_ix0[s] = (int)ix0;
-        seg_cnt[s] = ix1 >= ix0 ? ix1 - ix0 + 1 : 0;
-    }
-}
-
-// survivor of the geometric tests
-struct Pending {
-    long long rx;
-    int cand;
-    int pad;
-};
-
 // largest s with off[s] <= w (off nondecreasing, off[0] = 0)
 __device__ inline long long upper_index(const long long* off, long long n, long long w) {
     long long lo = 0, hi = n;
@@ -305,6 +278,38 @@ __device__ inline long long upper_index(const long long* off, long long n, long 
     }
     return lo;
 }
+
+// one thread per row segment (cand, iy, ix0, count): candidates own from 0 to
+// hundreds of rows, so rows, not candidates, are the parallel unit.  One
+// binary search per warp finds the first lane's candidate; lanes walk forward.
+__global__ void k_segments(long long n_cand, long long n_seg, const double* hps, const int* nhp,
+                           const int* row0, const long long* seg_off, Receivers R, int shard_count,
+                           int* seg_cand, int* seg_iy, int* seg_ix0, long long* seg_cnt) {
+    const unsigned FULL = 0xffffffffu;
+    int lane = threadIdx.x & 31;
+    long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    long long s_w = s - lane;
+    long long c0 = 0;
+    if (lane == 0 && s_w < n_seg) c0 = upper_index(seg_off, n_cand, s_w);
+    c0 = __shfl_sync(FULL, c0, 0);
+    if (s >= n_seg) return;
+    long long c = c0;
+    while (seg_off[c + 1] <= s) ++c;
+    long long iy = row0[c] + (s - seg_off[c]) * shard_count;
+    long long ix0, ix1;
+    row_interval(hps + c * HP_MAX * 3, nhp[c], R, iy, ix0, ix1);
+    seg_cand[s] = (int)c;
+    seg_iy[s] = (int)iy;
+    seg_ix0[s] = (int)ix0;
+    seg_cnt[s] = ix1 >= ix0 ? ix1 - ix0 + 1 : 0;
+}
+
+// survivor of the geometric tests
+struct Pending {
+    long long rx;
+    int cand;
+    int pad;
+};
 
 struct Segs {
     const long long* item_off;   // [S+1]
