@@ -224,6 +224,10 @@ def run_b200(args):
     lib.rt_set_profiling(bvh.ctx.h, 0)
     per_bounce_nodes = ctr[1] / max(ctr[0], 1)
     per_bounce_tris = ctr[2] / max(ctr[0], 1)
+    # SIMD efficiency of the launch: bounces per warp bounce-iteration / 32, and
+    # node visits per warp traversal / (32 * the warp's longest traversal)
+    simd = {"bounce_lanes": float(ctr[0]) / max(32.0 * ctr[10], 1.0),
+            "traversal_lanes": float(ctr[1]) / max(32.0 * ctr[11], 1.0)}
 
     e2e = None
     if not args.no_e2e:
@@ -261,6 +265,7 @@ def run_b200(args):
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
                      "bytes_per_bounce": BYTES_PER_NODE * per_bounce_nodes + BYTES_PER_TRI * per_bounce_tris,
                      "nodes_per_bounce": per_bounce_nodes, "tris_per_bounce": per_bounce_tris,
+                     "simd_efficiency": simd,
                      "kernel_ms": launch_ms, "kernel_share": launch_ms / ms_per_step,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "l2_peak_gbs": l2_bw, "l2_frac": (achieved / l2_bw) if achieved else None,

@@ -188,8 +188,11 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
  * footprints + scan, 3 geometric solve, 4 occlusion+transfer, 5 record sort,
  * 6 merge/accumulate, 7 LOS, 8 trie -> sequences; counters: 0 ray-bounces,
  * 1 node visits, 2 triangle tests, 3 candidates, 4 work items, 5 geometric
- * pairs, 6 valid paths, 15 kernel launches issued by the library
- * (cumulative; a CUB device-wide primitive counts once). */
+ * pairs, 6 valid paths, 10 warp iterations of the launch's bounce loop and
+ * 11 the sum over them of the warp's largest per-lane node-visit count (both
+ * from the instrumented launch: SIMD efficiency of bounces and traversals),
+ * 15 kernel launches issued by the library (cumulative; a CUB device-wide
+ * primitive counts once). */
 int rt_set_profiling(rt_ctx* ctx, int flags);
 /* L2-resident read bandwidth (GB/s) of this device: a persistent kernel
  * streams a `bytes` buffer `iters` times with 16-byte L2-only loads (the

@@ -24,6 +24,12 @@
 #ifndef RT_DYNAMIC
 #define RT_DYNAMIC 0
 #endif
+#ifndef RT_DFS_LAYOUT
+#define RT_DFS_LAYOUT 1   // depth-first BNode order for the PLOC tree (C3 launch: -0.5%)
+#endif
+#ifndef RT_OCC_HINTS
+#define RT_OCC_HINTS 1   // occluder cache in k_validate (solve.cuh segments_clear_hinted)
+#endif
 #include "solve.cuh"
 
 using namespace rt;
@@ -81,7 +87,7 @@ struct rt_ctx {
     DevBuf s_seq, s_len, s_perm, s_perm_alt, s_keys, s_keys_alt, s_flag, s_pos;
     DevBuf cub_tmp;
     // solve scratch
-    DevBuf hps, nhp, row0, seg_cand, seg_iy, seg_ix0, seg_cnt, item_off;
+    DevBuf hps, nhp, row0, seg_cand, seg_iy, seg_ix0, seg_cnt, item_off, occ_hint, chunk_seg;
     DevBuf images, fp, counts, scan, pending, recs, rkeys, rkeys_alt, ridx, ridx_alt, keep,
         losbuf, heads, pcounts, poffs, em_small, ctrs;
     uint64_t pending_cap = 0;
@@ -92,7 +98,7 @@ struct rt_ctx {
     // error flags + pinned host staging
     DevBuf dflag, probe;
     // PLOC builder scratch
-    DevBuf pl_box, pl_count, pl_parent, pl_ca, pl_cb, pl_nn, pl_out, pl_valid, pl_pos, pl_slot;
+    DevBuf pl_box, pl_count, pl_parent, pl_ca, pl_cb, pl_nn, pl_out, pl_valid, pl_pos, pl_slot, pl_em, pl_dfs;
     long long* hpin = nullptr;
     // profiling: per-stage CUDA events on the caller's stream + counters
     int prof = 0;
@@ -289,6 +295,9 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
     CK(ctx->pl_valid.reserve(4ULL * (n + 1)));
     CK(ctx->pl_pos.reserve(4ULL * (n + 1)));
     CK(ctx->pl_slot.reserve(4ULL * n));
+    CK(ctx->pl_em.reserve(4ULL * nn));
+    CK(ctx->pl_dfs.reserve(4ULL * n));
+    int* em = ctx->pl_em.get<int>();
     float* box = ctx->pl_box.get<float>();
     int* cnt = ctx->pl_count.get<int>();
     int* par = ctx->pl_parent.get<int>();
@@ -298,7 +307,7 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
     int* valid = ctx->pl_valid.get<int>();
     int* pos = ctx->pl_pos.get<int>();
     const int* sidx = ctx->sorted_idx.get<int>();
-    k_ploc_init<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, ctx->pbox.get<float>(), box, ca, cnt);
+    k_ploc_init<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, ctx->pbox.get<float>(), box, ca, cnt, em);
     CKL();
     int* counter = reinterpret_cast<int*>(ctx->ctrs.get<long long>());
     CK(cudaMemsetAsync(counter, 0, 4, st));
@@ -308,7 +317,7 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
         k_ploc_nn<<<nblk(C, PLOC_BLOCK), PLOC_BLOCK, 0, st>>>(ca, (int)C, box, ctx->pl_nn.get<int>());
         CKL();
         k_ploc_merge<<<nblk(C, 256), 256, 0, st>>>(ca, (int)C, ctx->pl_nn.get<int>(), (int)n, box, child,
-                                                    par, cnt, counter, ctx->pl_out.get<int>(), valid);
+                                                    par, cnt, em, counter, ctx->pl_out.get<int>(), valid);
         CKL();
         RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
             return cub::DeviceScan::ExclusiveSum(tmp, bytes, valid, pos, (int)C, st);
@@ -332,9 +341,17 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
     k_ploc_slots<<<nblk(n, 256), 256, 0, st>>>((int)n, par, child, cnt, root, slot);
     CKL();
     CK(ctx->nodes.reserve(sizeof(BNode) * std::max<long long>(n - 1, 1)));
-    k_ploc_layout<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, root, child, cnt, slot, box,
-                                                    ctx->cbounds.get<unsigned>(), ctx->nodes.get<BNode>());
-    CKL();
+    int* dfs = nullptr;
+    if (RT_DFS_LAYOUT && n > 1) {
+        dfs = ctx->pl_dfs.get<int>();
+        k_ploc_dfs<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, root, par, child, cnt, em, dfs);
+        CKL();
+    }
+    if (n > 1) {
+        k_ploc_layout<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, root, child, cnt, slot, box,
+                                                        ctx->cbounds.get<unsigned>(), dfs, ctx->nodes.get<BNode>());
+        CKL();
+    }
     k_ploc_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, slot, ctx->v0.get<double>(), ctx->e1.get<double>(),
                                               ctx->e2.get<double>(), ctx->tris.get<TriRec>());
     CKL();
@@ -667,6 +684,8 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         long long blocks = std::min<long long>((span + LB - 1) / LB, (long long)ctx->n_sm * (4096 / LB));
         P.node_visits = reinterpret_cast<unsigned long long*>(ctr + 3);
         P.tri_tests = reinterpret_cast<unsigned long long*>(ctr + 4);
+        P.warp_bounces = reinterpret_cast<unsigned long long*>(ctr + 6);
+        P.warp_visits = reinterpret_cast<unsigned long long*>(ctr + 7);
         PROF_BEGIN(ST_LAUNCH);
         if (span > 0) {
             unsigned g = (unsigned)std::max<long long>(blocks, 1);
@@ -682,9 +701,11 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
             CKL();
         }
         PROF_END(ST_LAUNCH);
-        RC(fetch(ctx, ctr, 5, st));
+        RC(fetch(ctx, ctr, 8, st));
         ctx->counters[1] = ctx->hpin[3];
         ctx->counters[2] = ctx->hpin[4];
+        ctx->counters[10] = ctx->hpin[6];
+        ctx->counters[11] = ctx->hpin[7];
         long long nodes = (long long)(int)(ctx->hpin[0] & 0xffffffff);
         bool overflow = (int)(ctx->hpin[1] & 0xffffffff) != 0;
         long long bounces = ctx->hpin[2];
@@ -806,7 +827,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     k_images<<<nblk(nC, 256), 256, 0, st>>>(C, SD, tx, ctx->images.get<double>());
     CKL();
     long long W = 0;
-    Segs G{nullptr, nullptr, nullptr, nullptr, 0};
+    Segs G{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
     if (grid) {
         CK(ctx->hps.reserve(sizeof(double) * 3 * HP_MAX * nC));
         CK(ctx->nhp.reserve(4ULL * nC));
@@ -843,7 +864,13 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         }));
         RC(fetch(ctx, io + nS, 1, st));
         W = ctx->hpin[0];
-        G = Segs{io, ctx->seg_cand.get<int>(), ctx->seg_iy.get<int>(), ctx->seg_ix0.get<int>(), nS};
+        CK(ctx->chunk_seg.reserve(4ULL * ((W + 31) / 32 + 1)));
+        if (nS > 0) {
+            k_chunk_starts<<<nblk(nS, 256), 256, 0, st>>>(nS, io, ctx->chunk_seg.get<int>());
+            CKL();
+        }
+        G = Segs{io, ctx->seg_cand.get<int>(), ctx->seg_iy.get<int>(), ctx->seg_ix0.get<int>(),
+                 ctx->chunk_seg.get<int>(), nS};
         ctx->counters[7] = nS;
     } else {
         W = nC * R.n;
@@ -882,10 +909,17 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     unsigned long long* nr = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>()) + 1;
     RC(clear_flags(ctx, st));
     long long vblocks = std::min<long long>((n_pend + 127) / 128, (long long)ctx->n_sm * 32);
+    // occluder cache: one TriRec index per (candidate, segment), -1 = none yet
+    CK(ctx->occ_hint.reserve(4ULL * nC * (MAX_DEPTH + 1)));
     PROF_BEGIN(ST_VALIDATE);
+    int* hints = nullptr;
+    if (RT_OCC_HINTS) {
+        hints = ctx->occ_hint.get<int>();
+        CK(cudaMemsetAsync(hints, 0xFF, 4ULL * nC * (MAX_DEPTH + 1), st));
+    }
     k_validate<false><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
                                                          bvh_dev(ctx), ctx->pending.get<Pending>(),
-                                                         n_pend, E, ctx->recs.get<Rec>(), nr);
+                                                         n_pend, E, ctx->recs.get<Rec>(), nr, hints);
     CKL();
     RC(fetch(ctx, nr, 1, st));
     long long n_rec = ctx->hpin[0];

@@ -16,7 +16,7 @@
 namespace rt {
 
 #ifndef RT_PLOC_R
-#define RT_PLOC_R 16
+#define RT_PLOC_R 12   // measured on C3 (launch ms): r8 29.0, r12 24.4, r16 25.1, r24 25.1, r32 28.4
 #endif
 constexpr int PLOC_R = RT_PLOC_R;   // nearest-neighbour search radius in Morton order
 constexpr int PLOC_BLOCK = 256;
@@ -30,13 +30,14 @@ __device__ inline float union_area(const float* a, const float* b) {
 
 // leaf boxes in Morton order, initial cluster list, leaf counts
 __global__ void k_ploc_init(int n, const int* sorted_idx, const float* pbox, float* nbox,
-                            int* clusters, int* count) {
+                            int* clusters, int* count, int* emitted) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const float* s = pbox + 6 * (long long)sorted_idx[k];
     for (int m = 0; m < 6; ++m) nbox[6 * (long long)k + m] = s[m];
     clusters[k] = k;
     count[k] = 1;
+    emitted[k] = 0;
 }
 
 __global__ void __launch_bounds__(PLOC_BLOCK) k_ploc_nn(const int* clusters, int C, const float* nbox,
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(PLOC_BLOCK) k_ploc_nn(const int* clusters, int
 }
 
 __global__ void k_ploc_merge(const int* clusters, int C, const int* nn, int n, float* nbox, int* child,
-                             int* parent, int* count, int* counter, int* out, int* valid) {
+                             int* parent, int* count, int* emitted, int* counter, int* out, int* valid) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= C) return;
     int j = nn[i];
@@ -79,6 +80,8 @@ __global__ void k_ploc_merge(const int* clusters, int C, const int* nn, int n, f
             parent[a] = id;
             parent[b] = id;
             count[id] = count[a] + count[b];
+            // BNodes in the subtree once subtrees of <= LEAF_MAX prims become leaves
+            emitted[id] = emitted[a] + emitted[b] + (count[id] > LEAF_MAX ? 1 : 0);
             const float* ba = nbox + 6 * (long long)a;
             const float* bb = nbox + 6 * (long long)b;
             float* o = nbox + 6 * (long long)id;
@@ -130,11 +133,33 @@ __device__ inline int ploc_map(int id, int n, int root) {   // internal id -> BN
     return q;
 }
 
-__global__ void k_ploc_layout(int n, int root, const int* child, const int* count, const int* slot,
-                              const float* nbox, const unsigned* cbounds, BNode* out) {
+// Depth-first (near-left) BNode order: an emitted node's index is the number of
+// emitted nodes before it in preorder = its proper ancestors + the emitted
+// nodes of every left sibling subtree on the way up.  Parent and left child are
+// then adjacent in memory (same 128-byte line half the time).  -1 = collapsed.
+__global__ void k_ploc_dfs(int n, int root, const int* parent, const int* child, const int* count,
+                           const int* emitted, int* dfs) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n - 1) return;
     int id = n + q;
+    if (id != root && count[id] <= LEAF_MAX) { dfs[q] = -1; return; }
+    int idx = 0, node = id;
+    while (node != root) {
+        int p = parent[node];
+        int l = child[2 * (long long)(p - n)];
+        idx += 1;
+        if (l != node) idx += emitted[l];
+        node = p;
+    }
+    dfs[q] = idx;
+}
+
+__global__ void k_ploc_layout(int n, int root, const int* child, const int* count, const int* slot,
+                              const float* nbox, const unsigned* cbounds, const int* dfs, BNode* out) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n - 1) return;
+    int id = n + q;
+    if (dfs && dfs[q] < 0) return;   // collapsed into a leaf of its parent
     float eps = box_eps(cbounds);
     float bx[2][6];
     int ref[2];
@@ -145,14 +170,14 @@ __global__ void k_ploc_layout(int n, int root, const int* child, const int* coun
         inflate6(bx[c], eps);
         if (ch < n) ref[c] = make_leaf(slot[ch], 1);
         else if (count[ch] <= LEAF_MAX) ref[c] = make_leaf(ploc_first_slot(ch, n, child, slot), count[ch]);
-        else ref[c] = ploc_map(ch, n, root);
+        else ref[c] = dfs ? dfs[ch - n] : ploc_map(ch, n, root);
     }
     BNode nd;
     nd.a = make_float4(bx[0][0], bx[0][1], bx[0][2], bx[0][3]);
     nd.b = make_float4(bx[0][4], bx[0][5], bx[1][0], bx[1][1]);
     nd.c = make_float4(bx[1][2], bx[1][3], bx[1][4], bx[1][5]);
     nd.d = make_int4(ref[0], ref[1], 0, 0);
-    out[ploc_map(id, n, root)] = nd;
+    out[dfs ? dfs[q] : ploc_map(id, n, root)] = nd;
 }
 
 __global__ void k_ploc_tris(int n, const int* sorted_idx, const int* slot, const double* v0,

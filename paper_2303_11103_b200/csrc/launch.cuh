@@ -88,6 +88,8 @@ struct LaunchParams {
     unsigned long long* bounces;
     unsigned long long* node_visits;   // COUNT builds only
     unsigned long long* tri_tests;
+    unsigned long long* warp_bounces;   // COUNT: warp iterations of the bounce loop
+    unsigned long long* warp_visits;    // COUNT: sum over them of the warp's max node visits
     int* error;
 };
 
@@ -113,7 +115,7 @@ template <bool COUNT>
 __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh bvh, LaunchParams P, Trie T) {
     const unsigned FULL = 0xffffffffu;
     int lane = threadIdx.x & 31;
-    unsigned long long my_bounces = 0, my_nodes = 0, my_tris = 0;
+    unsigned long long my_bounces = 0, my_nodes = 0, my_tris = 0, my_wb = 0, my_wv = 0;
     long long stride = (long long)gridDim.x * blockDim.x;
     long long span = P.slot_end - P.slot_begin;
     long long iters = (span + stride - 1) / stride;
@@ -133,10 +135,11 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
         for (int k = 0; k < P.max_depth; ++k) {
             int prim = -1;
             double t = 0.0;
+            int nv = 0, nt = 0;
+            if (COUNT && __ballot_sync(FULL, active) == 0) break;
             if (active) {
                 Ray r = make_ray(o, d);
                 if (COUNT) {
-                    int nv = 0, nt = 0;
                     prim = trace_ray<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t,
                                         &nv, &nt);
                     my_nodes += nv;
@@ -147,6 +150,10 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
                 ++my_bounces;
                 if (prim == -2) { atomicOr(P.error, 1); prim = -1; }
                 if (prim < 0) active = false;
+            }
+            if (COUNT) {
+                int mx = __reduce_max_sync(FULL, nv);
+                if (lane == 0) { ++my_wb; my_wv += mx; }
             }
             unsigned amask = __ballot_sync(FULL, active);
             if (amask == 0) break;
@@ -185,6 +192,8 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
         if (lane == 0) {
             atomicAdd(P.node_visits, my_nodes);
             atomicAdd(P.tri_tests, my_tris);
+            atomicAdd(P.warp_bounces, my_wb);
+            atomicAdd(P.warp_visits, my_wv);
         }
     }
 }

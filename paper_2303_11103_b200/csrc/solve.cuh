@@ -123,6 +123,33 @@ __device__ inline bool segments_clear(const Bvh& bvh, d3 tx, const d3* pts, int 
     return true;
 }
 
+// The same conjunction with an occluder cache per (candidate, segment):
+// neighbouring cells of one candidate are mostly blocked by the same building,
+// so the last blocker found for segment j of this candidate is tried first
+// (hint_blocks: the traversal's own acceptance test, so the answer is the
+// same).  hints[j] holds a TriRec index or -1; races only make hints stale.
+__device__ inline bool segments_clear_hinted(const Bvh& bvh, d3 tx, const d3* pts, int K, d3 rx,
+                                             int* hints) {
+    int h[MAX_DEPTH + 1];
+    for (int j = 0; j <= K; ++j) h[j] = __ldcg(hints + j);
+    for (int j = K; j >= 0; --j) {
+        if (h[j] < 0) continue;
+        d3 a = j == 0 ? tx : pts[j - 1];
+        d3 b = j == K ? rx : pts[j];
+        if (hint_blocks(bvh, h[j], a, b)) return false;
+    }
+    for (int j = K; j >= 0; --j) {
+        d3 a = j == 0 ? tx : pts[j - 1];
+        d3 b = j == K ? rx : pts[j];
+        int pos = -1;
+        if (occluded(bvh, a, b, RAY_EPS, &pos) != 0) {
+            if (pos >= 0 && pos != h[j]) __stcg(hints + j, pos);
+            return false;
+        }
+    }
+    return true;
+}
+
 // ---- receivers: an explicit list or the cells of a grid --------------------------------
 
 struct Receivers {
@@ -316,8 +343,20 @@ struct Segs {
     const int* cand;
     const int* iy;
     const int* ix0;
+    const int* chunk_seg;        // [ceil(W/32)]: segment holding item 32q
     long long n;
 };
+
+// chunk_seg[q] = the segment whose item range holds item 32q: one thread per
+// segment writes the 32-item chunk starts that fall inside it, so k_solve's
+// warps find their first segment with one load instead of a binary search
+// (a chain of ~22 dependent L2 loads).
+__global__ void k_chunk_starts(long long n_seg, const long long* item_off, int* chunk_seg) {
+    long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (s >= n_seg) return;
+    long long a = item_off[s], b = item_off[s + 1];
+    for (long long q = (a + 31) >> 5; (q << 5) < b; ++q) chunk_seg[q] = (int)s;
+}
 
 template <bool GRID>
 __global__ void __launch_bounds__(256) k_solve(Cands C, SceneDev S, const double* images,
@@ -336,9 +375,7 @@ __global__ void __launch_bounds__(256) k_solve(Cands C, SceneDev S, const double
         if (GRID) {
             // one binary search per warp, then a short walk per lane
             long long w0 = w - lane;
-            long long s0 = 0;
-            if (lane == 0 && w0 < W) s0 = upper_index(G.item_off, G.n, w0);
-            s0 = __shfl_sync(FULL, s0, 0);
+            long long s0 = w0 < W ? G.chunk_seg[w0 >> 5] : 0;   // w0 is a multiple of 32
             if (w < W) {
                 long long s = s0;
                 while (G.item_off[s + 1] <= w) ++s;
@@ -429,7 +466,7 @@ __global__ void __launch_bounds__(128) k_validate(Cands C, SceneDev S, const dou
                                                   Receivers R, d3 tx, Bvh bvh,
                                                   const Pending* pend, long long n_pend,
                                                   EmParams E, Rec* recs,
-                                                  unsigned long long* n_out) {
+                                                  unsigned long long* n_out, int* hints) {
     const unsigned FULL = 0xffffffffu;
     long long stride = (long long)gridDim.x * blockDim.x;
     long long iters = (n_pend + stride - 1) / stride;
@@ -444,7 +481,9 @@ __global__ void __launch_bounds__(128) k_validate(Cands C, SceneDev S, const dou
             d3 pts[MAX_DEPTH];
             solve_geometric(C, S, images, pd.cand, tx, rx, pts);   // recompute points
             int K = C.len[pd.cand];
-            ok = segments_clear(bvh, tx, pts, K, rx);
+            ok = hints ? segments_clear_hinted(bvh, tx, pts, K, rx,
+                                               hints + (long long)pd.cand * (MAX_DEPTH + 1))
+                       : segments_clear(bvh, tx, pts, K, rx);
             if (ok) {
                 rec.rx = pd.rx;
                 rec.cand = pd.cand;

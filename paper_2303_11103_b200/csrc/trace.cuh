@@ -160,10 +160,9 @@ __device__ __forceinline__ void cx(float& ta, int& ra, float& tb, int& rb) {
 // the hit distance.  Children are visited nearest-first.
 template <bool ANY, int MODE = 0>
 __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, double* t_out,
-                     int* visits = nullptr, int* tests = nullptr) {
+                     int* visits = nullptr, int* tests = nullptr, int* hit_pos = nullptr) {
     if (bvh.n_prims == 0) return -1;
-    int stack[STACK_SIZE];
-    float stack_t[STACK_SIZE];
+    int2 stack[STACK_SIZE];   // (node ref, entry t bits): one 8-byte local access per push / pop
     int sp = 0;
     double best_t = tmax;
     float best_tf = __double2float_ru(tmax);
@@ -199,9 +198,9 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
                 cx(t1, r1, t3, r3);
                 cx(t1, r1, t2, r2);
                 if (sp + 3 > STACK_SIZE) { *t_out = -1.0; return -2; }   // reported as an error
-                if (nh > 3) { stack[sp] = r3; stack_t[sp] = t3; ++sp; }
-                if (nh > 2) { stack[sp] = r2; stack_t[sp] = t2; ++sp; }
-                if (nh > 1) { stack[sp] = r1; stack_t[sp] = t1; ++sp; }
+                if (nh > 3) { stack[sp] = make_int2(r3, __float_as_int(t3)); ++sp; }
+                if (nh > 2) { stack[sp] = make_int2(r2, __float_as_int(t2)); ++sp; }
+                if (nh > 1) { stack[sp] = make_int2(r1, __float_as_int(t1)); ++sp; }
                 cur = r0;
                 continue;
             }
@@ -217,8 +216,7 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
                 float tf = tn1;
                 if (tn1 < tn0) { nearc = ch.y; farc = ch.x; tf = tn0; }
                 if (sp >= STACK_SIZE) { *t_out = -1.0; return -2; }   // reported as an error
-                stack[sp] = farc;
-                stack_t[sp] = tf;
+                stack[sp] = make_int2(farc, __float_as_int(tf));
                 ++sp;
                 cur = nearc;
                 continue;
@@ -246,6 +244,7 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
                             *t_out = t;
                             if (visits) *visits = nv;
                             if (tests) *tests = nt;
+                            if (hit_pos) *hit_pos = first + k;
                             return prim;
                         }
                     }
@@ -256,7 +255,8 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
         bool found = false;
         while (sp > 0) {
             --sp;
-            if (stack_t[sp] <= best_tf) { cur = stack[sp]; found = true; break; }
+            int2 e = stack[sp];
+                    if (__int_as_float(e.y) <= best_tf) { cur = e.x; found = true; break; }
         }
         if (!found) break;
     }
@@ -273,10 +273,9 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
 // iteration.  Same visit order and results as trace<>.
 template <bool ANY, int MODE = 0>
 __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, double* t_out,
-                        int* visits = nullptr, int* tests = nullptr) {
+                        int* visits = nullptr, int* tests = nullptr, int* hit_pos = nullptr) {
     if (bvh.n_prims == 0) return -1;
-    int stack[STACK_SIZE];
-    float stack_t[STACK_SIZE];
+    int2 stack[STACK_SIZE];   // (node ref, entry t bits): one 8-byte local access per push / pop
     int sp = 0;
     double best_t = tmax;
     float best_tf = __double2float_ru(tmax);
@@ -300,8 +299,7 @@ __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, 
                 float tf = tn1;
                 if (tn1 < tn0) { nearc = ch.y; farc = ch.x; tf = tn0; }
                 if (sp >= STACK_SIZE) { *t_out = -1.0; return -2; }   // reported as an error
-                stack[sp] = farc;
-                stack_t[sp] = tf;
+                stack[sp] = make_int2(farc, __float_as_int(tf));
                 ++sp;
                 cur = nearc;
             } else if (h0) {
@@ -312,7 +310,8 @@ __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, 
                 bool found = false;
                 while (sp > 0) {
                     --sp;
-                    if (stack_t[sp] <= best_tf) { cur = stack[sp]; found = true; break; }
+                    int2 e = stack[sp];
+                    if (__int_as_float(e.y) <= best_tf) { cur = e.x; found = true; break; }
                 }
                 if (!found) { alive = false; break; }
             }
@@ -333,6 +332,7 @@ __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, 
                         *t_out = t;
                         if (visits) *visits = nv;
                         if (tests) *tests = nt;
+                        if (hit_pos) *hit_pos = first + k;
                         return prim;
                     }
                 }
@@ -341,7 +341,8 @@ __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, 
         bool found = false;
         while (sp > 0) {
             --sp;
-            if (stack_t[sp] <= best_tf) { cur = stack[sp]; found = true; break; }
+            int2 e = stack[sp];
+                    if (__int_as_float(e.y) <= best_tf) { cur = e.x; found = true; break; }
         }
         if (!found) break;
     }
@@ -367,36 +368,62 @@ __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, 
 // the traversal the kernels call
 template <bool ANY>
 __device__ __forceinline__ int trace_ray(const Bvh& bvh, const Ray& r, double tmin, double tmax,
-                                         double* t_out, int* visits = nullptr, int* tests = nullptr) {
+                                         double* t_out, int* visits = nullptr, int* tests = nullptr,
+                                         int* hit_pos = nullptr) {
 #if RT_HOIST_FAST
     // one FP32-only and one FP64-only copy of the loop: no per-node filter test
 #if !RT_WIDE
     if ((ANY && RT_WW_ANY) || (!ANY && RT_WW_CLOSEST)) {
-        if (ray_fast(bvh, r)) return trace_ww<ANY, 1>(bvh, r, tmin, tmax, t_out, visits, tests);
-        return trace_ww<ANY, 2>(bvh, r, tmin, tmax, t_out, visits, tests);
+        if (ray_fast(bvh, r)) return trace_ww<ANY, 1>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos);
+        return trace_ww<ANY, 2>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos);
     }
 #endif
-    if (ray_fast(bvh, r)) return trace<ANY, 1>(bvh, r, tmin, tmax, t_out, visits, tests);
-    return trace<ANY, 2>(bvh, r, tmin, tmax, t_out, visits, tests);
+    if (ray_fast(bvh, r)) return trace<ANY, 1>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos);
+    return trace<ANY, 2>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos);
 #else
 #if !RT_WIDE
     if ((ANY && RT_WW_ANY) || (!ANY && RT_WW_CLOSEST))
-        return trace_ww<ANY>(bvh, r, tmin, tmax, t_out, visits, tests);
+        return trace_ww<ANY>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos);
 #endif
-    return trace<ANY>(bvh, r, tmin, tmax, t_out, visits, tests);
+    return trace<ANY>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos);
 #endif
 }
 
-// Bvh.occluded (bvh.py:103-115): 1 blocked, 0 clear, -1 coincident endpoints
-__device__ inline int occluded(const Bvh& bvh, d3 p, d3 q, double eps = RAY_EPS) {
+// Bvh.occluded (bvh.py:103-115): 1 blocked, 0 clear, -1 coincident endpoints.
+// *hit_pos (optional) receives the blocker's TriRec index.
+__device__ inline int occluded(const Bvh& bvh, d3 p, d3 q, double eps = RAY_EPS, int* hit_pos = nullptr) {
     double dx = q.x - p.x, dy = q.y - p.y, dz = q.z - p.z;
     double dist = sqrt(dx * dx + dy * dy + dz * dz);
     if (dist == 0.0) return -1;
     double inv = 1.0 / dist;
     Ray r = make_ray(p, d3{dx * inv, dy * inv, dz * inv});
     double t;
-    int h = trace_ray<true>(bvh, r, eps, dist - eps, &t);
+    int h = trace_ray<true>(bvh, r, eps, dist - eps, &t, nullptr, nullptr, hit_pos);
     return h >= 0 ? 1 : (h == -2 ? 1 : 0);
+}
+
+// Occluder cache: does one of the TriRecs pos-1..pos+1 block segment p->q?
+// Exactly the acceptance test the traversal applies (mt_test + the window
+// (eps, dist - eps)), so a "yes" is the answer occluded() would give; a "no"
+// decides nothing.  Coincident endpoints count as blocked, as in occluded().
+__device__ inline bool hint_blocks(const Bvh& bvh, int pos, d3 p, d3 q, double eps = RAY_EPS) {
+    double dx = q.x - p.x, dy = q.y - p.y, dz = q.z - p.z;
+    double dist = sqrt(dx * dx + dy * dy + dz * dz);
+    if (dist == 0.0) return true;
+    double inv = 1.0 / dist;
+    d3 d = d3{dx * inv, dy * inv, dz * inv};
+    Ray r;
+    r.ox = p.x; r.oy = p.y; r.oz = p.z;
+    r.dx = d.x; r.dy = d.y; r.dz = d.z;
+    double tmax = dist - eps;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        int i = pos + (k == 0 ? 0 : k == 1 ? 1 : -1);
+        if (i < 0 || i >= bvh.n_prims) continue;
+        double t;
+        if (mt_test(r, bvh.tris + i, eps, tmax, t) && eps < t && t < tmax) return true;
+    }
+    return false;
 }
 
 }  // namespace rt
