@@ -97,6 +97,27 @@ def l2_read_bandwidth(bvh):
     return out.value
 
 
+TRAFFIC_JSON = "profiles/r01_traffic.json"
+
+
+def committed_traffic(args):
+    """DRAM bytes per k_launch launch from the committed `ncu --set full` capture of
+    this same workload (tools/ncu_summary.py full ... <json>); None if absent or the
+    capture was of another configuration."""
+    import json as _json
+    path = os.path.join(REPO, TRAFFIC_JSON)
+    if not os.path.exists(path):
+        return None
+    d = _json.load(open(path))
+    if d.get("workload") != workload_name(args) or float(d.get("num_rays", -1)) != float(args.rays) \
+            or int(d.get("max_depth", -1)) != int(args.depth):
+        return None
+    for k, v in d.get("dram_bytes_per_launch", {}).items():
+        if "k_launch" in k:
+            return float(v)
+    return None
+
+
 def n_prims(sc):
     return sum(len(o.triangles) for o in sc.objects)
 
@@ -240,6 +261,7 @@ def run_b200(args):
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     l2_bw = l2_read_bandwidth(bvh)
+    traffic = committed_traffic(args)
     launch_ms = stage_ms[0]
     bounces_per_launch = bounces_local / args.steps
     alg_bytes = bounces_per_launch * (BYTES_PER_NODE * per_bounce_nodes + BYTES_PER_TRI * per_bounce_tris)
@@ -262,7 +284,8 @@ def run_b200(args):
         "stats": stats,
         "roofline": {"bound": "hbm", "kernel": "k_launch",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
+                     "traffic_source": TRAFFIC_JSON if traffic is not None else None,
                      "bytes_per_bounce": BYTES_PER_NODE * per_bounce_nodes + BYTES_PER_TRI * per_bounce_tris,
                      "nodes_per_bounce": per_bounce_nodes, "tris_per_bounce": per_bounce_tris,
                      "simd_efficiency": simd,

@@ -30,31 +30,54 @@ class Hit:
     normal: np.ndarray
 
 
+def _gather_geometry(scene):
+    """One pass over the objects into preallocated arrays: (vertices [V,3] f64,
+    tri_vertex [N,3] i64 with global vertex ids, prim_material [N] i32,
+    material_names, object index of each non-empty object, its triangle count)."""
+    objs = []
+    nv = nt = 0
+    for oi, obj in enumerate(scene.objects):
+        t = np.asarray(obj.triangles, dtype=np.int64).reshape(-1, 3)
+        if not len(t):
+            continue
+        v = np.asarray(obj.vertices, dtype=np.float64).reshape(-1, 3)
+        objs.append((oi, v, t))
+        nv += len(v)
+        nt += len(t)
+    names = list(scene.materials.keys())
+    mindex = {m: i for i, m in enumerate(names)}
+    verts = np.empty((nv, 3), dtype=np.float64)
+    tris = np.empty((nt, 3), dtype=np.int64)
+    pmat = np.empty(nt, dtype=np.int32)
+    obj_ids = np.empty(len(objs), dtype=np.int64)
+    counts = np.empty(len(objs), dtype=np.int64)
+    vb = tb = 0
+    for k, (oi, v, t) in enumerate(objs):
+        verts[vb:vb + len(v)] = v
+        np.add(t, vb, out=tris[tb:tb + len(t)])
+        pmat[tb:tb + len(t)] = mindex.get(scene.objects[oi].material, -1)
+        obj_ids[k] = oi
+        counts[k] = len(t)
+        vb += len(v)
+        tb += len(t)
+    return verts, tris, pmat, names, obj_ids, counts
+
+
+def _prim_ids(obj_ids, counts):
+    """(prim_object, prim_triangle) of the _gather order from per-object counts."""
+    n = int(counts.sum()) if len(counts) else 0
+    prim_object = np.repeat(obj_ids, counts)
+    starts = np.cumsum(counts) - counts
+    prim_triangle = np.arange(n, dtype=np.int64) - np.repeat(starts, counts)
+    return prim_object, prim_triangle
+
+
 def gather_meshes(scene):
     """Flatten objects into (vertices [V,3], tri_vertex [N,3], prim_object, prim_triangle,
     prim_material, material_names) in the reference's global primitive order."""
-    verts, tris, objs, tids = [], [], [], []
-    base = 0
-    for oi, obj in enumerate(scene.objects):
-        t = np.asarray(obj.triangles, dtype=np.int64).reshape(-1, 3)
-        v = np.asarray(obj.vertices, dtype=np.float64).reshape(-1, 3)
-        if not len(t):
-            continue
-        verts.append(v)
-        tris.append(t + base)
-        objs.append(np.full(len(t), oi))
-        tids.append(np.arange(len(t)))
-        base += len(v)
-    names = list(scene.materials.keys())
-    mindex = {m: i for i, m in enumerate(names)}
-    if not tris:
-        z = np.zeros((0, 3))
-        zi = np.zeros(0, dtype=np.int64)
-        return z, np.zeros((0, 3), dtype=np.int64), zi, zi.copy(), np.zeros(0, dtype=np.int32), names
-    prim_object = np.concatenate(objs)
-    mat_of_obj = np.array([mindex.get(o.material, -1) for o in scene.objects], dtype=np.int32)
-    return (np.concatenate(verts), np.concatenate(tris), prim_object, np.concatenate(tids),
-            mat_of_obj[prim_object], names)
+    verts, tris, pmat, names, obj_ids, counts = _gather_geometry(scene)
+    prim_object, prim_triangle = _prim_ids(obj_ids, counts)
+    return verts, tris, prim_object, prim_triangle, pmat, names
 
 
 class Bvh:
@@ -63,8 +86,9 @@ class Bvh:
     def __init__(self, scene, device=None):
         self.ctx = N.acquire_context(device)
         self.device = self.ctx.device
-        (verts, tris, self.prim_object, self.prim_triangle, prim_mat,
-         self.material_names) = gather_meshes(scene)
+        verts, tris, prim_mat, self.material_names, self._obj_ids, self._obj_counts = \
+            _gather_geometry(scene)
+        self._prim_ids = None
         self.num_prims = len(tris)
         self.frequency_hz = float(scene.frequency_hz)
         dev = self.device
@@ -88,6 +112,18 @@ class Bvh:
                 pass
 
     # -- per-primitive arrays (bit-identical to the reference's numpy ones) ------------
+    @property
+    def prim_object(self):
+        if self._prim_ids is None:
+            self._prim_ids = _prim_ids(self._obj_ids, self._obj_counts)
+        return self._prim_ids[0]
+
+    @property
+    def prim_triangle(self):
+        if self._prim_ids is None:
+            self._prim_ids = _prim_ids(self._obj_ids, self._obj_counts)
+        return self._prim_ids[1]
+
     def _fetch_arrays(self):
         if self._arrays is None:
             n = max(self.num_prims, 0)

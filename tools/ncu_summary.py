@@ -43,7 +43,7 @@ KEYS = ["Duration", "Compute (SM) Throughput", "Memory Throughput", "DRAM Throug
         "Warp Cycles Per Issued Instruction", "Branch Efficiency", "Executed Instructions"]
 
 
-def full(path, out):
+def full(path, out, traffic_json=None):
     txt = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
@@ -58,14 +58,16 @@ def full(path, out):
                          text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     rh = rr[0]
+    units = dict(zip(rh, rr[1])) if len(rr) > 1 else {}
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     dram = {}
     stalls = {}
     for r in rr[2:]:
         d = dict(zip(rh, r))
         k = (d.get("ID"), d.get("Kernel Name", "").split("(")[0])
         try:
-            dram[k] = float(d["dram__bytes_read.sum"].replace(",", "")) + float(
-                d["dram__bytes_write.sum"].replace(",", ""))
+            dram[k] = sum(float(d[m].replace(",", "")) * scale.get(units.get(m, "byte"), 1.0)
+                          for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         except (KeyError, ValueError):
             pass
         st = {}
@@ -84,7 +86,7 @@ def full(path, out):
                 if key in m:
                     fh.write(f"- {key}: {m[key]}\n")
             if k in dram:
-                fh.write(f"- dram bytes (read+write): {dram[k]:.4g}\n")
+                fh.write(f"- dram bytes (read+write): {dram[k]:.6g} B\n")
             st = stalls.get(k, {})
             tot = sum(st.values()) or 1.0
             top = sorted(st.items(), key=lambda kv: -kv[1])[:6]
@@ -92,5 +94,14 @@ def full(path, out):
                      ", ".join(f"{n} {100 * v / tot:.0f}%" for n, v in top) + "\n\n")
 
 
+    if traffic_json:   # traffic per kernel for bench.py's roofline "traffic" field
+        import json
+        tr = {}
+        for k, v in dram.items():
+            tr.setdefault(k[1], []).append(v)
+        json.dump({"source": path, "dram_bytes_per_launch": {k: sum(v) / len(v) for k, v in tr.items()}},
+                  open(traffic_json, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full}[sys.argv[1]](*sys.argv[2:])
