@@ -298,6 +298,35 @@ def drivers_case():
     print("drivers:", len(log6.rows), "learn iters,", len(log7.rows), "orient iters", flush=True)
 
 
+def artifacts_case():
+    """Byte formats of the CLI artifacts: the reference's own
+    dump_paths text (tracer.py:314-332), save_cir file (channel.py:75-84) and
+    CoverageMap.save_binary file (channel.py:164-171) for C1 and the small canyon."""
+    import tempfile
+    out = {}
+    for name, sc, depth, meth, nr in (("c1", to_ref(S.ground_box_scene()), 1, "fibonacci", 4096),
+                                       ("canyon", to_ref(_canyon_small()), 3, "fibonacci", 20000)):
+        tree = accel.build(sc)
+        ps = E.compute_paths(sc, tree, depth, method=meth, num_rays=nr)
+        cir = E.build_cir(E.compute_gains(sc, tree, ps))
+        out[f"{name}_scene"] = np.array(scene_json(sc))
+        out[f"{name}_spec"] = np.array([depth, nr])
+        out[f"{name}_dump"] = np.array(E.dump_paths(ps))
+        out[f"{name}_dump_norm"] = np.array(E.dump_paths(ps, normalize_delays=True))
+        with tempfile.TemporaryDirectory() as d:
+            f = os.path.join(d, "cir.bin")
+            E.save_cir(cir, f)
+            out[f"{name}_cir_file"] = np.frombuffer(open(f, "rb").read(), dtype=np.uint8)
+            if name == "c1":
+                grid = GridSpec((-20.0, -40.0), 5.0, 16, 16, 1.5)
+                cm = E.coverage_map(sc, tree, grid, 1, method="exhaustive", num_rays=4096)
+                f = os.path.join(d, "cov.bin")
+                cm.save_binary(f)
+                out["c1_cov_file"] = np.frombuffer(open(f, "rb").read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "artifacts.npz"), **out)
+    print("artifacts: done", flush=True)
+
+
 def main(which=None):
     cases = {
         "soup": soup_case,
@@ -326,6 +355,7 @@ def main(which=None):
         "geo_grads": geo_grad_case,
         "drivers": drivers_case,
         "explicit": explicit_case,
+        "artifacts": artifacts_case,
     }
     for k, fn in cases.items():
         if which and k not in which:
