@@ -219,7 +219,7 @@ __device__ inline void table_geom(const TransferArgs& A, long long p, Geom& g) {
 }
 
 // a[p, s, r] for every path and slant pair (em.py:291-312, 397-405)
-__global__ void k_transfer(TransferArgs A, double* a_out) {
+__global__ void k_transfer(const __grid_constant__ TransferArgs A, double* a_out) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= A.n * A.n_st) return;
     long long p = i / A.n_st;
@@ -236,7 +236,8 @@ __global__ void k_transfer(TransferArgs A, double* a_out) {
     }
 }
 
-__global__ void k_transfer_bwd(TransferArgs A, const double* grad_a, double* grad_eta) {
+__global__ void k_transfer_bwd(const __grid_constant__ TransferArgs A, const double* grad_a,
+                               double* grad_eta) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= A.n * A.n_st * A.n_sr) return;
     long long p = i / (A.n_st * A.n_sr);

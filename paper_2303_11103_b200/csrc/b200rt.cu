@@ -410,7 +410,7 @@ int rt_create(int device, rt_ctx** out) {
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
     if (cudaMallocHost(&ctx->hpin, 64 * sizeof(long long)) != cudaSuccess ||
-        ctx->dflag.reserve(64) != cudaSuccess || ctx->ctrs.reserve(64) != cudaSuccess) {
+        ctx->dflag.reserve(64) != cudaSuccess || ctx->ctrs.reserve(128) != cudaSuccess) {
         delete ctx;
         return RT_ENOMEM;
     }
@@ -655,7 +655,7 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         CK(ctx->t_depth.reserve((size_t)max_nodes));
         CK(cudaMemsetAsync(ctx->t_keys.p, 0xFF, 8 * cap, st));
         CK(cudaMemsetAsync(ctx->t_vals.p, 0xFF, 4 * cap, st));
-        CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
+        CK(cudaMemsetAsync(ctx->ctrs.p, 0, 128, st));
         RC(clear_flags(ctx, st));
         Trie T;
         T.keys = ctx->t_keys.get<unsigned long long>();
@@ -678,14 +678,10 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         P.perm = ctx->perm_band.get<int>();
         P.dirs = dirs;
         P.normals = ctx->nrm.get<double>();
-        P.bounces = reinterpret_cast<unsigned long long*>(ctr + 2);
+        P.stats = reinterpret_cast<unsigned long long*>(ctr + 2);
         P.error = reinterpret_cast<int*>(ctx->dflag.get<long long>());
         const int LB = RT_LAUNCH_BLOCK;
         long long blocks = std::min<long long>((span + LB - 1) / LB, (long long)ctx->n_sm * (4096 / LB));
-        P.node_visits = reinterpret_cast<unsigned long long*>(ctr + 3);
-        P.tri_tests = reinterpret_cast<unsigned long long*>(ctr + 4);
-        P.warp_bounces = reinterpret_cast<unsigned long long*>(ctr + 6);
-        P.warp_visits = reinterpret_cast<unsigned long long*>(ctr + 7);
         PROF_BEGIN(ST_LAUNCH);
         if (span > 0) {
             unsigned g = (unsigned)std::max<long long>(blocks, 1);
@@ -701,11 +697,12 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
             CKL();
         }
         PROF_END(ST_LAUNCH);
-        RC(fetch(ctx, ctr, 8, st));
+        RC(fetch(ctx, ctr, 9, st));
         ctx->counters[1] = ctx->hpin[3];
         ctx->counters[2] = ctx->hpin[4];
         ctx->counters[10] = ctx->hpin[6];
         ctx->counters[11] = ctx->hpin[7];
+        ctx->counters[12] = ctx->hpin[8];
         long long nodes = (long long)(int)(ctx->hpin[0] & 0xffffffff);
         bool overflow = (int)(ctx->hpin[1] & 0xffffffff) != 0;
         long long bounces = ctx->hpin[2];

@@ -200,7 +200,7 @@ struct JvpArgs {
 };
 
 // a[p, s, r] (value) and d a / d theta_w for tangent w: one thread per (p, s, w)
-__global__ void k_transfer_jvp(JvpArgs A, double* a_out /*[P*S*R*2]*/,
+__global__ void k_transfer_jvp(const __grid_constant__ JvpArgs A, double* a_out /*[P*S*R*2]*/,
                                double* jac /*[P*S*R*NJ*2]*/) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= A.n * A.n_st * NJ) return;

@@ -77,6 +77,10 @@ __device__ int trie_insert(const Trie& T, int parent, int prim, int depth) {
     return -1;
 }
 
+// Kept under 128 bytes on purpose: nvcc 12.9 stops scalarising a larger
+// by-value kernel parameter and then (observed on this kernel) forwarded the
+// initial origin P.tx into the bounce loop's o.x update — wrong third-bounce
+// origins.  The counters therefore live behind one pointer.
 struct LaunchParams {
     double tx, ty, tz;
     long long n_rays, slot_begin, slot_end;
@@ -85,13 +89,14 @@ struct LaunchParams {
     const int* perm;          // [B]
     const double* dirs;       // optional [n_rays*3]
     const double* normals;    // [n_prims*3] global order
-    unsigned long long* bounces;
-    unsigned long long* node_visits;   // COUNT builds only
-    unsigned long long* tri_tests;
-    unsigned long long* warp_bounces;   // COUNT: warp iterations of the bounce loop
-    unsigned long long* warp_visits;    // COUNT: sum over them of the warp's max node visits
+    // [0] ray-bounces; COUNT builds: [1] node visits, [2] triangle tests, [3]
+    // reserved (dynamic slot counter), [4] warp iterations of the bounce loop,
+    // [5] sum over them of the warp's max node visits, [6] node visits had
+    // t_max been the hit's t (RT_ORACLE_VISITS experiment)
+    unsigned long long* stats;
     int* error;
 };
+static_assert(sizeof(LaunchParams) <= 128, "see the LaunchParams comment");
 
 // geometry.py:70-76 for one index (on-device sin/cos; see DESIGN.md on ulps)
 __device__ inline d3 fib_dir(long long i, long long n) {
@@ -119,10 +124,11 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
     long long stride = (long long)gridDim.x * blockDim.x;
     long long span = P.slot_end - P.slot_begin;
     long long iters = (span + stride - 1) / stride;
+    const d3 tx = d3{P.tx, P.ty, P.tz};
     for (long long it = 0; it < iters; ++it) {
         long long slot = P.slot_begin + it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
         bool active = slot < P.slot_end;
-        d3 o = d3{P.tx, P.ty, P.tz}, d = d3{0, 0, 0};
+        d3 o = tx, d = d3{0, 0, 0};
         if (active) {
             long long i = slot;
             if (P.band > 0) {
@@ -144,6 +150,16 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
                                         &nv, &nt);
                     my_nodes += nv;
                     my_tris += nt;
+#ifdef RT_ORACLE_VISITS
+                    if (prim >= 0) {   // visits if t_max were known in advance
+                        int nv2 = 0, nt2 = 0;
+                        double t2;
+                        trace_ray<false>(bvh, r, RAY_EPS, t * (1.0 + 1e-9), &t2, &nv2, &nt2);
+                        atomicAdd(P.stats + 6, (unsigned long long)nv2);
+                    } else {
+                        atomicAdd(P.stats + 6, (unsigned long long)nv);
+                    }
+#endif
                 } else {
                     prim = trace_ray<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t);
                 }
@@ -183,17 +199,17 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
     }
     // warp-reduce the bounce count
     for (int s = 16; s; s >>= 1) my_bounces += __shfl_xor_sync(FULL, my_bounces, s);
-    if (lane == 0 && my_bounces) atomicAdd(P.bounces, my_bounces);
+    if (lane == 0 && my_bounces) atomicAdd(P.stats + 0, my_bounces);
     if (COUNT) {
         for (int s = 16; s; s >>= 1) {
             my_nodes += __shfl_xor_sync(FULL, my_nodes, s);
             my_tris += __shfl_xor_sync(FULL, my_tris, s);
         }
         if (lane == 0) {
-            atomicAdd(P.node_visits, my_nodes);
-            atomicAdd(P.tri_tests, my_tris);
-            atomicAdd(P.warp_bounces, my_wb);
-            atomicAdd(P.warp_visits, my_wv);
+            atomicAdd(P.stats + 1, my_nodes);
+            atomicAdd(P.stats + 2, my_tris);
+            atomicAdd(P.stats + 4, my_wb);
+            atomicAdd(P.stats + 5, my_wv);
         }
     }
 }
@@ -210,7 +226,8 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB)
     int lane = threadIdx.x & 31;
     unsigned long long my_bounces = 0, my_nodes = 0, my_tris = 0;
     bool active = false, more = true;
-    d3 o = d3{P.tx, P.ty, P.tz}, d = d3{0, 0, 0};
+    const d3 tx = d3{P.tx, P.ty, P.tz};
+    d3 o = tx, d = d3{0, 0, 0};
     int parent = 0, depth = 0;
     while (true) {
         // refill idle lanes from the global slot counter
@@ -229,7 +246,7 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB)
                         if ((b + 1) * P.band <= P.n_rays) i = b * P.band + P.perm[slot - b * P.band];
                     }
                     d = P.dirs ? ld3(P.dirs + 3 * i) : fib_dir(i, P.n_rays);
-                    o = d3{P.tx, P.ty, P.tz};
+                    o = tx;
                     parent = 0;
                     depth = 0;
                     active = true;
@@ -275,15 +292,15 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB)
         }
     }
     for (int s = 16; s; s >>= 1) my_bounces += __shfl_xor_sync(FULL, my_bounces, s);
-    if (lane == 0 && my_bounces) atomicAdd(P.bounces, my_bounces);
+    if (lane == 0 && my_bounces) atomicAdd(P.stats + 0, my_bounces);
     if (COUNT) {
         for (int s = 16; s; s >>= 1) {
             my_nodes += __shfl_xor_sync(FULL, my_nodes, s);
             my_tris += __shfl_xor_sync(FULL, my_tris, s);
         }
         if (lane == 0) {
-            atomicAdd(P.node_visits, my_nodes);
-            atomicAdd(P.tri_tests, my_tris);
+            atomicAdd(P.stats + 1, my_nodes);
+            atomicAdd(P.stats + 2, my_tris);
         }
     }
 }
