@@ -918,6 +918,16 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
                                                          bvh_dev(ctx), ctx->pending.get<Pending>(),
                                                          n_pend, E, ctx->recs.get<Rec>(), nr, hints);
     CKL();
+#ifdef RT_VALIDATE_STATS
+    {
+        unsigned long long hv[8];
+        cudaMemcpyFromSymbol(hv, g_vstats, sizeof(hv));
+        fprintf(stderr, "validate stats: items %llu rx-hint hits %llu other hint hits %llu traversals %llu "
+                "blocked %llu\n", hv[0], hv[1], hv[4], hv[2], hv[3]);
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(g_vstats, z, sizeof(z));
+    }
+#endif
     RC(fetch(ctx, nr, 1, st));
     long long n_rec = ctx->hpin[0];
     if (power && n_rec > 0) {

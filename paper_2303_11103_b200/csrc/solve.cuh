@@ -128,21 +128,30 @@ __device__ inline bool segments_clear(const Bvh& bvh, d3 tx, const d3* pts, int 
 // so the last blocker found for segment j of this candidate is tried first
 // (hint_blocks: the traversal's own acceptance test, so the answer is the
 // same).  hints[j] holds a TriRec index or -1; races only make hints stale.
+#ifdef RT_VALIDATE_STATS
+__device__ unsigned long long g_vstats[8];   // items, hint hits, traversals, blocked by traversal
+#define VSTAT(i) atomicAdd(&g_vstats[i], 1ULL)
+#else
+#define VSTAT(i) ((void)0)
+#endif
+
 __device__ inline bool segments_clear_hinted(const Bvh& bvh, d3 tx, const d3* pts, int K, d3 rx,
-                                             int* hints) {
+                                             int* hints, int skip = -1) {
     int h[MAX_DEPTH + 1];
     for (int j = 0; j <= K; ++j) h[j] = __ldcg(hints + j);
     for (int j = K; j >= 0; --j) {
-        if (h[j] < 0) continue;
+        if (h[j] < 0 || j == skip) continue;
         d3 a = j == 0 ? tx : pts[j - 1];
         d3 b = j == K ? rx : pts[j];
-        if (hint_blocks(bvh, h[j], a, b)) return false;
+        if (hint_blocks(bvh, h[j], a, b)) { VSTAT(4); return false; }
     }
     for (int j = K; j >= 0; --j) {
         d3 a = j == 0 ? tx : pts[j - 1];
         d3 b = j == K ? rx : pts[j];
         int pos = -1;
+        VSTAT(2);
         if (occluded(bvh, a, b, RAY_EPS, &pos) != 0) {
+            VSTAT(3);
             if (pos >= 0 && pos != h[j]) __stcg(hints + j, pos);
             return false;
         }
@@ -331,11 +340,13 @@ __global__ void k_segments(long long n_cand, long long n_seg, const double* hps,
     seg_cnt[s] = ix1 >= ix0 ? ix1 - ix0 + 1 : 0;
 }
 
-// survivor of the geometric tests
+// survivor of the geometric tests; carries its last interaction point so the
+// validation can try the receiver-side occluder hint before re-solving
 struct Pending {
     long long rx;
     int cand;
-    int pad;
+    int order;
+    double lx, ly, lz;
 };
 
 struct Segs {
@@ -387,9 +398,13 @@ __global__ void __launch_bounds__(256) k_solve(Cands C, SceneDev S, const double
             c = (int)(w % C.n);
             rxi = w / C.n;
         }
+        d3 last = d3{0, 0, 0};
+        int K = 0;
         if (w < W) {
             d3 pts[MAX_DEPTH];
             ok = solve_geometric(C, S, images, c, tx, receiver_pos(R, rxi), pts);
+            K = C.len[c];
+            if (ok) last = pts[K - 1];
         }
         unsigned m = __ballot_sync(FULL, ok);
         if (m) {
@@ -399,7 +414,12 @@ __global__ void __launch_bounds__(256) k_solve(Cands C, SceneDev S, const double
             base = __shfl_sync(FULL, base, leader);
             if (ok) {
                 unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
-                if (slot < cap) { out[slot].rx = rxi; out[slot].cand = c; }
+                if (slot < cap) {
+                    Pending q;
+                    q.rx = rxi; q.cand = c; q.order = K;
+                    q.lx = last.x; q.ly = last.y; q.lz = last.z;
+                    out[slot] = q;
+                }
             }
         }
     }
@@ -478,12 +498,20 @@ __global__ void __launch_bounds__(128) k_validate(Cands C, SceneDev S, const dou
         if (i < n_pend) {
             Pending pd = pend[i];
             d3 rx = receiver_pos(R, pd.rx);
+            int K = pd.order;
+            int* hc = hints ? hints + (long long)pd.cand * (MAX_DEPTH + 1) : nullptr;
+            VSTAT(0);
+            // receiver-side occluder hint first: it needs only the stored last point
+            int hK = hc ? __ldcg(hc + K) : -1;
             d3 pts[MAX_DEPTH];
-            solve_geometric(C, S, images, pd.cand, tx, rx, pts);   // recompute points
-            int K = C.len[pd.cand];
-            ok = hints ? segments_clear_hinted(bvh, tx, pts, K, rx,
-                                               hints + (long long)pd.cand * (MAX_DEPTH + 1))
-                       : segments_clear(bvh, tx, pts, K, rx);
+            if (hK >= 0 && hint_blocks(bvh, hK, d3{pd.lx, pd.ly, pd.lz}, rx)) {
+                VSTAT(1);
+                ok = false;
+            } else {
+                solve_geometric(C, S, images, pd.cand, tx, rx, pts);   // recompute points
+                ok = hc ? segments_clear_hinted(bvh, tx, pts, K, rx, hc, K)
+                        : segments_clear(bvh, tx, pts, K, rx);
+            }
             if (ok) {
                 rec.rx = pd.rx;
                 rec.cand = pd.cand;

@@ -402,7 +402,10 @@ __device__ inline int occluded(const Bvh& bvh, d3 p, d3 q, double eps = RAY_EPS,
     return h >= 0 ? 1 : (h == -2 ? 1 : 0);
 }
 
-// Occluder cache: does one of the TriRecs pos-1..pos+1 block segment p->q?
+#ifndef RT_HINT_R
+#define RT_HINT_R 2   // measured on C3 (validate ms): R0 5.85, R1 3.89, R2 3.84, R4 4.47
+#endif
+// Occluder cache: does one of the TriRecs pos-R..pos+R block segment p->q?
 // Exactly the acceptance test the traversal applies (mt_test + the window
 // (eps, dist - eps)), so a "yes" is the answer occluded() would give; a "no"
 // decides nothing.  Coincident endpoints count as blocked, as in occluded().
@@ -417,8 +420,8 @@ __device__ inline bool hint_blocks(const Bvh& bvh, int pos, d3 p, d3 q, double e
     r.dx = d.x; r.dy = d.y; r.dz = d.z;
     double tmax = dist - eps;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        int i = pos + (k == 0 ? 0 : k == 1 ? 1 : -1);
+    for (int k = 0; k < 2 * RT_HINT_R + 1; ++k) {
+        int i = pos + ((k & 1) ? (k + 1) / 2 : -(k / 2));   // pos, pos+1, pos-1, pos+2, ...
         if (i < 0 || i >= bvh.n_prims) continue;
         double t;
         if (mt_test(r, bvh.tris + i, eps, tmax, t) && eps < t && t < tmax) return true;
