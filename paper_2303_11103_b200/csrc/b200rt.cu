@@ -27,6 +27,13 @@
 #ifndef RT_DFS_LAYOUT
 #define RT_DFS_LAYOUT 1   // depth-first BNode order for the PLOC tree (C3 launch: -0.5%)
 #endif
+#ifndef RT_BAND_C
+// Coherence band B = pow2 >= sqrt(C n) (launch.cuh).  A warp takes 32 azimuth-
+// sorted rays of one band: 32 * 2pi / B wide and 2B / n tall in (azimuth, z),
+// square when B = sqrt(32 pi n).  Measured on C3 (launch ms): C = pi 24.3,
+// 8 pi 23.5, 32 pi 23.5, 128 pi 24.5.
+#define RT_BAND_C 100.53
+#endif
 #ifndef RT_OCC_HINTS
 #define RT_OCC_HINTS 1   // occluder cache in k_validate (solve.cuh segments_clear_hinted)
 #endif
@@ -615,9 +622,9 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         if (n_bounces_out) *n_bounces_out = slot_end - slot_begin;
         return RT_OK;
     }
-    // coherence band: ~sqrt(pi n) indices sorted by azimuth (launch.cuh)
+    // coherence band: ~sqrt(32 pi n) indices sorted by azimuth (launch.cuh)
     int B = 1;
-    while ((double)B * B < 3.14159 * (double)n_rays && B < 65536) B <<= 1;
+    while ((double)B * B < RT_BAND_C * (double)n_rays && B < (1 << 20)) B <<= 1;
     if (B < 32 || B > n_rays) B = 0;
     if (B != ctx->band_B) {
         if (B > 0) {
