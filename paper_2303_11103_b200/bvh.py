@@ -30,10 +30,43 @@ class Hit:
     normal: np.ndarray
 
 
-def _gather_geometry(scene):
+class _PinnedStaging:
+    """Reusable page-locked host buffers for the scene upload: no page faults on
+    refill and truly asynchronous H2D copies.  `ready` is recorded after the
+    copies are enqueued; a refill waits for it first."""
+
+    def __init__(self):
+        self.bufs = {}
+        self.ready = None
+
+    def get(self, name, shape, dtype):
+        n = int(np.prod(shape)) if len(shape) else 1
+        tdt = {np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32}[dtype]
+        b = self.bufs.get(name)
+        if b is None or b.numel() < n:
+            b = torch.empty(max(n, 1), dtype=tdt, pin_memory=True)
+            self.bufs[name] = b
+        return b[:n].numpy().reshape(shape)
+
+
+_STAGING = {}
+
+
+def _staging_for(device):
+    st = _STAGING.get(device)
+    if st is None:
+        st = _STAGING[device] = _PinnedStaging()
+    if st.ready is not None:
+        st.ready.synchronize()
+        st.ready = None
+    return st
+
+
+def _gather_geometry(scene, alloc=None):
     """One pass over the objects into preallocated arrays: (vertices [V,3] f64,
     tri_vertex [N,3] i64 with global vertex ids, prim_material [N] i32,
-    material_names, object index of each non-empty object, its triangle count)."""
+    material_names, object index of each non-empty object, its triangle count).
+    `alloc(name, shape, dtype)` supplies the output arrays (default np.empty)."""
     objs = []
     nv = nt = 0
     for oi, obj in enumerate(scene.objects):
@@ -46,9 +79,12 @@ def _gather_geometry(scene):
         nt += len(t)
     names = list(scene.materials.keys())
     mindex = {m: i for i, m in enumerate(names)}
-    verts = np.empty((nv, 3), dtype=np.float64)
-    tris = np.empty((nt, 3), dtype=np.int64)
-    pmat = np.empty(nt, dtype=np.int32)
+    if alloc is None:
+        def alloc(name, shape, dtype):
+            return np.empty(shape, dtype=dtype)
+    verts = alloc("verts", (nv, 3), np.float64)
+    tris = alloc("tris", (nt, 3), np.int64)
+    pmat = alloc("pmat", (nt,), np.int32)
     obj_ids = np.empty(len(objs), dtype=np.int64)
     counts = np.empty(len(objs), dtype=np.int64)
     vb = tb = 0
@@ -86,16 +122,20 @@ class Bvh:
     def __init__(self, scene, device=None):
         self.ctx = N.acquire_context(device)
         self.device = self.ctx.device
+        staging = _staging_for(self.device)
         verts, tris, prim_mat, self.material_names, self._obj_ids, self._obj_counts = \
-            _gather_geometry(scene)
+            _gather_geometry(scene, staging.get)
         self._prim_ids = None
         self.num_prims = len(tris)
         self.frequency_hz = float(scene.frequency_hz)
         dev = self.device
         with torch.cuda.device(dev):
-            self._verts = torch.from_numpy(np.ascontiguousarray(verts)).to(dev, non_blocking=True)
-            self._tris = torch.from_numpy(np.ascontiguousarray(tris)).to(dev, non_blocking=True)
-            self._pmat = torch.from_numpy(np.ascontiguousarray(prim_mat)).to(dev, non_blocking=True)
+            # pinned staging -> device on the current stream (the library's stream)
+            self._verts = torch.from_numpy(verts).to(dev, non_blocking=True)
+            self._tris = torch.from_numpy(tris).to(dev, non_blocking=True)
+            self._pmat = torch.from_numpy(prim_mat).to(dev, non_blocking=True)
+            staging.ready = torch.cuda.Event()
+            staging.ready.record()
             s = self.ctx.stream
             self.ctx.call("rt_scene_upload", N.ptr(self._verts), len(verts), N.ptr(self._tris),
                           N.ptr(self._pmat), self.num_prims, s)

@@ -34,6 +34,9 @@
 // 8 pi 23.5, 32 pi 23.5, 128 pi 24.5.
 #define RT_BAND_C 100.53
 #endif
+#ifndef RT_PLOC_TAIL
+#define RT_PLOC_TAIL 1   // last PLOC iterations in one block (bvh_ploc.cuh k_ploc_tail)
+#endif
 #ifndef RT_OCC_HINTS
 #define RT_OCC_HINTS 1   // occluder cache in k_validate (solve.cuh segments_clear_hinted)
 #endif
@@ -320,7 +323,16 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
     CK(cudaMemsetAsync(counter, 0, 4, st));
     long long C = n;
     int iters = 0;
+    int root = -1;
     while (C > 1) {
+        if (RT_PLOC_TAIL && C <= PLOC_TAIL) {   // finish in one block, no host round trips
+            k_ploc_tail<<<1, PLOC_TAIL_THREADS, 0, st>>>(ca, (int)C, (int)n, box, child, par, cnt, em,
+                                                          counter, pos);
+            CKL();
+            CK(cudaMemcpyAsync(&root, pos, 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            break;
+        }
         k_ploc_nn<<<nblk(C, PLOC_BLOCK), PLOC_BLOCK, 0, st>>>(ca, (int)C, box, ctx->pl_nn.get<int>());
         CKL();
         k_ploc_merge<<<nblk(C, 256), 256, 0, st>>>(ca, (int)C, ctx->pl_nn.get<int>(), (int)n, box, child,
@@ -340,9 +352,11 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
         std::swap(ca, cb);
         C = C2;
     }
-    int root = 0;
-    CK(cudaMemcpyAsync(&root, ca, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    if (root < 0) {
+        root = 0;
+        CK(cudaMemcpyAsync(&root, ca, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
     ctx->counters[9] = iters;
     int* slot = ctx->pl_slot.get<int>();
     k_ploc_slots<<<nblk(n, 256), 256, 0, st>>>((int)n, par, child, cnt, root, slot);

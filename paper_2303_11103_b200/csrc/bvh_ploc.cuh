@@ -100,6 +100,109 @@ __global__ void k_ploc_merge(const int* clusters, int C, const int* nn, int n, f
     }
 }
 
+// The last PLOC iterations (C <= PLOC_TAIL clusters) in one block: the same
+// nearest-neighbour / mutual-merge / ordered-compaction rules as the
+// k_ploc_nn -> k_ploc_merge -> scan -> k_ploc_compact loop, with block
+// barriers instead of a host round trip per iteration.  Writes the root id.
+constexpr int PLOC_TAIL = 2048;
+constexpr int PLOC_TAIL_THREADS = 1024;
+
+__global__ void __launch_bounds__(PLOC_TAIL_THREADS) k_ploc_tail(const int* clusters_in, int C0, int n,
+                                                                 float* nbox, int* child, int* parent,
+                                                                 int* count, int* emitted, int* counter,
+                                                                 int* root_out) {
+    __shared__ int cl[2][PLOC_TAIL];
+    __shared__ int nn[PLOC_TAIL];
+    __shared__ int warp_sum[PLOC_TAIL_THREADS / 32];
+    __shared__ int total;
+    const int T = PLOC_TAIL_THREADS, PER = PLOC_TAIL / PLOC_TAIL_THREADS;
+    int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < C0; i += T) cl[0][i] = clusters_in[i];
+    int C = C0, cur = 0;
+    __syncthreads();
+    while (C > 1) {
+        const int* c = cl[cur];
+        for (int i = tid; i < C; i += T) {   // nearest neighbour within +-PLOC_R (k_ploc_nn)
+            const float* me = nbox + 6 * (long long)c[i];
+            float m[6];
+            for (int k = 0; k < 6; ++k) m[k] = me[k];
+            float best = INFINITY;
+            int bj = -1;
+            for (int d = -PLOC_R; d <= PLOC_R; ++d) {
+                int j = i + d;
+                if (d == 0 || j < 0 || j >= C) continue;
+                float a = union_area(m, nbox + 6 * (long long)c[j]);
+                if (a < best) { best = a; bj = j; }
+            }
+            nn[i] = bj;
+        }
+        __syncthreads();
+        int out[PER], val[PER];
+        for (int q = 0; q < PER; ++q) {   // mutual nearest neighbours merge (k_ploc_merge)
+            int i = tid * PER + q;
+            out[q] = 0;
+            val[q] = 0;
+            if (i >= C) continue;
+            int j = nn[i];
+            if (j >= 0 && nn[j] == i) {
+                if (i < j) {
+                    int id = n + atomicAdd(counter, 1);
+                    int a = c[i], b = c[j];
+                    child[2 * (long long)(id - n)] = a;
+                    child[2 * (long long)(id - n) + 1] = b;
+                    parent[a] = id;
+                    parent[b] = id;
+                    count[id] = count[a] + count[b];
+                    emitted[id] = emitted[a] + emitted[b] + (count[id] > LEAF_MAX ? 1 : 0);
+                    const float* ba = nbox + 6 * (long long)a;
+                    const float* bb = nbox + 6 * (long long)b;
+                    float* o = nbox + 6 * (long long)id;
+                    for (int m = 0; m < 3; ++m) {
+                        o[m] = fminf(ba[m], bb[m]);
+                        o[3 + m] = fmaxf(ba[3 + m], bb[3 + m]);
+                    }
+                    out[q] = id;
+                    val[q] = 1;
+                }
+            } else {
+                out[q] = c[i];
+                val[q] = 1;
+            }
+        }
+        // ordered compaction: block exclusive scan of the keep flags
+        int mine = 0;
+        for (int q = 0; q < PER; ++q) mine += val[q];
+        int incl = mine;
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) warp_sum[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            int v = lane < T / 32 ? warp_sum[lane] : 0;
+            int w = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            if (lane < T / 32) warp_sum[lane] = w - v;   // exclusive warp offsets
+            if (lane == 31) total = w;
+        }
+        __syncthreads();
+        int pos = warp_sum[wid] + incl - mine;
+        int* nx = cl[cur ^ 1];
+        for (int q = 0; q < PER; ++q)
+            if (val[q]) nx[pos++] = out[q];
+        __threadfence_block();
+        __syncthreads();
+        C = total;
+        cur ^= 1;
+        __syncthreads();
+    }
+    if (tid == 0) *root_out = cl[cur][0];
+}
+
 __global__ void k_ploc_compact(const int* out, const int* valid, const int* pos, int C, int* next) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < C && valid[i]) next[pos[i]] = out[i];

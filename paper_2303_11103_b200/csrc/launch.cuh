@@ -42,12 +42,27 @@ __device__ inline unsigned hash64(unsigned long long k) {
     return (unsigned)k;
 }
 
+#ifndef RT_TRIE_CACHED
+#define RT_TRIE_CACHED 1   // cached first probe (write-once slots); C3 launch -0.15 ms
+#endif
+
 // insert-or-get (parent, prim) -> node id (>= 1); -1 on overflow
 __device__ int trie_insert(const Trie& T, int parent, int prim, int depth) {
     unsigned long long key = ((unsigned long long)(unsigned)parent << 32) | (unsigned)prim;
     unsigned h = hash64(key) & T.mask;
     for (unsigned probe = 0; probe <= T.mask; ++probe) {
+#if RT_TRIE_CACHED
+        // keys and values are write-once, so a cached read is either current
+        // or EMPTY/-1 (stale), and those fall through to the atomic / spin path
+        unsigned long long k = __ldca(T.keys + h);
+        if (k == key) {
+            int v = __ldca(T.vals + h);
+            if (v >= 0) return v;
+        }
+        if (k == EMPTY_KEY) k = *((volatile unsigned long long*)(T.keys + h));
+#else
         unsigned long long k = *((volatile unsigned long long*)(T.keys + h));
+#endif
         if (k == EMPTY_KEY) {
             unsigned long long prev = atomicCAS(T.keys + h, EMPTY_KEY, key);
             if (prev == EMPTY_KEY) {

@@ -25,13 +25,18 @@ def main():
         bvh = P.build(sc)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
+        b2 = P.build(sc)   # second build on a warm pooled context
+        torch.cuda.synchronize()
+        t2b = time.perf_counter()
+        del b2
         g, b = parallel.coverage_map(sc, bvh, grid, args.depth, int(args.rays))
         torch.cuda.synchronize()
         t3 = time.perf_counter()
-        rows.append((t1 - t0, t2 - t1, t3 - t2))
+        rows.append((t1 - t0, t2 - t1, t3 - t2b, t2b - t2))
         del bvh
     for r in rows[2:]:
-        print("gather %.2f ms  build(incl. gather) %.2f ms  coverage %.2f ms" % tuple(1e3 * x for x in r))
+        print("gather %.2f ms  build(incl. gather) %.2f ms  coverage %.2f ms  2nd build %.2f ms"
+              % tuple(1e3 * x for x in r))
 
 
 if __name__ == "__main__":
