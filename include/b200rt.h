@@ -90,6 +90,14 @@ int rt_occluded(rt_ctx* ctx, const double* p, const double* q, int64_t n, int32_
 int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
               int64_t slot_end, int max_depth, const double* dirs, int64_t* n_cand_out,
               int64_t* n_bounces_out, void* stream);
+/* rt_launch over one shard of the lattice for multi-GPU runs (SURVEY 8e stage 1):
+ * whole coherence bands go round-robin to the shard_count ranks, so each rank
+ * traces the same mix of latitudes (contiguous slot ranges would give one rank
+ * the upward rays that escape after one bounce).  The union over shards of
+ * the candidate sets equals the single launch's; bounce counts add up. */
+int rt_launch_shard(rt_ctx* ctx, const double* tx, int64_t n_rays, int shard_index, int shard_count,
+                    int max_depth, const double* dirs, int64_t* n_cand_out, int64_t* n_bounces_out,
+                    void* stream);
 /* enumerate_candidates (tracer.py:196-214); RT_ECAP when n^max_depth > cap */
 int rt_enumerate(rt_ctx* ctx, int max_depth, int64_t cap, int64_t* n_cand_out, void* stream);
 /* install an arbitrary candidate list (device seq [n*max_len] i32 -1 padded,

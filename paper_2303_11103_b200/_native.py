@@ -31,6 +31,7 @@ EXPORTS = [
     "rt_candidates_set", "rt_candidates_get", "rt_num_candidates", "rt_candidates_max_len",
     "rt_paths", "rt_paths_get", "rt_transfer", "rt_transfer_bwd", "rt_coverage",
     "rt_set_profiling", "rt_get_profile", "rt_l2_probe", "rt_transfer_jvp", "rt_solve_pairs",
+    "rt_launch_shard",
 ]
 
 _lib = None
@@ -91,6 +92,7 @@ def lib():
             "rt_trace": (i32, [P, P, P, P, P, i64, i32, P, P, P]),
             "rt_occluded": (i32, [P, P, P, i64, P, P]),
             "rt_launch": (i32, [P, P, i64, i64, i64, i32, P, pi64, pi64, P]),
+            "rt_launch_shard": (i32, [P, P, i64, i32, i32, i32, P, pi64, pi64, P]),
             "rt_enumerate": (i32, [P, i32, i64, pi64, P]),
             "rt_candidates_set": (i32, [P, P, P, i64, i32, pi64, P]),
             "rt_candidates_get": (i32, [P, P, P, i32, P]),

@@ -617,23 +617,61 @@ int rt_occluded(rt_ctx* ctx, const double* p, const double* q, int64_t n, int32_
     return RT_OK;
 }
 
+namespace {
+int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin, int64_t slot_end,
+                int shard_index, int shard_count, int max_depth, const double* dirs,
+                int64_t* n_cand_out, int64_t* n_bounces_out, void* stream);
+}
+
 int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
               int64_t slot_end, int max_depth, const double* dirs, int64_t* n_cand_out,
               int64_t* n_bounces_out, void* stream) {
     if (!ctx || !tx || n_rays < 1 || max_depth < 1)
         return fail(ctx, RT_EINVAL, "need num_rays >= 1 and max_depth >= 1");
-    if (max_depth > MAX_DEPTH) return fail(ctx, RT_EINVAL, "max_depth above the compiled bound (8)");
     if (slot_begin < 0 || slot_end > n_rays || slot_begin > slot_end)
         return fail(ctx, RT_EINVAL, "bad ray slot range");
+    return launch_impl(ctx, tx, n_rays, slot_begin, slot_end, 0, 1, max_depth, dirs, n_cand_out,
+                       n_bounces_out, stream);
+}
+
+int rt_launch_shard(rt_ctx* ctx, const double* tx, int64_t n_rays, int shard_index, int shard_count,
+                    int max_depth, const double* dirs, int64_t* n_cand_out, int64_t* n_bounces_out,
+                    void* stream) {
+    if (!ctx || !tx || n_rays < 1 || max_depth < 1)
+        return fail(ctx, RT_EINVAL, "need num_rays >= 1 and max_depth >= 1");
+    if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
+        return fail(ctx, RT_EINVAL, "bad shard index/count");
+    return launch_impl(ctx, tx, n_rays, 0, 0, shard_index, shard_count, max_depth, dirs, n_cand_out,
+                       n_bounces_out, stream);
+}
+
+}  // extern "C"
+
+namespace {
+int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin, int64_t slot_end,
+                int shard_index, int shard_count, int max_depth, const double* dirs,
+                int64_t* n_cand_out, int64_t* n_bounces_out, void* stream) {
+    if (max_depth > MAX_DEPTH) return fail(ctx, RT_EINVAL, "max_depth above the compiled bound (8)");
     if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ST(stream);
     if (n_bounces_out) *n_bounces_out = 0;
+    // sharded launches take whole coherence bands (units) round-robin, so every
+    // rank gets the same mix of latitudes; local slot l of rank r maps to
+    // global unit (l / unit) * W + r (launch.cuh)
+    auto shard_slots = [&](long long unit) {
+        long long units = (n_rays + unit - 1) / unit;
+        long long mine = shard_index < units ? (units - shard_index + shard_count - 1) / shard_count : 0;
+        long long cnt = mine * unit;
+        long long last = (units - 1) % shard_count == shard_index ? units * unit - n_rays : 0;
+        return std::make_pair(mine * unit, cnt - last);   // (local range, rays owned)
+    };
     if (ctx->n_prims == 0) {
         RC(sort_unique_candidates(ctx, 0, max_depth, st));
         if (n_cand_out) *n_cand_out = 0;
         // every ray still costs one (missing) intersect call
-        if (n_bounces_out) *n_bounces_out = slot_end - slot_begin;
+        if (n_bounces_out)
+            *n_bounces_out = shard_count > 1 ? shard_slots(4096).second : slot_end - slot_begin;
         return RT_OK;
     }
     // coherence band: ~sqrt(32 pi n) indices sorted by azimuth (launch.cuh)
@@ -655,6 +693,11 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
             CK(cudaMemcpy(ctx->perm_band.p, perm.data(), 4 * B, cudaMemcpyHostToDevice));
         }
         ctx->band_B = B;
+    }
+    long long unit = B > 0 ? B : 4096;
+    if (shard_count > 1) {
+        slot_begin = 0;
+        slot_end = shard_slots(unit).first;
     }
     long long span = slot_end - slot_begin;
     // The trie holds one node per unique hit prefix, far fewer than rays x depth
@@ -694,6 +737,9 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         P.n_rays = n_rays;
         P.slot_begin = slot_begin;
         P.slot_end = slot_end;
+        P.shard_unit = unit;
+        P.shard_index = shard_index;
+        P.shard_count = shard_count;
         P.max_depth = max_depth;
         P.band = B;
         P.perm = ctx->perm_band.get<int>();
@@ -706,7 +752,7 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
         PROF_BEGIN(ST_LAUNCH);
         if (span > 0) {
             unsigned g = (unsigned)std::max<long long>(blocks, 1);
-            if (RT_DYNAMIC) {   // persistent grid, dynamic ray fetch from ctr[5]
+            if (RT_DYNAMIC && shard_count == 1) {   // persistent grid, dynamic ray fetch from ctr[5]
                 unsigned long long* sc = reinterpret_cast<unsigned long long*>(ctr + 5);
                 unsigned gp = (unsigned)std::min<long long>(g, (long long)ctx->n_sm * RT_LAUNCH_MINB);
                 if (ctx->prof & 2) k_launch_dyn<true><<<gp, LB, 0, st>>>(bvh_dev(ctx), P, T, sc);
@@ -755,6 +801,9 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
     }
     return fail(ctx, RT_ENOMEM, "candidate trie overflow after growing");
 }
+}  // namespace
+
+extern "C" {
 
 int rt_enumerate(rt_ctx* ctx, int max_depth, int64_t cap, int64_t* n_cand_out, void* stream) {
     if (!ctx) return RT_EINVAL;

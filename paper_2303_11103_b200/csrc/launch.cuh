@@ -99,6 +99,8 @@ __device__ int trie_insert(const Trie& T, int parent, int prim, int depth) {
 struct LaunchParams {
     double tx, ty, tz;
     long long n_rays, slot_begin, slot_end;
+    long long shard_unit;     // sharded launch: local slot l -> global unit (l/unit)*count+index
+    int shard_index, shard_count;
     int max_depth;
     int band;                 // B; 0 disables the permutation
     const int* perm;          // [B]
@@ -143,6 +145,11 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
     for (long long it = 0; it < iters; ++it) {
         long long slot = P.slot_begin + it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
         bool active = slot < P.slot_end;
+        if (P.shard_count > 1) {   // band-interleaved shard (rt_launch_shard)
+            long long lu = slot / P.shard_unit;
+            slot = (lu * P.shard_count + P.shard_index) * P.shard_unit + (slot - lu * P.shard_unit);
+            active = active && slot < P.n_rays;
+        }
         d3 o = tx, d = d3{0, 0, 0};
         if (active) {
             long long i = slot;

@@ -1,8 +1,9 @@
 """Multi-GPU coverage maps: one process per GPU over torch.distributed (NCCL).
 
 SURVEY §8e.  The path shards in two stages with exactly two exchange points:
-  stage 1  rays: rank r launches lattice slots [r n / W, (r+1) n / W); its
-           candidate trie is local.  all_gather of the (padded) candidate
+  stage 1  rays: rank r launches the coherence bands b = r mod W of the
+           Fibonacci lattice (rt_launch_shard; every rank gets the same mix of
+           latitudes, unlike contiguous slot ranges); its candidate trie is local.  all_gather of the (padded) candidate
            rows, then every rank installs the union (sorted + unique on the
            device) so all ranks hold the identical global candidate list.
   stage 2  cells: rank r solves the grid rows iy = r mod W (round-robin rows
@@ -30,6 +31,24 @@ def _dist():
 def shard_range(n: int, rank: int, world: int):
     """Contiguous slot range of one rank (balanced to within one)."""
     return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def band_unit(n: int) -> int:
+    """The launch's coherence band size B (b200rt.cu rt_launch: pow2 >= sqrt(32 pi n),
+    0 below 32 or above n) or the 4096-slot unit used without bands."""
+    b = 1
+    while b * b < 100.53 * n and b < (1 << 20):
+        b <<= 1
+    return 4096 if (b < 32 or b > n) else b
+
+
+def shard_slots(n: int, rank: int, world: int):
+    """Host restatement of rt_launch_shard's slot set: units of band_unit(n)
+    slots, unit u belongs to rank u mod world."""
+    unit = band_unit(n)
+    units = (n + unit - 1) // unit
+    out = [np.arange(u * unit, min((u + 1) * unit, n)) for u in range(rank, units, world)]
+    return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
 
 
 def rows_of_shard(ny: int, rank: int, world: int):
@@ -102,8 +121,7 @@ def coverage_step(scene, bvh, tx_dev, grid, max_depth, num_rays, rank=0, world=1
     """One sharded coverage map with device-resident inputs.
 
     Returns (local ray-bounces, stats, gains tensor [ny, nx] on the device)."""
-    s0, s1 = shard_range(num_rays, rank, world)
-    _, bounces = run_launch(bvh, tx_dev.position, max_depth, num_rays, s0, s1)
+    _, bounces = run_launch(bvh, tx_dev.position, max_depth, num_rays, shard=(rank, world))
     if world > 1:
         seq, ln = get_candidates(bvh)
         seq, ln = gather_candidates(seq, ln, world)

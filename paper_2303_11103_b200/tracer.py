@@ -164,8 +164,12 @@ def _pos3(p):
     return np.ascontiguousarray([float(p[0]), float(p[1]), float(p[2])], dtype=np.float64)
 
 
-def run_launch(bvh: Bvh, tx_pos, max_depth, num_rays, slot_begin=0, slot_end=None, dirs=None):
-    """rt_launch on the device; returns (n_candidates, n_ray_bounces)."""
+def run_launch(bvh: Bvh, tx_pos, max_depth, num_rays, slot_begin=0, slot_end=None, dirs=None,
+               shard=None):
+    """rt_launch on the device; returns (n_candidates, n_ray_bounces).
+
+    shard=(index, count) launches that rank's band-interleaved share of the
+    lattice (rt_launch_shard) instead of the slot range."""
     if num_rays < 1 or max_depth < 1:
         raise TracerError("need num_rays >= 1 and max_depth >= 1")
     slot_end = num_rays if slot_end is None else slot_end
@@ -176,9 +180,14 @@ def run_launch(bvh: Bvh, tx_pos, max_depth, num_rays, slot_begin=0, slot_end=Non
     if dirs is not None:
         d = torch.as_tensor(dirs, dtype=torch.float64, device=bvh.device).reshape(-1, 3).contiguous()
     with torch.cuda.device(bvh.device):
-        bvh.ctx.call("rt_launch", N.ptr(txh), int(num_rays), int(slot_begin), int(slot_end),
-                     int(max_depth), N.ptr(d), ctypes.byref(nc), ctypes.byref(nb), bvh.ctx.stream,
-                     exc_map=_TRACER_ERRORS)
+        if shard is not None and int(shard[1]) > 1:
+            bvh.ctx.call("rt_launch_shard", N.ptr(txh), int(num_rays), int(shard[0]), int(shard[1]),
+                         int(max_depth), N.ptr(d), ctypes.byref(nc), ctypes.byref(nb),
+                         bvh.ctx.stream, exc_map=_TRACER_ERRORS)
+        else:
+            bvh.ctx.call("rt_launch", N.ptr(txh), int(num_rays), int(slot_begin), int(slot_end),
+                         int(max_depth), N.ptr(d), ctypes.byref(nc), ctypes.byref(nb), bvh.ctx.stream,
+                         exc_map=_TRACER_ERRORS)
     return nc.value, nb.value
 
 

@@ -151,6 +151,30 @@ def test_launch_matches_oracle_larger(P):
     assert got == want, (len(got), len(want), sorted(got ^ want)[:10])
 
 
+def test_sharded_launch_union_equals_single_launch(P):
+    """rt_launch_shard (multi-GPU stage 1, band-interleaved): the union of the W
+    shards' candidate sets is the single launch's set and the bounces add up."""
+    from paper_2303_11103_b200 import scenes
+    from paper_2303_11103_b200.tracer import get_candidates, run_launch
+    sc = scenes.street_canyon(n_per_row=100, n_rx=(2, 1))
+    b = _bvh(P, sc)
+    tx = sc.transmitters[0].position
+
+    def cand_set():
+        seq, ln = get_candidates(b)
+        s, n = seq.cpu().numpy(), ln.cpu().numpy()
+        return {tuple(int(x) for x in s[i, :n[i]]) for i in range(len(n))}
+    _, nb = run_launch(b, tx, 3, 300_000)
+    want = cand_set()
+    for w in (2, 3, 8):
+        got, total = set(), 0
+        for r in range(w):
+            _, nbr = run_launch(b, tx, 3, 300_000, shard=(r, w))
+            total += nbr
+            got |= cand_set()
+        assert total == nb and got == want, (w, total, nb, len(got ^ want))
+
+
 @pytest.mark.parametrize("case", ["box", "two_ray", "c1", "canyon"])
 def test_coverage_matches_reference(P, golden, case):
     g = golden(case)

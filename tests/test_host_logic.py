@@ -90,6 +90,23 @@ def test_shard_ranges_cover_every_slot_and_row():
     assert rows == list(range(513))
 
 
+def test_band_interleaved_shards_partition_the_lattice():
+    """rt_launch_shard's slot sets (host restatement): disjoint, cover every slot,
+    whole bands per rank, and balanced latitude mix (mean z equal across ranks)."""
+    from paper_2303_11103_b200.parallel import band_unit, shard_slots
+    for n in (5, 4096, 100_003, 2_000_000):
+        unit = band_unit(n)
+        for w in (1, 2, 3, 8):
+            parts = [shard_slots(n, r, w) for r in range(w)]
+            allv = np.concatenate(parts)
+            assert len(allv) == n and np.array_equal(np.sort(allv), np.arange(n))
+            for r, p in enumerate(parts):
+                assert np.all((p // unit) % w == r)
+            if n >= 2_000_000:
+                z = [np.mean(1.0 - (2.0 * p + 1.0) / n) for p in parts]
+                assert max(abs(v) for v in z) < 0.15, z   # contiguous ranges would give +-0.875
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
