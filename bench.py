@@ -43,7 +43,7 @@ BYTES_PER_NODE = 64    # BNode: two float child boxes + refs (rt_common.cuh)
 BYTES_PER_TRI = 80     # TriRec: FP64 v0/e1/e2 + prim id
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--config", default="c3", choices=["c3", "c5"],
                     help="c3: 200k tris, 512^2 cells, 1e8 rays (default); "
                          "c5: 2M tris, 2048^2 cells, 1e9 rays")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     if args.config == "c5":
         args.side, args.cells = 448, 2048
         if args.rays == 1e8:
