@@ -132,7 +132,7 @@ template <bool COUNT>
 #define RT_LAUNCH_BLOCK 256
 #endif
 #ifndef RT_LAUNCH_MINB
-#define RT_LAUNCH_MINB 3   // <= 85 registers: 24 resident warps per SM (measured best)
+#define RT_LAUNCH_MINB 4   // 64 registers (92 B spill), 32 warps per SM: C3 launch 22.75 vs 23.37 ms (minB 3), 26.9 (minB 5)
 #endif
 __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh bvh, LaunchParams P, Trie T) {
     const unsigned FULL = 0xffffffffu;

@@ -369,8 +369,11 @@ __global__ void k_chunk_starts(long long n_seg, const long long* item_off, int* 
     for (long long q = (a + 31) >> 5; (q << 5) < b; ++q) chunk_seg[q] = (int)s;
 }
 
+#ifndef RT_SOLVE_MINB
+#define RT_SOLVE_MINB 5   // C3 solve 2.01 ms vs 2.16 (no minB), 2.10 (minB 6)
+#endif
 template <bool GRID>
-__global__ void __launch_bounds__(256) k_solve(Cands C, SceneDev S, const double* images,
+__global__ void __launch_bounds__(256, RT_SOLVE_MINB) k_solve(Cands C, SceneDev S, const double* images,
                                                Receivers R, d3 tx, long long W, Segs G,
                                                Pending* out, unsigned long long* n_out,
                                                unsigned long long cap) {
@@ -481,8 +484,11 @@ __device__ inline void probe_powers(const Geom& g, const EmParams& E, double& pt
     pp = ap.re * ap.re + ap.im * ap.im;
 }
 
+#ifndef RT_VAL_MINB
+#define RT_VAL_MINB 8   // 64 registers: C3 validate 3.60 ms vs 4.65 (minB 1, 110 regs), 3.84 (minB 6)
+#endif
 template <bool POWER>
-__global__ void __launch_bounds__(128) k_validate(Cands C, SceneDev S, const double* images,
+__global__ void __launch_bounds__(128, RT_VAL_MINB) k_validate(Cands C, SceneDev S, const double* images,
                                                   Receivers R, d3 tx, Bvh bvh,
                                                   const Pending* pend, long long n_pend,
                                                   EmParams E, Rec* recs,
