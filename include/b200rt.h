@@ -199,6 +199,8 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
  * pairs, 6 valid paths, 10 warp iterations of the launch's bounce loop and
  * 11 the sum over them of the warp's largest per-lane node-visit count (both
  * from the instrumented launch: SIMD efficiency of bounces and traversals),
+ * 13 depth of the last built tree (rt_bvh_build fails with RT_ECAP when it
+ * exceeds the traversal stack),
  * 15 kernel launches issued by the library (cumulative; a CUB device-wide
  * primitive counts once). */
 int rt_set_profiling(rt_ctx* ctx, int flags);

@@ -12,15 +12,19 @@
 #include <vector>
 
 #include "../../include/b200rt.h"
+#ifndef RT_PLOC
+#define RT_PLOC 1   // measured on C3: 30.9 vs 42.2 node visits per bounce (Karras LBVH)
+#endif
+#if RT_PLOC
+#define RT_PLOC_BUILD 1   // depth-verified trees: traversal skips the per-push stack check
+#endif
 #include "api_kernels.cuh"
 #include "bvh_build.cuh"
 #include "bvh_ploc.cuh"
 #include "em_jvp.cuh"
 #include "launch.cuh"
 
-#ifndef RT_PLOC
-#define RT_PLOC 1   // measured on C3: 30.9 vs 42.2 node visits per bounce (Karras LBVH)
-#endif
+
 #ifndef RT_DYNAMIC
 #define RT_DYNAMIC 0
 #endif
@@ -84,6 +88,7 @@ struct rt_ctx {
     DevBuf nodes4, frontier, frontier2, map4, nodes, tris, sorted_idx, morton, morton_alt, idx_alt, child, parent_int, parent_leaf,
         rfirst, rlast, nbox, flags;
     bool bvh_ready = false;
+    int bvh_depth = -1;           // deepest BNode (root 0); -1 = not measured
     double origin_limit = 0.0;
     // candidates
     DevBuf cand_seq, cand_len;
@@ -363,10 +368,21 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
     CKL();
     CK(ctx->nodes.reserve(sizeof(BNode) * std::max<long long>(n - 1, 1)));
     int* dfs = nullptr;
-    if (RT_DFS_LAYOUT && n > 1) {
+    if (n > 1) {   // depth-first order + tree depth (always measured: it bounds the stack)
         dfs = ctx->pl_dfs.get<int>();
-        k_ploc_dfs<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, root, par, child, cnt, em, dfs);
+        int* dmax = reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 15);
+        CK(cudaMemsetAsync(dmax, 0, 4, st));
+        k_ploc_dfs<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, root, par, child, cnt, em, dfs, dmax);
         CKL();
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, dmax, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        ctx->bvh_depth = h;
+        ctx->counters[13] = h;
+        if (!RT_STACK_CHECK && h + 2 > STACK_SIZE)
+            return fail(ctx, RT_ECAP, "BVH depth " + std::to_string(h) + " exceeds the traversal stack (" +
+                                          std::to_string(STACK_SIZE) + " entries)");
+        if (!RT_DFS_LAYOUT) dfs = nullptr;
     }
     if (n > 1) {
         k_ploc_layout<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, root, child, cnt, slot, box,

@@ -241,20 +241,22 @@ __device__ inline int ploc_map(int id, int n, int root) {   // internal id -> BN
 // nodes of every left sibling subtree on the way up.  Parent and left child are
 // then adjacent in memory (same 128-byte line half the time).  -1 = collapsed.
 __global__ void k_ploc_dfs(int n, int root, const int* parent, const int* child, const int* count,
-                           const int* emitted, int* dfs) {
+                           const int* emitted, int* dfs, int* max_depth) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n - 1) return;
     int id = n + q;
     if (id != root && count[id] <= LEAF_MAX) { dfs[q] = -1; return; }
-    int idx = 0, node = id;
+    int idx = 0, node = id, depth = 0;
     while (node != root) {
         int p = parent[node];
         int l = child[2 * (long long)(p - n)];
         idx += 1;
+        ++depth;
         if (l != node) idx += emitted[l];
         node = p;
     }
     dfs[q] = idx;
+    atomicMax(max_depth, depth);   // BNode depth (root 0): bounds the traversal stack
 }
 
 __global__ void k_ploc_layout(int n, int root, const int* child, const int* count, const int* slot,
