@@ -48,9 +48,13 @@ __device__ inline Ray make_ray(d3 o, d3 d) {
     // inf - inf = NaN on one plane and +-inf on the other, which mis-culls a
     // slab the ray lies inside; a 1e-30 direction component moves the ray by
     // < 1e-25 m over any scene, far inside eps_box.
-    r.fix = (float)fmin(fmax(inv_dir(d.x), -1e30), 1e30);
-    r.fiy = (float)fmin(fmax(inv_dir(d.y), -1e30), 1e30);
-    r.fiz = (float)fmin(fmax(inv_dir(d.z), -1e30), 1e30);
+    // FP32 reciprocal of the FP32-rounded component: two roundings (2^-23
+    // relative) instead of the FP64 quotient's one, which the slab32 error
+    // budget absorbs (13 of its 16 units of 2^-24 S); no FP64 divides per bounce.
+    // d = +-0 gives +-inf -> +-1e30: min/max over the two planes is symmetric.
+    r.fix = fminf(fmaxf(__frcp_rn(__double2float_rn(d.x)), -1e30f), 1e30f);
+    r.fiy = fminf(fmaxf(__frcp_rn(__double2float_rn(d.y)), -1e30f), 1e30f);
+    r.fiz = fminf(fmaxf(__frcp_rn(__double2float_rn(d.z)), -1e30f), 1e30f);
     r.oix = (float)o.x * r.fix; r.oiy = (float)o.y * r.fiy; r.oiz = (float)o.z * r.fiz;
     return r;
 }
@@ -59,7 +63,8 @@ __device__ inline Ray make_ray(d3 o, d3 d) {
 // Conservative by construction: node boxes are inflated by eps_box = 2^-20 S
 // (S = max |scene coordinate|).  For |o| <= 2S the spatial error of a plane
 // distance is <= 2^-24 (|o| [origin rounding] + |o| [o*inv rounding] +
-// |bound - o| [1/d rounding] + |t d| [fma rounding]) <= 10 * 2^-24 S < eps_box.
+// 2 |bound - o| [1/d: d rounded to FP32, then rcp] + |t d| [fma rounding])
+// <= (2 + 2 + 6 + 3) * 2^-24 S = 13 * 2^-24 S < eps_box = 16 * 2^-24 S.
 // tmin is rounded down and tmax up by the caller; 1/d is clamped (make_ray)
 // so no plane distance is NaN.
 __device__ __forceinline__ bool slab32(const Ray& r, float lx, float ly, float lz, float hx,
