@@ -95,7 +95,7 @@ struct rt_ctx {
     int64_t n_cand = 0;
     int cand_max_len = 1;
     // launch scratch
-    DevBuf t_keys, t_vals, t_parent, t_prim, t_depth, t_counter, perm_band;
+    DevBuf t_keys, perm_band;
     int band_B = -1;
     uint64_t trie_cap = 0;
     // sort / unique scratch
@@ -727,24 +727,14 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
     }
     for (int attempt = 0; attempt < 6; ++attempt) {
         uint64_t cap = ctx->trie_cap;
-        int max_nodes = (int)std::min<uint64_t>(cap / 2, (1ULL << 31) - 2);
+        if (cap > (1ULL << 31)) return fail(ctx, RT_ENOMEM, "candidate trie above 2^31 slots");
         CK(ctx->t_keys.reserve(8 * cap));
-        CK(ctx->t_vals.reserve(4 * cap));
-        CK(ctx->t_parent.reserve(4ULL * max_nodes));
-        CK(ctx->t_prim.reserve(4ULL * max_nodes));
-        CK(ctx->t_depth.reserve((size_t)max_nodes));
         CK(cudaMemsetAsync(ctx->t_keys.p, 0xFF, 8 * cap, st));
-        CK(cudaMemsetAsync(ctx->t_vals.p, 0xFF, 4 * cap, st));
         CK(cudaMemsetAsync(ctx->ctrs.p, 0, 128, st));
         RC(clear_flags(ctx, st));
         Trie T;
         T.keys = ctx->t_keys.get<unsigned long long>();
-        T.vals = ctx->t_vals.get<int>();
-        T.node_parent = ctx->t_parent.get<int>();
-        T.node_prim = ctx->t_prim.get<int>();
-        T.node_depth = ctx->t_depth.get<signed char>();
         T.mask = (unsigned)(cap - 1);
-        T.max_nodes = max_nodes;
         long long* ctr = ctx->ctrs.get<long long>();
         T.counter = reinterpret_cast<int*>(ctr + 0);
         T.overflow = reinterpret_cast<int*>(ctr + 1);
@@ -790,10 +780,11 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
         bool overflow = (int)(ctx->hpin[1] & 0xffffffff) != 0;
         long long bounces = ctx->hpin[2];
         RC(check_flags(ctx, st));
-        if (overflow) {
+        if (overflow) {   // a probe chain ran out of slots: results incomplete, relaunch
             ctx->trie_cap *= 4;
             continue;
         }
+        if ((uint64_t)nodes * 2 > cap) ctx->trie_cap *= 4;   // keep later launches under half full
         if (n_bounces_out) *n_bounces_out = bounces;
         ctx->counters[0] = bounces;
         // materialize sequences and sort them
@@ -801,10 +792,10 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
         CK(ctx->s_len.reserve((size_t)std::max<long long>(nodes, 1)));
         PROF_BEGIN(ST_TRIE_SEQ);
         if (nodes > 0) {
-            k_trie_sequences<<<nblk(nodes, 256), 256, 0, st>>>((int)nodes, T.node_parent, T.node_prim,
-                                                               T.node_depth, max_depth,
-                                                               ctx->s_seq.get<int>(),
-                                                               ctx->s_len.get<signed char>());
+            k_trie_sequences<<<nblk(cap, 256), 256, 0, st>>>((long long)cap, T.keys, max_depth,
+                                                             ctx->s_seq.get<int>(),
+                                                             ctx->s_len.get<signed char>(),
+                                                             reinterpret_cast<int*>(ctr + 10));
             CKL();
         }
         PROF_END(ST_TRIE_SEQ);

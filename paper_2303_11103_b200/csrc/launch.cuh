@@ -21,16 +21,18 @@ namespace rt {
 
 constexpr unsigned long long EMPTY_KEY = 0xFFFFFFFFFFFFFFFFULL;
 
+// Open-addressing table of trie edges.  A node IS its table slot: the node
+// for prefix (parent node, prim) lives in the slot holding that key and its
+// id is slot + 1 (0 = root, the empty prefix).  Slots are written once (CAS
+// from EMPTY), so an insert needs no id counter and no value publication:
+// the id is known as soon as the key is found or placed.  The node's parent
+// and prim are the key's halves, so the sequences are recovered from the
+// keys alone (k_trie_sequences).
 struct Trie {
     unsigned long long* keys;   // [cap]
-    int* vals;                  // [cap], -1 = not yet published
-    int* node_parent;           // [max_nodes]
-    int* node_prim;
-    signed char* node_depth;
-    unsigned mask;
-    int max_nodes;
-    int* counter;               // nodes allocated (root = 0 is implicit)
-    int* overflow;
+    unsigned mask;              // cap - 1
+    int* counter;               // occupied slots (load factor -> growth)
+    int* overflow;              // a probe sequence ran out of slots: relaunch
 };
 
 __device__ inline unsigned hash64(unsigned long long k) {
@@ -42,49 +44,22 @@ __device__ inline unsigned hash64(unsigned long long k) {
     return (unsigned)k;
 }
 
-#ifndef RT_TRIE_CACHED
-#define RT_TRIE_CACHED 1   // cached first probe (write-once slots); C3 launch -0.15 ms
-#endif
-
-// insert-or-get (parent, prim) -> node id (>= 1); -1 on overflow
-__device__ int trie_insert(const Trie& T, int parent, int prim, int depth) {
+// insert-or-get (parent, prim) -> node id (>= 1); -1 when the table is full
+__device__ int trie_insert(const Trie& T, int parent, int prim) {
     unsigned long long key = ((unsigned long long)(unsigned)parent << 32) | (unsigned)prim;
     unsigned h = hash64(key) & T.mask;
     for (unsigned probe = 0; probe <= T.mask; ++probe) {
-#if RT_TRIE_CACHED
-        // keys and values are write-once, so a cached read is either current
-        // or EMPTY/-1 (stale), and those fall through to the atomic / spin path
+        // write-once slots: a cached read is current or a stale EMPTY, and a
+        // stale EMPTY only sends us to the CAS, which returns the truth
         unsigned long long k = __ldca(T.keys + h);
-        if (k == key) {
-            int v = __ldca(T.vals + h);
-            if (v >= 0) return v;
-        }
-        if (k == EMPTY_KEY) k = *((volatile unsigned long long*)(T.keys + h));
-#else
-        unsigned long long k = *((volatile unsigned long long*)(T.keys + h));
-#endif
+        if (k == key) return (int)h + 1;
         if (k == EMPTY_KEY) {
-            unsigned long long prev = atomicCAS(T.keys + h, EMPTY_KEY, key);
-            if (prev == EMPTY_KEY) {
-                int id = atomicAdd(T.counter, 1) + 1;
-                if (id >= T.max_nodes) {
-                    atomicExch(T.overflow, 1);
-                    atomicExch(T.vals + h, -2);
-                    return -1;
-                }
-                T.node_parent[id] = parent;
-                T.node_prim[id] = prim;
-                T.node_depth[id] = (signed char)depth;
-                __threadfence();
-                atomicExch(T.vals + h, id);
-                return id;
+            k = atomicCAS(T.keys + h, EMPTY_KEY, key);
+            if (k == EMPTY_KEY) {
+                atomicAdd(T.counter, 1);
+                return (int)h + 1;
             }
-            k = prev;
-        }
-        if (k == key) {
-            int v;
-            while ((v = *((volatile int*)(T.vals + h))) == -1) {}
-            return v >= 0 ? v : -1;
+            if (k == key) return (int)h + 1;
         }
         h = (h + 1) & T.mask;
     }
@@ -201,7 +176,7 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
                 int leader = __ffs(peers) - 1;
                 int id = 0;
 #ifndef RT_NO_TRIE
-                if (lane == leader) id = trie_insert(T, parent, prim, k + 1);
+                if (lane == leader) id = trie_insert(T, parent, prim);
 #else
                 id = 1;   // timing experiment only: traversal without candidate bookkeeping
 #endif
@@ -300,7 +275,7 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB)
             unsigned peers = __match_any_sync(hmask, key);
             int leader = __ffs(peers) - 1;
             int id = 0;
-            if (lane == leader) id = trie_insert(T, parent, prim, depth + 1);
+            if (lane == leader) id = trie_insert(T, parent, prim);
             id = __shfl_sync(peers, id, leader);
             parent = id;
             d3 n = ld3(P.normals + 3 * (long long)prim);
@@ -329,19 +304,25 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB)
 
 // ---- candidate materialization ----------------------------------------------------------
 
-// node id (1..n_nodes) -> padded sequence + length
-__global__ void k_trie_sequences(int n_nodes, const int* node_parent, const int* node_prim,
-                                 const signed char* node_depth, int max_len, int* seq,
-                                 signed char* len) {
-    int id = blockIdx.x * blockDim.x + threadIdx.x + 1;
-    if (id > n_nodes) return;
-    int L = node_depth[id];
-    int row = id - 1;
-    for (int k = L; k < max_len; ++k) seq[(long long)row * max_len + k] = -1;
-    int cur = id;
-    for (int k = L - 1; k >= 0; --k) {
-        seq[(long long)row * max_len + k] = node_prim[cur];
-        cur = node_parent[cur];
+// every occupied slot (a trie node) -> one padded sequence row (row order is
+// irrelevant: the rows are sorted next).  The key chain gives the prims from
+// the node up to the root.
+__global__ void k_trie_sequences(long long cap, const unsigned long long* keys, int max_len, int* seq,
+                                 signed char* len, int* rows) {
+    long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (s >= cap) return;
+    unsigned long long k = keys[s];
+    if (k == EMPTY_KEY) return;
+    int L = 1;
+    for (unsigned long long c = k; (int)(c >> 32) != 0; c = keys[(int)(c >> 32) - 1]) ++L;
+    int row = atomicAdd(rows, 1);
+    int* out = seq + (long long)row * max_len;
+    for (int j = L; j < max_len; ++j) out[j] = -1;
+    unsigned long long c = k;
+    for (int j = L - 1; j >= 0; --j) {
+        out[j] = (int)(c & 0xffffffffu);
+        int parent = (int)(c >> 32);
+        if (parent) c = keys[parent - 1];
     }
     len[row] = (signed char)L;
 }
