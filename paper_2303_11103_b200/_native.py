@@ -199,3 +199,36 @@ def acquire_context(device=None) -> Context:
 def release_context(ctx: Context):
     with _pool_lock:
         _pool.setdefault(ctx.device.index, []).append(ctx)
+
+
+class _SmallH2D:
+    """Per-device pinned ring for small parameter uploads: one page-locked
+    buffer, refilled only after the previous copy out of it completed."""
+
+    CAP = 1 << 20
+
+    def __init__(self):
+        self.buf = torch.empty(self.CAP, dtype=torch.uint8, pin_memory=True)
+        self.ready = None
+
+
+_SMALL = {}
+
+
+def h2d(array, device):
+    """Device copy of a small host array via reusable pinned memory (async on
+    the current stream; falls back to a plain copy above 1 MiB)."""
+    a = np.ascontiguousarray(array)
+    if a.nbytes == 0 or a.nbytes > _SmallH2D.CAP:
+        return torch.as_tensor(a, device=device)
+    st = _SMALL.get(device)
+    if st is None:
+        st = _SMALL[device] = _SmallH2D()
+    if st.ready is not None:
+        st.ready.synchronize()
+    view = st.buf[:a.nbytes].numpy().view(a.dtype).reshape(a.shape)
+    view[...] = a
+    out = torch.from_numpy(view).to(device, non_blocking=True)
+    st.ready = torch.cuda.Event()
+    st.ready.record()
+    return out

@@ -64,14 +64,27 @@ def build_cir(gains, los: bool = True, reflection: bool = True,
         kind = (T.order > 0).to(torch.int64)
         keep = ((kind == 0) & los) | ((kind == 1) & reflection)
         idx = torch.nonzero(keep).flatten()
-        rxm = torch.tensor([rx_names.index(n) for n in T.rx_names], device=dev)[T.rx.long()[idx]]
-        txm = torch.tensor([tx_names.index(n) for n in T.tx_names], device=dev)[T.tx.long()[idx]]
+        # table name order -> scene order (identity in the common case: no upload)
+        if list(T.rx_names) == rx_names:
+            rxm = T.rx.long()[idx]
+        else:
+            rxm = N.h2d(np.array([rx_names.index(n) for n in T.rx_names]), dev)[T.rx.long()[idx]]
+        if list(T.tx_names) == tx_names:
+            txm = T.tx.long()[idx]
+        else:
+            txm = N.h2d(np.array([tx_names.index(n) for n in T.tx_names]), dev)[T.tx.long()[idx]]
         pair = rxm * len(tx_names) + txm
         delay = (gains.delay if gains.delay is not None else T.delay)[idx]
         # (pair, delay, kind, seq) lexicographic via stable sorts, least significant first
         order = torch.arange(idx.numel(), device=dev)
-        seqrank = _seq_rank(T.seq[idx], T.order[idx])
-        for key in (seqrank, kind[idx], delay, pair):
+        n_prims = sum(len(o.triangles) for o in scene.objects)
+        seqrank = _seq_rank(T.seq[idx], T.order[idx], n_prims)
+        # (kind, seq) share one key: kind (0 LOS, 1 specular) above the sequence rank,
+        # which is < 2^62 packed or < 2^31 as a rank
+        ks = kind[idx] * (1 << 62) + seqrank if int(T.L) * int(n_prims + 1).bit_length() <= 62 \
+            else None
+        keys = (ks, delay, pair) if ks is not None else (seqrank, kind[idx], delay, pair)
+        for key in keys:
             k = key[order]
             _, o2 = torch.sort(k, stable=True)
             order = order[o2]
@@ -101,12 +114,20 @@ def build_cir(gains, los: bool = True, reflection: bool = True,
     return cir
 
 
-def _seq_rank(seq, order):
+def _seq_rank(seq, order, n_prims=None):
     """Tuple order of the interaction sequences as an integer key."""
     if seq.numel() == 0:
         return torch.zeros(0, dtype=torch.int64, device=seq.device)
     s = seq.to(torch.int64) + 1
     L = s.shape[1]
+    if n_prims is not None and L * int(n_prims + 1).bit_length() <= 63:
+        # columns (prim + 1, 0 = padding) packed most significant first: the
+        # integer order is the tuple order (a prefix sorts first)
+        b = int(n_prims + 1).bit_length()
+        key = s[:, 0]
+        for j in range(1, L):
+            key = (key << b) | s[:, j]
+        return key
     key = torch.zeros(s.shape[0], dtype=torch.int64, device=seq.device)
     # lexicographic rank via successive stable sorts on the columns
     ordr = torch.arange(s.shape[0], device=seq.device)

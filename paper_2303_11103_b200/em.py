@@ -61,7 +61,15 @@ class EvalContext:
         self.positions = positions or {}
 
     def rotation_rows(self, device):
-        return rotation_entries(*self.orientations.get(device.name, device.orientation))
+        ypr = self.orientations.get(device.name, device.orientation)
+        if any(isinstance(v, torch.Tensor) for v in ypr):   # autograd leaves: no memo
+            return rotation_entries(*ypr)
+        key = (float(ypr[0]), float(ypr[1]), float(ypr[2]))   # many receivers share one
+        memo = self.__dict__.setdefault("_rows_memo", {})
+        rows = memo.get(key)
+        if rows is None:
+            rows = memo[key] = rotation_entries(*key)
+        return rows
 
     def eta_table(self, bvh):
         """Complex permittivity per material in the scene's material order, [n_mat, 2]."""
@@ -337,23 +345,33 @@ def _aperture(off, rows):
 
 def _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows, rx_rows):
     """em.py:344-356 for every (tx, rx) pair, vectorized over the path table."""
-    ap_t = [_aperture(off_tx, r) for r in tx_rows]
-    ap_r = [_aperture(off_rx, r) for r in rx_rows]
+    memo = {}   # rows are shared tuples (EvalContext.rotation_rows memo): one aperture each
+
+    def ap(off, r, tag):
+        k = (tag, r) if isinstance(r, tuple) else None
+        if k is None:
+            return _aperture(off, r)
+        v = memo.get(k)
+        if v is None:
+            v = memo[k] = _aperture(off, r)
+        return v
+    ap_t = [ap(off_tx, r, 0) for r in tx_rows]
+    ap_r = [ap(off_rx, r, 1) for r in rx_rows]
     if max(ap_t + ap_r + [0.0]) == 0.0:
         return
     n_rx = len(T.rx_names)
-    pair = (T.tx.long() * n_rx + T.rx.long()).cpu().numpy()
-    length = T.length.cpu().numpy()
-    mins = np.full(len(T.tx_names) * n_rx, np.inf)
-    np.minimum.at(mins, pair, length)
-    for k in np.flatnonzero(np.isfinite(mins)):
+    pair = T.tx.long() * n_rx + T.rx.long()
+    mins_d = torch.full((len(T.tx_names) * n_rx,), float("inf"), dtype=torch.float64,
+                        device=T.length.device)
+    mins_d.scatter_reduce_(0, pair, T.length, reduce="amin")
+    mins = mins_d.cpu().numpy()   # shortest path per (tx, rx) pair: one small read-back
+    a_pair = np.maximum(np.asarray(ap_t)[:, None], np.asarray(ap_r)[None, :]).reshape(-1)
+    fr_pair = 2.0 * a_pair * a_pair / scene.wavelength
+    for k in np.flatnonzero(np.isfinite(mins) & (a_pair > 0.0) & (mins < fr_pair)):
         ti, ri = divmod(int(k), n_rx)
-        aperture = max(ap_t[ti], ap_r[ri])
-        fr = 2.0 * aperture * aperture / scene.wavelength
-        if aperture > 0.0 and mins[k] < fr:
-            warnings.warn(f"path {T.tx_names[ti]}->{T.rx_names[ri]} at {mins[k]:.1f} m is inside "
-                          f"the Fraunhofer distance {fr:.1f} m; the plane-wave synthetic-array "
-                          "assumption degrades here", stacklevel=3)
+        warnings.warn(f"path {T.tx_names[ti]}->{T.rx_names[ri]} at {mins[k]:.1f} m is inside "
+                      f"the Fraunhofer distance {fr_pair[k]:.1f} m; the plane-wave synthetic-array "
+                      "assumption degrades here", stacklevel=3)
 
 
 def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=None) -> ChannelGains:
@@ -382,27 +400,35 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
                                rx_rows_dev, devs, eta)
     tx_idx = T.tx.long()
     rx_idx = T.rx.long()
-    tx_rows = _rows_tensor(tx_rows_dev, dev)[tx_idx].contiguous()
-    rx_rows = _rows_tensor(rx_rows_dev, dev)[rx_idx].contiguous()
     st = sorted(set(float(s) for s in sl_tx))
     sr = sorted(set(float(s) for s in sl_rx))
+    # every small host-side parameter in one pinned upload
+    n_td, n_rd = len(tx_rows_dev), len(rx_rows_dev)
+    parts = [np.asarray(tx_rows_dev, dtype=np.float64).reshape(-1),
+             np.asarray(rx_rows_dev, dtype=np.float64).reshape(-1),
+             np.asarray(off_tx, dtype=np.float64).reshape(-1),
+             np.asarray(off_rx, dtype=np.float64).reshape(-1),
+             np.array([st.index(float(x)) for x in sl_tx], dtype=np.float64),
+             np.array([sr.index(float(x)) for x in sl_rx], dtype=np.float64)]
+    cuts = np.cumsum([0] + [len(x) for x in parts])
+    allp = N.h2d(np.concatenate(parts), dev)
+    seg = [allp[cuts[i]:cuts[i + 1]] for i in range(len(parts))]
+    Rt, Rr = seg[0].reshape(n_td, 3, 3), seg[1].reshape(n_rd, 3, 3)
+    offt, offr = seg[2].reshape(-1, 3), seg[3].reshape(-1, 3)
+    s_index, r_index = seg[4].long(), seg[5].long()
+    tx_rows = Rt.reshape(n_td, 9)[tx_idx].contiguous()
+    rx_rows = Rr.reshape(n_rd, 9)[rx_idx].contiguous()
     if eta is None:
         eta = ctx.eta_table(bvh)
     base = path_coefficients(bvh, T, eta, tx_rows, rx_rows, tx_arr.pattern, rx_arr.pattern, st, sr,
                              lam, scene.frequency_hz)                       # [P, S, R]
     # world-frame element offsets per device (em.py:372-379)
-    Rt = torch.tensor(np.asarray(tx_rows_dev, dtype=np.float64), device=dev)   # [n_tx, 3, 3]
-    Rr = torch.tensor(np.asarray(rx_rows_dev, dtype=np.float64), device=dev)
-    offt = torch.tensor(off_tx, dtype=torch.float64, device=dev)
-    offr = torch.tensor(off_rx, dtype=torch.float64, device=dev)
     off_tx_w = torch.einsum("ek,dmk->dem", offt, Rt)                           # [n_tx, E, 3]
     off_rx_w = torch.einsum("ek,dmk->dem", offr, Rr)
     if scene.synthetic_array:
         _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows_dev, rx_rows_dev)
     ph_tx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", off_tx_w[tx_idx], T.kdep) / lam)
     ph_rx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", off_rx_w[rx_idx], -T.karr) / lam)
-    s_index = torch.tensor([st.index(float(s)) for s in sl_tx], device=dev)
-    r_index = torch.tensor([sr.index(float(s)) for s in sl_rx], device=dev)
     b = base[:, s_index][:, :, r_index].transpose(1, 2)                       # [P, rx_el, tx_el]
     a = b * ph_rx[:, :, None] * ph_tx[:, None, :]
     return ChannelGains(scene, T, a[..., None], np.zeros(1))

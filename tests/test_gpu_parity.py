@@ -516,3 +516,28 @@ def test_c3_full_size_shard_invariance_and_properties(P):
     assert np.isfinite(gh).all() and (gh >= 0).all()
     assert 0 < (gh > 0).sum() < gh.size
     assert st1["candidates"] == len(ln1) and st1["valid_paths"] > 0
+
+
+@pytest.mark.parametrize("rx_x,warns", [(12.0, True), (5000.0, False)])
+def test_fraunhofer_warning_like_reference(P, rx_x, warns):
+    """em.py:344-356 / T/test_em.py:436-445: a 16 m aperture array on a 12 m link
+    warns about the plane-wave assumption; a 5 km link does not."""
+    import warnings as W
+    from paper_2303_11103_b200 import scenes as S
+    from paper_2303_11103_b200.scene import (AntennaArray, RadioDevice, RadioMaterial, Scene,
+                                             SceneObject)
+    v, t = S.quad([(-1e4, -1e4, 0), (1e4, -1e4, 0), (1e4, 1e4, 0), (-1e4, 1e4, 0)])
+    iso = AntennaArray(pattern="iso", polarization="H")
+    big = AntennaArray(num_rows=8, num_cols=8, vertical_spacing=2.0, horizontal_spacing=2.0,
+                       pattern="iso", polarization="H")
+    sc = Scene(1e9, [SceneObject("ground", "ground", v, t)],
+               {"ground": RadioMaterial("ground", "constant", 15.0, 0.015)}, big, iso,
+               [RadioDevice("tx", "tx", np.array([0.0, 0.0, 10.0])),
+                RadioDevice("rx", "rx", np.array([rx_x, 0.0, 10.0]))])
+    b = _bvh(P, sc)
+    ps = P.compute_paths(sc, b, 0)
+    with W.catch_warnings(record=True) as rec:
+        W.simplefilter("always")
+        P.compute_gains(sc, b, ps)
+    hit = [w for w in rec if "Fraunhofer" in str(w.message)]
+    assert bool(hit) == warns
