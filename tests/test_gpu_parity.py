@@ -541,3 +541,23 @@ def test_fraunhofer_warning_like_reference(P, rx_x, warns):
         P.compute_gains(sc, b, ps)
     hit = [w for w in rec if "Fraunhofer" in str(w.message)]
     assert bool(hit) == warns
+
+
+def test_c3_scene_depth5_coverage_matches_oracle(P):
+    """The full C3 city (200k triangles) at depth 5: 1e6 Fibonacci rays, 16x16
+    cells of 3 m around the transmitter, every cell against the C oracle."""
+    import sys
+    import oracle as O
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    sc, tx, _ = bench.make_workload(bench.parse([]))
+    b = _bvh(P, sc)
+    grid = P.GridSpec((float(tx.position[0]) - 24.0, float(tx.position[1]) - 24.0), 3.0, 16, 16, 1.5)
+    cm = P.coverage_map(sc, b, grid, 5, method="fibonacci", num_rays=1_000_000)
+    ob = O.Bvh(O.SceneArrays(sc))
+    want = O.coverage_map(sc, ob, grid.origin, grid.cell_size, grid.nx, grid.ny, grid.height, 5,
+                          method="fibonacci", num_rays=1_000_000)
+    assert np.array_equal(cm.gains == 0.0, want == 0.0)
+    nz = want > 0
+    assert nz.sum() > 0
+    assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz])
