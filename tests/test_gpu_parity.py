@@ -561,3 +561,53 @@ def test_c3_scene_depth5_coverage_matches_oracle(P):
     nz = want > 0
     assert nz.sum() > 0
     assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz])
+
+
+def test_far_origins_take_the_fp64_filter_and_match_oracle(P):
+    """Origins beyond 2 S (S = max |scene coordinate|) use the FP64 slab filter
+    (trace.cuh MODE 2); hits, t and occlusion must still equal the oracle's, and
+    a far transmitter's launch candidates must equal the oracle launch."""
+    import oracle as O
+    from paper_2303_11103_b200 import scenes
+    sc = scenes.city(n_side=4, seed=5)
+    b = _bvh(P, sc)
+    ob = O.Bvh(O.SceneArrays(sc))
+    S = max(float(np.abs(np.asarray(o.vertices)).max()) for o in sc.objects)
+    rng = np.random.RandomState(11)
+    far = rng.normal(size=(3000, 3))
+    far /= np.linalg.norm(far, axis=1)[:, None]
+    o = far * (3.0 * S)
+    o[:, 2] = np.abs(o[:, 2]) + 5.0
+    d = -o + rng.uniform(-0.3 * S, 0.3 * S, o.shape)
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    t, p = b.trace(o, d)
+    ot, op = ob.trace(o, d, 1e-4, np.inf)
+    assert np.array_equal(p.cpu().numpy(), op) and (op >= 0).sum() > 100
+    hit = op >= 0
+    assert np.array_equal(t.cpu().numpy()[hit], ot[hit])
+    q = o + d * (3.5 * S)
+    occ = b.occluded_batch(o, q).cpu().numpy()
+    want = np.array([ob.occluded(a, c) for a, c in zip(o[:1500], q[:1500])])
+    assert np.array_equal(occ[:1500] == 1, want)
+    tx = np.array([2.5 * S, 0.4 * S, 1.2 * S])
+    got = P.launch_candidates(sc, b, tx, 3, 50_000)
+    assert got == O.launch_candidates(ob, tx, 3, 50_000) and len(got) > 0
+
+
+def test_degenerate_arguments_fail_loudly(P):
+    """Error behaviour of the reference API on the device path: max_depth < 0,
+    zero rays, coincident tx/probe, cell cap."""
+    from paper_2303_11103_b200 import scenes
+    from paper_2303_11103_b200.channel import ChannelError
+    from paper_2303_11103_b200.tracer import TracerError
+    sc = scenes.ground_box_scene()
+    b = _bvh(P, sc)
+    tx = [d for d in sc.devices if d.kind == "tx"][0]
+    with pytest.raises(TracerError):
+        P.launch_candidates(sc, b, tx.position, 2, 0)
+    with pytest.raises(TracerError):
+        P.compute_paths(sc, b, -1)
+    with pytest.raises(ChannelError):
+        P.coverage_map(sc, b, P.GridSpec((0.0, 0.0), 1.0, 600, 600, 1.5), 1)
+    with pytest.raises(ValueError):   # tx and probe coincide (channel.py:190-233 via los_path)
+        P.point_path_gain(sc, b, tx, np.asarray(tx.position, dtype=float), 1, "exhaustive", 4096)
