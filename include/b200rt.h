@@ -94,7 +94,10 @@ int rt_launch(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begin,
  * whole coherence bands go round-robin to the shard_count ranks, so each rank
  * traces the same mix of latitudes (contiguous slot ranges would give one rank
  * the upward rays that escape after one bounce).  The union over shards of
- * the candidate sets equals the single launch's; bounce counts add up. */
+ * the candidate sets equals the single launch's; bounce counts add up.  With
+ * shard_count > 1 the shard's candidates are left unsorted (rt_candidates_get
+ * returns them); path / coverage calls refuse them (RT_ESTATE) until the union
+ * is installed with rt_candidates_set, which sorts it once. */
 int rt_launch_shard(rt_ctx* ctx, const double* tx, int64_t n_rays, int shard_index, int shard_count,
                     int max_depth, const double* dirs, int64_t* n_cand_out, int64_t* n_bounces_out,
                     void* stream);
@@ -175,8 +178,9 @@ int rt_transfer_jvp(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* ord
  * receives sum_paths sum_{theta,phi probes} |a|^2 over the current candidate
  * set, with per-cell merge; tx_mode 0 = central element (slants[0]), 1 =
  * coherent sum over n_el elements with world offsets offsets_w [n_el*3] and
- * slants [n_el] (host arrays).  Rows with iy % shard_count == shard_index are
- * computed; other cells are written 0 (sum-allreduce the shards).
+ * slants [n_el] (host arrays).  Rows with (iy / 8) % shard_count == shard_index
+ * (8-row blocks, round-robin) are computed; other cells are written 0
+ * (sum-allreduce the shards).
  * gains_out: device [ny*nx] f64.  stats_out (host [8], may be NULL):
  * work items, geometric pairs, valid paths, cells, candidates. */
 int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,

@@ -93,6 +93,7 @@ struct rt_ctx {
     // candidates
     DevBuf cand_seq, cand_len;
     int64_t n_cand = 0;
+    bool cand_sorted = true;      // false after a sharded launch until rt_candidates_set
     int cand_max_len = 1;
     // launch scratch
     DevBuf t_keys, perm_band;
@@ -239,6 +240,7 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st) {
     ctx->cand_max_len = std::max(L, 1);
     if (n == 0) {
         ctx->n_cand = 0;
+        ctx->cand_sorted = true;
         CK(ctx->cand_seq.reserve(sizeof(int) * ctx->cand_max_len));
         CK(ctx->cand_len.reserve(1));
         return RT_OK;
@@ -290,6 +292,7 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st) {
                                                    ctx->cand_len.get<signed char>());
     CKL();
     ctx->n_cand = n_unique;
+    ctx->cand_sorted = true;
     return RT_OK;
 }
 
@@ -800,7 +803,22 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
         }
         PROF_END(ST_TRIE_SEQ);
         PROF_BEGIN(ST_CAND_SORT);
-        RC(sort_unique_candidates(ctx, nodes, max_depth, st));
+        if (shard_count > 1) {
+            // a shard's rows are unique already; the union of all shards is sorted
+            // once by rt_candidates_set, so skip the per-shard sort
+            ctx->cand_max_len = std::max(max_depth, 1);
+            CK(ctx->cand_seq.reserve(4ULL * std::max<long long>(nodes, 1) * max_depth));
+            CK(ctx->cand_len.reserve((size_t)std::max<long long>(nodes, 1)));
+            if (nodes > 0) {
+                CK(cudaMemcpyAsync(ctx->cand_seq.p, ctx->s_seq.p, 4ULL * nodes * max_depth,
+                                   cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(ctx->cand_len.p, ctx->s_len.p, (size_t)nodes, cudaMemcpyDeviceToDevice, st));
+            }
+            ctx->n_cand = nodes;
+            ctx->cand_sorted = false;
+        } else {
+            RC(sort_unique_candidates(ctx, nodes, max_depth, st));
+        }
         PROF_END(ST_CAND_SORT);
         ctx->counters[3] = ctx->n_cand;
         if (n_cand_out) *n_cand_out = ctx->n_cand;
@@ -850,6 +868,7 @@ int rt_enumerate(rt_ctx* ctx, int max_depth, int64_t cap, int64_t* n_cand_out, v
     CKL();
     CK(cudaStreamSynchronize(st));
     ctx->n_cand = total;
+    ctx->cand_sorted = true;   // enumerated directly in (length, lex) order
     ctx->cand_max_len = max_depth;
     if (n_cand_out) *n_cand_out = total;
     return RT_OK;
@@ -895,6 +914,9 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     SceneDev SD = scene_dev(ctx);
     long long nC = C.n;
     *n_rec_out = 0;
+    if (!ctx->cand_sorted)   // the merge's candidate rank needs the (len, lex) order
+        return fail(ctx, RT_ESTATE, "candidates of a sharded launch: install the union with "
+                                    "rt_candidates_set first");
     if (nC == 0 || R.n == 0) return RT_OK;
     PROF_BEGIN(ST_FOOTPRINT);
     CK(ctx->images.reserve(24ULL * nC * C.max_len));

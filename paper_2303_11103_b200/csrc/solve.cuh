@@ -216,6 +216,32 @@ __device__ inline int clip_poly(const double* px, const double* py, int n, doubl
     return m;
 }
 
+// Stage-2 row shards: blocks of RT_ROW_BLOCK grid rows go round-robin to the
+// shard_count ranks (row iy belongs to shard (iy / RB) % count).  Blocks keep a
+// candidate's footprint rows together on one rank (occluder hints stay warm)
+// while the round-robin keeps the valid-path density balanced.
+#ifndef RT_ROW_BLOCK
+#define RT_ROW_BLOCK 8
+#endif
+__host__ __device__ inline bool row_in_shard(long long iy, int index, int count) {
+    return (iy / RT_ROW_BLOCK) % count == index;
+}
+
+// rows of [0, x] owned by the shard
+__host__ __device__ inline long long shard_rows_upto(long long x, int index, int count) {
+    long long n = x + 1, nb = n / RT_ROW_BLOCK, rem = n - nb * RT_ROW_BLOCK;
+    long long full = nb > index ? (nb - index + count - 1) / count : 0;
+    return full * RT_ROW_BLOCK + ((nb % count == index) ? rem : 0);
+}
+
+// the s-th owned row at or after `first` (an owned row)
+__host__ __device__ inline long long shard_row(long long first, long long s, int count) {
+    long long bf = first / RT_ROW_BLOCK, off = first - bf * RT_ROW_BLOCK;
+    if (s < RT_ROW_BLOCK - off) return first + s;
+    long long t = s - (RT_ROW_BLOCK - off);
+    return (bf + (t / RT_ROW_BLOCK + 1) * count) * RT_ROW_BLOCK + t % RT_ROW_BLOCK;
+}
+
 __global__ void k_halfplanes(Cands C, SceneDev S, const double* images, Receivers R,
                              int shard_index, int shard_count, double* hps /*[n*HP_MAX*3]*/,
                              int* nhp, int* row0, long long* seg_counts /*[n+1]*/) {
@@ -279,8 +305,12 @@ __global__ void k_halfplanes(Cands C, SceneDev S, const double* images, Receiver
         long long iy0 = (long long)fmax(floor((ylo - R.oy) / R.cell - 0.5) - 1.0, 0.0);
         long long iy1 = (long long)fmin(ceil((yhi - R.oy) / R.cell - 0.5) + 1.0, (double)(R.ny - 1));
         if (iy0 <= iy1) {
-            first = iy0 + ((shard_index - iy0 % shard_count) + shard_count) % shard_count;
-            rows = first <= iy1 ? (iy1 - first) / shard_count + 1 : 0;
+            long long b0 = iy0 / RT_ROW_BLOCK;
+            long long bf = b0 + ((shard_index - b0 % shard_count) + shard_count) % shard_count;
+            first = bf == b0 ? iy0 : bf * RT_ROW_BLOCK;
+            rows = first <= iy1 ? shard_rows_upto(iy1, shard_index, shard_count) -
+                                      shard_rows_upto(first - 1, shard_index, shard_count)
+                                : 0;
         }
     }
     row0[c] = (int)first;
@@ -331,7 +361,7 @@ __global__ void k_segments(long long n_cand, long long n_seg, const double* hps,
     if (s >= n_seg) return;
     long long c = c0;
     while (seg_off[c + 1] <= s) ++c;
-    long long iy = row0[c] + (s - seg_off[c]) * shard_count;
+    long long iy = shard_row(row0[c], s - seg_off[c], shard_count);
     long long ix0, ix1;
     row_interval(hps + c * HP_MAX * 3, nhp[c], R, iy, ix0, ix1);
     seg_cand[s] = (int)c;
@@ -625,7 +655,7 @@ __global__ void k_los(Receivers R, d3 tx, Bvh bvh, SceneDev S, EmParams E,
     if (r >= R.n) return;
     if (COVERAGE) {
         long long iy = r / R.nx;
-        if (iy % shard_count != shard_index) { gains[r] = 0.0; return; }
+        if (!row_in_shard(iy, shard_index, shard_count)) { gains[r] = 0.0; return; }
     }
     d3 rx = receiver_pos(R, r);
     // np.allclose(tx, rx): |a-b| <= 1e-8 + 1e-5 |b|

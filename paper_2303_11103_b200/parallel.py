@@ -6,9 +6,10 @@ SURVEY §8e.  The path shards in two stages with exactly two exchange points:
            latitudes, unlike contiguous slot ranges); its candidate trie is local.  all_gather of the (padded) candidate
            rows, then every rank installs the union (sorted + unique on the
            device) so all ranks hold the identical global candidate list.
-  stage 2  cells: rank r solves the grid rows iy = r mod W (round-robin rows
-           balance the valid-path density); other rows stay 0 and a sum
-           all_reduce of the [ny, nx] grid assembles the map.
+  stage 2  cells: rank r solves the grid rows of the 8-row blocks b = r mod W
+           (round-robin blocks balance the valid-path density and keep a
+           footprint's rows together); other rows stay 0 and a sum all_reduce
+           of the [ny, nx] grid assembles the map.
 Per-cell merging needs every candidate of that cell, so candidates are never
 sharded in stage 2.  The collectives work on any backend (gloo on CPU for
 the host-logic tests, NCCL over NVLink on the GPU box).
@@ -51,8 +52,12 @@ def shard_slots(n: int, rank: int, world: int):
     return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
 
 
+ROW_BLOCK = 8   # solve.cuh RT_ROW_BLOCK
+
+
 def rows_of_shard(ny: int, rank: int, world: int):
-    return list(range(rank, ny, world))
+    """Grid rows of one stage-2 shard: blocks of ROW_BLOCK rows round-robin."""
+    return [iy for iy in range(ny) if (iy // ROW_BLOCK) % world == rank]
 
 
 def barrier(world):

@@ -174,6 +174,11 @@ def test_sharded_launch_union_equals_single_launch(P):
             total += nbr
             got |= cand_set()
         assert total == nb and got == want, (w, total, nb, len(got ^ want))
+    # a shard's candidates are unsorted until the union is installed: refused
+    from paper_2303_11103_b200.channel import coverage_from_candidates
+    grid = P.GridSpec((0.0, -10.0), 5.0, 4, 4, 1.5)
+    with pytest.raises(Exception, match="rt_candidates_set"):
+        coverage_from_candidates(sc, b, sc.transmitters[0], grid)
 
 
 @pytest.mark.parametrize("case", ["box", "two_ray", "c1", "canyon"])
