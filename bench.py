@@ -250,6 +250,7 @@ def run_b200(args):
     simd = {"bounce_lanes": float(ctr[0]) / max(32.0 * ctr[10], 1.0),
             "traversal_lanes": float(ctr[1]) / max(32.0 * ctr[11], 1.0)}
     simd["bvh_depth"] = int(ctr[13])
+    simd["bvh_sah_node_visits"] = float(ctr[14]) / 1000.0   # 1 + sum internal-child area / root area
     if ctr[12] > 0:   # RT_ORACLE_VISITS builds: node visits had t_max been known in advance
         simd["oracle_nodes_per_bounce"] = float(ctr[12]) / max(ctr[0], 1)
 

@@ -205,6 +205,8 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
  * from the instrumented launch: SIMD efficiency of bounces and traversals),
  * 13 depth of the last built tree (rt_bvh_build fails with RT_ECAP when it
  * exceeds the traversal stack),
+ * 14 1000 x the tree's surface-area estimate of internal-node visits per ray
+ * (1 + sum of internal child box areas / root area),
  * 15 kernel launches issued by the library (cumulative; a CUB device-wide
  * primitive counts once). */
 int rt_set_profiling(rt_ctx* ctx, int flags);

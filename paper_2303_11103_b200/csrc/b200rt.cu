@@ -395,6 +395,19 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
     k_ploc_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, slot, ctx->v0.get<double>(), ctx->e1.get<double>(),
                                               ctx->e2.get<double>(), ctx->tris.get<TriRec>());
     CKL();
+    if (n > 2 && dfs) {   // tree cost diagnostic (counters 13/14): emitted nodes = em[root]
+        int n_nodes = 0;
+        CK(cudaMemcpyAsync(&n_nodes, em + root, 4, cudaMemcpyDeviceToHost, st));
+        double* sums = reinterpret_cast<double*>(ctx->ctrs.get<long long>() + 12);
+        CK(cudaMemsetAsync(sums, 0, 24, st));
+        CK(cudaStreamSynchronize(st));
+        k_tree_sah<<<nblk(n_nodes, 256), 256, 0, st>>>(ctx->nodes.get<BNode>(), n_nodes, sums);
+        CKL();
+        double h[3];
+        CK(cudaMemcpyAsync(h, sums, 24, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        ctx->counters[14] = (long long)llround(1000.0 * (1.0 + h[0] / h[2]));   // milli-visits
+    }
     return RT_OK;
 }
 

@@ -16,7 +16,7 @@
 namespace rt {
 
 #ifndef RT_PLOC_R
-#define RT_PLOC_R 12   // measured on C3 (launch ms): r8 29.0, r12 24.4, r16 25.1, r24 25.1, r32 28.4
+#define RT_PLOC_R 24   // with isotropic Morton codes, C3 launch over 6 tx: r16 58.6, r24 58.1 ms (r32 worse on C3)
 #endif
 constexpr int PLOC_R = RT_PLOC_R;   // nearest-neighbour search radius in Morton order
 constexpr int PLOC_BLOCK = 256;
@@ -283,6 +283,34 @@ __global__ void k_ploc_layout(int n, int root, const int* child, const int* coun
     nd.c = make_float4(bx[1][2], bx[1][3], bx[1][4], bx[1][5]);
     nd.d = make_int4(ref[0], ref[1], 0, 0);
     out[dfs ? dfs[q] : ploc_map(id, n, root)] = nd;
+}
+
+// Surface-area cost of the laid-out tree (diagnostic, reported by the bench):
+// sums[0] = sum of internal-child box areas, sums[1] = sum of leaf box area x
+// triangle count, sums[2] = root area; expected internal-node visits of a
+// random ray ~ 1 + sums[0] / sums[2], expected triangle tests ~ sums[1] / sums[2].
+__global__ void k_tree_sah(const BNode* nodes, int n_nodes, double* sums) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_nodes) return;
+    BNode nd = nodes[q];
+    float b[2][6] = {{nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.b.x, nd.b.y},
+                     {nd.b.z, nd.b.w, nd.c.x, nd.c.y, nd.c.z, nd.c.w}};
+    int ref[2] = {nd.d.x, nd.d.y};
+    double in = 0.0, lf = 0.0;
+    for (int c = 0; c < 2; ++c) {
+        double dx = b[c][3] - b[c][0], dy = b[c][4] - b[c][1], dz = b[c][5] - b[c][2];
+        double sa = dx * dy + dy * dz + dz * dx;
+        if (ref_is_leaf(ref[c])) lf += sa * leaf_count(ref[c]);
+        else in += sa;
+    }
+    atomicAdd(sums + 0, in);
+    atomicAdd(sums + 1, lf);
+    if (q == 0) {
+        double lx = fmin(b[0][0], b[1][0]), ly = fmin(b[0][1], b[1][1]), lz = fmin(b[0][2], b[1][2]);
+        double hx = fmax(b[0][3], b[1][3]), hy = fmax(b[0][4], b[1][4]), hz = fmax(b[0][5], b[1][5]);
+        double dx = hx - lx, dy = hy - ly, dz = hz - lz;
+        sums[2] = dx * dy + dy * dz + dz * dx;
+    }
 }
 
 __global__ void k_ploc_tris(int n, const int* sorted_idx, const int* slot, const double* v0,
