@@ -89,6 +89,7 @@ struct rt_ctx {
         rfirst, rlast, nbox, flags;
     bool bvh_ready = false;
     int bvh_depth = -1;           // deepest BNode (root 0); -1 = not measured
+    bool tail_smem_set = false;   // k_ploc_tail's dynamic shared memory opt-in done
     double origin_limit = 0.0;
     // candidates
     DevBuf cand_seq, cand_len;
@@ -329,36 +330,53 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
     CKL();
     int* counter = reinterpret_cast<int*>(ctx->ctrs.get<long long>());
     CK(cudaMemsetAsync(counter, 0, 4, st));
+    // live cluster counts (ping-pong): the loop runs PLOC_BATCH iterations per
+    // host sync, sizing grids by the last count it read (an upper bound)
+    int* dC[2] = {reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 10),
+                  reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 11)};
+    {
+        int n32 = (int)n;
+        CK(cudaMemcpyAsync(dC[0], &n32, 4, cudaMemcpyHostToDevice, st));
+    }
     long long C = n;
-    int iters = 0;
+    int iters = 0, cur = 0;
     int root = -1;
+    const int PLOC_BATCH = 4;
     while (C > 1) {
         if (RT_PLOC_TAIL && C <= PLOC_TAIL) {   // finish in one block, no host round trips
-            k_ploc_tail<<<1, PLOC_TAIL_THREADS, 0, st>>>(ca, (int)C, (int)n, box, child, par, cnt, em,
-                                                          counter, pos);
+            if (!ctx->tail_smem_set) {   // 48 KB of staged boxes: opt in once per context
+                CK(cudaFuncSetAttribute(k_ploc_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        PLOC_TAIL_SMEM));
+                ctx->tail_smem_set = true;
+            }
+            k_ploc_tail<<<1, PLOC_TAIL_THREADS, PLOC_TAIL_SMEM, st>>>(ca, (int)C, (int)n, box, child, par,
+                                                                       cnt, em, counter, pos);
             CKL();
             CK(cudaMemcpyAsync(&root, pos, 4, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             break;
         }
-        k_ploc_nn<<<nblk(C, PLOC_BLOCK), PLOC_BLOCK, 0, st>>>(ca, (int)C, box, ctx->pl_nn.get<int>());
-        CKL();
-        k_ploc_merge<<<nblk(C, 256), 256, 0, st>>>(ca, (int)C, ctx->pl_nn.get<int>(), (int)n, box, child,
-                                                    par, cnt, em, counter, ctx->pl_out.get<int>(), valid);
-        CKL();
-        RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
-            return cub::DeviceScan::ExclusiveSum(tmp, bytes, valid, pos, (int)C, st);
-        }));
-        int h[2] = {0, 0};
-        CK(cudaMemcpyAsync(&h[0], pos + C - 1, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&h[1], valid + C - 1, 4, cudaMemcpyDeviceToHost, st));
+        for (int b = 0; b < PLOC_BATCH; ++b, ++iters) {
+            k_ploc_nn<<<nblk(C, PLOC_BLOCK), PLOC_BLOCK, 0, st>>>(ca, dC[cur], box, ctx->pl_nn.get<int>());
+            CKL();
+            k_ploc_merge<<<nblk(C, 256), 256, 0, st>>>(ca, dC[cur], (int)C, ctx->pl_nn.get<int>(), (int)n, box,
+                                                        child, par, cnt, em, counter, ctx->pl_out.get<int>(),
+                                                        valid);
+            CKL();
+            RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+                return cub::DeviceScan::ExclusiveSum(tmp, bytes, valid, pos, (int)C, st);
+            }));
+            k_ploc_compact<<<nblk(C, 256), 256, 0, st>>>(ctx->pl_out.get<int>(), valid, pos, dC[cur], cb,
+                                                          dC[cur ^ 1]);
+            CKL();
+            std::swap(ca, cb);
+            cur ^= 1;
+        }
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, dC[cur], 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        long long C2 = (long long)h[0] + h[1];
-        if (C2 >= C || ++iters > 100000) return fail(ctx, RT_ECUDA, "PLOC made no progress");
-        k_ploc_compact<<<nblk(C, 256), 256, 0, st>>>(ctx->pl_out.get<int>(), valid, pos, (int)C, cb);
-        CKL();
-        std::swap(ca, cb);
-        C = C2;
+        if (h >= C || iters > 100000) return fail(ctx, RT_ECUDA, "PLOC made no progress");
+        C = h;
     }
     if (root < 0) {
         root = 0;

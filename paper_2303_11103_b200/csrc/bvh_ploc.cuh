@@ -40,8 +40,12 @@ __global__ void k_ploc_init(int n, const int* sorted_idx, const float* pbox, flo
     emitted[k] = 0;
 }
 
-__global__ void __launch_bounds__(PLOC_BLOCK) k_ploc_nn(const int* clusters, int C, const float* nbox,
-                                                       int* nn) {
+// The iteration kernels read the live cluster count C from device memory (the
+// host only knows an upper bound between its occasional syncs).
+__global__ void __launch_bounds__(PLOC_BLOCK) k_ploc_nn(const int* clusters, const int* dC,
+                                                       const float* nbox, int* nn) {
+    const int C = *dC;
+    if ((int)(blockIdx.x * PLOC_BLOCK) >= C) return;
     __shared__ float sb[PLOC_BLOCK + 2 * PLOC_R][6];
     int base = blockIdx.x * PLOC_BLOCK;
     for (int k = threadIdx.x; k < PLOC_BLOCK + 2 * PLOC_R; k += blockDim.x) {
@@ -66,10 +70,15 @@ __global__ void __launch_bounds__(PLOC_BLOCK) k_ploc_nn(const int* clusters, int
     nn[i] = bj;
 }
 
-__global__ void k_ploc_merge(const int* clusters, int C, const int* nn, int n, float* nbox, int* child,
-                             int* parent, int* count, int* emitted, int* counter, int* out, int* valid) {
+__global__ void k_ploc_merge(const int* clusters, const int* dC, int Cmax, const int* nn, int n, float* nbox,
+                             int* child, int* parent, int* count, int* emitted, int* counter, int* out,
+                             int* valid) {
+    const int C = *dC;
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= C) return;
+    if (i >= C) {   // the scan runs over the host's bound Cmax
+        if (i < Cmax) valid[i] = 0;
+        return;
+    }
     int j = nn[i];
     if (j >= 0 && nn[j] == i) {
         if (i < j) {
@@ -106,6 +115,7 @@ __global__ void k_ploc_merge(const int* clusters, int C, const int* nn, int n, f
 // barriers instead of a host round trip per iteration.  Writes the root id.
 constexpr int PLOC_TAIL = 2048;
 constexpr int PLOC_TAIL_THREADS = 1024;
+constexpr int PLOC_TAIL_SMEM = PLOC_TAIL * 6 * 4;   // dynamic shared memory of k_ploc_tail
 
 __global__ void __launch_bounds__(PLOC_TAIL_THREADS) k_ploc_tail(const int* clusters_in, int C0, int n,
                                                                  float* nbox, int* child, int* parent,
@@ -115,6 +125,7 @@ __global__ void __launch_bounds__(PLOC_TAIL_THREADS) k_ploc_tail(const int* clus
     __shared__ int nn[PLOC_TAIL];
     __shared__ int warp_sum[PLOC_TAIL_THREADS / 32];
     __shared__ int total;
+    extern __shared__ float sbox[];   // [PLOC_TAIL][6]: the current clusters' boxes
     const int T = PLOC_TAIL_THREADS, PER = PLOC_TAIL / PLOC_TAIL_THREADS;
     int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int i = tid; i < C0; i += T) cl[0][i] = clusters_in[i];
@@ -122,16 +133,19 @@ __global__ void __launch_bounds__(PLOC_TAIL_THREADS) k_ploc_tail(const int* clus
     __syncthreads();
     while (C > 1) {
         const int* c = cl[cur];
+        for (int i = tid; i < C; i += T) {   // stage the boxes in shared memory
+            const float* g = nbox + 6 * (long long)c[i];
+            for (int k = 0; k < 6; ++k) sbox[6 * i + k] = g[k];
+        }
+        __syncthreads();
         for (int i = tid; i < C; i += T) {   // nearest neighbour within +-PLOC_R (k_ploc_nn)
-            const float* me = nbox + 6 * (long long)c[i];
-            float m[6];
-            for (int k = 0; k < 6; ++k) m[k] = me[k];
+            const float* m = sbox + 6 * i;
             float best = INFINITY;
             int bj = -1;
             for (int d = -PLOC_R; d <= PLOC_R; ++d) {
                 int j = i + d;
                 if (d == 0 || j < 0 || j >= C) continue;
-                float a = union_area(m, nbox + 6 * (long long)c[j]);
+                float a = union_area(m, sbox + 6 * j);
                 if (a < best) { best = a; bj = j; }
             }
             nn[i] = bj;
@@ -203,9 +217,12 @@ __global__ void __launch_bounds__(PLOC_TAIL_THREADS) k_ploc_tail(const int* clus
     if (tid == 0) *root_out = cl[cur][0];
 }
 
-__global__ void k_ploc_compact(const int* out, const int* valid, const int* pos, int C, int* next) {
+__global__ void k_ploc_compact(const int* out, const int* valid, const int* pos, const int* dC, int* next,
+                               int* dC_next) {
+    const int C = *dC;
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < C && valid[i]) next[pos[i]] = out[i];
+    if (i == C - 1) *dC_next = pos[i] + valid[i];
 }
 
 // depth-first triangle slot of every leaf: sum of left-sibling subtree sizes
