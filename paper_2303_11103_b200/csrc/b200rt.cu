@@ -21,6 +21,7 @@
 #include "api_kernels.cuh"
 #include "bvh_build.cuh"
 #include "bvh_ploc.cuh"
+#include "bvh_sah.cuh"
 #include "em_jvp.cuh"
 #include "launch.cuh"
 
@@ -37,6 +38,9 @@
 // square when B = sqrt(32 pi n).  Measured on C3 (launch ms): C = pi 24.3,
 // 8 pi 23.5, 32 pi 23.5, 128 pi 24.5.
 #define RT_BAND_C 100.53
+#endif
+#ifndef RT_SAH
+#define RT_SAH 1   // top-down binned SAH (bvh_sah.cuh); 0 = RT_PLOC's choice
 #endif
 #ifndef RT_PLOC_TAIL
 #define RT_PLOC_TAIL 1   // last PLOC iterations in one block (bvh_ploc.cuh k_ploc_tail)
@@ -116,6 +120,7 @@ struct rt_ctx {
     DevBuf dflag, probe;
     // PLOC builder scratch
     DevBuf pl_box, pl_count, pl_parent, pl_ca, pl_cb, pl_nn, pl_out, pl_valid, pl_pos, pl_slot, pl_em, pl_dfs;
+    DevBuf sah_tasks;
     long long* hpin = nullptr;
     // profiling: per-stage CUDA events on the caller's stream + counters
     int prof = 0;
@@ -298,10 +303,11 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st) {
 }
 
 int build_karras(rt_ctx* ctx, long long n, const uint64_t* kout, const int* vout, cudaStream_t st);
+int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st);
+int build_morton(rt_ctx* ctx, long long n, cudaStream_t st);
 
-// PLOC hierarchy over the Morton-sorted prims (sorted_idx), then the
-// depth-first child-pair layout + triangle records (bvh_ploc.cuh)
-int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
+// PLOC-format scratch shared by the PLOC and SAH builders
+int reserve_tree(rt_ctx* ctx, long long n) {
     long long nn = 2 * n - 1;
     CK(ctx->pl_box.reserve(24ULL * nn));
     CK(ctx->pl_count.reserve(4ULL * nn));
@@ -309,13 +315,139 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
     CK(ctx->child.reserve(8ULL * n));
     CK(ctx->pl_ca.reserve(4ULL * n));
     CK(ctx->pl_cb.reserve(4ULL * n));
+    CK(ctx->pl_slot.reserve(4ULL * n));
+    CK(ctx->pl_em.reserve(4ULL * nn));
+    CK(ctx->pl_dfs.reserve(4ULL * n));
+    return RT_OK;
+}
+
+// top-down binned-SAH hierarchy (bvh_sah.cuh): ranges of > SAH_BIG prims are
+// split level by level with one CTA per SAH_CHUNK-prim chunk, ranges of
+// SAH_SMALL < m <= SAH_BIG with one CTA per range, then one thread finishes
+// each small range; the emitted-node counts are then computed bottom-up.  One
+// host round trip per level (the next level's grid sizes).
+int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
+    RC(reserve_tree(ctx, n));
+    const long long cap_med = n / (SAH_SMALL + 1) + 2, cap_small = n + 2;
+    const long long cap_big = 2 * (n / SAH_BIG) + 2, cap_chunk = n / SAH_CHUNK + cap_big + 2;
+    size_t bytes = sizeof(SahTask) * (2 * cap_med + cap_small + 2 * cap_big) + sizeof(int2) * 2 * cap_big +
+                   sizeof(int) * 3 * cap_chunk + sizeof(unsigned) * 2 * cap_big * SAH_RB +
+                   16 * 16;   // alignment of the 12 sub-buffers
+    CK(ctx->sah_tasks.reserve(bytes));
+    CK(ctx->flags.reserve(4 * n));
+    char* q = ctx->sah_tasks.get<char>();
+    auto take = [&](size_t nb) { char* r = q; q += (nb + 15) / 16 * 16; return r; };
+    SahTask* med[2] = {(SahTask*)take(sizeof(SahTask) * cap_med), (SahTask*)take(sizeof(SahTask) * cap_med)};
+    SahTask* small = (SahTask*)take(sizeof(SahTask) * cap_small);
+    SahTask* big[2] = {(SahTask*)take(sizeof(SahTask) * cap_big), (SahTask*)take(sizeof(SahTask) * cap_big)};
+    int2* bigc[2] = {(int2*)take(sizeof(int2) * cap_big), (int2*)take(sizeof(int2) * cap_big)};
+    int* ctask[2] = {(int*)take(sizeof(int) * cap_chunk), (int*)take(sizeof(int) * cap_chunk)};
+    int* cleft = (int*)take(sizeof(int) * cap_chunk);
+    unsigned* rb[2] = {(unsigned*)take(sizeof(unsigned) * cap_big * SAH_RB),
+                       (unsigned*)take(sizeof(unsigned) * cap_big * SAH_RB)};
+    if ((size_t)(q - ctx->sah_tasks.get<char>()) > ctx->sah_tasks.bytes)
+        return fail(ctx, RT_ECUDA, "SAH scratch layout overflow");
+    int* em = ctx->pl_em.get<int>();
+    float* box = ctx->pl_box.get<float>();
+    int* cnt = ctx->pl_count.get<int>();
+    int* par = ctx->pl_parent.get<int>();
+    int* child = ctx->child.get<int>();
+    int* idx0 = ctx->pl_ca.get<int>();
+    int* idx1 = ctx->pl_cb.get<int>();
+    int* sidx = ctx->sorted_idx.get<int>();
+    const float* pbox = ctx->pbox.get<float>();
+    const float* cent = ctx->cent.get<float>();
+    // device ints: [0,1] big ranges (ping-pong), [2,3] their chunks, [4,5] medium
+    // ranges (ping-pong), [6] small ranges, [7] root
+    int* dc = reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 16);
+    k_iota<<<nblk(n, 256), 256, 0, st>>>(sidx, n);
+    CKL();
+    k_ploc_init<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, pbox, box, idx0, cnt, em);
+    CKL();
+    int h[8] = {0, 0, 0, 0, 0, 0, 0, -1};
+    SahTask root_task{0, (int)n, -1, 0};
+    if (n <= SAH_SMALL) {
+        h[6] = 1;
+        CK(cudaMemcpyAsync(small, &root_task, sizeof(SahTask), cudaMemcpyHostToDevice, st));
+    } else if (n <= SAH_BIG) {
+        h[4] = 1;
+        CK(cudaMemcpyAsync(med[0], &root_task, sizeof(SahTask), cudaMemcpyHostToDevice, st));
+    } else {
+        int nc = (int)((n + SAH_CHUNK - 1) / SAH_CHUNK);
+        h[0] = 1;
+        h[2] = nc;
+        int2 ch = make_int2(0, nc);
+        CK(cudaMemcpyAsync(big[0], &root_task, sizeof(SahTask), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(bigc[0], &ch, sizeof(int2), cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(ctask[0], 0, sizeof(int) * nc, st));
+    }
+    CK(cudaMemcpyAsync(dc, h, sizeof(h), cudaMemcpyHostToDevice, st));
+    int levels = 0, cur = 0;
+    long long nbig = h[0], nchunk = h[2];
+    while (nbig > 0) {   // ranges of > SAH_BIG prims
+        int nx = cur ^ 1;
+        SahOut O{small, dc + 6, med[0], dc + 4, big[nx], bigc[nx], dc + nx, ctask[nx], dc + 2 + nx};
+        CK(cudaMemsetAsync(dc + nx, 0, 4, st));
+        CK(cudaMemsetAsync(dc + 2 + nx, 0, 4, st));
+        k_sahb_init<<<nbig, 128, 0, st>>>(dc + cur, rb[cur]);
+        k_sahb_bounds<<<nchunk, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
+                                                    pbox, cent, rb[cur]);
+        k_sahb_bins<<<nchunk, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
+                                                  pbox, cent, rb[cur]);
+        k_sahb_split<<<nbig, 64, 0, st>>>(big[cur], dc + cur, rb[cur], (int)n, box, child, par, cnt, dc + 7, O);
+        k_sahb_count<<<nchunk, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
+                                                   cent, rb[cur], cleft);
+        k_sahb_write<<<nchunk, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
+                                                   cent, rb[cur], cleft);
+        CKL();
+        cur = nx;
+        ++levels;
+        CK(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        nbig = h[cur];
+        nchunk = h[2 + cur];
+        if (levels > 4096) return fail(ctx, RT_ECUDA, "SAH build made no progress");
+    }
+    int mcur = 0;
+    long long nmed = h[4];
+    while (nmed > 0) {   // ranges of SAH_SMALL < m <= SAH_BIG prims
+        int nx = mcur ^ 1;
+        SahOut O{small, dc + 6, med[nx], dc + 4 + nx, nullptr, nullptr, nullptr, nullptr, nullptr};
+        CK(cudaMemsetAsync(dc + 4 + nx, 0, 4, st));
+        k_sah_large<<<nmed, SAH_BLOCK, 0, st>>>(med[mcur], dc + 4 + mcur, idx0, idx1, pbox, cent, (int)n, box,
+                                                child, par, cnt, dc + 7, O);
+        CKL();
+        mcur = nx;
+        ++levels;
+        CK(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        nmed = h[4 + mcur];
+        if (levels > 4096) return fail(ctx, RT_ECUDA, "SAH build made no progress");
+    }
+    if (h[6] > 0) {
+        k_sah_small<<<nblk(h[6], 128), 128, 0, st>>>(small, dc + 6, idx0, idx1, pbox, cent, (int)n, box, child,
+                                                     par, cnt, dc + 7);
+        CKL();
+    }
+    CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
+    k_sah_emitted<<<nblk(n, 256), 256, 0, st>>>((int)n, par, child, cnt, em, ctx->flags.get<int>());
+    CKL();
+    int root = -1;
+    CK(cudaMemcpyAsync(&root, dc + 7, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (root < (int)n) return fail(ctx, RT_ECUDA, "SAH build produced no root");
+    ctx->counters[9] = levels;
+    return finish_tree(ctx, n, root, st);
+}
+
+// PLOC hierarchy over the Morton-sorted prims (sorted_idx), then the
+// depth-first child-pair layout + triangle records (bvh_ploc.cuh)
+int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
+    RC(reserve_tree(ctx, n));
     CK(ctx->pl_nn.reserve(4ULL * n));
     CK(ctx->pl_out.reserve(4ULL * n));
     CK(ctx->pl_valid.reserve(4ULL * (n + 1)));
     CK(ctx->pl_pos.reserve(4ULL * (n + 1)));
-    CK(ctx->pl_slot.reserve(4ULL * n));
-    CK(ctx->pl_em.reserve(4ULL * nn));
-    CK(ctx->pl_dfs.reserve(4ULL * n));
     int* em = ctx->pl_em.get<int>();
     float* box = ctx->pl_box.get<float>();
     int* cnt = ctx->pl_count.get<int>();
@@ -384,6 +516,18 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
         CK(cudaStreamSynchronize(st));
     }
     ctx->counters[9] = iters;
+    return finish_tree(ctx, n, root, st);
+}
+
+// depth-first child-pair layout + triangle records of a hierarchy in the PLOC
+// arrays (leaves [0, n) with sorted_idx, internal nodes [n, 2n-1), root id)
+int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st) {
+    int* em = ctx->pl_em.get<int>();
+    float* box = ctx->pl_box.get<float>();
+    int* cnt = ctx->pl_count.get<int>();
+    int* par = ctx->pl_parent.get<int>();
+    int* child = ctx->child.get<int>();
+    const int* sidx = ctx->sorted_idx.get<int>();
     int* slot = ctx->pl_slot.get<int>();
     k_ploc_slots<<<nblk(n, 256), 256, 0, st>>>((int)n, par, child, cnt, root, slot);
     CKL();
@@ -481,7 +625,7 @@ int rt_create(int device, rt_ctx** out) {
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
     if (cudaMallocHost(&ctx->hpin, 64 * sizeof(long long)) != cudaSuccess ||
-        ctx->dflag.reserve(64) != cudaSuccess || ctx->ctrs.reserve(128) != cudaSuccess) {
+        ctx->dflag.reserve(64) != cudaSuccess || ctx->ctrs.reserve(256) != cudaSuccess) {
         delete ctx;
         return RT_ENOMEM;
     }
@@ -568,6 +712,19 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
         CKL();
         return RT_WIDE ? collapse4(ctx, 1, st) : RT_OK;
     }
+    if (RT_SAH) {
+        RC(build_sah(ctx, n, st));
+    } else {
+        RC(build_morton(ctx, n, st));
+    }
+    return RT_WIDE ? collapse4(ctx, n - 1, st) : RT_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// Morton codes + radix sort, then the PLOC or Karras hierarchy over them
+int build_morton(rt_ctx* ctx, long long n, cudaStream_t st) {
     CK(ctx->morton.reserve(8 * n));
     CK(ctx->morton_alt.reserve(8 * n));
     CK(ctx->idx_alt.reserve(4 * n));
@@ -589,13 +746,9 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
         return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, 64, st);
     }));
-    RC(RT_PLOC ? build_ploc(ctx, n, st) : build_karras(ctx, n, kout, vout, st));
-    return RT_WIDE ? collapse4(ctx, n - 1, st) : RT_OK;
+    return RT_PLOC ? build_ploc(ctx, n, st) : build_karras(ctx, n, kout, vout, st);
 }
 
-}  // extern "C"
-
-namespace {
 // Karras (2012) LBVH hierarchy from the sorted Morton keys (A/B alternative to PLOC)
 int build_karras(rt_ctx* ctx, long long n, const uint64_t* kout, const int* vout, cudaStream_t st) {
     CK(cudaMemsetAsync(ctx->parent_int.p, 0xFF, 4 * n, st));

@@ -306,22 +306,37 @@ __global__ void k_ploc_layout(int n, int root, const int* child, const int* coun
 // sums[0] = sum of internal-child box areas, sums[1] = sum of leaf box area x
 // triangle count, sums[2] = root area; expected internal-node visits of a
 // random ray ~ 1 + sums[0] / sums[2], expected triangle tests ~ sums[1] / sums[2].
-__global__ void k_tree_sah(const BNode* nodes, int n_nodes, double* sums) {
+__device__ inline void tree_sah_node(const BNode* nodes, int q, double& in, double& lf, double* sums);
+
+__global__ void __launch_bounds__(256) k_tree_sah(const BNode* nodes, int n_nodes, double* sums) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n_nodes) return;
+    __shared__ double part[2][8];
+    double in = 0.0, lf = 0.0;
+    if (q < n_nodes) tree_sah_node(nodes, q, in, lf, sums);
+    for (int o = 16; o; o >>= 1) {   // one atomic pair per block, not per node
+        in += __shfl_xor_sync(0xffffffffu, in, o);
+        lf += __shfl_xor_sync(0xffffffffu, lf, o);
+    }
+    if ((threadIdx.x & 31) == 0) { part[0][threadIdx.x >> 5] = in; part[1][threadIdx.x >> 5] = lf; }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[threadIdx.x][w];
+        atomicAdd(sums + threadIdx.x, s);
+    }
+}
+
+__device__ inline void tree_sah_node(const BNode* nodes, int q, double& in, double& lf, double* sums) {
     BNode nd = nodes[q];
     float b[2][6] = {{nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.b.x, nd.b.y},
                      {nd.b.z, nd.b.w, nd.c.x, nd.c.y, nd.c.z, nd.c.w}};
     int ref[2] = {nd.d.x, nd.d.y};
-    double in = 0.0, lf = 0.0;
     for (int c = 0; c < 2; ++c) {
         double dx = b[c][3] - b[c][0], dy = b[c][4] - b[c][1], dz = b[c][5] - b[c][2];
         double sa = dx * dy + dy * dz + dz * dx;
         if (ref_is_leaf(ref[c])) lf += sa * leaf_count(ref[c]);
         else in += sa;
     }
-    atomicAdd(sums + 0, in);
-    atomicAdd(sums + 1, lf);
     if (q == 0) {
         double lx = fmin(b[0][0], b[1][0]), ly = fmin(b[0][1], b[1][1]), lz = fmin(b[0][2], b[1][2]);
         double hx = fmax(b[0][3], b[1][3]), hy = fmax(b[0][4], b[1][4]), hz = fmax(b[0][5], b[1][5]);

@@ -76,6 +76,40 @@ def test_intersect_brute_force_random_soups(P):
         assert np.array_equal(t.cpu().numpy()[hit], ot[hit])
 
 
+def test_builder_coincident_centroids_match_oracle(P):
+    """SAH builder edge cases: ranges whose centroids all coincide (middle
+    split), big multi-CTA ranges (> 8192 prims) and one-thread small ranges."""
+    import oracle as O
+    from paper_2303_11103_b200.scene import AntennaArray, RadioDevice, RadioMaterial, Scene, SceneObject
+    rng = np.random.RandomState(7)
+    tris = []
+    for c in rng.uniform(-40, 40, (6, 3)):   # 6 centres x 1500 triangles sharing the centroid
+        for _ in range(1500):
+            a, b = rng.randn(3), rng.randn(3)
+            tris.append(np.stack([c + a, c + b, c - a - b]))
+    centers = rng.uniform(-50, 50, (4000, 3))
+    for c in centers:
+        tris.append(c + rng.uniform(-1.5, 1.5, (3, 3)))
+    verts = np.concatenate(tris)
+    sc = Scene(1e9, [SceneObject("soup", "m", verts, np.arange(len(verts)).reshape(-1, 3))],
+               {"m": RadioMaterial("m", "constant", eps_r=2.0)}, AntennaArray(), AntennaArray(),
+               [RadioDevice("tx", "tx", np.array([0.0, 0, 100.0])),
+                RadioDevice("rx", "rx", np.array([1.0, 0, 100.0]))])
+    b = _bvh(P, sc)
+    ob = O.Bvh(O.SceneArrays(sc))
+    o = rng.uniform(-60, 60, (20000, 3))
+    d = rng.randn(20000, 3)
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    t, p = b.trace(o, d)
+    ot, op = ob.trace(o, d, 1e-4, np.inf)
+    assert np.array_equal(p.cpu().numpy(), op)
+    hit = op >= 0
+    assert hit.mean() > 0.2
+    assert np.array_equal(t.cpu().numpy()[hit], ot[hit])
+    occ = b.occluded_batch(o, o + 30.0 * d).cpu().numpy()
+    assert np.array_equal(occ == 1, (op >= 0) & (ot < 30.0 - 1e-4))
+
+
 def test_empty_and_tiny_scenes(P):
     from paper_2303_11103_b200 import scenes
     from paper_2303_11103_b200.scene import Scene, AntennaArray, RadioDevice
