@@ -148,6 +148,33 @@ int rt_transfer_bwd(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* ord
                     double wavelength, double frequency_hz, const double* grad_a,
                     double* grad_eta, void* stream);
 
+/* ---- synthetic-array gains and CIR packing (no autograd) ----
+ * rt_gains_synthetic (em.py:359-422, _gain_synthetic): a[p, i, j] = base[p,
+ * s(j), r(i)] * exp(j 2 pi off_rx_w[rx_dev[p], i] . (-k_arr[p]) / lambda) *
+ * exp(j 2 pi off_tx_w[tx_dev[p], j] . k_dep[p] / lambda).  All device: base
+ * [P*S*R*2] (rt_transfer's output), tx_dev/rx_dev [P], k_dep/k_arr [P*3],
+ * off_tx_w [n_tx_dev*Et*3], off_rx_w [n_rx_dev*Er*3] (world-frame element
+ * offsets), slant indices [Et] / [Er]; out a [P*Er*Et*2]. */
+int rt_gains_synthetic(rt_ctx* ctx, int64_t n_paths, int n_tx_slants, int n_rx_slants,
+                       const double* base, const int32_t* tx_dev, const int32_t* rx_dev,
+                       const double* k_dep, const double* k_arr, int n_tx_el,
+                       const double* off_tx_w, const int32_t* tx_slant_index, int n_rx_el,
+                       const double* off_rx_w, const int32_t* rx_slant_index, double wavelength,
+                       double* a_out, void* stream);
+/* build_cir (channel.py:40-72), two calls.  rt_cir_plan keeps LOS and/or
+ * specular paths, buckets them by scene (rx, tx) pair (rx_of/tx_of [P]
+ * device) and orders every bucket by (delay, kind, sequence); *n_path_out =
+ * the largest bucket (host sync).  rt_cir_scatter then writes a_in [P*Er*
+ * Et*n_t*2] into the caller-zeroed a_out [n_rx*Er*n_tx*Et*n_path*n_t*2] and
+ * tau_out [n_rx*n_tx*n_path] (delays minus the pair's first arrival when
+ * normalize != 0). */
+int rt_cir_plan(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, const int32_t* seq,
+                const double* delay, const int32_t* rx_of, const int32_t* tx_of, int n_rx, int n_tx,
+                int los, int reflection, int64_t* n_path_out, void* stream);
+int rt_cir_scatter(rt_ctx* ctx, int64_t n_paths, const double* delay, int normalize,
+                   const double* a_in, int n_rx_el, int n_tx_el, int n_t, int64_t n_path,
+                   double* a_out, double* tau_out, void* stream);
+
 /* Batched image_solve of independent (tx, rx, sequence) triples (tracer.py:
  * 150-183; order-0 rows are LOS visibility checks, tracer.py:190) — the
  * explicit-array gains (em.py:425-459) and single image_solve queries.

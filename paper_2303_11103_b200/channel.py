@@ -60,6 +60,10 @@ def build_cir(gains, los: bool = True, reflection: bool = True,
         a = torch.zeros((len(rx_names), n_rx_el, len(tx_names), n_tx_el, 0, n_t),
                         dtype=torch.complex128, device=dev)
         tau = torch.zeros((len(rx_names), len(tx_names), 0), dtype=torch.float64, device=dev)
+    elif getattr(gains, "ctx", None) is not None and a_all.is_cuda and not a_all.requires_grad:
+        delay_all = gains.delay if gains.delay is not None else T.delay
+        return _build_cir_device(gains, T, a_all, delay_all, rx_names, tx_names, n_rx_el, n_tx_el, n_t,
+                                 los, reflection, normalize_delays, to_host)
     else:
         kind = (T.order > 0).to(torch.int64)
         keep = ((kind == 0) & los) | ((kind == 1) & reflection)
@@ -109,8 +113,44 @@ def build_cir(gains, los: bool = True, reflection: bool = True,
     cir = Cir(a=None, tau=None, rx_names=rx_names, tx_names=tx_names,
               sample_times=gains.sample_times, a_dev=a, tau_dev=tau)
     if to_host:
-        cir.a = a.cpu().numpy()
-        cir.tau = tau.cpu().numpy()
+        cir.a = N.d2h(a)
+        cir.tau = N.d2h(tau)
+    return cir
+
+
+def _build_cir_device(gains, T, a_all, delay, rx_names, tx_names, n_rx_el, n_tx_el, n_t, los, reflection,
+                      normalize_delays, to_host):
+    """build_cir through rt_cir_plan / rt_cir_scatter: bucket by (rx, tx) pair,
+    order by (delay, kind, sequence), scatter — one host sync for the path count."""
+    dev = a_all.device
+    ctx = gains.ctx
+    if list(T.rx_names) == rx_names:
+        rx_of = T.rx
+    else:
+        rx_of = N.h2d(np.array([rx_names.index(n) for n in T.rx_names], dtype=np.int32), dev)[T.rx.long()]
+    if list(T.tx_names) == tx_names:
+        tx_of = T.tx
+    else:
+        tx_of = N.h2d(np.array([tx_names.index(n) for n in T.tx_names], dtype=np.int32), dev)[T.tx.long()]
+    rx_of, tx_of = rx_of.to(torch.int32).contiguous(), tx_of.to(torch.int32).contiguous()
+    delay = delay.to(torch.float64).contiguous()
+    a_in = a_all.contiguous()
+    n = ctypes.c_int64()
+    with torch.cuda.device(dev):
+        ctx.call("rt_cir_plan", T.n, int(T.L), N.ptr(T.order), N.ptr(T.seq), N.ptr(delay), N.ptr(rx_of),
+                 N.ptr(tx_of), len(rx_names), len(tx_names), int(bool(los)), int(bool(reflection)),
+                 ctypes.byref(n), ctx.stream, exc_map={N.RT_EINVAL: ChannelError})
+        n_path = int(n.value)
+        a = torch.zeros((len(rx_names), n_rx_el, len(tx_names), n_tx_el, n_path, n_t),
+                        dtype=torch.complex128, device=dev)
+        tau = torch.zeros((len(rx_names), len(tx_names), n_path), dtype=torch.float64, device=dev)
+        ctx.call("rt_cir_scatter", T.n, N.ptr(delay), int(bool(normalize_delays)), N.ptr(a_in), n_rx_el,
+                 n_tx_el, n_t, n_path, N.ptr(a), N.ptr(tau), ctx.stream, exc_map={N.RT_EINVAL: ChannelError})
+    cir = Cir(a=None, tau=None, rx_names=rx_names, tx_names=tx_names, sample_times=gains.sample_times,
+              a_dev=a, tau_dev=tau)
+    if to_host:
+        cir.a = N.d2h(a)
+        cir.tau = N.d2h(tau)
     return cir
 
 
@@ -184,7 +224,7 @@ def frequency_response(cir: Cir, num_subcarriers: int, spacing: float) -> FreqRe
     h = torch.einsum("abcdpt,acpk->abcdkt", a, phase)
     nr, nre, nt, nte = a.shape[:4]
     h = h.reshape(nr * nre, nt * nte, num_subcarriers, a.shape[-1])
-    return FreqResponse(h=h.cpu().numpy(), frequencies=f)
+    return FreqResponse(h=N.d2h(h), frequencies=f)
 
 
 # -- coverage ---------------------------------------------------------------------------------
@@ -311,7 +351,7 @@ def coverage_map(scene, bvh, grid: GridSpec, max_depth: int, method: str = "exha
         set_candidates(bvh, np.zeros((0, 1), dtype=np.int32), np.zeros(0, dtype=np.int8), 1)
     g, stats = coverage_from_candidates(scene, bvh, tx_dev, grid, tx_mode)
     stats["ray_bounces"] = int(bounces)
-    return CoverageMap(grid=grid, gains=g.cpu().numpy(), frequency_hz=scene.frequency_hz,
+    return CoverageMap(grid=grid, gains=N.d2h(g), frequency_hz=scene.frequency_hz,
                        stats=stats, gains_dev=g)
 
 

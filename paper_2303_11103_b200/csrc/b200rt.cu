@@ -22,6 +22,7 @@
 #include "bvh_build.cuh"
 #include "bvh_ploc.cuh"
 #include "bvh_sah.cuh"
+#include "cir.cuh"
 #include "em_jvp.cuh"
 #include "launch.cuh"
 
@@ -121,6 +122,10 @@ struct rt_ctx {
     // PLOC builder scratch
     DevBuf pl_box, pl_count, pl_parent, pl_ca, pl_cb, pl_nn, pl_out, pl_valid, pl_pos, pl_slot, pl_em, pl_dfs;
     DevBuf sah_tasks;
+    // CIR packing scratch (rt_cir_plan -> rt_cir_scatter)
+    DevBuf cir_pair, cir_count, cir_off, cir_fill, cir_bucket, cir_slot, cir_first;
+    int64_t cir_n = 0;
+    int cir_ntx = 0;
     long long* hpin = nullptr;
     // profiling: per-stage CUDA events on the caller's stream + counters
     int prof = 0;
@@ -323,12 +328,13 @@ int reserve_tree(rt_ctx* ctx, long long n) {
 
 // top-down binned-SAH hierarchy (bvh_sah.cuh): ranges of > SAH_BIG prims are
 // split level by level with one CTA per SAH_CHUNK-prim chunk, ranges of
-// SAH_SMALL < m <= SAH_BIG with one CTA per range, then one thread finishes
+// small_max < m <= SAH_BIG with one CTA per range, then one thread finishes
 // each small range; the emitted-node counts are then computed bottom-up.  One
 // host round trip per level (the next level's grid sizes).
 int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     RC(reserve_tree(ctx, n));
-    const long long cap_med = n / (SAH_SMALL + 1) + 2, cap_small = n + 2;
+    const int small_max = n < SAH_LATENCY_PRIMS ? SAH_SMALL_LATENCY : SAH_SMALL;
+    const long long cap_med = n / (small_max + 1) + 2, cap_small = n + 2;
     const long long cap_big = 2 * (n / SAH_BIG) + 2, cap_chunk = n / SAH_CHUNK + cap_big + 2;
     size_t bytes = sizeof(SahTask) * (2 * cap_med + cap_small + 2 * cap_big) + sizeof(int2) * 2 * cap_big +
                    sizeof(int) * 3 * cap_chunk + sizeof(unsigned) * 2 * cap_big * SAH_RB +
@@ -366,7 +372,7 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     CKL();
     int h[8] = {0, 0, 0, 0, 0, 0, 0, -1};
     SahTask root_task{0, (int)n, -1, 0};
-    if (n <= SAH_SMALL) {
+    if (n <= small_max) {
         h[6] = 1;
         CK(cudaMemcpyAsync(small, &root_task, sizeof(SahTask), cudaMemcpyHostToDevice, st));
     } else if (n <= SAH_BIG) {
@@ -386,7 +392,7 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     long long nbig = h[0], nchunk = h[2];
     while (nbig > 0) {   // ranges of > SAH_BIG prims
         int nx = cur ^ 1;
-        SahOut O{small, dc + 6, med[0], dc + 4, big[nx], bigc[nx], dc + nx, ctask[nx], dc + 2 + nx};
+        SahOut O{small_max, small, dc + 6, med[0], dc + 4, big[nx], bigc[nx], dc + nx, ctask[nx], dc + 2 + nx};
         CK(cudaMemsetAsync(dc + nx, 0, 4, st));
         CK(cudaMemsetAsync(dc + 2 + nx, 0, 4, st));
         k_sahb_init<<<nbig, 128, 0, st>>>(dc + cur, rb[cur]);
@@ -408,17 +414,25 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
         nchunk = h[2 + cur];
         if (levels > 4096) return fail(ctx, RT_ECUDA, "SAH build made no progress");
     }
+    // ranges of small_max < m <= SAH_BIG prims: SAH_MED_BATCH levels per host
+    // round trip, each grid sized by the bound (ranges at most double per level;
+    // CTAs past the live count exit at once)
+    const int SAH_MED_BATCH = 4;
     int mcur = 0;
     long long nmed = h[4];
-    while (nmed > 0) {   // ranges of SAH_SMALL < m <= SAH_BIG prims
-        int nx = mcur ^ 1;
-        SahOut O{small, dc + 6, med[nx], dc + 4 + nx, nullptr, nullptr, nullptr, nullptr, nullptr};
-        CK(cudaMemsetAsync(dc + 4 + nx, 0, 4, st));
-        k_sah_large<<<nmed, SAH_BLOCK, 0, st>>>(med[mcur], dc + 4 + mcur, idx0, idx1, pbox, cent, (int)n, box,
-                                                child, par, cnt, dc + 7, O);
-        CKL();
-        mcur = nx;
-        ++levels;
+    while (nmed > 0) {
+        long long bound = nmed;
+        for (int b = 0; b < SAH_MED_BATCH; ++b) {
+            int nx = mcur ^ 1;
+            SahOut O{small_max, small, dc + 6, med[nx], dc + 4 + nx, nullptr, nullptr, nullptr, nullptr, nullptr};
+            CK(cudaMemsetAsync(dc + 4 + nx, 0, 4, st));
+            k_sah_large<<<bound, SAH_BLOCK, 0, st>>>(med[mcur], dc + 4 + mcur, idx0, idx1, pbox, cent, (int)n,
+                                                     box, child, par, cnt, dc + 7, O);
+            CKL();
+            mcur = nx;
+            ++levels;
+            bound = std::min(2 * bound, cap_med);
+        }
         CK(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         nmed = h[4 + mcur];
@@ -1606,3 +1620,90 @@ int rt_get_profile(rt_ctx* ctx, double* ms_out, int64_t* counters_out) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int rt_gains_synthetic(rt_ctx* ctx, int64_t n_paths, int n_tx_slants, int n_rx_slants,
+                       const double* base, const int32_t* tx_dev, const int32_t* rx_dev,
+                       const double* k_dep, const double* k_arr, int n_tx_el,
+                       const double* off_tx_w, const int32_t* tx_slant_index, int n_rx_el,
+                       const double* off_rx_w, const int32_t* rx_slant_index, double wavelength,
+                       double* a_out, void* stream) {
+    if (!ctx || n_paths < 0 || n_tx_slants < 1 || n_rx_slants < 1 || n_tx_el < 1 || n_rx_el < 1 ||
+        !(wavelength > 0.0))
+        return fail(ctx, RT_EINVAL, "bad synthetic-gains arguments");
+    long long n = (long long)n_paths * n_tx_el * n_rx_el;
+    if (n == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    k_gains_synth<<<nblk(n, 256), 256, 0, ST(stream)>>>(n_paths, n_tx_slants, n_rx_slants, base, tx_dev, rx_dev,
+                                                        k_dep, k_arr, n_tx_el, off_tx_w, tx_slant_index,
+                                                        n_rx_el, off_rx_w, rx_slant_index, wavelength, a_out);
+    CKL();
+    return RT_OK;
+}
+
+int rt_cir_plan(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, const int32_t* seq,
+                const double* delay, const int32_t* rx_of, const int32_t* tx_of, int n_rx, int n_tx,
+                int los, int reflection, int64_t* n_path_out, void* stream) {
+    if (!ctx || n_paths < 0 || max_len < 1 || n_rx < 1 || n_tx < 1 || !n_path_out)
+        return fail(ctx, RT_EINVAL, "bad CIR arguments");
+    *n_path_out = 0;
+    ctx->cir_n = n_paths;
+    ctx->cir_ntx = n_tx;
+    if (n_paths == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    long long np = (long long)n_rx * n_tx;
+    CK(ctx->cir_pair.reserve(4 * n_paths));
+    CK(ctx->cir_count.reserve(4 * (np + 1)));
+    CK(ctx->cir_off.reserve(4 * (np + 1)));
+    CK(ctx->cir_fill.reserve(4 * np));
+    CK(ctx->cir_bucket.reserve(4 * n_paths));
+    CK(ctx->cir_slot.reserve(4 * n_paths));
+    CK(ctx->cir_first.reserve(8 * n_paths));
+    int* count = ctx->cir_count.get<int>();
+    int* off = ctx->cir_off.get<int>();
+    int* pair = ctx->cir_pair.get<int>();
+    CK(cudaMemsetAsync(count, 0, 4 * (np + 1), st));
+    CK(cudaMemsetAsync(ctx->cir_fill.p, 0, 4 * np, st));
+    k_cir_count<<<nblk(n_paths, 256), 256, 0, st>>>(n_paths, (const signed char*)order, rx_of, tx_of, n_tx, los,
+                                                    reflection, pair, count);
+    CKL();
+    RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+        return cub::DeviceScan::ExclusiveSum(tmp, bytes, count, off, (int)(np + 1), st);
+    }));
+    int* dmax = reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 24);
+    RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
+        return cub::DeviceReduce::Max(tmp, bytes, count, dmax, (int)np, st);
+    }));
+    k_cir_bucket<<<nblk(n_paths, 256), 256, 0, st>>>(n_paths, pair, off, ctx->cir_fill.get<int>(),
+                                                     ctx->cir_bucket.get<int>());
+    k_cir_slot<<<nblk(n_paths, 128), 128, 0, st>>>(n_paths, pair, off, count, ctx->cir_bucket.get<int>(), delay,
+                                                   (const signed char*)order, seq, max_len,
+                                                   ctx->cir_slot.get<int>(), ctx->cir_first.get<double>());
+    CKL();
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, dmax, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *n_path_out = h;
+    return RT_OK;
+}
+
+int rt_cir_scatter(rt_ctx* ctx, int64_t n_paths, const double* delay, int normalize,
+                   const double* a_in, int n_rx_el, int n_tx_el, int n_t, int64_t n_path,
+                   double* a_out, double* tau_out, void* stream) {
+    if (!ctx || n_paths != ctx->cir_n || n_rx_el < 1 || n_tx_el < 1 || n_t < 1 || n_path < 0)
+        return fail(ctx, RT_EINVAL, "rt_cir_scatter does not match the last rt_cir_plan");
+    long long n = (long long)n_paths * n_rx_el * n_tx_el * n_t;
+    if (n == 0 || n_path == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    k_cir_scatter<<<nblk(n, 256), 256, 0, ST(stream)>>>(n_paths, ctx->cir_pair.get<int>(), ctx->cir_slot.get<int>(),
+                                                        ctx->cir_first.get<double>(), delay, normalize,
+                                                        ctx->cir_ntx, n_rx_el, n_tx_el, n_t, n_path, a_in,
+                                                        a_out, tau_out);
+    CKL();
+    return RT_OK;
+}
+
+}  // extern "C"
+

@@ -6,10 +6,10 @@
 // depth 5: the surface-area estimate drops 27.9 -> 22.7).  The Manhattan grid
 // defeats the Morton-order neighbourhood PLOC merges within.
 //
-// Level-synchronous: every range of > SAH_SMALL primitives is one CTA
+// Level-synchronous: every range of > small_max primitives is one CTA
 // (k_sah_large): centroid bounds, SAH_BINS bins per axis in shared memory,
 // the cheapest split, a stable partition into the other index buffer.
-// Ranges of 2..SAH_SMALL primitives go to a list that k_sah_small finishes
+// Ranges of 2..small_max (16, or 4 for small scenes) primitives go to a list that k_sah_small finishes
 // one thread per range with the exact sweep SAH.  The tree is split all the
 // way to single primitives; the PLOC layout path then collapses subtrees of
 // <= LEAF_MAX primitives into leaves.
@@ -34,7 +34,14 @@ constexpr int SAH_BINS = RT_SAH_BINS;
 #ifndef RT_SAH_BIG
 #define RT_SAH_BIG 8192
 #endif
-constexpr int SAH_SMALL = RT_SAH_SMALL;   // ranges of <= SAH_SMALL prims: one thread, exact sweep
+// Ranges of <= small_max prims: one thread, exact sweep.  small_max is chosen
+// per build (rt_bvh_build): SAH_SMALL for big scenes (throughput: one thread
+// per range beats a CTA per range), SAH_SMALL_LATENCY below
+// SAH_LATENCY_PRIMS (latency: one thread's serial sweep over 16 prims took
+// 0.19 ms of the 2,002-tri canyon build, ranges of <= 4 take microseconds).
+constexpr int SAH_SMALL = RT_SAH_SMALL;
+constexpr int SAH_SMALL_LATENCY = 4;
+constexpr long long SAH_LATENCY_PRIMS = 65536;
 constexpr int SAH_BLOCK = 256;
 constexpr int SAH_BIG = RT_SAH_BIG;       // ranges above this: several CTAs (SAH_CHUNK prims each)
 constexpr int SAH_CHUNK = 2048;
@@ -224,9 +231,10 @@ __device__ __forceinline__ void sah_link(int id, int par, int side, int n, int* 
 }
 
 // Output lists of one split: single prims whose slot is final are linked
-// directly (dst_ready), <= SAH_SMALL -> small, <= SAH_BIG -> med, else big
+// directly (dst_ready), <= small_max -> small, <= SAH_BIG -> med, else big
 // (with SAH_CHUNK-prim chunks mapped in chunk_task).
 struct SahOut {
+    int small_max;
     SahTask* small; int* n_small;
     SahTask* med; int* n_med;
     SahTask* big; int2* big_chunks; int* n_big; int* chunk_task; int* n_chunk;
@@ -249,7 +257,7 @@ __device__ void sah_emit(const SahTask& T, const float box[6], const int* sp, in
             int p = dst[cb];
             child[2 * (long long)(id - n) + c] = p;
             parent[p] = id;
-        } else if (sz <= SAH_SMALL) {
+        } else if (sz <= O.small_max) {
             O.small[atomicAdd(O.n_small, 1)] = ct;
         } else if (sz <= SAH_BIG) {
             O.med[atomicAdd(O.n_med, 1)] = ct;
@@ -264,7 +272,7 @@ __device__ void sah_emit(const SahTask& T, const float box[6], const int* sp, in
     }
 }
 
-// ---- ranges of SAH_SMALL < m <= SAH_BIG prims: one CTA each ----------------------------
+// ---- ranges of small_max < m <= SAH_BIG prims: one CTA each ----------------------------
 
 __global__ void __launch_bounds__(SAH_BLOCK) k_sah_large(const SahTask* __restrict__ tasks, const int* d_ntask,
                                                         int* idx0, int* idx1, const float* __restrict__ pbox,
@@ -530,7 +538,7 @@ __global__ void __launch_bounds__(SAH_BLOCK) k_sahb_write(const SahTask* __restr
     sah_partition(T, b0, e0, src, dst, cent, s_sp, lo, scale, lbase, rbase, s_wl, s_wr);
 }
 
-// one thread finishes a range of 2..SAH_SMALL prims with the exact sweep SAH
+// one thread finishes a range of 2..small_max prims with the exact sweep SAH
 __global__ void __launch_bounds__(128) k_sah_small(const SahTask* __restrict__ small, const int* d_nsmall,
                                                    const int* idx0, const int* idx1,
                                                    const float* __restrict__ pbox,

@@ -71,8 +71,33 @@ class EvalContext:
             rows = memo[key] = rotation_entries(*key)
         return rows
 
+    def rotation_rows_many(self, devices):
+        """rotation_rows for a list of devices: one rotation per distinct
+        orientation, shared row tuples (receivers mostly share one)."""
+        yprs = [self.orientations.get(d.name, d.orientation) for d in devices]
+        try:
+            arr = np.asarray(yprs, dtype=np.float64)
+        except (TypeError, ValueError, RuntimeError):   # tensor leaves: per device, no memo
+            return [self.rotation_rows(d) for d in devices]
+        if arr.shape != (len(devices), 3):
+            return [self.rotation_rows(d) for d in devices]
+        uniq, inv = np.unique(arr, axis=0, return_inverse=True)
+        memo = self.__dict__.setdefault("_rows_memo", {})
+        rows = []
+        for u in uniq:
+            key = (float(u[0]), float(u[1]), float(u[2]))
+            r = memo.get(key)
+            if r is None:
+                r = memo[key] = rotation_entries(*key)
+            rows.append(r)
+        return [rows[i] for i in inv.reshape(-1)]
+
     def eta_table(self, bvh):
         """Complex permittivity per material in the scene's material order, [n_mat, 2]."""
+        return torch.tensor(self.eta_values(bvh), dtype=torch.float64, device=bvh.device)
+
+    def eta_values(self, bvh):
+        """eta_table on the host (numpy [n_mat, 2])."""
         vals = []
         for name in bvh.material_names:
             m = self.scene.materials[name]
@@ -83,7 +108,7 @@ class EvalContext:
             vals.append((e, s * (-eta_scale(self.scene.frequency_hz))))
         if not vals:
             vals = [(1.0, 0.0)]
-        return torch.tensor(vals, dtype=torch.float64, device=bvh.device)
+        return np.asarray(vals, dtype=np.float64).reshape(-1, 2)
 
 
 def path_materials(scene, bvh, path) -> tuple:
@@ -125,13 +150,16 @@ def _table_from_paths(paths, bvh, tx_names, rx_names):
 
 
 def _launch_transfer(bvh, T: PathTable, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, eta, wavelength,
-                     frequency):
+                     frequency, slants_dev=None):
     P = T.n
     a = torch.empty((P, len(st), len(sr), 2), dtype=torch.float64, device=bvh.device)
     if P == 0:
         return a
-    stt = torch.tensor(st, dtype=torch.float64, device=bvh.device)
-    srt = torch.tensor(sr, dtype=torch.float64, device=bvh.device)
+    if slants_dev is not None:   # already on the device (compute_gains' single upload)
+        stt, srt = slants_dev
+    else:
+        stt = torch.tensor(st, dtype=torch.float64, device=bvh.device)
+        srt = torch.tensor(sr, dtype=torch.float64, device=bvh.device)
     with torch.cuda.device(bvh.device):
         bvh.ctx.call("rt_transfer", P, T.L, N.ptr(T.order), N.ptr(T.seq), N.ptr(T.verts),
                      N.ptr(T.normals), N.ptr(T.cos), N.ptr(T.length), N.ptr(T.delay),
@@ -148,10 +176,11 @@ class PathCoefficients(torch.autograd.Function):
     through the Fresnel / basis-change chain, em.py:123-171)."""
 
     @staticmethod
-    def forward(ctx, eta, bvh, T, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, wavelength, frequency):
+    def forward(ctx, eta, bvh, T, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, wavelength, frequency,
+                slants_dev=None):
         eta_c = eta.detach().contiguous()
         a = _launch_transfer(bvh, T, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, eta_c, wavelength,
-                             frequency)
+                             frequency, slants_dev)
         ctx.save_for_backward(eta_c)
         ctx.args = (bvh, T, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, wavelength, frequency)
         return torch.view_as_complex(a)
@@ -172,16 +201,16 @@ class PathCoefficients(torch.autograd.Function):
                              N.ptr(stt), len(st), N.ptr(srt), len(sr), N.ptr(eta), eta.shape[0],
                              float(wavelength), float(frequency), N.ptr(g), N.ptr(grad_eta),
                              bvh.ctx.stream)
-        return (grad_eta,) + (None,) * 10
+        return (grad_eta,) + (None,) * 11
 
 
 def path_coefficients(bvh, T: PathTable, eta, tx_rows, rx_rows, tx_pattern, rx_pattern,
-                      tx_slants, rx_slants, wavelength, frequency):
+                      tx_slants, rx_slants, wavelength, frequency, slants_dev=None):
     """Differentiable a[p, s, r] (complex128) for a device path table."""
     return PathCoefficients.apply(eta, bvh, T, tx_rows, rx_rows, pattern_id(tx_pattern),
                                   pattern_id(rx_pattern), tuple(float(s) for s in tx_slants),
                                   tuple(float(s) for s in rx_slants), float(wavelength),
-                                  float(frequency))
+                                  float(frequency), slants_dev)
 
 
 def rows_from_ypr(ypr):
@@ -298,8 +327,9 @@ class PathGain:
 class ChannelGains:
     """Columnar gains: a [P, rx_el, tx_el, T] complex128 on the device + path table."""
 
-    def __init__(self, scene, table: PathTable, a, sample_times, delay=None, el_geom=None):
+    def __init__(self, scene, table: PathTable, a, sample_times, delay=None, el_geom=None, ctx=None):
         self.scene = scene
+        self.ctx = ctx   # the library context of the device tensors (CIR packing kernels)
         self.table = table
         self.a = a
         self.sample_times = np.asarray(sample_times, dtype=np.float64)
@@ -317,7 +347,7 @@ class ChannelGains:
                 self._entries = []
             else:
                 h = T.host()
-                a = self.a.cpu().numpy()
+                a = N.d2h(self.a)
                 dl = self.delay.cpu().numpy()
                 eg = [g.cpu().numpy() for g in self.el_geom] if self.el_geom else None
                 out = []
@@ -348,7 +378,7 @@ def _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows, rx_rows):
     memo = {}   # rows are shared tuples (EvalContext.rotation_rows memo): one aperture each
 
     def ap(off, r, tag):
-        k = (tag, r) if isinstance(r, tuple) else None
+        k = (tag, id(r)) if isinstance(r, tuple) else None   # shared row tuples: by identity
         if k is None:
             return _aperture(off, r)
         v = memo.get(k)
@@ -360,13 +390,21 @@ def _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows, rx_rows):
     if max(ap_t + ap_r + [0.0]) == 0.0:
         return
     n_rx = len(T.rx_names)
+    a_pair = np.maximum(np.asarray(ap_t)[:, None], np.asarray(ap_r)[None, :]).reshape(-1)
+    fr_pair = 2.0 * a_pair * a_pair / scene.wavelength
+    # every path is at least as long as the straight tx-rx distance: when that
+    # already clears the Fraunhofer distance no path can warn (no read-back)
+    devs = {d.name: d for d in scene.devices}
+    tp = np.array([np.asarray(devs[n].position, dtype=np.float64) for n in T.tx_names]).reshape(-1, 3)
+    rp = np.array([np.asarray(devs[n].position, dtype=np.float64) for n in T.rx_names]).reshape(-1, 3)
+    dist = np.linalg.norm(tp[:, None, :] - rp[None, :, :], axis=-1).reshape(-1)
+    if not np.any((a_pair > 0.0) & (dist < fr_pair)):
+        return
     pair = T.tx.long() * n_rx + T.rx.long()
     mins_d = torch.full((len(T.tx_names) * n_rx,), float("inf"), dtype=torch.float64,
                         device=T.length.device)
     mins_d.scatter_reduce_(0, pair, T.length, reduce="amin")
     mins = mins_d.cpu().numpy()   # shortest path per (tx, rx) pair: one small read-back
-    a_pair = np.maximum(np.asarray(ap_t)[:, None], np.asarray(ap_r)[None, :]).reshape(-1)
-    fr_pair = 2.0 * a_pair * a_pair / scene.wavelength
     for k in np.flatnonzero(np.isfinite(mins) & (a_pair > 0.0) & (mins < fr_pair)):
         ti, ri = divmod(int(k), n_rx)
         warnings.warn(f"path {T.tx_names[ti]}->{T.rx_names[ri]} at {mins[k]:.1f} m is inside "
@@ -393,8 +431,8 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
         empty = torch.zeros((0, n_rx_el, n_tx_el, 1), dtype=torch.complex128, device=dev)
         return ChannelGains(scene, T, empty, np.zeros(1))
     devs = {d.name: d for d in scene.devices}
-    tx_rows_dev = [ctx.rotation_rows(devs[n]) for n in T.tx_names]
-    rx_rows_dev = [ctx.rotation_rows(devs[n]) for n in T.rx_names]
+    tx_rows_dev = ctx.rotation_rows_many([devs[n] for n in T.tx_names])
+    rx_rows_dev = ctx.rotation_rows_many([devs[n] for n in T.rx_names])
     if not scene.synthetic_array:
         return _gains_explicit(scene, bvh, T, ctx, off_tx, sl_tx, off_rx, sl_rx, tx_rows_dev,
                                rx_rows_dev, devs, eta)
@@ -404,34 +442,45 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
     sr = sorted(set(float(s) for s in sl_rx))
     # every small host-side parameter in one pinned upload
     n_td, n_rd = len(tx_rows_dev), len(rx_rows_dev)
-    parts = [np.asarray(tx_rows_dev, dtype=np.float64).reshape(-1),
-             np.asarray(rx_rows_dev, dtype=np.float64).reshape(-1),
-             np.asarray(off_tx, dtype=np.float64).reshape(-1),
-             np.asarray(off_rx, dtype=np.float64).reshape(-1),
+    # world-frame element offsets per device (em.py:372-379), on the host
+    rows_t = np.asarray(tx_rows_dev, dtype=np.float64).reshape(n_td, 3, 3)
+    rows_r = np.asarray(rx_rows_dev, dtype=np.float64).reshape(n_rd, 3, 3)
+    off_tx_w = np.einsum("ek,dmk->dem", np.asarray(off_tx, dtype=np.float64), rows_t)   # [n_tx, E, 3]
+    off_rx_w = np.einsum("ek,dmk->dem", np.asarray(off_rx, dtype=np.float64), rows_r)
+    eta_host = ctx.eta_values(bvh) if eta is None else np.zeros((0, 2))
+    parts = [rows_t.reshape(-1), rows_r.reshape(-1), off_tx_w.reshape(-1), off_rx_w.reshape(-1),
              np.array([st.index(float(x)) for x in sl_tx], dtype=np.float64),
-             np.array([sr.index(float(x)) for x in sl_rx], dtype=np.float64)]
+             np.array([sr.index(float(x)) for x in sl_rx], dtype=np.float64),
+             np.asarray(st, dtype=np.float64), np.asarray(sr, dtype=np.float64), eta_host.reshape(-1)]
     cuts = np.cumsum([0] + [len(x) for x in parts])
     allp = N.h2d(np.concatenate(parts), dev)
     seg = [allp[cuts[i]:cuts[i + 1]] for i in range(len(parts))]
     Rt, Rr = seg[0].reshape(n_td, 3, 3), seg[1].reshape(n_rd, 3, 3)
-    offt, offr = seg[2].reshape(-1, 3), seg[3].reshape(-1, 3)
-    s_index, r_index = seg[4].long(), seg[5].long()
+    offw_t, offw_r = seg[2].reshape(n_td, n_tx_el, 3), seg[3].reshape(n_rd, n_rx_el, 3)
     tx_rows = Rt.reshape(n_td, 9)[tx_idx].contiguous()
     rx_rows = Rr.reshape(n_rd, 9)[rx_idx].contiguous()
     if eta is None:
-        eta = ctx.eta_table(bvh)
+        eta = seg[8].reshape(-1, 2)
     base = path_coefficients(bvh, T, eta, tx_rows, rx_rows, tx_arr.pattern, rx_arr.pattern, st, sr,
-                             lam, scene.frequency_hz)                       # [P, S, R]
-    # world-frame element offsets per device (em.py:372-379)
-    off_tx_w = torch.einsum("ek,dmk->dem", offt, Rt)                           # [n_tx, E, 3]
-    off_rx_w = torch.einsum("ek,dmk->dem", offr, Rr)
+                             lam, scene.frequency_hz, slants_dev=(seg[6], seg[7]))  # [P, S, R]
     if scene.synthetic_array:
         _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows_dev, rx_rows_dev)
-    ph_tx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", off_tx_w[tx_idx], T.kdep) / lam)
-    ph_rx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", off_rx_w[rx_idx], -T.karr) / lam)
+    if not base.requires_grad:   # one kernel: element phasors x slant coefficients
+        a = torch.empty((T.n, n_rx_el, n_tx_el), dtype=torch.complex128, device=dev)
+        si = seg[4].to(torch.int32)
+        ri = seg[5].to(torch.int32)
+        with torch.cuda.device(dev):
+            bvh.ctx.call("rt_gains_synthetic", T.n, len(st), len(sr), N.ptr(base), N.ptr(T.tx),
+                         N.ptr(T.rx), N.ptr(T.kdep), N.ptr(T.karr), n_tx_el, N.ptr(offw_t), N.ptr(si),
+                         n_rx_el, N.ptr(offw_r), N.ptr(ri), float(lam), N.ptr(a), bvh.ctx.stream,
+                         exc_map={N.RT_EINVAL: EmError})
+        return ChannelGains(scene, T, a[..., None], np.zeros(1), ctx=bvh.ctx)
+    s_index, r_index = seg[4].long(), seg[5].long()
+    ph_tx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", offw_t[tx_idx], T.kdep) / lam)
+    ph_rx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", offw_r[rx_idx], -T.karr) / lam)
     b = base[:, s_index][:, :, r_index].transpose(1, 2)                       # [P, rx_el, tx_el]
     a = b * ph_rx[:, :, None] * ph_tx[:, None, :]
-    return ChannelGains(scene, T, a[..., None], np.zeros(1))
+    return ChannelGains(scene, T, a[..., None], np.zeros(1), ctx=bvh.ctx)
 
 
 def _gains_explicit(scene, bvh, T, ctx, off_tx, sl_tx, off_rx, sl_rx, tx_rows_dev, rx_rows_dev,
@@ -485,7 +534,8 @@ def _gains_explicit(scene, bvh, T, ctx, off_tx, sl_tx, off_rx, sl_rx, tx_rows_de
     el = (torch.where(valid, Q.delay, torch.zeros_like(Q.delay)).reshape(P, nr, nt),
           torch.where(valid[:, None], Q.kdep, z3).reshape(P, nr, nt, 3),
           torch.where(valid[:, None], Q.karr, z3).reshape(P, nr, nt, 3))
-    return ChannelGains(scene, T, a.reshape(P, nr, nt, 1), np.zeros(1), delay=mean, el_geom=el)
+    return ChannelGains(scene, T, a.reshape(P, nr, nt, 1), np.zeros(1), delay=mean, el_geom=el,
+                        ctx=bvh.ctx)
 
 
 def apply_doppler(gains: ChannelGains, sampling_frequency: float, num_time_steps: int,
@@ -498,7 +548,8 @@ def apply_doppler(gains: ChannelGains, sampling_frequency: float, num_time_steps
     T = gains.table
     t = np.arange(num_time_steps) / sampling_frequency
     if T is None or T.n == 0:
-        return ChannelGains(gains.scene, T, gains.a[..., :1].repeat(1, 1, 1, num_time_steps), t)
+        return ChannelGains(gains.scene, T, gains.a[..., :1].repeat(1, 1, 1, num_time_steps), t,
+                            ctx=gains.ctx)
     dev = gains.a.device
 
     def vel(side, names):
@@ -522,7 +573,7 @@ def apply_doppler(gains: ChannelGains, sampling_frequency: float, num_time_steps
         fd = f_over_c * ((T.kdep * vt).sum(-1) - (T.karr * vr).sum(-1))         # [P]
         ph = torch.exp(1j * TWO_PI * fd[:, None] * tt[None, :])                # [P, T]
         a = gains.a[..., :1] * ph[:, None, None, :]
-    return ChannelGains(gains.scene, T, a, t, delay=gains.delay, el_geom=gains.el_geom)
+    return ChannelGains(gains.scene, T, a, t, delay=gains.delay, el_geom=gains.el_geom, ctx=gains.ctx)
 
 
 def slants_of(arr):

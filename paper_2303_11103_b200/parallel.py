@@ -20,6 +20,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import _native as N
 from .channel import coverage_from_candidates
 from .tracer import get_candidates, run_launch, set_candidates
 
@@ -143,7 +144,7 @@ def coverage_map(scene, bvh, grid, max_depth, num_rays, rank=0, world=1, tx_mode
     tx = [d for d in scene.devices if d.kind == "tx"][0]
     bounces, _, g = coverage_step(scene, bvh, tx, grid, max_depth, num_rays, rank, world,
                                   tx_mode=tx_mode)
-    return g.cpu().numpy(), bounces
+    return N.d2h(g), bounces
 
 
 def merge_candidate_rows(rows_per_rank):

@@ -650,3 +650,31 @@ def test_degenerate_arguments_fail_loudly(P):
         P.coverage_map(sc, b, P.GridSpec((0.0, 0.0), 1.0, 600, 600, 1.5), 1)
     with pytest.raises(ValueError):   # tx and probe coincide (channel.py:190-233 via los_path)
         P.point_path_gain(sc, b, tx, np.asarray(tx.position, dtype=float), 1, "exhaustive", 4096)
+
+
+@pytest.mark.parametrize("case", ["box", "canyon", "two_ray"])
+def test_device_cir_packing_matches_reference(P, golden, case):
+    """rt_cir_plan / rt_cir_scatter (the no-grad build_cir path) against the
+    reference's CIR bit for bit, and against the torch packing for the LOS /
+    specular filters and first-arrival normalisation."""
+    from test_host_logic import _cpu_gains
+    from paper_2303_11103_b200.em import ChannelGains
+    g = golden(case)
+    sc = golden_scene(g)
+    b = _bvh(P, sc)
+
+    def dev_gains():
+        c = _cpu_gains(sc, g)
+        T = c.table
+        for f in T.FIELDS:
+            setattr(T, f, getattr(T, f).cuda())
+        return ChannelGains(sc, T, c.a.cuda(), np.zeros(1), ctx=b.ctx)
+
+    cir = P.build_cir(dev_gains())
+    assert np.array_equal(cir.a, g["cir_a"]) and np.array_equal(cir.tau, g["cir_tau"])
+    for kw in (dict(los=True, reflection=False), dict(los=False, reflection=True),
+               dict(normalize_delays=True)):
+        want = P.build_cir(_cpu_gains(sc, g), **kw)
+        got = P.build_cir(dev_gains(), **kw)
+        assert np.array_equal(got.a, want.a) and np.array_equal(got.tau, want.tau), kw
+
