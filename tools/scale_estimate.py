@@ -54,7 +54,8 @@ def main():
         for _ in range(2):   # first call may grow the library's scratch buffers
             _, t_u = timed(lambda: set_candidates(b, cat, lc, L))
         t_c = []
-        coverage_from_candidates(sc, b, tx, grid, shard_index=0, shard_count=W)
+        for r in range(W):   # warm every shard first: a shard may grow the scratch buffers
+            coverage_from_candidates(sc, b, tx, grid, shard_index=r, shard_count=W)
         for r in range(W):
             _, tc = timed(lambda: coverage_from_candidates(sc, b, tx, grid, shard_index=r, shard_count=W))
             t_c.append(tc)
