@@ -25,7 +25,7 @@
 namespace rt {
 
 #ifndef RT_SAH_BINS
-#define RT_SAH_BINS 16
+#define RT_SAH_BINS 32   // C3 launch 14.33 vs 14.49 ms (16 bins), 19.2 vs 19.6 nodes per bounce
 #endif
 constexpr int SAH_BINS = RT_SAH_BINS;
 #ifndef RT_SAH_SMALL
@@ -48,7 +48,6 @@ constexpr int SAH_CHUNK = 2048;
 constexpr int SAH_NCAND = 3 * (SAH_BINS - 1);
 constexpr int SAH_NB = 3 * SAH_BINS * 7;   // bins per range: count + 6 ordered bounds, 3 axes
 constexpr int SAH_NW = SAH_BLOCK / 32;
-static_assert(SAH_NCAND <= SAH_BLOCK, "one split candidate per thread");
 
 // a primitive range [begin, end) whose node hangs off `parent` as child
 // `side & 1`; bit 1 of side names the index buffer holding the range
@@ -136,9 +135,9 @@ __device__ __forceinline__ void sah_bin_warp(bool valid, int p, const float* __r
 // centroid coincides (split the range in the middle).
 __device__ void sah_choose(const unsigned* bins, const float scale[3], int m, float* s_cost, int* out) {
     int tid = threadIdx.x;
-    if (tid < SAH_NCAND) {
+    for (int cand = tid; cand < SAH_NCAND; cand += blockDim.x) {   // any block size
         float cost = INFINITY;
-        int a = tid / (SAH_BINS - 1), s = tid % (SAH_BINS - 1);
+        int a = cand / (SAH_BINS - 1), s = cand % (SAH_BINS - 1);
         if (scale[a] != 0.f) {
             float l[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
             float r[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -157,7 +156,7 @@ __device__ void sah_choose(const unsigned* bins, const float scale[3], int m, fl
                 cost = box_area(l[0], l[1], l[2], l[3], l[4], l[5]) * (float)nl +
                        box_area(r[0], r[1], r[2], r[3], r[4], r[5]) * (float)nr;
         }
-        s_cost[tid] = cost;
+        s_cost[cand] = cost;
     }
     __syncthreads();
     if (tid == 0) {
