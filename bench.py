@@ -17,6 +17,10 @@ N > 1   = torchrun, one rank per GPU: rays sharded by slot range (stage 1),
           grids sum-all-reduced over NCCL.  "scaling": "weak" is not claimed —
           total work is fixed (strong scaling).
 
+Also on the line: c2_paths_cir (BASELINE metric part 2, C2 compute_paths +
+CIR latency through the public API) and c4_material_grad (C4: one gradient
+step of the material-learning loss through the adjoint).
+
 --impl reference runs the CPU oracle (a restatement of the reference
 algorithm, pinned to its golden vectors) on the host cores: each step is a
 bounded sample of the same workload (see cpu_baseline.sample).
@@ -310,6 +314,7 @@ def run_b200(args):
         line["e2e"] = e2e
     if not args.no_c2:
         line["c2_paths_cir"] = c2_latency(args)
+        line["c4_material_grad"] = c4_latency(args)
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, sc, tx, grid, samples=1)
     return line
@@ -340,6 +345,48 @@ def c2_latency(args):
             "unit": "ms", "higher_is_better": False, "paths": out[0], "cir_a_shape": out[1],
             "triangles": out[2], "rx": 256, "tx_elements": 64, "num_rays": 1_000_000, "max_depth": 3,
             "includes": "build(scene) H2D + launch + paths + gains + CIR D2H"}
+
+
+def c4_latency(args):
+    """Config 4 (learning radio materials): one gradient step of the NMSE
+    frequency-response loss w.r.t. (eps_r, sigma) of the 4 trainable materials
+    through the hand-written adjoint — calib scene, 400 receivers, 128
+    subcarriers at 30 kHz, depth 2, paths frozen (optim.MaterialProblem)."""
+    import torch
+    from paper_2303_11103_b200 import optim, scenes
+    truth, init = scenes.calib_scene(truth=True), scenes.calib_scene(truth=False)
+    pos = np.array([d.position for d in truth.devices if d.kind == "rx"], dtype=np.float64)
+    ds = optim.generate_dataset(truth, pos, 128, 30e3, max_depth=2)
+    h = np.array([r.h for r in ds.records])
+    keep = (np.abs(h) ** 2).sum(-1) > 0.0   # receivers inside buildings have no response
+    pos, h = pos[keep], h[keep]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prob = optim.MaterialProblem(init, pos, h, 2, 128, 30e3)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    times, grads, loss = [], {}, None
+    for i in range(args.warmup + args.steps):
+        vals = {n: tuple(torch.tensor(float(getattr(init.materials[n], k)), dtype=torch.float64,
+                                      device=prob.bvh.device, requires_grad=True)
+                         for k in ("eps_r", "sigma")) for n in prob.names}
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        lo = prob.loss(vals)
+        lo.backward()
+        grads = {f"{n}:{k}": float(v.grad) for n, pair in vals.items() for k, v in zip(("eps_r", "sigma"), pair)}
+        loss = float(lo.detach())
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            times.append(t1 - t0)
+    return {"metric": "material-gradient step latency", "value_ms": 1e3 * float(np.median(times)),
+            "unit": "ms", "higher_is_better": False, "setup_ms": 1e3 * setup, "records": len(pos),
+            "receivers_generated": int(len(keep)),
+            "materials": len(prob.names), "paths": int(prob.T.n), "subcarriers": 128, "max_depth": 2,
+            "loss": loss, "grads": grads,
+            "includes": "forward (rt_transfer + OFDM responses + NMSE) + backward (rt_transfer_bwd "
+                        "adjoint) + 8 gradient read-backs; setup = build + exhaustive candidates + path solve of "
+                        "the records (frozen topology)"}
 
 
 def _profile(bvh):
