@@ -1031,12 +1031,12 @@ extern "C" {
 int rt_enumerate(rt_ctx* ctx, int max_depth, int64_t cap, int64_t* n_cand_out, void* stream) {
     if (!ctx) return RT_EINVAL;
     if (max_depth < 1) return fail(ctx, RT_EINVAL, "max_depth must be >= 1 for candidate enumeration");
-    if (max_depth > MAX_DEPTH) return fail(ctx, RT_EINVAL, "max_depth above the compiled bound (8)");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ST(stream);
     long long n = ctx->n_prims;
+    // the reference's order of checks (tracer.py:198-207): empty scene, then the cap
     if (n == 0) {
-        RC(sort_unique_candidates(ctx, 0, max_depth, st));
+        RC(sort_unique_candidates(ctx, 0, std::min(max_depth, MAX_DEPTH), st));
         if (n_cand_out) *n_cand_out = 0;
         return RT_OK;
     }
@@ -1049,6 +1049,7 @@ int rt_enumerate(rt_ctx* ctx, int max_depth, int64_t cap, int64_t* n_cand_out, v
                  n, max_depth, (double)cap);
         return fail(ctx, RT_ECAP, buf);
     }
+    if (max_depth > MAX_DEPTH) return fail(ctx, RT_EINVAL, "max_depth above the compiled bound (8)");
     std::vector<long long> start(max_depth + 1, 0);
     long long level = n, total = 0;
     for (int k = 0; k < max_depth; ++k) {

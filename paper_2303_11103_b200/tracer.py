@@ -331,6 +331,10 @@ def solve_pairs(bvh: Bvh, tx_pos, rx_pos, seqs, lens):
         tx_pos = np.array(tx_pos)
     if isinstance(rx_pos, np.ndarray) and not rx_pos.flags.writeable:
         rx_pos = np.array(rx_pos)
+    if not isinstance(tx_pos, torch.Tensor):
+        tx_pos = np.asarray(tx_pos, dtype=np.float64)
+    if not isinstance(rx_pos, torch.Tensor):
+        rx_pos = np.asarray(rx_pos, dtype=np.float64)
     tx = torch.as_tensor(tx_pos, **f64).reshape(-1, 3).contiguous()
     rx = torch.as_tensor(rx_pos, **f64).reshape(-1, 3).contiguous()
     sq = torch.as_tensor(seqs, dtype=torch.int32, device=dev).contiguous()

@@ -1,0 +1,283 @@
+"""Known-answer tests of the reference suite, restated against the CUDA path.
+
+Each test reproduces one known answer the reference's own tests pin
+(file:line under /root/reference/pkg/tests, cited per test) — analytic values,
+invariants and error behaviour — through this package's public API, i.e.
+through libb200rt.  The scenes are rebuilt here from their descriptions.
+"""
+
+import cmath
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_scene
+
+pytestmark = pytest.mark.gpu
+
+C0 = 299792458.0
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2303_11103_b200 as P
+    assert torch.cuda.is_available()
+    return P
+
+
+def _quad(P, name, material, corners):
+    return P.SceneObject(name, material, np.array(corners, dtype=float), np.array([[0, 1, 2], [0, 2, 3]]))
+
+
+def _scene(P, objects=(), materials=(), devices=(), frequency_hz=1e9, arr=None):
+    arr = arr or P.AntennaArray(pattern="iso", polarization="V")
+    sc = P.Scene(frequency_hz, list(objects), {m.name: m for m in materials}, arr, arr, list(devices))
+    sc.validate()
+    return sc
+
+
+def _dev(P, kind, name, pos):
+    return P.RadioDevice(kind, name, np.array(pos, dtype=float))
+
+
+def _ground(P, tx=(0, 0, 10), rx=(100, 0, 10), L=10000.0, eps_r=15.0, sigma=0.015):
+    return _scene(P, [_quad(P, "ground", "ground", [(-L, -L, 0), (L, -L, 0), (L, L, 0), (-L, L, 0)])],
+                  [P.RadioMaterial("ground", "constant", eps_r, sigma)],
+                  [_dev(P, "tx", "tx", tx), _dev(P, "rx", "rx", rx)],
+                  arr=P.AntennaArray(pattern="iso", polarization="H"))
+
+
+def _corner(P):
+    """Two perpendicular metal walls meeting on the z axis (a retroreflector)."""
+    return _scene(P, [_quad(P, "wall_a", "metal", [(0, 0, 0), (0, 10, 0), (0, 10, 10), (0, 0, 10)]),
+                      _quad(P, "wall_b", "metal", [(0, 0, 0), (10, 0, 0), (10, 0, 10), (0, 0, 10)])],
+                  [P.RadioMaterial("metal", "constant", 1.0, 1e7)],
+                  [_dev(P, "tx", "tx", (4.0, 3.0, 5.0)), _dev(P, "rx", "rx", (3.0, 4.0, 5.0))])
+
+
+def _cube(P, L=2.0, mat=5.0):
+    faces = [[(-L, -L, -L), (L, -L, -L), (L, L, -L), (-L, L, -L)],
+             [(-L, -L, L), (L, -L, L), (L, L, L), (-L, L, L)],
+             [(-L, -L, -L), (L, -L, -L), (L, -L, L), (-L, -L, L)],
+             [(-L, L, -L), (L, L, -L), (L, L, L), (-L, L, L)],
+             [(-L, -L, -L), (-L, L, -L), (-L, L, L), (-L, -L, L)],
+             [(L, -L, -L), (L, L, -L), (L, L, L), (L, -L, L)]]
+    return [_quad(P, f"f{i}", "m", c) for i, c in enumerate(faces)], [P.RadioMaterial("m", "constant", mat)]
+
+
+def _free_space(P):
+    return _scene(P, devices=[_dev(P, "tx", "tx", (0, 0, 1.5)), _dev(P, "rx", "rx", (100.0, 0, 1.5))])
+
+
+# ---- LOS (T/test_tracer.py:31-70) ----------------------------------------------------------
+
+def test_los_free_space_delay(P):
+    sc = _scene(P, devices=[_dev(P, "tx", "tx", (0, 0, 0)), _dev(P, "rx", "rx", (100.0, 0, 0))])
+    p = P.los_path(sc, P.build(sc), sc.device("tx"), sc.device("rx"))
+    assert p is not None and p.kind == "los" and p.order == 0
+    assert p.length_m == 100.0
+    assert p.delay_s == pytest.approx(100.0 / C0, rel=1e-15)
+    assert p.delay_s == pytest.approx(333.564095e-9, rel=1e-8)
+
+
+def test_los_wall_blocks_and_open_edge_clears(P):
+    wall = _quad(P, "wall", "m", [(5, -5, 0), (5, 5, 0), (5, 5, 20), (5, -5, 20)])
+    m = [P.RadioMaterial("m", "constant", 3.0)]
+    sc = _scene(P, [wall], m, [_dev(P, "tx", "tx", (0, 0, 10)), _dev(P, "rx", "rx", (10, 0, 10))])
+    assert P.los_path(sc, P.build(sc), sc.device("tx"), sc.device("rx")) is None
+    sc2 = _scene(P, [wall], m, [_dev(P, "tx", "tx", (0, 8, 10)), _dev(P, "rx", "rx", (10, 8, 10))])
+    assert P.los_path(sc2, P.build(sc2), sc2.device("tx"), sc2.device("rx")) is not None
+
+
+def test_los_coincident_devices_rejected(P):
+    sc = _scene(P, devices=[_dev(P, "tx", "tx", (1, 1, 1)), _dev(P, "rx", "rx", (1, 1, 1))])
+    with pytest.raises(P.TracerError, match="coincide"):
+        P.los_path(sc, P.build(sc), sc.device("tx"), sc.device("rx"))
+
+
+# ---- enumeration, image method (T/test_tracer.py:73-150) -----------------------------------
+
+def test_enumerate_two_prims(P):
+    b = P.build(_ground(P))
+    assert set(P.enumerate_candidates(b, 2)) == {(0,), (1,), (0, 1), (1, 0)}
+    assert set(P.enumerate_candidates(b, 3)) == {(0,), (1,), (0, 1), (1, 0), (0, 1, 0), (1, 0, 1)}
+    with pytest.raises(P.TracerError, match="fibonacci"):
+        P.enumerate_candidates(b, 60, cap=10**6)
+
+
+def test_image_solve_single_bounce_symmetric(P):
+    b = P.build(_ground(P, tx=(0, 0, 10), rx=(20, 0, 10)))
+    paths = [P.image_solve("tx", "rx", [0, 0, 10], [20, 0, 10], s, b) for s in [(0,), (1,)]]
+    p = next(x for x in paths if x is not None)
+    assert np.allclose(p.vertices[1], [10, 0, 0], atol=1e-9)
+    assert p.length_m == pytest.approx(2 * math.hypot(10, 10), rel=1e-12)
+    assert p.length_m == pytest.approx(28.2843, abs=1e-4)
+
+
+def test_image_solve_outside_primitive_and_wrong_side_invalid(P):
+    small = _scene(P, [_quad(P, "ground", "ground", [(-5, -5, 0), (5, -5, 0), (5, 5, 0), (-5, 5, 0)])],
+                   [P.RadioMaterial("ground", "constant", 15.0, 0.015)],
+                   [_dev(P, "tx", "tx", (0, 0, 10)), _dev(P, "rx", "rx", (20, 0, 10))])
+    b = P.build(small)
+    assert all(P.image_solve("tx", "rx", [0, 0, 10], [20, 0, 10], s, b) is None for s in [(0,), (1,)])
+    b2 = P.build(_ground(P, L=50))
+    assert all(P.image_solve("tx", "rx", [0, 0, 10], [20, 0, -10], s, b2) is None for s in [(0,), (1,)])
+
+
+def test_on_plane_invariants(P):
+    sc = _ground(P, tx=(3, -7, 12), rx=(25, 11, 6))
+    paths = P.compute_paths_between(sc, P.build(sc), sc.device("tx"), sc.device("rx"), 1)
+    refl = [p for p in paths if p.kind == "specular"]
+    assert len(refl) == 1
+    p = refl[0]
+    assert abs(p.vertices[1][2]) < 1e-6
+    d_in = (p.vertices[1] - p.vertices[0]) / np.linalg.norm(p.vertices[1] - p.vertices[0])
+    d_out = (p.vertices[2] - p.vertices[1]) / np.linalg.norm(p.vertices[2] - p.vertices[1])
+    n = p.normals[0]
+    assert abs(math.acos(-d_in @ n) - math.acos(d_out @ n)) < 1e-9
+    assert p.delay_s * C0 == pytest.approx(p.length_m, rel=1e-12)
+
+
+def test_corner_retroreflector_antiparallel(P):
+    sc = _corner(P)
+    dbl = [p for p in P.compute_paths_between(sc, P.build(sc), sc.device("tx"), sc.device("rx"), 2)
+           if p.order == 2]
+    assert dbl
+    for p in dbl:
+        assert np.dot(p.k_dep, p.k_arr) < 0 and np.linalg.norm(np.cross(p.k_dep, p.k_arr)) < 1e-9
+
+
+# ---- launch (T/test_tracer.py:153-182) ------------------------------------------------------
+
+def test_launch_known_answers(P):
+    sc = _ground(P)
+    got = P.launch_candidates(sc, P.build(sc), [0, 0, 10], max_depth=1, num_rays=1000)
+    assert got and got <= {(0,), (1,)}
+    c = _corner(P)
+    bc = P.build(c)
+    got = P.launch_candidates(c, bc, [4, 3, 5], max_depth=2, num_rays=2000)
+    assert got <= set(P.enumerate_candidates(bc, 2))
+    assert any(len(s) == 2 and s[0] in {0, 1} and s[1] in {2, 3} for s in got)
+    got = P.launch_candidates(c, bc, [4, 3, 5], max_depth=2, num_rays=500)
+    assert all(s[:1] in got for s in got if len(s) == 2)
+
+
+# ---- compute_paths (T/test_tracer.py:185-285) -----------------------------------------------
+
+def test_sealed_cube_blocks_every_path(P):
+    objs, mats = _cube(P)
+    sc = _scene(P, objs, mats, [_dev(P, "tx", "tx", (30, 0, 0)), _dev(P, "rx", "rx", (0, 0, 0))])
+    assert P.compute_paths(sc, P.build(sc), max_depth=2).paths == []
+
+
+@pytest.mark.parametrize("depth,rays", [(2, 4096), (3, 16384)])
+def test_fibonacci_equals_exhaustive_on_box(P, golden, depth, rays):
+    sc = golden_scene(golden("box"))
+    b = P.build(sc)
+    ex = P.compute_paths(sc, b, max_depth=depth, method="exhaustive")
+    fib = P.compute_paths(sc, b, max_depth=depth, method="fibonacci", num_rays=rays)
+    key = lambda p: (p.kind, p.seq)  # noqa: E731
+    assert {key(p) for p in fib.paths} == {key(p) for p in ex.paths}
+    lens = {key(p): p.length_m for p in ex.paths}
+    assert all(p.length_m == pytest.approx(lens[key(p)], rel=1e-12) for p in fib.paths)
+
+
+def test_snell_reciprocity_and_uniqueness_on_box(P, golden):
+    sc = golden_scene(golden("box"))
+    b = P.build(sc)
+    ps = P.compute_paths(sc, b, max_depth=2)
+    for p in ps.paths:
+        for k in range(p.order):
+            d_in = p.vertices[k + 1] - p.vertices[k]
+            d_out = p.vertices[k + 2] - p.vertices[k + 1]
+            d_in, d_out = d_in / np.linalg.norm(d_in), d_out / np.linalg.norm(d_out)
+            n = p.normals[k]
+            assert abs(math.acos(np.clip(-d_in @ n, -1, 1)) - math.acos(np.clip(d_out @ n, -1, 1))) < 1e-9
+            assert abs(np.cross(d_in, n) @ d_out) < 1e-9
+    keys = [(p.kind, p.seq) for p in ps.paths]
+    assert len(keys) == len(set(keys))
+    tx, rx = sc.device("tx"), sc.device("rx")
+    sw = P.Scene(sc.frequency_hz, sc.objects, sc.materials, sc.tx_array, sc.rx_array,
+                 [P.RadioDevice("tx", "tx2", rx.position.copy()), P.RadioDevice("rx", "rx2", tx.position.copy())])
+    back = P.compute_paths(sw, P.build(sw), max_depth=2)
+    fwd = sorted((p.kind, p.seq, round(p.length_m, 9)) for p in ps.paths)
+    bwd = sorted((p.kind, tuple(reversed(p.seq)), round(p.length_m, 9)) for p in back.paths)
+    assert fwd == bwd
+
+
+def test_two_ray_depth_one_and_coplanar_merge(P, golden):
+    sc = golden_scene(golden("two_ray"))
+    b = P.build(sc)
+    ps = P.compute_paths(sc, b, max_depth=1)
+    assert [p.kind for p in ps.paths] == ["los", "specular"]
+    assert [p.kind for p in P.compute_paths(sc, b, max_depth=0).paths] == ["los"]
+    with pytest.raises(P.TracerError, match="method"):
+        P.compute_paths(sc, b, 1, method="magic")
+    lone = _scene(P, devices=[_dev(P, "tx", "tx", (0, 0, 0))])
+    with pytest.raises(P.TracerError):
+        P.compute_paths(lone, P.build(lone), 1)
+
+
+# ---- field transfer (T/test_em.py:205-223) --------------------------------------------------
+
+def test_friis_amplitude_and_phase(P):
+    sc = _free_space(P)
+    b = P.build(sc)
+    ps = P.compute_paths(sc, b, 1)
+    a = P.compute_gains(sc, b, ps).entries[0].a[0, 0, 0]
+    want = sc.wavelength / (4 * math.pi * 100.0)
+    assert abs(a) == pytest.approx(want, rel=1e-12)
+    assert abs(a) == pytest.approx(2.3856e-4, rel=1e-4)
+    d = (cmath.phase(a) + 2 * math.pi * sc.frequency_hz * ps.paths[0].delay_s) % (2 * math.pi)
+    assert min(d, 2 * math.pi - d) < 1e-6
+
+
+# ---- coverage and CIR layout (T/test_channel.py:151-214,249-276) -----------------------------
+
+def test_coverage_free_space_cell_is_friis(P):
+    sc = _free_space(P)
+    cm = P.coverage_map(sc, P.build(sc), P.GridSpec((95.0, -5.0), 10.0, 1, 1, 1.5), max_depth=1)
+    assert cm.gains[0, 0] == pytest.approx((sc.wavelength / (4 * math.pi * 100.0)) ** 2, rel=1e-9)
+
+
+def test_coverage_enclosed_cell_is_exactly_zero(P):
+    objs, mats = _cube(P)
+    sc = _scene(P, objs, mats, [_dev(P, "tx", "tx", (30, 0, 0.5)), _dev(P, "rx", "rx", (40, 0, 0.5))])
+    cm = P.coverage_map(sc, P.build(sc), P.GridSpec((-1.0, -1.0), 2.0, 1, 1, 0.0), max_depth=2)
+    assert cm.gains[0, 0] == 0.0
+
+
+def test_coverage_invariant_under_scene_permutation(P):
+    mats = [P.RadioMaterial("m", "constant", 4.0, 0.02)]
+    wall = lambda: _quad(P, "wall", "m", [(20, -10, 0), (20, 10, 0), (20, 10, 20), (20, -10, 20)])  # noqa: E731
+    ground = _quad(P, "ground", "m", [(-50, -50, 0), (50, -50, 0), (50, 50, 0), (-50, 50, 0)])
+    devs = lambda: [_dev(P, "tx", "tx", (0, 0, 10)), _dev(P, "rx", "rx", (10, 0, 1.5))]  # noqa: E731
+    grid = P.GridSpec((0.0, -10.0), 5.0, 3, 3, 1.5)
+    w2 = wall()
+    w2.triangles = w2.triangles[::-1].copy()
+    s1 = _scene(P, [ground, wall()], mats, devs())
+    s2 = _scene(P, [w2, ground], mats, devs())
+    g1 = P.coverage_map(s1, P.build(s1), grid, max_depth=2).gains
+    g2 = P.coverage_map(s2, P.build(s2), grid, max_depth=2).gains
+    assert np.allclose(g1, g2, rtol=1e-9, atol=0)
+
+
+def test_multi_device_dual_pol_cir_layout(P):
+    sc = _ground(P)
+    sc.devices = [_dev(P, "tx", "tx1", (0, 0, 10)), _dev(P, "tx", "tx2", (5, 5, 12)),
+                  _dev(P, "rx", "rx1", (80, 0, 10)), _dev(P, "rx", "rx2", (60, -20, 3))]
+    sc.tx_array = P.AntennaArray(num_rows=2, num_cols=1, pattern="iso", polarization="VH")
+    sc.rx_array = P.AntennaArray(pattern="iso", polarization="cross")
+    b = P.build(sc)
+    g = P.apply_doppler(P.compute_gains(sc, b, P.compute_paths(sc, b, 1)), 1e6, 3,
+                        tx_velocities={"tx1": [1, 0, 0]})
+    cir = P.build_cir(g)
+    assert cir.a.shape == (2, 2, 2, 4, 2, 3) and cir.tau.shape == (2, 2, 2)
+    fr = P.frequency_response(cir, 16, 30e3)
+    assert fr.h.shape == (4, 8, 16, 3)
+    r, re_, t, te, ti, k = 1, 0, 0, 2, 1, 5
+    manual = sum(cir.a[r, re_, t, te, p, ti] * np.exp(-2j * np.pi * fr.frequencies[k] * cir.tau[r, t, p])
+                 for p in range(cir.a.shape[4]))
+    assert fr.h[r * 2 + re_, t * 4 + te, k, ti] == pytest.approx(manual, abs=1e-18)
