@@ -281,3 +281,37 @@ def test_multi_device_dual_pol_cir_layout(P):
     manual = sum(cir.a[r, re_, t, te, p, ti] * np.exp(-2j * np.pi * fr.frequencies[k] * cir.tau[r, t, p])
                  for p in range(cir.a.shape[4]))
     assert fr.h[r * 2 + re_, t * 4 + te, k, ti] == pytest.approx(manual, abs=1e-18)
+
+
+# ---- acceptance criteria 1-2 (T/test_acceptance.py:34-78) ------------------------------------
+
+def test_acceptance_two_ray_analytic(P):
+    """Two-ray power within 0.1 dB of the closed-form grazing-angle model, 50..500 m."""
+    f_c, eps_r, sigma = 1e9, 15.0, 0.015
+    lam = C0 / f_c
+    k = 2 * math.pi / lam
+    eta = eps_r - 1j * sigma / (2 * math.pi * f_c * 8.8541878128e-12)
+    worst = 0.0
+    for d in range(50, 501, 50):
+        sc = _ground(P, tx=(0, 0, 10), rx=(d, 0, 10), eps_r=eps_r, sigma=sigma)
+        b = P.build(sc)
+        g = P.compute_gains(sc, b, P.compute_paths(sc, b, 1))
+        assert len(g.entries) == 2
+        power = abs(sum(e.a[0, 0, 0] for e in g.entries)) ** 2
+        d1, psi = math.hypot(d, 20.0), math.atan2(20.0, d)
+        root = cmath.sqrt(eta - math.cos(psi) ** 2)
+        gamma = (math.sin(psi) - root) / (math.sin(psi) + root)
+        field = cmath.exp(-1j * k * d) / d + gamma * cmath.exp(-1j * k * d1) / d1
+        model = (lam / (4 * math.pi)) ** 2 * abs(field) ** 2
+        worst = max(worst, abs(10 * math.log10(power / model)))
+    assert worst < 0.1
+
+
+def test_acceptance_friis_free_space(P):
+    sc = _free_space(P)
+    b = P.build(sc)
+    for d in (10.0, 100.0, 1000.0):
+        sc.device("rx").position[0] = d
+        got = abs(P.compute_gains(sc, b, P.compute_paths(sc, b, 1)).entries[0].a[0, 0, 0]) ** 2
+        want = (sc.wavelength / (4 * math.pi * d)) ** 2
+        assert abs(got - want) <= 1e-9 * want
