@@ -104,10 +104,11 @@ def l2_read_bandwidth(bvh):
 TRAFFIC_JSON = "profiles/r01_traffic.json"
 
 
-def committed_traffic(args):
-    """DRAM bytes per k_launch launch from the committed `ncu --set full` capture of
-    this same workload (tools/ncu_summary.py full ... <json>); None if absent or the
-    capture was of another configuration."""
+def committed_traffic(args, field="dram_bytes_per_launch"):
+    """Per-launch k_launch figure (DRAM bytes, or warp instructions executed with
+    field="warp_instructions_per_launch") from the committed `ncu --set full`
+    capture of this same workload (tools/ncu_summary.py full ... <json>); None if
+    absent or the capture was of another configuration."""
     import json as _json
     path = os.path.join(REPO, TRAFFIC_JSON)
     if not os.path.exists(path):
@@ -116,7 +117,7 @@ def committed_traffic(args):
     if d.get("workload") != workload_name(args) or float(d.get("num_rays", -1)) != float(args.rays) \
             or int(d.get("max_depth", -1)) != int(args.depth):
         return None
-    for k, v in d.get("dram_bytes_per_launch", {}).items():
+    for k, v in d.get(field, {}).items():
         if "k_launch" in k:
             return float(v)
     return None
@@ -310,6 +311,20 @@ def run_b200(args):
         "clocks": clocks.summary(),
         "gpu_launches": int(round(launches)),
     }
+    # the binding roofline of k_launch: warp-instruction issue (4 per SM per cycle)
+    insts = committed_traffic(args, "warp_instructions_per_launch")
+    if insts and launch_ms > 0:
+        import torch
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        clk = line["clocks"].get("sm_mhz") or line["clocks"].get("sm_max_mhz") or 1965.0
+        peak = n_sm * 4 * float(clk) * 1e6
+        line["roofline"]["issue"] = {
+            "bound": "warp-instruction issue", "unit": "warp-instructions/s",
+            "achieved": insts / (launch_ms / 1e3), "peak": peak, "frac": insts / (launch_ms / 1e3) / peak,
+            "warp_instructions_per_launch": insts,
+            "warp_instructions_per_bounce": insts / max(bounces_per_launch, 1.0),
+            "source": TRAFFIC_JSON + " (ncu inst_executed of this workload); peak = SMs x 4 "
+                      "schedulers x SM clock under load"}
     if e2e:
         line["e2e"] = e2e
     if not args.no_c2:

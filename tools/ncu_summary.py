@@ -62,9 +62,14 @@ def full(path, out, traffic_json=None):
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     dram = {}
     stalls = {}
+    insts = {}
     for r in rr[2:]:
         d = dict(zip(rh, r))
         k = (d.get("ID"), d.get("Kernel Name", "").split("(")[0])
+        try:
+            insts[k] = float(d["inst_executed"].replace(",", ""))
+        except (KeyError, ValueError):
+            pass
         try:
             dram[k] = sum(float(d[m].replace(",", "")) * scale.get(units.get(m, "byte"), 1.0)
                           for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
@@ -96,10 +101,13 @@ def full(path, out, traffic_json=None):
 
     if traffic_json:   # traffic per kernel for bench.py's roofline "traffic" field
         import json
-        tr = {}
+        tr, ins = {}, {}
         for k, v in dram.items():
             tr.setdefault(k[1], []).append(v)
-        json.dump({"source": path, "dram_bytes_per_launch": {k: sum(v) / len(v) for k, v in tr.items()}},
+        for k, v in insts.items():
+            ins.setdefault(k[1], []).append(v)
+        json.dump({"source": path, "dram_bytes_per_launch": {k: sum(v) / len(v) for k, v in tr.items()},
+                   "warp_instructions_per_launch": {k: sum(v) / len(v) for k, v in ins.items()}},
                   open(traffic_json, "w"), indent=1)
 
 
