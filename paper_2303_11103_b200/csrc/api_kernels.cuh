@@ -182,7 +182,7 @@ __global__ void k_solve_pairs(SceneDev S, Bvh bvh, long long n, int L, const dou
             if (sqrt(dx * dx + dy * dy + dz * dz) <= 2 * RAY_EPS) ok = false;
             a = b;
         }
-        if (ok) ok = segments_clear(bvh, tx, pts, K, rx);
+        if (ok) ok = segments_clear(bvh, tx, pts, K, rx, sq, S.nrm);
     } else {
         ok = S.n == 0 || occluded(bvh, tx, rx) == 0;
     }

@@ -90,12 +90,13 @@ struct rt_ctx {
     int64_t n_prims = 0;
     DevBuf v0, e1, e2, nrm, poff, prim_mat, pbox, cent, cbounds;
     // bvh
-    DevBuf nodes4, frontier, frontier2, map4, nodes, tris, sorted_idx, morton, morton_alt, idx_alt, child, parent_int, parent_leaf,
+    DevBuf nodes4, frontier, frontier2, map4, nodes, dbox, skip_tab, tris, sorted_idx, morton, morton_alt, idx_alt, child, parent_int, parent_leaf,
         rfirst, rlast, nbox, flags;
     bool bvh_ready = false;
     int bvh_depth = -1;           // deepest BNode (root 0); -1 = not measured
     bool tail_smem_set = false;   // k_ploc_tail's dynamic shared memory opt-in done
     double origin_limit = 0.0;
+    bool has_skip = false;        // origin skip table built with the tree (bvh_ploc.cuh)
     // candidates
     DevBuf cand_seq, cand_len;
     int64_t n_cand = 0;
@@ -187,6 +188,7 @@ rt::Bvh bvh_dev(rt_ctx* ctx) {
     b.tris = ctx->tris.get<TriRec>();
     b.n_prims = (int)ctx->n_prims;
     b.origin_limit = ctx->origin_limit;
+    b.skip = ctx->has_skip ? ctx->skip_tab.get<int>() : nullptr;
     return b;
 }
 
@@ -568,6 +570,21 @@ int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st) {
                                                         ctx->cbounds.get<unsigned>(), dfs, ctx->nodes.get<BNode>());
         CKL();
     }
+    if (RT_ORIGIN_SKIP && n > 1 && dfs) {   // exact FP64 boxes -> per-prim origin skip refs
+        CK(ctx->dbox.reserve(48ULL * (2 * n - 1)));
+        CK(ctx->skip_tab.reserve(8ULL * n));
+        CK(ctx->flags.reserve(4ULL * n));
+        CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
+        CK(cudaMemsetAsync(par + root, 0xFF, 4, st));   // the refit climb stops at the root
+        k_dbox_refit<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, ctx->v0.get<double>(), ctx->e1.get<double>(),
+                                                   ctx->e2.get<double>(), par, child, ctx->dbox.get<double>(),
+                                                   ctx->flags.get<int>());
+        k_skip_table<<<nblk(n, 256), 256, 0, st>>>((int)n, root, sidx, par, child, cnt, slot, dfs,
+                                                   ctx->dbox.get<double>(), ctx->nrm.get<double>(),
+                                                   ctx->poff.get<double>(), ctx->skip_tab.get<int>());
+        CKL();
+        ctx->has_skip = true;
+    }
     k_ploc_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, slot, ctx->v0.get<double>(), ctx->e1.get<double>(),
                                               ctx->e2.get<double>(), ctx->tris.get<TriRec>());
     CKL();
@@ -703,6 +720,7 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     cudaStream_t st = ST(stream);
     long long n = ctx->n_prims;
     ctx->bvh_ready = true;
+    ctx->has_skip = false;
     if (n == 0) return RT_OK;
     {   // scene scale S (ordered float in cbounds[6]) -> FP32 filter origin bound 2S
         unsigned u = 0;

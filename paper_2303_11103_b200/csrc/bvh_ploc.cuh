@@ -302,6 +302,80 @@ __global__ void k_ploc_layout(int n, int root, const int* child, const int* coun
     out[dfs ? dfs[q] : ploc_map(id, n, root)] = nd;
 }
 
+// ---- origin skip table ------------------------------------------------------------------
+//
+// A secondary ray starts ON the prim P it reflected off and leaves to one side
+// of P's plane.  Every subtree whose exact box lies in the closed half-space
+// on the other side holds no point the ray reaches at t > t_min, yet the FP32
+// filter (boxes inflated ~2e-3 m at C3 scale) walks the ray down into the very
+// building it leaves: 3 extra node visits and 1.2 extra triangle tests per
+// secondary bounce.  Per prim and side the table holds the child ref of the
+// highest ancestor of P's leaf that lies entirely behind P's plane (exact FP64
+// boxes, margin SKIP_MARGIN); the traversal treats that child as a miss.
+
+constexpr double SKIP_MARGIN = 1e-7;   // m: >> rounding, the 1e-12 barycentric slack of km-sized triangles
+
+// Exact FP64 boxes of the tree nodes (PLOC ids): leaf k = corners v0, v0 + e1,
+// v0 + e2 of prim sorted_idx[k]; internal nodes bottom-up (second arrival).
+__global__ void k_dbox_refit(int n, const int* sorted_idx, const double* v0, const double* e1,
+                             const double* e2, const int* parent, const int* child, double* dbox,
+                             int* flags) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int p = sorted_idx[k];
+    double* o = dbox + 6 * (long long)k;
+    for (int a = 0; a < 3; ++a) {
+        double x0 = v0[3 * (long long)p + a];
+        double x1 = x0 + e1[3 * (long long)p + a], x2 = x0 + e2[3 * (long long)p + a];
+        o[a] = fmin(x0, fmin(x1, x2));
+        o[3 + a] = fmax(x0, fmax(x1, x2));
+    }
+    int node = parent[k];
+    while (node >= 0) {
+        __threadfence();
+        if (atomicAdd(&flags[node - n], 1) == 0) return;
+        const double* ca = dbox + 6 * (long long)child[2 * (long long)(node - n)];
+        const double* cb = dbox + 6 * (long long)child[2 * (long long)(node - n) + 1];
+        double* q = dbox + 6 * (long long)node;
+        for (int a = 0; a < 3; ++a) {
+            q[a] = fmin(__ldcg(ca + a), __ldcg(cb + a));
+            q[3 + a] = fmax(__ldcg(ca + 3 + a), __ldcg(cb + 3 + a));
+        }
+        node = parent[node];
+    }
+}
+
+// one thread per leaf: skip[2 p + s] for prim p, s = 1 for rays leaving to the
+// side the stored normal points to, 0 for the other (EMPTY_REF = nothing)
+__global__ void k_skip_table(int n, int root, const int* sorted_idx, const int* parent, const int* child,
+                             const int* count, const int* slot, const int* dfs, const double* dbox,
+                             const double* nrm, const double* poff, int* skip) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int p = sorted_idx[k];
+    double nx = nrm[3 * (long long)p], ny = nrm[3 * (long long)p + 1], nz = nrm[3 * (long long)p + 2];
+    double c = poff[p];
+    for (int s = 0; s < 2; ++s) {
+        double sg = s ? 1.0 : -1.0;   // the side the ray goes to: sg (n.x - c) > 0
+        int best = EMPTY_REF;
+        int node = k;
+        while (node != root) {
+            // largest sg (n.x - c) over the box corners must stay <= margin
+            const double* b = dbox + 6 * (long long)node;
+            double m = sg * nx > 0 ? b[3] * nx : b[0] * nx;
+            m += sg * ny > 0 ? b[4] * ny : b[1] * ny;
+            m += sg * nz > 0 ? b[5] * nz : b[2] * nz;
+            if (sg * (m - c) > SKIP_MARGIN) break;
+            int par = parent[node];
+            int cnt = node < n ? 1 : count[node];
+            if (cnt > LEAF_MAX) best = dfs[node - n];                                  // a BNode
+            else if (count[par] > LEAF_MAX) best = make_leaf(ploc_first_slot(node, n, child, slot), cnt);
+            node = par;
+        }
+        skip[2 * (long long)p + s] = best;
+    }
+}
+
 // Surface-area cost of the laid-out tree (diagnostic, reported by the bench):
 // sums[0] = sum of internal-child box areas, sums[1] = sum of leaf box area x
 // triangle count, sums[2] = root area; expected internal-node visits of a

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
             d = P.dirs ? ld3(P.dirs + 3 * i) : fib_dir(i, P.n_rays);
         }
         int parent = 0;
+        int skip = EMPTY_REF;   // the subtree behind the wall the ray leaves (trace.cuh origin_skip)
         for (int k = 0; k < P.max_depth; ++k) {
             int prim = -1;
             double t = 0.0;
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
                 Ray r = make_ray(o, d);
                 if (COUNT) {
                     prim = trace_ray<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t,
-                                        &nv, &nt);
+                                            &nv, &nt, nullptr, skip);
                     my_nodes += nv;
                     my_tris += nt;
 #ifdef RT_ORACLE_VISITS
@@ -158,7 +159,8 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
                     }
 #endif
                 } else {
-                    prim = trace_ray<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t);
+                    prim = trace_ray<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t,
+                                            nullptr, nullptr, nullptr, skip);
                 }
                 ++my_bounces;
                 if (prim == -2) { atomicOr(P.error, 1); prim = -1; }
@@ -185,12 +187,15 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
                 parent = id;
                 // Bvh.intersect normal orientation (bvh.py:98-100), hit point (:101)
                 d3 n = ld3(P.normals + 3 * (long long)prim);
-                if (dot_blas(n, d) > 0.0) n = d3{-n.x, -n.y, -n.z};
+                bool flip = dot_blas(n, d) > 0.0;
+                if (flip) n = d3{-n.x, -n.y, -n.z};
                 d3 pt = d3{o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
                 // tracer.py:242-243
                 double kk = 2.0 * dot_blas(d, n);
                 d = d3{d.x - kk * n.x, d.y - kk * n.y, d.z - kk * n.z};
                 o = pt;
+                // the reflected ray leaves to the side of the facing normal: n_f . d_new = -kk / 2
+                skip = origin_skip(bvh, prim, flip ? 0.5 * kk : -0.5 * kk);
             }
         }
     }

@@ -114,11 +114,13 @@ __device__ inline bool solve_geometric(const Cands& C, const SceneDev& S, const 
 
 // occlusion of every segment (tracer.py:181-182); the conjunction is order-free,
 // so the receiver-side segment (most often blocked near the ground) goes first
-__device__ inline bool segments_clear(const Bvh& bvh, d3 tx, const d3* pts, int K, d3 rx) {
+// (a segment from an interaction point skips the subtree behind its wall)
+__device__ inline bool segments_clear(const Bvh& bvh, d3 tx, const d3* pts, int K, d3 rx, const int* seq,
+                                      const double* nrm) {
     for (int j = K; j >= 0; --j) {
         d3 a = j == 0 ? tx : pts[j - 1];
         d3 b = j == K ? rx : pts[j];
-        if (occluded(bvh, a, b) != 0) return false;
+        if (occluded(bvh, a, b, RAY_EPS, nullptr, j == 0 ? -1 : seq[j - 1], nrm) != 0) return false;
     }
     return true;
 }
@@ -136,7 +138,7 @@ __device__ unsigned long long g_vstats[8];   // items, hint hits, traversals, bl
 #endif
 
 __device__ inline bool segments_clear_hinted(const Bvh& bvh, d3 tx, const d3* pts, int K, d3 rx,
-                                             int* hints, int skip = -1) {
+                                             int* hints, const int* seq, const double* nrm, int skip = -1) {
     int h[MAX_DEPTH + 1];
     for (int j = 0; j <= K; ++j) h[j] = __ldcg(hints + j);
     for (int j = K; j >= 0; --j) {
@@ -150,7 +152,7 @@ __device__ inline bool segments_clear_hinted(const Bvh& bvh, d3 tx, const d3* pt
         d3 b = j == K ? rx : pts[j];
         int pos = -1;
         VSTAT(2);
-        if (occluded(bvh, a, b, RAY_EPS, &pos) != 0) {
+        if (occluded(bvh, a, b, RAY_EPS, &pos, j == 0 ? -1 : seq[j - 1], nrm) != 0) {
             VSTAT(3);
             if (pos >= 0 && pos != h[j]) __stcg(hints + j, pos);
             return false;
@@ -545,8 +547,9 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_validate(Cands C, SceneDev
                 ok = false;
             } else {
                 solve_geometric(C, S, images, pd.cand, tx, rx, pts);   // recompute points
-                ok = hc ? segments_clear_hinted(bvh, tx, pts, K, rx, hc, K)
-                        : segments_clear(bvh, tx, pts, K, rx);
+                const int* sq = C.seq + (long long)pd.cand * C.max_len;
+                ok = hc ? segments_clear_hinted(bvh, tx, pts, K, rx, hc, sq, S.nrm, K)
+                        : segments_clear(bvh, tx, pts, K, rx, sq, S.nrm);
             }
             if (ok) {
                 rec.rx = pd.rx;

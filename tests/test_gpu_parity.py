@@ -186,6 +186,22 @@ def test_launch_matches_oracle_larger(P):
     assert got == want, (len(got), len(want), sorted(got ^ want)[:10])
 
 
+def test_launch_matches_oracle_city_depth5(P):
+    """C3 city (201,642 tris), 300k rays, depth 5: device launch == oracle launch.
+    Secondary rays start on walls and skip the subtree behind them (origin skip
+    table); the oracle walks the reference's median-split BVH."""
+    import oracle as O
+    from paper_2303_11103_b200 import scenes
+    sc = scenes.city()
+    b = _bvh(P, sc)
+    ob = O.Bvh(O.SceneArrays(sc))
+    tx = sc.transmitters[0].position
+    for n in (300_000, 7_919):
+        got = P.launch_candidates(sc, b, tx, 5, n)
+        want = O.launch_candidates(ob, tx, 5, n)
+        assert got == want, (n, len(got), len(want), sorted(got ^ want)[:10])
+
+
 def test_sharded_launch_union_equals_single_launch(P):
     """rt_launch_shard (multi-GPU stage 1, band-interleaved): the union of the W
     shards' candidate sets is the single launch's set and the bounces add up."""
