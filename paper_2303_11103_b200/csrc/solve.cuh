@@ -120,7 +120,8 @@ __device__ inline bool segments_clear(const Bvh& bvh, d3 tx, const d3* pts, int 
     for (int j = K; j >= 0; --j) {
         d3 a = j == 0 ? tx : pts[j - 1];
         d3 b = j == K ? rx : pts[j];
-        if (occluded(bvh, a, b, RAY_EPS, nullptr, j == 0 ? -1 : seq[j - 1], nrm) != 0) return false;
+        if (occluded(bvh, a, b, RAY_EPS, nullptr, j == 0 ? -1 : seq[j - 1], nrm, j == K ? -1 : seq[j]) != 0)
+            return false;
     }
     return true;
 }
@@ -152,7 +153,7 @@ __device__ inline bool segments_clear_hinted(const Bvh& bvh, d3 tx, const d3* pt
         d3 b = j == K ? rx : pts[j];
         int pos = -1;
         VSTAT(2);
-        if (occluded(bvh, a, b, RAY_EPS, &pos, j == 0 ? -1 : seq[j - 1], nrm) != 0) {
+        if (occluded(bvh, a, b, RAY_EPS, &pos, j == 0 ? -1 : seq[j - 1], nrm, j == K ? -1 : seq[j]) != 0) {
             VSTAT(3);
             if (pos >= 0 && pos != h[j]) __stcg(hints + j, pos);
             return false;
