@@ -43,8 +43,8 @@ def main():
     for W in (2, 4, 8):
         seqs, lens, t_l = [], [], []
         for r in range(W):
-            _, tl = timed(lambda: run_launch(b, tx.position, depth, n, shard=(r, W)))
-            t_l.append(tl)
+            ts = sorted(timed(lambda: run_launch(b, tx.position, depth, n, shard=(r, W)))[1] for _ in range(3))
+            t_l.append(ts[1])
             s, ln = get_candidates(b)
             seqs.append(s.clone())
             lens.append(ln.clone())
@@ -56,9 +56,10 @@ def main():
         t_c = []
         for r in range(W):   # warm every shard first: a shard may grow the scratch buffers
             coverage_from_candidates(sc, b, tx, grid, shard_index=r, shard_count=W)
-        for r in range(W):
-            _, tc = timed(lambda: coverage_from_candidates(sc, b, tx, grid, shard_index=r, shard_count=W))
-            t_c.append(tc)
+        for r in range(W):   # median of 3: one-off hiccups do not decide the max over ranks
+            ts = sorted(timed(lambda: coverage_from_candidates(sc, b, tx, grid, shard_index=r,
+                                                               shard_count=W))[1] for _ in range(3))
+            t_c.append(ts[1])
         per = [a + t_u + c for a, c in zip(t_l, t_c)]
         tw = max(per)
         print(f"W={W}: launch max {max(t_l):.2f} (min {min(t_l):.2f}), union sort {t_u:.2f}, "
