@@ -97,6 +97,9 @@ struct rt_ctx {
     bool tail_smem_set = false;   // k_ploc_tail's dynamic shared memory opt-in done
     double origin_limit = 0.0;
     bool has_skip = false;        // origin skip table built with the tree (bvh_ploc.cuh)
+    DevBuf tree_diag;             // [0] deepest BNode; doubles at +8: surface-area sums
+    int diag_root = -1;           // root id of the last PLOC/SAH tree for the SAH estimate
+    bool diag_pending = false;    // tree diagnostics not yet read back
     // candidates
     DevBuf cand_seq, cand_len;
     int64_t n_cand = 0;
@@ -311,6 +314,7 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st) {
 
 int build_karras(rt_ctx* ctx, long long n, const uint64_t* kout, const int* vout, cudaStream_t st);
 int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st);
+int tree_diagnostics(rt_ctx* ctx, cudaStream_t st);
 int build_morton(rt_ctx* ctx, long long n, cudaStream_t st);
 
 // PLOC-format scratch shared by the PLOC and SAH builders
@@ -392,24 +396,33 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     CK(cudaMemcpyAsync(dc, h, sizeof(h), cudaMemcpyHostToDevice, st));
     int levels = 0, cur = 0;
     long long nbig = h[0], nchunk = h[2];
-    while (nbig > 0) {   // ranges of > SAH_BIG prims
-        int nx = cur ^ 1;
-        SahOut O{small_max, small, dc + 6, med[0], dc + 4, big[nx], bigc[nx], dc + nx, ctask[nx], dc + 2 + nx};
-        CK(cudaMemsetAsync(dc + nx, 0, 4, st));
-        CK(cudaMemsetAsync(dc + 2 + nx, 0, 4, st));
-        k_sahb_init<<<nbig, 128, 0, st>>>(dc + cur, rb[cur]);
-        k_sahb_bounds<<<nchunk, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
+    // ranges of > SAH_BIG prims: SAH_BIG_BATCH levels per host round trip, grids
+    // sized by bounds (ranges at most double per level; a level's chunks are at
+    // most n / SAH_CHUNK + its ranges); blocks past the live counts exit at once
+    const int SAH_BIG_BATCH = 3;
+    while (nbig > 0) {
+        long long bb = nbig, bc = nchunk;
+        for (int bt = 0; bt < SAH_BIG_BATCH; ++bt) {
+            int nx = cur ^ 1;
+            SahOut O{small_max, small, dc + 6, med[0], dc + 4, big[nx], bigc[nx], dc + nx, ctask[nx], dc + 2 + nx};
+            CK(cudaMemsetAsync(dc + nx, 0, 4, st));
+            CK(cudaMemsetAsync(dc + 2 + nx, 0, 4, st));
+            k_sahb_init<<<bb, 128, 0, st>>>(dc + cur, rb[cur]);
+            k_sahb_bounds<<<bc, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
                                                     pbox, cent, rb[cur]);
-        k_sahb_bins<<<nchunk, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
+            k_sahb_bins<<<bc, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
                                                   pbox, cent, rb[cur]);
-        k_sahb_split<<<nbig, 64, 0, st>>>(big[cur], dc + cur, rb[cur], (int)n, box, child, par, cnt, dc + 7, O);
-        k_sahb_count<<<nchunk, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
+            k_sahb_split<<<bb, 64, 0, st>>>(big[cur], dc + cur, rb[cur], (int)n, box, child, par, cnt, dc + 7, O);
+            k_sahb_count<<<bc, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
                                                    cent, rb[cur], cleft);
-        k_sahb_write<<<nchunk, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
+            k_sahb_write<<<bc, SAH_BLOCK, 0, st>>>(big[cur], bigc[cur], ctask[cur], dc + 2 + cur, idx0, idx1,
                                                    cent, rb[cur], cleft);
-        CKL();
-        cur = nx;
-        ++levels;
+            CKL();
+            cur = nx;
+            ++levels;
+            bb = std::min(2 * bb, cap_big);
+            bc = std::min(n / SAH_CHUNK + 1 + bb, cap_chunk);
+        }
         CK(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         nbig = h[cur];
@@ -551,18 +564,20 @@ int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st) {
     int* dfs = nullptr;
     if (n > 1) {   // depth-first order + tree depth (always measured: it bounds the stack)
         dfs = ctx->pl_dfs.get<int>();
-        int* dmax = reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 15);
+        CK(ctx->tree_diag.reserve(64));
+        int* dmax = ctx->tree_diag.get<int>();
         CK(cudaMemsetAsync(dmax, 0, 4, st));
         k_ploc_dfs<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, root, par, child, cnt, em, dfs, dmax);
         CKL();
-        int h = 0;
-        CK(cudaMemcpyAsync(&h, dmax, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        ctx->bvh_depth = h;
-        ctx->counters[13] = h;
-        if (!RT_STACK_CHECK && h + 2 > STACK_SIZE)
-            return fail(ctx, RT_ECAP, "BVH depth " + std::to_string(h) + " exceeds the traversal stack (" +
-                                          std::to_string(STACK_SIZE) + " entries)");
+        if (!RT_STACK_CHECK) {   // unchecked pushes: the depth must fit the stack now
+            int h = 0;
+            CK(cudaMemcpyAsync(&h, dmax, 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            ctx->bvh_depth = h;
+            if (h + 2 > STACK_SIZE)
+                return fail(ctx, RT_ECAP, "BVH depth " + std::to_string(h) + " exceeds the traversal stack (" +
+                                              std::to_string(STACK_SIZE) + " entries)");
+        }
         if (!RT_DFS_LAYOUT) dfs = nullptr;
     }
     if (n > 1) {
@@ -588,19 +603,34 @@ int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st) {
     k_ploc_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, slot, ctx->v0.get<double>(), ctx->e1.get<double>(),
                                               ctx->e2.get<double>(), ctx->tris.get<TriRec>());
     CKL();
-    if (n > 2 && dfs) {   // tree cost diagnostic (counters 13/14): emitted nodes = em[root]
-        int n_nodes = 0;
-        CK(cudaMemcpyAsync(&n_nodes, em + root, 4, cudaMemcpyDeviceToHost, st));
-        double* sums = reinterpret_cast<double*>(ctx->ctrs.get<long long>() + 12);
-        CK(cudaMemsetAsync(sums, 0, 24, st));
-        CK(cudaStreamSynchronize(st));
-        k_tree_sah<<<nblk(n_nodes, 256), 256, 0, st>>>(ctx->nodes.get<BNode>(), n_nodes, sums);
-        CKL();
-        double h[3];
-        CK(cudaMemcpyAsync(h, sums, 24, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        ctx->counters[14] = (long long)llround(1000.0 * (1.0 + h[0] / h[2]));   // milli-visits
-    }
+    // tree diagnostics (depth, surface-area estimate) are computed on demand by
+    // rt_get_profile: no host round trip on the build path
+    ctx->diag_root = (n > 2 && dfs) ? root : -1;
+    ctx->diag_pending = n > 1;
+    return RT_OK;
+}
+
+// counters 13 (tree depth) and 14 (surface-area estimate) of the last build
+int tree_diagnostics(rt_ctx* ctx, cudaStream_t st) {
+    if (!ctx->diag_pending) return RT_OK;
+    ctx->diag_pending = false;
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, ctx->tree_diag.get<int>(), 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->bvh_depth = h;
+    ctx->counters[13] = h;
+    if (ctx->diag_root < 0) return RT_OK;
+    int n_nodes = 0;
+    CK(cudaMemcpyAsync(&n_nodes, ctx->pl_em.get<int>() + ctx->diag_root, 4, cudaMemcpyDeviceToHost, st));
+    double* sums = reinterpret_cast<double*>(ctx->tree_diag.get<int>() + 2);
+    CK(cudaMemsetAsync(sums, 0, 24, st));
+    CK(cudaStreamSynchronize(st));
+    k_tree_sah<<<nblk(n_nodes, 256), 256, 0, st>>>(ctx->nodes.get<BNode>(), n_nodes, sums);
+    CKL();
+    double d[3];
+    CK(cudaMemcpyAsync(d, sums, 24, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->counters[14] = (long long)llround(1000.0 * (1.0 + d[0] / d[2]));   // milli-visits
     return RT_OK;
 }
 
@@ -1624,6 +1654,7 @@ int rt_set_profiling(rt_ctx* ctx, int flags) {
 int rt_get_profile(rt_ctx* ctx, double* ms_out, int64_t* counters_out) {
     if (!ctx) return RT_EINVAL;
     CK(cudaSetDevice(ctx->device));
+    RC(tree_diagnostics(ctx, 0));
     for (int i = 0; i < RT_NSTAGE; ++i) {
         double v = -1.0;
         if (ctx->ev_used[i] && ctx->ev[i][0] && ctx->ev[i][1]) {
