@@ -202,6 +202,40 @@ def test_launch_matches_oracle_city_depth5(P):
         assert got == want, (n, len(got), len(want), sorted(got ^ want)[:10])
 
 
+def test_origin_skip_touching_and_offset_walls_match_oracle(P):
+    """Origin skip table edge cases: boxes sharing a face, a face offset by
+    1e-8 m (inside the table's margin) and by 1e-3 m (outside it), coplanar
+    neighbours and a ground plane; depth-4 launch sets and occlusion-checked
+    coverage cells equal the oracle's."""
+    import oracle as O
+    from paper_2303_11103_b200 import scenes
+    from paper_2303_11103_b200.scene import (AntennaArray, RadioDevice, RadioMaterial, Scene,
+                                             SceneObject)
+    boxes = [(0, 10, 0, 10, 0, 12), (10, 20, 0, 10, 0, 8),            # shared face x = 10
+             (20 + 1e-8, 30, 0, 10, 0, 15), (30 + 1e-3, 40, 0, 10, 0, 9),  # offset faces
+             (0, 10, 10, 20, 0, 12), (5, 15, -30, -20, 0, 20)]          # coplanar z-walls
+    verts = np.concatenate([scenes.box_vertices(*b) for b in boxes])
+    tris = np.concatenate([scenes._BOX_TRIS + 8 * i for i in range(len(boxes))])
+    gv, gt = scenes.quad([(-200, -200, 0), (200, -200, 0), (200, 200, 0), (-200, 200, 0)])
+    sc = Scene(3.5e9, [SceneObject("ground", "g", gv, gt), SceneObject("b", "w", verts, tris)],
+               {"g": RadioMaterial("g", "constant", 5.0, 0.01), "w": RadioMaterial("w", "constant", 6.0, 0.05)},
+               AntennaArray(), AntennaArray(),
+               [RadioDevice("tx", "tx", np.array([12.0, -6.0, 5.0])),
+                RadioDevice("rx", "rx", np.array([25.0, 14.0, 1.5]))])
+    b = _bvh(P, sc)
+    ob = O.Bvh(O.SceneArrays(sc))
+    tx = sc.transmitters[0].position
+    got = P.launch_candidates(sc, b, tx, 4, 200_000)
+    want = O.launch_candidates(ob, tx, 4, 200_000)
+    assert got == want, (len(got), len(want), sorted(got ^ want)[:10])
+    grid = P.GridSpec((-10.0, -40.0), 2.0, 32, 40, 1.5)
+    cm = P.coverage_map(sc, b, grid, 3, method="fibonacci", num_rays=200_000)
+    ocm = O.coverage_map(sc, ob, grid.origin, grid.cell_size, grid.nx, grid.ny, grid.height, 3,
+                         method="fibonacci", num_rays=200_000)
+    assert np.array_equal(cm.gains == 0.0, ocm == 0.0)
+    assert np.allclose(cm.gains, ocm, rtol=1e-9, atol=0.0)
+
+
 def test_sharded_launch_union_equals_single_launch(P):
     """rt_launch_shard (multi-GPU stage 1, band-interleaved): the union of the W
     shards' candidate sets is the single launch's set and the bounces add up."""
