@@ -75,6 +75,9 @@ class EvalContext:
         """rotation_rows for a list of devices: one rotation per distinct
         orientation, shared row tuples (receivers mostly share one)."""
         yprs = [self.orientations.get(d.name, d.orientation) for d in devices]
+        if yprs and all(y is yprs[0] for y in yprs) and not any(isinstance(v, torch.Tensor) for v in yprs[0]):
+            r = self.rotation_rows(devices[0])   # one shared orientation object (the default)
+            return [r] * len(devices)
         try:
             arr = np.asarray(yprs, dtype=np.float64)
         except (TypeError, ValueError, RuntimeError):   # tensor leaves: per device, no memo
@@ -385,8 +388,12 @@ def _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows, rx_rows):
         if v is None:
             v = memo[k] = _aperture(off, r)
         return v
-    ap_t = [ap(off_tx, r, 0) for r in tx_rows]
-    ap_r = [ap(off_rx, r, 1) for r in rx_rows]
+    def aps(off, rows, tag):   # shared row tuples: one aperture per distinct object
+        if rows and all(r is rows[0] for r in rows):
+            return [ap(off, rows[0], tag)] * len(rows)
+        return [ap(off, r, tag) for r in rows]
+    ap_t = aps(off_tx, tx_rows, 0)
+    ap_r = aps(off_rx, rx_rows, 1)
     if max(ap_t + ap_r + [0.0]) == 0.0:
         return
     n_rx = len(T.rx_names)
@@ -395,8 +402,8 @@ def _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows, rx_rows):
     # every path is at least as long as the straight tx-rx distance: when that
     # already clears the Fraunhofer distance no path can warn (no read-back)
     devs = {d.name: d for d in scene.devices}
-    tp = np.array([np.asarray(devs[n].position, dtype=np.float64) for n in T.tx_names]).reshape(-1, 3)
-    rp = np.array([np.asarray(devs[n].position, dtype=np.float64) for n in T.rx_names]).reshape(-1, 3)
+    tp = np.array([devs[n].position for n in T.tx_names], dtype=np.float64).reshape(-1, 3)
+    rp = np.array([devs[n].position for n in T.rx_names], dtype=np.float64).reshape(-1, 3)
     dist = np.linalg.norm(tp[:, None, :] - rp[None, :, :], axis=-1).reshape(-1)
     if not np.any((a_pair > 0.0) & (dist < fr_pair)):
         return
