@@ -252,12 +252,7 @@ __global__ void k_layout(int n, const int* sorted_idx, const float* pbox, const 
         for (int m = 0; m < 6; ++m) bx[c][m] = src[m];
         inflate6(bx[c], eps);
     }
-    BNode nd;
-    nd.a = make_float4(bx[0][0], bx[0][1], bx[0][2], bx[0][3]);
-    nd.b = make_float4(bx[0][4], bx[0][5], bx[1][0], bx[1][1]);
-    nd.c = make_float4(bx[1][2], bx[1][3], bx[1][4], bx[1][5]);
-    nd.d = make_int4(ref[0], ref[1], 0, 0);
-    out[i] = nd;
+    out[i] = pack_bnode(bx, ref[0], ref[1]);
 }
 
 // single-prim scene: root with the one leaf on both sides
@@ -265,12 +260,9 @@ __global__ void k_layout_one(const float* pbox, const unsigned* cbounds, BNode* 
     float s[6];
     for (int m = 0; m < 6; ++m) s[m] = pbox[m];
     inflate6(s, box_eps(cbounds));
-    BNode nd;
-    nd.a = make_float4(s[0], s[1], s[2], s[3]);
-    nd.b = make_float4(s[4], s[5], s[0], s[1]);
-    nd.c = make_float4(s[2], s[3], s[4], s[5]);
-    nd.d = make_int4(make_leaf(0, 1), make_leaf(0, 1), 0, 0);
-    out[0] = nd;
+    float bx[2][6];
+    for (int m = 0; m < 6; ++m) bx[0][m] = bx[1][m] = s[m];
+    out[0] = pack_bnode(bx, make_leaf(0, 1), make_leaf(0, 1));
 }
 
 // ---- 4-wide collapse (level-synchronous, top-down) ---------------------------------------
@@ -284,13 +276,8 @@ __device__ inline float box_area(const float* b) {
 }
 
 __device__ inline void bin_child(const BNode& nd, int c, int& ref, float* b) {
-    if (c == 0) {
-        b[0] = nd.a.x; b[1] = nd.a.y; b[2] = nd.a.z; b[3] = nd.a.w; b[4] = nd.b.x; b[5] = nd.b.y;
-        ref = nd.d.x;
-    } else {
-        b[0] = nd.b.z; b[1] = nd.b.w; b[2] = nd.c.x; b[3] = nd.c.y; b[4] = nd.c.z; b[5] = nd.c.w;
-        ref = nd.d.y;
-    }
+    unpack_bnode(nd, c, b);
+    ref = c == 0 ? nd.d.x : nd.d.y;
 }
 
 __global__ void k_collapse(const BNode* bin, const int* frontier, int nf, BNode4* out, int* out_count,

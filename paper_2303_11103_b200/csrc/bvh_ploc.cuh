@@ -294,12 +294,7 @@ __global__ void k_ploc_layout(int n, int root, const int* child, const int* coun
         else if (count[ch] <= LEAF_MAX) ref[c] = make_leaf(ploc_first_slot(ch, n, child, slot), count[ch]);
         else ref[c] = dfs ? dfs[ch - n] : ploc_map(ch, n, root);
     }
-    BNode nd;
-    nd.a = make_float4(bx[0][0], bx[0][1], bx[0][2], bx[0][3]);
-    nd.b = make_float4(bx[0][4], bx[0][5], bx[1][0], bx[1][1]);
-    nd.c = make_float4(bx[1][2], bx[1][3], bx[1][4], bx[1][5]);
-    nd.d = make_int4(ref[0], ref[1], 0, 0);
-    out[dfs ? dfs[q] : ploc_map(id, n, root)] = nd;
+    out[dfs ? dfs[q] : ploc_map(id, n, root)] = pack_bnode(bx, ref[0], ref[1]);
 }
 
 // ---- origin skip table ------------------------------------------------------------------
@@ -402,8 +397,9 @@ __global__ void __launch_bounds__(256) k_tree_sah(const BNode* nodes, int n_node
 
 __device__ inline void tree_sah_node(const BNode* nodes, int q, double& in, double& lf, double* sums) {
     BNode nd = nodes[q];
-    float b[2][6] = {{nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.b.x, nd.b.y},
-                     {nd.b.z, nd.b.w, nd.c.x, nd.c.y, nd.c.z, nd.c.w}};
+    float b[2][6];
+    unpack_bnode(nd, 0, b[0]);
+    unpack_bnode(nd, 1, b[1]);
     int ref[2] = {nd.d.x, nd.d.y};
     for (int c = 0; c < 2; ++c) {
         double dx = b[c][3] - b[c][0], dy = b[c][4] - b[c][1], dz = b[c][5] - b[c][2];

@@ -52,12 +52,32 @@ __device__ inline void st3(double* p, d3 v) { p[0] = v.x; p[1] = v.y; p[2] = v.z
 // BVH node: both children's boxes (float, rounded outward) + child refs.
 // A child ref >= 0 is an internal node index; a leaf ref has bit 31 set,
 // bits 28..30 = count-1, bits 0..27 = first slot in the sorted triangle array.
+// Each (lo, hi) pair of one child and axis sits in an aligned register pair
+// after the 16-byte loads, so the box filter computes both slab planes with
+// one packed FFMA2 (trace.cuh slab32).
 struct __align__(16) BNode {
-    float4 a;   // lo0.x lo0.y lo0.z hi0.x
-    float4 b;   // hi0.y hi0.z lo1.x lo1.y
-    float4 c;   // lo1.z hi1.x hi1.y hi1.z
+    float4 a;   // lo0.x hi0.x lo0.y hi0.y
+    float4 b;   // lo0.z hi0.z lo1.x hi1.x
+    float4 c;   // lo1.y hi1.y lo1.z hi1.z
     int4 d;     // child0 child1 - -
 };
+
+// child boxes bx[c] = {lo.x, lo.y, lo.z, hi.x, hi.y, hi.z} <-> BNode
+__host__ __device__ inline BNode pack_bnode(const float bx[2][6], int ref0, int ref1) {
+    BNode nd;
+    nd.a = make_float4(bx[0][0], bx[0][3], bx[0][1], bx[0][4]);
+    nd.b = make_float4(bx[0][2], bx[0][5], bx[1][0], bx[1][3]);
+    nd.c = make_float4(bx[1][1], bx[1][4], bx[1][2], bx[1][5]);
+    nd.d = make_int4(ref0, ref1, 0, 0);
+    return nd;
+}
+__host__ __device__ inline void unpack_bnode(const BNode& nd, int c, float* b) {
+    if (c == 0) {
+        b[0] = nd.a.x; b[3] = nd.a.y; b[1] = nd.a.z; b[4] = nd.a.w; b[2] = nd.b.x; b[5] = nd.b.y;
+    } else {
+        b[0] = nd.b.z; b[3] = nd.b.w; b[1] = nd.c.x; b[4] = nd.c.y; b[2] = nd.c.z; b[5] = nd.c.w;
+    }
+}
 
 // 4-wide node (collapsed from the binary LBVH): per-axis float4 of the four
 // children's bounds + refs; unused slots hold EMPTY_REF.

@@ -47,7 +47,7 @@ namespace rt {
 struct Ray {
     double ox, oy, oz, dx, dy, dz;
     float fix, fiy, fiz;      // FP32 1/d for the box filter
-    float oix, oiy, oiz;      // FP32 o * (1/d): slab planes are fma(bound, inv, -oi)
+    float oix, oiy, oiz;      // FP32 -(o * (1/d)): slab planes are fma(bound, inv, oi)
 };
 
 // 1/d, +inf where d == 0 (bvh.py:120-122)
@@ -70,7 +70,7 @@ __device__ inline Ray make_ray(d3 o, d3 d) {
     r.fix = fminf(fmaxf(__frcp_rn(__double2float_rn(d.x)), -1e30f), 1e30f);
     r.fiy = fminf(fmaxf(__frcp_rn(__double2float_rn(d.y)), -1e30f), 1e30f);
     r.fiz = fminf(fmaxf(__frcp_rn(__double2float_rn(d.z)), -1e30f), 1e30f);
-    r.oix = (float)o.x * r.fix; r.oiy = (float)o.y * r.fiy; r.oiz = (float)o.z * r.fiz;
+    r.oix = -((float)o.x * r.fix); r.oiy = -((float)o.y * r.fiy); r.oiz = -((float)o.z * r.fiz);
     return r;
 }
 
@@ -82,13 +82,25 @@ __device__ inline Ray make_ray(d3 o, d3 d) {
 // <= (2 + 2 + 6 + 3) * 2^-24 S = 13 * 2^-24 S < eps_box = 16 * 2^-24 S.
 // tmin is rounded down and tmax up by the caller; 1/d is clamped (make_ray)
 // so no plane distance is NaN.
-__device__ __forceinline__ bool slab32(const Ray& r, float lx, float ly, float lz, float hx,
-                                       float hy, float hz, float tmin, float tmax, float& tnear) {
-    float t0x = __fmaf_rn(lx, r.fix, -r.oix), t1x = __fmaf_rn(hx, r.fix, -r.oix);
-    float t0y = __fmaf_rn(ly, r.fiy, -r.oiy), t1y = __fmaf_rn(hy, r.fiy, -r.oiy);
-    float t0z = __fmaf_rn(lz, r.fiz, -r.oiz), t1z = __fmaf_rn(hz, r.fiz, -r.oiz);
-    float n = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), tmin));
-    float f = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fminf(fmaxf(t0z, t1z), tmax));
+// both planes of one slab in one packed FFMA2 (sm_100): (lo, hi) * inv + oi,
+// inv and oi broadcast; per lane an IEEE fma, bit-identical to two FFMAs
+__device__ __forceinline__ float2 slab_planes(float2 lohi, float inv, float oi) {
+    unsigned long long x, s, t, o;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(lohi.x), "f"(lohi.y));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(s) : "f"(inv));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(t) : "f"(oi));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(o) : "l"(x), "l"(s), "l"(t));
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(o));
+    return v;
+}
+
+__device__ __forceinline__ bool slab32(const Ray& r, float2 x, float2 y, float2 z, float tmin, float tmax,
+                                       float& tnear) {
+    float2 tx = slab_planes(x, r.fix, r.oix), ty = slab_planes(y, r.fiy, r.oiy),
+           tz = slab_planes(z, r.fiz, r.oiz);
+    float n = fmaxf(fmaxf(fminf(tx.x, tx.y), fminf(ty.x, ty.y)), fmaxf(fminf(tz.x, tz.y), tmin));
+    float f = fminf(fminf(fmaxf(tx.x, tx.y), fmaxf(ty.x, ty.y)), fminf(fmaxf(tz.x, tz.y), tmax));
     tnear = n;
     return n <= f;
 }
@@ -107,12 +119,12 @@ __device__ __forceinline__ bool slab(const Ray& r, float lx, float ly, float lz,
     return n <= f;
 }
 
-__device__ __forceinline__ bool box_hit(const Ray& r, bool fast, float lx, float ly, float lz,
-                                        float hx, float hy, float hz, double tmin, double tmax,
-                                        float tmin_f, float tmax_f, float& tn) {
-    if (fast) return slab32(r, lx, ly, lz, hx, hy, hz, tmin_f, tmax_f, tn);
+// a child box as its three (lo, hi) pairs (BNode layout)
+__device__ __forceinline__ bool box_hit(const Ray& r, bool fast, float2 x, float2 y, float2 z, double tmin,
+                                        double tmax, float tmin_f, float tmax_f, float& tn) {
+    if (fast) return slab32(r, x, y, z, tmin_f, tmax_f, tn);
     double d;
-    bool h = slab(r, lx, ly, lz, hx, hy, hz, tmin, tmax, d);
+    bool h = slab(r, x.x, y.x, z.x, x.y, y.y, z.y, tmin, tmax, d);
     tn = __double2float_rd(d);
     return h;
 }
@@ -229,10 +241,14 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
             float4 hx = __ldg(np + 3), hy = __ldg(np + 4), hz = __ldg(np + 5);
             int4 ch = __ldg(reinterpret_cast<const int4*>(np + 6));
             float t0, t1, t2, t3;
-            bool h0 = box_hit(r, fast, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, tmin, best_t, tmin_f, best_tf, t0);
-            bool h1 = box_hit(r, fast, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, tmin, best_t, tmin_f, best_tf, t1);
-            bool h2 = box_hit(r, fast, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, tmin, best_t, tmin_f, best_tf, t2);
-            bool h3 = box_hit(r, fast, lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, tmin, best_t, tmin_f, best_tf, t3);
+            bool h0 = box_hit(r, fast, make_float2(lx.x, hx.x), make_float2(ly.x, hy.x), make_float2(lz.x, hz.x),
+                              tmin, best_t, tmin_f, best_tf, t0);
+            bool h1 = box_hit(r, fast, make_float2(lx.y, hx.y), make_float2(ly.y, hy.y), make_float2(lz.y, hz.y),
+                              tmin, best_t, tmin_f, best_tf, t1);
+            bool h2 = box_hit(r, fast, make_float2(lx.z, hx.z), make_float2(ly.z, hy.z), make_float2(lz.z, hz.z),
+                              tmin, best_t, tmin_f, best_tf, t2);
+            bool h3 = box_hit(r, fast, make_float2(lx.w, hx.w), make_float2(ly.w, hy.w), make_float2(lz.w, hz.w),
+                              tmin, best_t, tmin_f, best_tf, t3);
             const float INF = __int_as_float(0x7f800000);
             int r0 = ch.x, r1 = ch.y, r2 = ch.z, r3 = ch.w;
             if (!h0 || r0 == EMPTY_REF) t0 = INF;
@@ -258,9 +274,11 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
             float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
             int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
             float tn0, tn1;
-            bool h0 = box_hit(r, fast, a.x, a.y, a.z, a.w, b.x, b.y, tmin, best_t, tmin_f, best_tf, tn0) &&
+            bool h0 = box_hit(r, fast, make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(b.x, b.y), tmin,
+                              best_t, tmin_f, best_tf, tn0) &&
                       !RT_SKIPPED(ch.x);   // the subtree behind the ray's own wall (origin skip table)
-            bool h1 = box_hit(r, fast, b.z, b.w, c.x, c.y, c.z, c.w, tmin, best_t, tmin_f, best_tf, tn1) &&
+            bool h1 = box_hit(r, fast, make_float2(b.z, b.w), make_float2(c.x, c.y), make_float2(c.z, c.w), tmin,
+                              best_t, tmin_f, best_tf, tn1) &&
                       !RT_SKIPPED(ch.y);
             if (h0 && h1) {
                 int nearc = ch.x, farc = ch.y;
@@ -347,9 +365,11 @@ __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, 
             float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
             int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
             float tn0, tn1;
-            bool h0 = box_hit(r, fast, a.x, a.y, a.z, a.w, b.x, b.y, tmin, best_t, tmin_f, best_tf, tn0) &&
+            bool h0 = box_hit(r, fast, make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(b.x, b.y), tmin,
+                              best_t, tmin_f, best_tf, tn0) &&
                       !RT_SKIPPED(ch.x);   // the subtree behind the ray's own wall (origin skip table)
-            bool h1 = box_hit(r, fast, b.z, b.w, c.x, c.y, c.z, c.w, tmin, best_t, tmin_f, best_tf, tn1) &&
+            bool h1 = box_hit(r, fast, make_float2(b.z, b.w), make_float2(c.x, c.y), make_float2(c.z, c.w), tmin,
+                              best_t, tmin_f, best_tf, tn1) &&
                       !RT_SKIPPED(ch.y);
             if (h0 && h1) {
                 int nearc = ch.x, farc = ch.y;
