@@ -220,11 +220,13 @@ __device__ inline int clip_poly(const double* px, const double* py, int n, doubl
 }
 
 // Stage-2 row shards: blocks of RT_ROW_BLOCK grid rows go round-robin to the
-// shard_count ranks (row iy belongs to shard (iy / RB) % count).  Blocks keep a
-// candidate's footprint rows together on one rank (occluder hints stay warm)
-// while the round-robin keeps the valid-path density balanced.
+// shard_count ranks (row iy belongs to shard (iy / RB) % count).  Measured per
+// rank at 8 ranks (tools/scale_estimate.py --ranks): C5 rows 6.9-7.1 ms with
+// single rows vs 6.1-7.6 ms with 8-row blocks (the city's 25 m street period
+// beats against the block pattern), C3 unchanged; warmer occluder hints in
+// larger blocks do not pay for the imbalance.
 #ifndef RT_ROW_BLOCK
-#define RT_ROW_BLOCK 8
+#define RT_ROW_BLOCK 1
 #endif
 __host__ __device__ inline bool row_in_shard(long long iy, int index, int count) {
     return (iy / RT_ROW_BLOCK) % count == index;

@@ -6,7 +6,7 @@ SURVEY §8e.  The path shards in two stages with exactly two exchange points:
            latitudes, unlike contiguous slot ranges); its candidate trie is local.  all_gather of the (padded) candidate
            rows, then every rank installs the union (sorted + unique on the
            device) so all ranks hold the identical global candidate list.
-  stage 2  cells: rank r solves the grid rows of the 8-row blocks b = r mod W
+  stage 2  cells: rank r solves the grid rows iy = r mod W
            (round-robin blocks balance the valid-path density and keep a
            footprint's rows together); other rows stay 0 and a sum all_reduce
            of the [ny, nx] grid assembles the map.
@@ -53,7 +53,7 @@ def shard_slots(n: int, rank: int, world: int):
     return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
 
 
-ROW_BLOCK = 8   # solve.cuh RT_ROW_BLOCK
+ROW_BLOCK = 1   # solve.cuh RT_ROW_BLOCK
 
 
 def rows_of_shard(ny: int, rank: int, world: int):

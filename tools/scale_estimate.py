@@ -29,7 +29,7 @@ def timed(fn):
 
 
 def main():
-    args = bench.parse(sys.argv[1:])
+    args = bench.parse([a for a in sys.argv[1:] if a != "--ranks"])
     sc, tx, grid = bench.make_workload(args)
     b = P.build(sc)
     n, depth = int(args.rays), args.depth
@@ -62,6 +62,8 @@ def main():
             t_c.append(ts[1])
         per = [a + t_u + c for a, c in zip(t_l, t_c)]
         tw = max(per)
+        if "--ranks" in sys.argv:
+            print(f"  W={W} per-rank rows ms: " + " ".join(f"{x:.2f}" for x in t_c))
         print(f"W={W}: launch max {max(t_l):.2f} (min {min(t_l):.2f}), union sort {t_u:.2f}, "
               f"rows max {max(t_c):.2f} (min {min(t_c):.2f}) -> step {tw:.2f} ms, "
               f"efficiency {t1 / (W * tw):.3f}")
