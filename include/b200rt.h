@@ -59,8 +59,11 @@ const char* rt_last_error(const rt_ctx* ctx);
 int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
                     const int64_t* tri_vertex, const int32_t* prim_material, int64_t n_prims,
                     void* stream);
-/* LBVH over the uploaded primitives (Morton codes, radix sort, Karras
- * hierarchy, atomic refit, leaf collapse to <=4 prims). */
+/* BVH over the uploaded primitives (replaces Bvh._build, bvh.py:59-79):
+ * top-down binned SAH on the device, depth-first child-pair layout with
+ * subtrees of <= 2 prims collapsed into leaves, plus the per-prim origin skip
+ * table (the subtree behind each prim, per side).  Build-time variants: PLOC
+ * or the Karras LBVH over Morton codes.  Tree shape never changes results. */
 int rt_bvh_build(rt_ctx* ctx, void* stream);
 int64_t rt_num_prims(const rt_ctx* ctx);
 /* copy the per-primitive arrays (device outputs, any may be NULL) */

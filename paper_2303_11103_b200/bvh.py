@@ -1,4 +1,4 @@
-"""Acceleration structure: GPU LBVH over the scene triangles.
+"""Acceleration structure: GPU BVH (binned SAH) over the scene triangles.
 
 Drop-in for /root/reference/pkg/src/emtrace/bvh.py: ``build(scene) -> Bvh``
 with ``Bvh.intersect`` (:83-101), ``Bvh.occluded`` (:103-115) and the
@@ -117,7 +117,7 @@ def gather_meshes(scene):
 
 
 class Bvh:
-    """Device-resident scene + LBVH; immutable after build, queries are stream-ordered."""
+    """Device-resident scene + BVH; immutable after build, queries are stream-ordered."""
 
     def __init__(self, scene, device=None):
         self.ctx = N.acquire_context(device)

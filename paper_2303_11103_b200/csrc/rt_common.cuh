@@ -79,7 +79,7 @@ __host__ __device__ inline void unpack_bnode(const BNode& nd, int c, float* b) {
     }
 }
 
-// 4-wide node (collapsed from the binary LBVH): per-axis float4 of the four
+// 4-wide node (collapsed from the binary tree): per-axis float4 of the four
 // children's bounds + refs; unused slots hold EMPTY_REF.
 struct __align__(16) BNode4 {
     float4 lox, loy, loz, hix, hiy, hiz;

@@ -1,4 +1,4 @@
-// trace.cuh — LBVH traversal with the reference's FP64 Moller-Trumbore test.
+// trace.cuh — BVH traversal with the reference's FP64 Moller-Trumbore test.
 //
 // Semantics (bvh.py:117-177 restated as a closest-hit query): the hit is the
 // triangle with the smallest t in (t_min, t_max) among all triangles whose
@@ -9,7 +9,7 @@
 // outward to float) so the tree never culls a triangle the exact test accepts.
 //
 // RT_WIDE selects the node format walked: 0 = binary child-pair nodes (BNode),
-// 1 = 4-wide nodes (BNode4) collapsed from the same LBVH.
+// 1 = 4-wide nodes (BNode4) collapsed from the same binary tree.
 #pragma once
 #include "rt_common.cuh"
 
