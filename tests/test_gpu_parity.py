@@ -700,6 +700,16 @@ def test_degenerate_arguments_fail_loudly(P):
         P.coverage_map(sc, b, P.GridSpec((0.0, 0.0), 1.0, 600, 600, 1.5), 1)
     with pytest.raises(ValueError):   # tx and probe coincide (channel.py:190-233 via los_path)
         P.point_path_gain(sc, b, tx, np.asarray(tx.position, dtype=float), 1, "exhaustive", 4096)
+    # the CIR / gains entry points of the C ABI refuse inconsistent calls
+    import ctypes
+    from paper_2303_11103_b200 import _native as N
+    L, h = b.ctx.lib, b.ctx.h
+    n = ctypes.c_int64()
+    assert L.rt_cir_plan(h, 1, 0, None, None, None, None, None, 1, 1, 1, 1, ctypes.byref(n), None) == N.RT_EINVAL
+    assert L.rt_cir_plan(h, 0, 1, None, None, None, None, None, 1, 1, 1, 1, ctypes.byref(n), None) == N.RT_OK
+    assert L.rt_cir_scatter(h, 5, None, 0, None, 1, 1, 1, 1, None, None, None) == N.RT_EINVAL   # != planned count
+    assert L.rt_gains_synthetic(h, 1, 1, 1, None, None, None, None, None, 1, None, None, 1, None, None,
+                                0.0, None, None) == N.RT_EINVAL   # wavelength <= 0
 
 
 @pytest.mark.parametrize("case", ["box", "canyon", "two_ray"])
