@@ -140,6 +140,18 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        # NVML in a thread at 5 ms (the timed region lasts ~0.1 s; an nvidia-smi
+        # child needs ~0.1 s just to start); nvidia-smi -lms 100 as the fallback
+        self.stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.th = threading.Thread(target=self._poll_nvml, args=(pynvml, h), daemon=True)
+            self.th.start()
+            return self
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -151,6 +163,19 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll_nvml(self, nv, h):
+        bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                ("sw_power_cap", 0x4)]
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                break
+            self.rows.append([str(sm), str(mx), ""] + ["Active" if rs & b else "Not Active" for _, b in bits])
+            self.stop.wait(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
@@ -158,6 +183,9 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def __exit__(self, *exc):
+        self.stop.set()
+        if getattr(self, "th", None) is not None and self.proc is None:
+            self.th.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
