@@ -426,6 +426,77 @@ def test_position_orientation_gradients_match_reference_tape(P, golden):
         np.abs(got - want).max()
 
 
+def test_gradients_match_central_differences(P, golden):
+    """Both gradient paths against central finite differences of this
+    package's own forward pass (north_star: gradients within 1e-3 of the
+    reference or of finite differences): the hand-written material adjoint
+    (C4 NMSE loss, 8 leaves) and the forward-mode geometry Jacobian (|a|^2 of
+    the canyon paths w.r.t. tx / rx position and yaw / pitch / roll)."""
+    from paper_2303_11103_b200 import em, optim
+    from paper_2303_11103_b200.scene import POLARIZATION_SLANTS
+    g = golden("calib")
+    init = golden_scene(g, "scene_init")
+    prob = optim.MaterialProblem(init, g["positions"], g["h"], int(g["max_depth"]),
+                                 int(g["num_subcarriers"]), float(g["spacing"]))
+    dev = prob.bvh.device
+    base = {n: (float(init.materials[n].eps_r), float(init.materials[n].sigma)) for n in prob.names}
+
+    def loss_at(vals, grad=False):
+        t = {n: tuple(torch.tensor(x, dtype=torch.float64, device=dev, requires_grad=grad) for x in v)
+             for n, v in vals.items()}
+        return prob.loss(t), t
+
+    lo, leaves = loss_at(base, True)
+    lo.backward()
+    for n in prob.names:
+        for k in range(2):
+            h = 1e-6 * max(abs(base[n][k]), 1e-3)
+            up = {m: list(v) for m, v in base.items()}
+            dn = {m: list(v) for m, v in base.items()}
+            up[n][k] += h
+            dn[n][k] -= h
+            with torch.no_grad():
+                fd = (float(loss_at(up)[0]) - float(loss_at(dn)[0])) / (2 * h)
+            got = float(leaves[n][k].grad)
+            assert abs(got - fd) <= 1e-3 * abs(fd) + 1e-9, (n, k, got, fd)
+
+    gg = golden("geo_grads")
+    sc = golden_scene(gg)
+    b = _bvh(P, sc)
+    T = P.compute_paths(sc, b, 3, method="fibonacci", num_rays=int(gg["num_rays"])).table
+    devs = {d.name: d for d in sc.devices}
+    txd = [devs[T.tx_names[i]] for i in T.tx.cpu().numpy()]
+    rxd = [devs[T.rx_names[i]] for i in T.rx.cpu().numpy()]
+    x0 = np.concatenate([np.array([d.position for d in txd], dtype=np.float64),
+                         np.array([d.position for d in rxd], dtype=np.float64),
+                         np.array([d.orientation for d in txd], dtype=np.float64),
+                         np.array([d.orientation for d in rxd], dtype=np.float64)], axis=1)   # [P, 12]
+    eta = em.EvalContext(sc).eta_table(b)
+    st = [POLARIZATION_SLANTS[sc.tx_array.polarization][0]]
+    sr = [POLARIZATION_SLANTS[sc.rx_array.polarization][0]]
+
+    def power(x, grad=False):
+        xt = torch.tensor(x, device=b.device, requires_grad=grad)
+        a = em.path_coefficients_geo(b, T, eta, xt[:, 0:3], xt[:, 3:6], xt[:, 6:9], xt[:, 9:12],
+                                     sc.tx_array.pattern, sc.rx_array.pattern, st, sr, sc.wavelength,
+                                     sc.frequency_hz)[:, 0, 0]
+        return (a.abs() ** 2), xt
+
+    pw, xt = power(x0, True)
+    pw.sum().backward()
+    got = xt.grad.cpu().numpy()
+    fd = np.zeros_like(x0)
+    for j in range(12):
+        h = 1e-6 if j < 6 else 1e-7
+        xu, xd = x0.copy(), x0.copy()
+        xu[:, j] += h
+        xd[:, j] -= h
+        with torch.no_grad():
+            fd[:, j] = ((power(xu)[0] - power(xd)[0]) / (2 * h)).cpu().numpy()
+    scale = np.abs(fd).max(axis=1, keepdims=True)
+    assert np.all(np.abs(got - fd) <= 1e-3 * np.abs(fd) + 1e-4 * scale), np.abs(got - fd).max()
+
+
 @pytest.mark.parametrize("name", ["ground", "canyon"])
 def test_explicit_arrays_and_doppler_match_reference(P, golden, name):
     """synthetic_array=False (em.py:425-459): every element pair re-solved with
