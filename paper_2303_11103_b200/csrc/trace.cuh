@@ -433,13 +433,14 @@ overflow:
 }
 #endif
 
-// measured on C3: while-while wins for the any-hit occlusion queries
-// (7.4 vs 8.4 ms) and loses slightly for the launch's closest-hit (36.0 vs 35.3 ms)
+// measured on C3: while-while wins for the any-hit occlusion queries (7.4 vs
+// 8.4 ms) and, since the origin skip table and the FFMA2 box filter, for the
+// launch's closest-hit too (12.00 vs 12.27 ms; it lost 36.0 vs 35.3 before)
 #ifndef RT_WW_ANY
 #define RT_WW_ANY 1
 #endif
 #ifndef RT_WW_CLOSEST
-#define RT_WW_CLOSEST 0
+#define RT_WW_CLOSEST 1
 #endif
 #ifndef RT_HOIST_FAST
 #define RT_HOIST_FAST 1   // measured on C3: launch 25.8 vs 26.8 ms, validate 5.5 vs 6.3 ms
@@ -502,7 +503,7 @@ __device__ inline int occluded(const Bvh& bvh, d3 p, d3 q, double eps = RAY_EPS,
 }
 
 #ifndef RT_HINT_R
-#define RT_HINT_R 2   // measured on C3 (validate ms): R0 5.85, R1 3.89, R2 3.84, R4 4.47
+#define RT_HINT_R 1   // C3 validate ms: R0 5.85, R1 3.89, R2 3.84, R4 4.47; with the skip table R1 2.88 vs R2 2.95
 #endif
 // Occluder cache: does one of the TriRecs pos-R..pos+R block segment p->q?
 // Exactly the acceptance test the traversal applies (mt_test + the window
