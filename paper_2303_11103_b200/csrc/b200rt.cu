@@ -432,7 +432,7 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     // ranges of small_max < m <= SAH_BIG prims: SAH_MED_BATCH levels per host
     // round trip, each grid sized by the bound (ranges at most double per level;
     // CTAs past the live count exit at once)
-    const int SAH_MED_BATCH = 4;
+    const int SAH_MED_BATCH = 8;
     int mcur = 0;
     long long nmed = h[4];
     while (nmed > 0) {
