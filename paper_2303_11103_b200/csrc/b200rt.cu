@@ -1363,7 +1363,8 @@ int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx, int6
                                                   ctx->losbuf.get<unsigned char>(), nullptr,
                                                   reinterpret_cast<int*>(ctx->dflag.get<long long>()));
     CKL();
-    RC(check_flags(ctx, st));
+    // the LOS error flags travel back with the path count (one host round trip)
+    CK(cudaMemcpyAsync(ctx->hpin + 1, ctx->dflag.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemsetAsync(ctx->heads.p, 0xFF, 4ULL * n_rx, st));
     if (n_rec > 0) {
         k_merge<false><<<nblk(n_rec, 128), 128, 0, st>>>(cands_dev(ctx), scene_dev(ctx), ctx->images.get<double>(),
@@ -1387,6 +1388,11 @@ int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx, int6
     }));
     CK(cudaMemcpyAsync(ctx->hpin, off + n_rx, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    {
+        long long f = ctx->hpin[1];
+        if (f & 1) return fail(ctx, RT_ECUDA, "BVH traversal stack overflow");
+        if (f & 4) return fail(ctx, RT_ECOINCIDE, "transmitter and probe/receiver coincide");
+    }
     long long P = reinterpret_cast<int*>(ctx->hpin)[0];
     int L = ctx->path_L;
     size_t Pn = (size_t)std::max<long long>(P, 1);
