@@ -267,7 +267,7 @@ def prepare_candidates(bvh: Bvh, tx_pos, max_depth, method, num_rays):
 def paths_to_receivers(bvh: Bvh, tx_pos, rx_pos, tx_index=0) -> PathTable:
     """rt_paths for the current candidate set; returns the device path table."""
     dev = bvh.device
-    rx = torch.as_tensor(np.asarray(rx_pos, dtype=np.float64).reshape(-1, 3), device=dev).contiguous()
+    rx = N.h2d(np.asarray(rx_pos, dtype=np.float64).reshape(-1, 3), dev)   # pinned, async
     n = ctypes.c_int64()
     txh = _pos3(tx_pos)
     with torch.cuda.device(dev):
@@ -310,7 +310,7 @@ def compute_paths(scene, bvh: Bvh, max_depth: int, method: str = "exhaustive",
         raise TracerError("scene needs at least one transmitter and one receiver")
     if max_depth < 0:
         raise TracerError("max_depth must be >= 0")
-    rx_pos = np.array([[float(x) for x in r.position] for r in rxs], dtype=np.float64)
+    rx_pos = np.array([r.position for r in rxs], dtype=np.float64).reshape(-1, 3)
     tables = []
     for ti, tx in enumerate(txs):
         prepare_candidates(bvh, tx.position, max_depth, method, num_rays)
