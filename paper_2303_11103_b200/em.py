@@ -369,6 +369,14 @@ class ChannelGains:
         return self._entries
 
 
+def _rows_array(rows):
+    """[n, 3, 3] rotation rows; devices sharing one row object cost one conversion."""
+    if rows and all(r is rows[0] for r in rows):
+        one = np.asarray(rows[0], dtype=np.float64).reshape(1, 3, 3)
+        return np.broadcast_to(one, (len(rows), 3, 3))
+    return np.asarray(rows, dtype=np.float64).reshape(len(rows), 3, 3)
+
+
 def _aperture(off, rows):
     if len(off) <= 1:
         return 0.0
@@ -450,8 +458,8 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
     # every small host-side parameter in one pinned upload
     n_td, n_rd = len(tx_rows_dev), len(rx_rows_dev)
     # world-frame element offsets per device (em.py:372-379), on the host
-    rows_t = np.asarray(tx_rows_dev, dtype=np.float64).reshape(n_td, 3, 3)
-    rows_r = np.asarray(rx_rows_dev, dtype=np.float64).reshape(n_rd, 3, 3)
+    rows_t = _rows_array(tx_rows_dev)
+    rows_r = _rows_array(rx_rows_dev)
     off_tx_w = np.einsum("ek,dmk->dem", np.asarray(off_tx, dtype=np.float64), rows_t)   # [n_tx, E, 3]
     off_rx_w = np.einsum("ek,dmk->dem", np.asarray(off_rx, dtype=np.float64), rows_r)
     eta_host = ctx.eta_values(bvh) if eta is None else np.zeros((0, 2))
