@@ -733,14 +733,14 @@ int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
     ctx->origin_limit = 0.0;
     if (n_prims == 0) return RT_OK;
     CK(cudaMemcpyAsync(ctx->prim_mat.p, prim_material, 4 * n_prims, cudaMemcpyDeviceToDevice, st));
-    unsigned init[7] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, 0u};
-    CK(cudaMemcpyAsync(ctx->cbounds.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    // ordered-float bounds: mins start at 0xFFFFFFFF, maxima (and the scale) at 0
+    CK(cudaMemsetAsync(ctx->cbounds.p, 0xFF, 3 * sizeof(unsigned), st));
+    CK(cudaMemsetAsync(ctx->cbounds.get<unsigned>() + 3, 0, 4 * sizeof(unsigned), st));
     k_gather<<<nblk(n_prims, 256), 256, 0, st>>>(
         vertices, tri_vertex, n_prims, ctx->v0.get<double>(), ctx->e1.get<double>(),
         ctx->e2.get<double>(), ctx->nrm.get<double>(), ctx->poff.get<double>(),
         ctx->pbox.get<float>(), ctx->cent.get<float>(), ctx->cbounds.get<unsigned>());
     CKL();
-    CK(cudaStreamSynchronize(st));   // `init` lives on the host stack
     return RT_OK;
 }
 
