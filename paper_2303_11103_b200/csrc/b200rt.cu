@@ -252,7 +252,9 @@ int cub_call(rt_ctx* ctx, F&& f) {
 
 // Sort rows (s_seq/s_len, n rows, width L) by (length, lexicographic) and
 // drop duplicates into cand_seq/cand_len (LSD radix over digit columns).
-int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st) {
+// unique_in: the rows are known to be distinct (one launch's trie): the
+// duplicate flags, their scan and the count read-back are skipped
+int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st, bool unique_in = false) {
     ctx->cand_max_len = std::max(L, 1);
     if (n == 0) {
         ctx->n_cand = 0;
@@ -287,6 +289,16 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st) {
                                                    (int)n, 0, end_bit, st);
         }));
         std::swap(perm, perm_alt);
+    }
+    if (unique_in) {
+        CK(ctx->cand_seq.reserve(sizeof(int) * n * L));
+        CK(ctx->cand_len.reserve(n));
+        k_gather_rows<<<nblk(n, 256), 256, 0, st>>>(n, perm, seq, len, L, ctx->cand_seq.get<int>(),
+                                                    ctx->cand_len.get<signed char>());
+        CKL();
+        ctx->n_cand = n;
+        ctx->cand_sorted = true;
+        return RT_OK;
     }
     int* flag = ctx->s_flag.get<int>();
     int* pos = ctx->s_pos.get<int>();
@@ -1063,7 +1075,7 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
             ctx->n_cand = nodes;
             ctx->cand_sorted = false;
         } else {
-            RC(sort_unique_candidates(ctx, nodes, max_depth, st));
+            RC(sort_unique_candidates(ctx, nodes, max_depth, st, true));   // trie rows are distinct
         }
         PROF_END(ST_CAND_SORT);
         ctx->counters[3] = ctx->n_cand;

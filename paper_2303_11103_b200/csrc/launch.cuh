@@ -377,6 +377,17 @@ __global__ void k_scatter_unique(long long n, const int* perm, const int* flag, 
     len_out[dst] = (signed char)L;
 }
 
+// rows in sorted order (perm) when they are distinct already
+__global__ void k_gather_rows(long long n, const int* perm, const int* seq_in, const signed char* len_in,
+                              int max_len, int* seq_out, signed char* len_out) {
+    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    long long src = perm[r];
+    int L = len_in[src];
+    for (int j = 0; j < max_len; ++j) seq_out[r * max_len + j] = j < L ? seq_in[src * max_len + j] : -1;
+    len_out[r] = (signed char)L;
+}
+
 // exhaustive enumeration (tracer.py:196-214) directly in (length, lex) order
 __global__ void k_enumerate(long long total, int n, int max_depth, const long long* level_start,
                             int* seq, signed char* len) {
