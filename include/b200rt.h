@@ -72,12 +72,15 @@ int rt_scene_arrays(rt_ctx* ctx, double* v0, double* e1, double* e2, double* nor
 
 /* ---- queries (bvh.py:83-115 Bvh.intersect / Bvh.occluded) ----
  * rt_trace: n rays (device o,d [n*3], tmin,tmax [n]); closest hit (t, global
- * prim id, -1 on miss) or, with any_hit, the first hit found. */
+ * prim id, -1 on miss) or, with any_hit, the first hit found.  Synchronizes
+ * the stream: a traversal stack overflow fails the call (RT_ECUDA). */
 int rt_trace(rt_ctx* ctx, const double* o, const double* d, const double* tmin,
              const double* tmax, int64_t n, int any_hit, double* t_out, int32_t* prim_out,
              void* stream);
 /* rt_occluded: segments p->q (device [n*3]); out[i] = 1 blocked, 0 clear,
- * -1 endpoints coincide (bvh.py:109-110 raises). */
+ * -1 endpoints coincide (bvh.py:109-110 raises).  Synchronizes the stream: a
+ * traversal stack overflow fails the call (RT_ECUDA) instead of reading as
+ * "blocked". */
 int rt_occluded(rt_ctx* ctx, const double* p, const double* q, int64_t n, int32_t* out,
                 void* stream);
 
@@ -129,11 +132,14 @@ int rt_paths_get(rt_ctx* ctx, int32_t* rx_index, int32_t* cand, int8_t* order, i
 /* ---- polarized field transfer (em.py:98-171,291-312) ----
  * For every path p and element-slant pair (s, r): a[p, s, r] (complex as 2
  * doubles) of the geometry given by vertices [P*(L+2)*3], oriented normals
- * [P*L*3], cosines [P*L], length, delay; materials per interaction from the
- * scene's prim_material and eta [n_mat*2] (device).  tx_rows/rx_rows are
- * per-path 3x3 row-major rotations (device [P*9]). */
+ * [P*L*3], cosines [P*L], length, delay; the material of interaction j is
+ * interaction_mat[p*L+j] when that (device) array is given, else the scene's
+ * prim_material[seq[p*L+j]]; eta [n_mat*2] (device).  With interaction_mat
+ * no scene needs to be uploaded (em.py:291-312 transfer takes material names
+ * per interaction, not prim ids).  tx_rows/rx_rows are per-path 3x3
+ * row-major rotations (device [P*9]). */
 int rt_transfer(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
-                const int32_t* seq, const double* vertices, const double* normals,
+                const int32_t* seq, const int32_t* interaction_mat, const double* vertices, const double* normals,
                 const double* cos_inc, const double* length, const double* delay,
                 const double* tx_rows, const double* rx_rows, int tx_pattern, int rx_pattern,
                 const double* tx_slants, int n_tx_slants, const double* rx_slants,
@@ -141,9 +147,11 @@ int rt_transfer(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
                 double frequency_hz, double* a_out, void* stream);
 /* Hand-written adjoint of rt_transfer w.r.t. eta: given grad_a (device
  * [P*S*R*2], PyTorch's dL/dRe + j dL/dIm convention) accumulate
- * grad_eta[m] = (dL/dRe eta_m, dL/dIm eta_m) into device [n_mat*2]. */
+ * grad_eta[m] = (dL/dRe eta_m, dL/dIm eta_m) into device [n_mat*2].
+ * Deterministic: per-interaction contributions are summed per material in a
+ * fixed order (no atomics), so repeated calls give identical bits. */
 int rt_transfer_bwd(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
-                    const int32_t* seq, const double* vertices, const double* normals,
+                    const int32_t* seq, const int32_t* interaction_mat, const double* vertices, const double* normals,
                     const double* cos_inc, const double* length, const double* delay,
                     const double* tx_rows, const double* rx_rows, int tx_pattern,
                     int rx_pattern, const double* tx_slants, int n_tx_slants,

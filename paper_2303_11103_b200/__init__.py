@@ -9,8 +9,9 @@ from .bvh import Bvh, Hit, build
 from .channel import (ChannelError, Cir, CoverageMap, FreqResponse, GridSpec, build_cir,
                       coverage_map, frequency_response, load_cir, point_path_gain,
                       probe_receiver, save_cir, subcarrier_frequencies)
-from .em import (ChannelGains, EmError, EvalContext, PathGain, apply_doppler, compute_gains,
-                 path_materials, transfer)
+from .em import (ChannelGains, DiffComplex, EmError, EvalContext, PathGain, PathGeometry,
+                 apply_doppler, compute_gains, geometry_for_positions, geometry_from_path,
+                 path_geometry, path_materials, transfer)
 from .scene import (AntennaArray, RadioDevice, RadioMaterial, Scene, SceneError, SceneObject,
                     load_scene, look_at, material_eta, write_scene)
 from .tracer import (PathSet, PropagationPath, TracerError, compute_paths,

@@ -16,10 +16,6 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_native", "libb200rt.so")
-# experiment hook: load an alternative build of the same ABI (e.g. a variant
-# compiled with other -D flags into _native/); the default is the product build
-if os.environ.get("B200RT_LIB"):
-    LIB_PATH = os.path.join(HERE, "_native", os.path.basename(os.environ["B200RT_LIB"]))
 SRC_DIR = os.path.join(HERE, "csrc")
 
 RT_OK, RT_EINVAL, RT_ECAP, RT_ECOINCIDE, RT_ECUDA, RT_ENOMEM, RT_ESTATE = 0, -1, -2, -3, -4, -5, -6
@@ -100,9 +96,9 @@ def lib():
             "rt_candidates_max_len": (i32, [P]),
             "rt_paths": (i32, [P, P, P, i64, pi64, P]),
             "rt_paths_get": (i32, [P] + [P] * 11 + [P]),
-            "rt_transfer": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P, i32,
+            "rt_transfer": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P, i32,
                                   P, i32, f64, f64, P, P]),
-            "rt_transfer_bwd": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P,
+            "rt_transfer_bwd": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P,
                                       i32, P, i32, f64, f64, P, P, P]),
             "rt_coverage": (i32, [P, P, f64, f64, f64, i64, i64, f64, P, P, i32, P, P, i32, i32, P,
                                   i32, f64, f64, i32, i32, P, P, P]),
@@ -225,6 +221,7 @@ def h2d(array, device):
     a = np.ascontiguousarray(array)
     if a.nbytes == 0 or a.nbytes > _SmallH2D.CAP:
         return torch.as_tensor(a, device=device)
+    device = torch.device(device)
     st = _SMALL.get(device)
     if st is None:
         st = _SMALL[device] = _SmallH2D()
@@ -232,9 +229,12 @@ def h2d(array, device):
         st.ready.synchronize()
     view = st.buf[:a.nbytes].numpy().view(a.dtype).reshape(a.shape)
     view[...] = a
-    out = torch.from_numpy(view).to(device, non_blocking=True)
-    st.ready = torch.cuda.Event()
-    st.ready.record()
+    with torch.cuda.device(device):
+        out = torch.from_numpy(view).to(device, non_blocking=True)
+        # the copy runs on the destination device's current stream: the buffer
+        # may be refilled only after that stream passed this point
+        st.ready = torch.cuda.Event()
+        st.ready.record(torch.cuda.current_stream(device))
     return out
 
 

@@ -209,13 +209,19 @@ struct TransferArgs {
     int n_sr;
     const double* eta;
     const int* prim_mat;
+    const int* imat;   // [P*L] material per interaction, or null (prim_mat[seq])
     double wavelength, frequency;
 };
 
 __device__ inline void table_geom(const TransferArgs& A, long long p, Geom& g) {
     int K = A.order[p];
     geom_from_table(K, A.verts + p * (A.L + 2) * 3, A.nrm + p * A.L * 3, A.cosv + p * A.L,
-                    A.seq + p * A.L, A.prim_mat, A.length[p], A.delay[p], g);
+                    A.seq + p * A.L, A.prim_mat, A.imat ? A.imat + p * A.L : nullptr, A.length[p],
+                    A.delay[p], g);
+}
+
+__device__ __forceinline__ int interaction_material(const TransferArgs& A, long long p, int j) {
+    return A.imat ? A.imat[p * A.L + j] : A.prim_mat[A.seq[p * A.L + j]];
 }
 
 // a[p, s, r] for every path and slant pair (em.py:291-312, 397-405)
@@ -236,19 +242,59 @@ __global__ void k_transfer(const __grid_constant__ TransferArgs A, double* a_out
     }
 }
 
+// per (path, slant pair) item: each interaction's eta-gradient contribution
+// into contrib[item * L + j] (zeros past the path's order or for G = 0)
 __global__ void k_transfer_bwd(const __grid_constant__ TransferArgs A, const double* grad_a,
-                               double* grad_eta) {
+                               double2* contrib) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= A.n * A.n_st * A.n_sr) return;
     long long p = i / (A.n_st * A.n_sr);
     int rem = (int)(i - p * A.n_st * A.n_sr);
     int s = rem / A.n_sr, r = rem - s * A.n_sr;
+    double2* out = contrib + i * A.L;
+    for (int j = 0; j < A.L; ++j) out[j] = make_double2(0.0, 0.0);
     c2 G = c2{grad_a[2 * i], grad_a[2 * i + 1]};
     if (G.re == 0.0 && G.im == 0.0) return;
     Geom g;
     table_geom(A, p, g);
     transfer_adjoint(g, A.tx_pat, A.tx_slants[s], A.tx_rows + 9 * p, A.rx_pat, A.rx_slants[r],
-                     A.rx_rows + 9 * p, A.eta, A.wavelength, A.frequency, G, grad_eta);
+                     A.rx_rows + 9 * p, A.eta, A.wavelength, A.frequency, G, out);
+}
+
+// grad_eta[m] += sum of the contributions of material m, in a fixed order: one
+// block per material, thread t sums entries t, t + B, t + 2B, ... in index
+// order, then a fixed shared-memory tree.  No atomics: the result is the same
+// bit pattern on every run (reference criterion 10, byte-identical logs).
+constexpr int ADJ_BLOCK = 256;
+__global__ void __launch_bounds__(ADJ_BLOCK) k_grad_eta_reduce(const __grid_constant__ TransferArgs A,
+                                                                const double2* contrib, double* grad_eta) {
+    __shared__ double sre[ADJ_BLOCK], sim[ADJ_BLOCK];
+    const int m = blockIdx.x;
+    const long long items = A.n * A.n_st * A.n_sr, per_path = (long long)A.n_st * A.n_sr;
+    double re = 0.0, im = 0.0;
+    for (long long e = threadIdx.x; e < items * A.L; e += ADJ_BLOCK) {
+        long long i = e / A.L;
+        int j = (int)(e - i * A.L);
+        long long p = i / per_path;
+        if (j >= A.order[p] || interaction_material(A, p, j) != m) continue;
+        double2 c = contrib[e];
+        re += c.x;
+        im += c.y;
+    }
+    sre[threadIdx.x] = re;
+    sim[threadIdx.x] = im;
+    __syncthreads();
+    for (int w = ADJ_BLOCK / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sre[threadIdx.x] += sre[threadIdx.x + w];
+            sim[threadIdx.x] += sim[threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        grad_eta[2 * m] += sre[0];
+        grad_eta[2 * m + 1] += sim[0];
+    }
 }
 
 }  // namespace rt

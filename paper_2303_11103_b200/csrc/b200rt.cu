@@ -12,12 +12,6 @@
 #include <vector>
 
 #include "../../include/b200rt.h"
-#ifndef RT_PLOC
-#define RT_PLOC 1   // measured on C3: 30.9 vs 42.2 node visits per bounce (Karras LBVH)
-#endif
-#if RT_PLOC
-#define RT_PLOC_BUILD 1   // depth-verified trees: traversal skips the per-push stack check
-#endif
 #include "api_kernels.cuh"
 #include "bvh_build.cuh"
 #include "bvh_ploc.cuh"
@@ -27,9 +21,6 @@
 #include "launch.cuh"
 
 
-#ifndef RT_DYNAMIC
-#define RT_DYNAMIC 0
-#endif
 #ifndef RT_DFS_LAYOUT
 #define RT_DFS_LAYOUT 1   // depth-first BNode order for the PLOC tree (C3 launch: -0.5%)
 #endif
@@ -90,8 +81,7 @@ struct rt_ctx {
     int64_t n_prims = 0;
     DevBuf v0, e1, e2, nrm, poff, prim_mat, pbox, cent, cbounds;
     // bvh
-    DevBuf nodes4, frontier, frontier2, map4, nodes, dbox, skip_tab, tris, sorted_idx, morton, morton_alt, idx_alt, child, parent_int, parent_leaf,
-        rfirst, rlast, nbox, flags;
+    DevBuf nodes, dbox, skip_tab, tris, sorted_idx, morton, morton_alt, idx_alt, child, flags;
     bool bvh_ready = false;
     int bvh_depth = -1;           // deepest BNode (root 0); -1 = not measured
     bool tail_smem_set = false;   // k_ploc_tail's dynamic shared memory opt-in done
@@ -100,6 +90,7 @@ struct rt_ctx {
     DevBuf tree_diag;             // [0] deepest BNode; doubles at +8: surface-area sums
     int diag_root = -1;           // root id of the last PLOC/SAH tree for the SAH estimate
     bool diag_pending = false;    // tree diagnostics not yet read back
+    cudaEvent_t diag_ev = nullptr;  // end of the last build on the caller's stream
     // candidates
     DevBuf cand_seq, cand_len;
     int64_t n_cand = 0;
@@ -123,6 +114,7 @@ struct rt_ctx {
     DevBuf p_rx, p_cand, p_order, p_seq, p_verts, p_len, p_delay, p_kdep, p_karr, p_nrm, p_cos;
     // error flags + pinned host staging
     DevBuf dflag, probe;
+    DevBuf adj;   // adjoint contributions [items * L] (rt_transfer_bwd)
     // PLOC builder scratch
     DevBuf pl_box, pl_count, pl_parent, pl_ca, pl_cb, pl_nn, pl_out, pl_valid, pl_pos, pl_slot, pl_em, pl_dfs;
     DevBuf sah_tasks;
@@ -183,15 +175,12 @@ SceneDev scene_dev(rt_ctx* ctx) {
 
 rt::Bvh bvh_dev(rt_ctx* ctx) {
     rt::Bvh b;
-#if RT_WIDE
-    b.nodes = ctx->nodes4.get<BNode4>();
-#else
     b.nodes = ctx->nodes.get<BNode>();
-#endif
     b.tris = ctx->tris.get<TriRec>();
     b.n_prims = (int)ctx->n_prims;
     b.origin_limit = ctx->origin_limit;
     b.skip = ctx->has_skip ? ctx->skip_tab.get<int>() : nullptr;
+    b.err = reinterpret_cast<int*>(ctx->dflag.get<long long>());
     return b;
 }
 
@@ -324,7 +313,6 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st, boo
     return RT_OK;
 }
 
-int build_karras(rt_ctx* ctx, long long n, const uint64_t* kout, const int* vout, cudaStream_t st);
 int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st);
 int tree_diagnostics(rt_ctx* ctx, cudaStream_t st);
 int build_morton(rt_ctx* ctx, long long n, cudaStream_t st);
@@ -619,6 +607,8 @@ int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st) {
     // rt_get_profile: no host round trip on the build path
     ctx->diag_root = (n > 2 && dfs) ? root : -1;
     ctx->diag_pending = n > 1;
+    if (!ctx->diag_ev) CK(cudaEventCreateWithFlags(&ctx->diag_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->diag_ev, st));
     return RT_OK;
 }
 
@@ -626,6 +616,8 @@ int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st) {
 int tree_diagnostics(rt_ctx* ctx, cudaStream_t st) {
     if (!ctx->diag_pending) return RT_OK;
     ctx->diag_pending = false;
+    // the build ran on the caller's (possibly non-blocking) stream: wait for it
+    if (ctx->diag_ev) CK(cudaEventSynchronize(ctx->diag_ev));
     int h = 0;
     CK(cudaMemcpyAsync(&h, ctx->tree_diag.get<int>(), 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -643,41 +635,6 @@ int tree_diagnostics(rt_ctx* ctx, cudaStream_t st) {
     CK(cudaMemcpyAsync(d, sums, 24, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     ctx->counters[14] = (long long)llround(1000.0 * (1.0 + d[0] / d[2]));   // milli-visits
-    return RT_OK;
-}
-
-// binary child-pair nodes (n_bin of them, root 0) -> 4-wide nodes
-int collapse4(rt_ctx* ctx, long long n_bin, cudaStream_t st) {
-    long long cap = std::max<long long>(n_bin, 1);
-    CK(ctx->nodes4.reserve(sizeof(BNode4) * cap));
-    CK(ctx->frontier.reserve(4 * cap));
-    CK(ctx->frontier2.reserve(4 * cap));
-    CK(ctx->map4.reserve(4 * cap));
-    int* cnt = reinterpret_cast<int*>(ctx->ctrs.get<long long>());   // [0] out nodes, [2] next size
-    CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
-    int zero = 0;
-    CK(cudaMemcpyAsync(ctx->frontier.p, &zero, 4, cudaMemcpyHostToDevice, st));
-    int* f = ctx->frontier.get<int>();
-    int* g = ctx->frontier2.get<int>();
-    long long nf = 1;
-    while (nf > 0) {
-        CK(cudaMemsetAsync(cnt + 2, 0, 4, st));
-        k_collapse<<<nblk(nf, 128), 128, 0, st>>>(ctx->nodes.get<BNode>(), f, (int)nf,
-                                                  ctx->nodes4.get<BNode4>(), cnt, ctx->map4.get<int>(),
-                                                  g, cnt + 2);
-        CKL();
-        int nxt = 0;
-        CK(cudaMemcpyAsync(&nxt, cnt + 2, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        nf = nxt;
-        std::swap(f, g);
-    }
-    int n4 = 0;
-    CK(cudaMemcpyAsync(&n4, cnt, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    k_fix_refs<<<nblk(n4, 128), 128, 0, st>>>(ctx->nodes4.get<BNode4>(), n4, ctx->map4.get<int>());
-    CKL();
-    ctx->counters[8] = n4;
     return RT_OK;
 }
 
@@ -711,6 +668,10 @@ int rt_destroy(rt_ctx* ctx) {
     if (!ctx) return RT_OK;
     cudaSetDevice(ctx->device);
     if (ctx->hpin) cudaFreeHost(ctx->hpin);
+    if (ctx->diag_ev) cudaEventDestroy(ctx->diag_ev);
+    for (auto& pair : ctx->ev)
+        for (cudaEvent_t e : pair)
+            if (e) cudaEventDestroy(e);
     delete ctx;
     return RT_OK;
 }
@@ -784,30 +745,25 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
                                         ctx->e1.get<double>(), ctx->e2.get<double>(),
                                         ctx->tris.get<TriRec>());
         CKL();
-        return RT_WIDE ? collapse4(ctx, 1, st) : RT_OK;
+        return RT_OK;
     }
     if (RT_SAH) {
         RC(build_sah(ctx, n, st));
     } else {
         RC(build_morton(ctx, n, st));
     }
-    return RT_WIDE ? collapse4(ctx, n - 1, st) : RT_OK;
+    return RT_OK;
 }
 
 }  // extern "C"
 
 namespace {
-// Morton codes + radix sort, then the PLOC or Karras hierarchy over them
+// Morton codes + radix sort, then the PLOC hierarchy over them (RT_SAH=0 variant)
 int build_morton(rt_ctx* ctx, long long n, cudaStream_t st) {
     CK(ctx->morton.reserve(8 * n));
     CK(ctx->morton_alt.reserve(8 * n));
     CK(ctx->idx_alt.reserve(4 * n));
     CK(ctx->child.reserve(8 * n));
-    CK(ctx->parent_int.reserve(4 * n));
-    CK(ctx->parent_leaf.reserve(4 * n));
-    CK(ctx->rfirst.reserve(4 * n));
-    CK(ctx->rlast.reserve(4 * n));
-    CK(ctx->nbox.reserve(24 * n));
     CK(ctx->flags.reserve(4 * n));
     k_morton<<<nblk(n, 256), 256, 0, st>>>(ctx->cent.get<float>(), ctx->pbox.get<float>(),
                                           ctx->cbounds.get<unsigned>(), n,
@@ -820,31 +776,11 @@ int build_morton(rt_ctx* ctx, long long n, cudaStream_t st) {
     RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
         return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, 64, st);
     }));
-    return RT_PLOC ? build_ploc(ctx, n, st) : build_karras(ctx, n, kout, vout, st);
+    (void)kout;
+    (void)vout;
+    return build_ploc(ctx, n, st);
 }
 
-// Karras (2012) LBVH hierarchy from the sorted Morton keys (A/B alternative to PLOC)
-int build_karras(rt_ctx* ctx, long long n, const uint64_t* kout, const int* vout, cudaStream_t st) {
-    CK(cudaMemsetAsync(ctx->parent_int.p, 0xFF, 4 * n, st));
-    CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
-    k_karras<<<nblk(n - 1, 256), 256, 0, st>>>(kout, (int)n, ctx->child.get<int>(),
-                                               ctx->parent_int.get<int>(), ctx->parent_leaf.get<int>(),
-                                               ctx->rfirst.get<int>(), ctx->rlast.get<int>());
-    CKL();
-    k_refit<<<nblk(n, 256), 256, 0, st>>>((int)n, vout, ctx->pbox.get<float>(), ctx->child.get<int>(),
-                                          ctx->parent_int.get<int>(), ctx->parent_leaf.get<int>(),
-                                          ctx->nbox.get<float>(), ctx->flags.get<int>());
-    CKL();
-    k_layout<<<nblk(n - 1, 256), 256, 0, st>>>((int)n, vout, ctx->pbox.get<float>(), ctx->child.get<int>(),
-                                               ctx->nbox.get<float>(), ctx->rfirst.get<int>(),
-                                               ctx->rlast.get<int>(), ctx->cbounds.get<unsigned>(),
-                                               ctx->nodes.get<BNode>());
-    CKL();
-    k_sorted_tris<<<nblk(n, 256), 256, 0, st>>>((int)n, vout, ctx->v0.get<double>(), ctx->e1.get<double>(),
-                                                ctx->e2.get<double>(), ctx->tris.get<TriRec>());
-    CKL();
-    return RT_OK;
-}
 }  // namespace
 
 extern "C" {
@@ -880,7 +816,7 @@ int rt_trace(rt_ctx* ctx, const double* o, const double* d, const double* tmin,
         k_trace_batch<false><<<nblk(n, 128), 128, 0, st>>>(bvh_dev(ctx), o, d, tmin, tmax, n, t_out,
                                                            prim_out, ctx->dflag.get<long long>());
     CKL();
-    return RT_OK;
+    return check_flags(ctx, st);
 }
 
 int rt_occluded(rt_ctx* ctx, const double* p, const double* q, int64_t n, int32_t* out,
@@ -889,9 +825,11 @@ int rt_occluded(rt_ctx* ctx, const double* p, const double* q, int64_t n, int32_
     if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
     if (n == 0) return RT_OK;
     CK(cudaSetDevice(ctx->device));
-    k_occluded_batch<<<nblk(n, 128), 128, 0, ST(stream)>>>(bvh_dev(ctx), p, q, n, out);
+    cudaStream_t st = ST(stream);
+    RC(clear_flags(ctx, st));
+    k_occluded_batch<<<nblk(n, 128), 128, 0, st>>>(bvh_dev(ctx), p, q, n, out);
     CKL();
-    return RT_OK;
+    return check_flags(ctx, st);   // a stack overflow fails the call instead of reading as "blocked"
 }
 
 namespace {
@@ -988,7 +926,8 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
     }
     for (int attempt = 0; attempt < 6; ++attempt) {
         uint64_t cap = ctx->trie_cap;
-        if (cap > (1ULL << 31)) return fail(ctx, RT_ENOMEM, "candidate trie above 2^31 slots");
+        // slot ids travel as int (trie_insert returns slot + 1): cap must stay below 2^31
+        if (cap >= (1ULL << 31)) return fail(ctx, RT_ENOMEM, "candidate trie at or above 2^31 slots");
         CK(ctx->t_keys.reserve(8 * cap));
         CK(cudaMemsetAsync(ctx->t_keys.p, 0xFF, 8 * cap, st));
         CK(cudaMemsetAsync(ctx->ctrs.p, 0, 128, st));
@@ -1019,15 +958,8 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
         PROF_BEGIN(ST_LAUNCH);
         if (span > 0) {
             unsigned g = (unsigned)std::max<long long>(blocks, 1);
-            if (RT_DYNAMIC && shard_count == 1) {   // persistent grid, dynamic ray fetch from ctr[5]
-                unsigned long long* sc = reinterpret_cast<unsigned long long*>(ctr + 5);
-                unsigned gp = (unsigned)std::min<long long>(g, (long long)ctx->n_sm * RT_LAUNCH_MINB);
-                if (ctx->prof & 2) k_launch_dyn<true><<<gp, LB, 0, st>>>(bvh_dev(ctx), P, T, sc);
-                else k_launch_dyn<false><<<gp, LB, 0, st>>>(bvh_dev(ctx), P, T, sc);
-            } else {
-                if (ctx->prof & 2) k_launch<true><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
-                else k_launch<false><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
-            }
+            if (ctx->prof & 2) k_launch<true><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
+            else k_launch<false><<<g, LB, 0, st>>>(bvh_dev(ctx), P, T);
             CKL();
         }
         PROF_END(ST_LAUNCH);
@@ -1471,7 +1403,7 @@ int rt_paths_get(rt_ctx* ctx, int32_t* rx_index, int32_t* cand, int8_t* order, i
 }
 
 int rt_transfer(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, const int32_t* seq,
-                const double* vertices, const double* normals, const double* cos_inc,
+                const int32_t* interaction_mat, const double* vertices, const double* normals, const double* cos_inc,
                 const double* length, const double* delay, const double* tx_rows,
                 const double* rx_rows, int tx_pattern, int rx_pattern, const double* tx_slants,
                 int n_tx_slants, const double* rx_slants, int n_rx_slants, const double* eta,
@@ -1485,14 +1417,17 @@ int rt_transfer(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, 
     (void)n_mat;
     TransferArgs A{n_paths, max_len, (const signed char*)order, seq, vertices, normals, cos_inc, length,
                    delay, tx_rows, rx_rows, tx_pattern, rx_pattern, tx_slants, n_tx_slants,
-                   rx_slants, n_rx_slants, eta, ctx->prim_mat.get<int>(), wavelength, frequency_hz};
+                   rx_slants, n_rx_slants, eta, ctx->prim_mat.get<int>(), interaction_mat, wavelength,
+                   frequency_hz};
+    if (!interaction_mat && ctx->n_prims == 0)
+        return fail(ctx, RT_EINVAL, "transfer needs interaction materials or an uploaded scene");
     k_transfer<<<nblk(n_paths * n_tx_slants, 128), 128, 0, ST(stream)>>>(A, a_out);
     CKL();
     return RT_OK;
 }
 
 int rt_transfer_bwd(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order,
-                    const int32_t* seq, const double* vertices, const double* normals,
+                    const int32_t* seq, const int32_t* interaction_mat, const double* vertices, const double* normals,
                     const double* cos_inc, const double* length, const double* delay,
                     const double* tx_rows, const double* rx_rows, int tx_pattern, int rx_pattern,
                     const double* tx_slants, int n_tx_slants, const double* rx_slants,
@@ -1502,12 +1437,19 @@ int rt_transfer_bwd(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* ord
         return fail(ctx, RT_EINVAL, "bad transfer arguments");
     if (n_paths == 0) return RT_OK;
     CK(cudaSetDevice(ctx->device));
-    (void)n_mat;
     TransferArgs A{n_paths, max_len, (const signed char*)order, seq, vertices, normals, cos_inc, length,
                    delay, tx_rows, rx_rows, tx_pattern, rx_pattern, tx_slants, n_tx_slants,
-                   rx_slants, n_rx_slants, eta, ctx->prim_mat.get<int>(), wavelength, frequency_hz};
+                   rx_slants, n_rx_slants, eta, ctx->prim_mat.get<int>(), interaction_mat, wavelength,
+                   frequency_hz};
+    if (!interaction_mat && ctx->n_prims == 0)
+        return fail(ctx, RT_EINVAL, "transfer needs interaction materials or an uploaded scene");
+    if (n_mat < 1) return fail(ctx, RT_EINVAL, "need n_mat >= 1");
     long long n = n_paths * n_tx_slants * n_rx_slants;
-    k_transfer_bwd<<<nblk(n, 128), 128, 0, ST(stream)>>>(A, grad_a, grad_eta);
+    CK(ctx->adj.reserve(sizeof(double2) * (size_t)n * max_len));
+    double2* contrib = ctx->adj.get<double2>();
+    k_transfer_bwd<<<nblk(n, 128), 128, 0, ST(stream)>>>(A, grad_a, contrib);
+    CKL();
+    k_grad_eta_reduce<<<n_mat, ADJ_BLOCK, 0, ST(stream)>>>(A, contrib, grad_eta);
     CKL();
     return RT_OK;
 }

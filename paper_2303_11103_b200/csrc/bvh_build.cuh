@@ -5,9 +5,10 @@
 // target); the per-primitive arrays are bit-identical to the
 // reference's numpy ones and first-hit semantics are those of trace.cuh.
 //
-// Build: prim AABBs + centroids -> 63-bit Morton codes -> CUB radix sort ->
-// Karras (2012) hierarchy -> bottom-up refit with atomic flags -> child-pair
-// node layout with subtrees of <= LEAF_MAX prims collapsed into leaves.
+// Ingest: prim AABBs + centroids, the scene bounds and 63-bit Morton codes
+// (the PLOC variant's input).  The product tree is the binned-SAH build of
+// bvh_sah.cuh; the Karras LBVH and the 4-wide collapse measured slower (DESIGN
+// §4) and were removed from the library.
 #pragma once
 #include <cub/cub.cuh>
 #include "rt_common.cuh"
@@ -153,72 +154,6 @@ __global__ void k_morton(const float* cent, const float* pbox, const unsigned* c
     idx[i] = (int)i;
 }
 
-__device__ inline int delta(const uint64_t* keys, int n, int i, int j) {
-    if (j < 0 || j >= n) return -1;
-    uint64_t a = keys[i], b = keys[j];
-    if (a == b) return 64 + __clz((unsigned)(i ^ j));
-    return __clzll(a ^ b);
-}
-
-// Karras 2012: internal node i covers [first, last]; children are internal
-// nodes (>= 0) or leaves (~sorted index).
-__global__ void k_karras(const uint64_t* keys, int n, int* child /*[2*(n-1)]*/, int* parent_int,
-                         int* parent_leaf, int* rfirst, int* rlast) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n - 1) return;
-    int d = (delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1)) >= 0 ? 1 : -1;
-    int dmin = delta(keys, n, i, i - d);
-    int lmax = 2;
-    while (delta(keys, n, i, i + lmax * d) > dmin) lmax <<= 1;
-    int l = 0;
-    for (int t = lmax >> 1; t >= 1; t >>= 1)
-        if (delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
-    int j = i + l * d;
-    int dnode = delta(keys, n, i, j);
-    int s = 0;
-    int span = l;
-    for (int t = (span + 1) >> 1;; t = (t + 1) >> 1) {
-        if (delta(keys, n, i, i + (s + t) * d) > dnode) s += t;
-        if (t == 1) break;
-    }
-    int gamma = i + s * d + (d < 0 ? -1 : 0);
-    int first = i < j ? i : j, last = i < j ? j : i;
-    int left = (first == gamma) ? ~gamma : gamma;
-    int right = (last == gamma + 1) ? ~(gamma + 1) : gamma + 1;
-    child[2 * i] = left;
-    child[2 * i + 1] = right;
-    if (left < 0) parent_leaf[~left] = i; else parent_int[left] = i;
-    if (right < 0) parent_leaf[~right] = i; else parent_int[right] = i;
-    rfirst[i] = first;
-    rlast[i] = last;
-}
-
-// bottom-up union of boxes; the second thread to reach a node computes it
-__global__ void k_refit(int n, const int* sorted_idx, const float* pbox, const int* child,
-                        const int* parent_int, const int* parent_leaf, float* nbox /*[(n-1)*6]*/,
-                        int* flags) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int node = parent_leaf[k];
-    while (node >= 0) {
-        __threadfence();
-        if (atomicAdd(flags + node, 1) == 0) return;
-        __threadfence();
-        float b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        for (int c = 0; c < 2; ++c) {
-            int ch = child[2 * node + c];
-            const float* src = ch < 0 ? pbox + 6 * (int64_t)sorted_idx[~ch] : nbox + 6 * (int64_t)ch;
-            for (int m = 0; m < 3; ++m) {
-                float lo = __ldcg(src + m), hi = __ldcg(src + 3 + m);
-                b[m] = fminf(b[m], lo);
-                b[3 + m] = fmaxf(b[3 + m], hi);
-            }
-        }
-        for (int m = 0; m < 6; ++m) __stcg(nbox + 6 * (int64_t)node + m, b[m]);
-        node = parent_int[node];
-    }
-}
-
 // eps_box = 2^-20 * max(S, 1), S = max |coordinate| (trace.cuh slab32)
 __device__ inline float box_eps(const unsigned* cbounds) {
     return fmaxf(ordered_to_float(cbounds[6]), 1.0f) * 9.5367431640625e-07f;
@@ -230,31 +165,6 @@ __device__ inline void inflate6(float* b, float e) {
     }
 }
 
-__global__ void k_layout(int n, const int* sorted_idx, const float* pbox, const int* child,
-                         const float* nbox, const int* rfirst, const int* rlast,
-                         const unsigned* cbounds, BNode* out) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n - 1) return;
-    float eps = box_eps(cbounds);
-    float bx[2][6];
-    int ref[2];
-    for (int c = 0; c < 2; ++c) {
-        int ch = child[2 * i + c];
-        const float* src;
-        if (ch < 0) {
-            src = pbox + 6 * (int64_t)sorted_idx[~ch];
-            ref[c] = make_leaf(~ch, 1);
-        } else {
-            src = nbox + 6 * (int64_t)ch;
-            int cnt = rlast[ch] - rfirst[ch] + 1;
-            ref[c] = cnt <= LEAF_MAX ? make_leaf(rfirst[ch], cnt) : ch;
-        }
-        for (int m = 0; m < 6; ++m) bx[c][m] = src[m];
-        inflate6(bx[c], eps);
-    }
-    out[i] = pack_bnode(bx, ref[0], ref[1]);
-}
-
 // single-prim scene: root with the one leaf on both sides
 __global__ void k_layout_one(const float* pbox, const unsigned* cbounds, BNode* out) {
     float s[6];
@@ -263,81 +173,6 @@ __global__ void k_layout_one(const float* pbox, const unsigned* cbounds, BNode* 
     float bx[2][6];
     for (int m = 0; m < 6; ++m) bx[0][m] = bx[1][m] = s[m];
     out[0] = pack_bnode(bx, make_leaf(0, 1), make_leaf(0, 1));
-}
-
-// ---- 4-wide collapse (level-synchronous, top-down) ---------------------------------------
-// BVH4 node = binary node X; its children = X's two children with the internal
-// child of largest surface area repeatedly replaced by its own two children
-// until there are four (or only leaves remain).
-
-__device__ inline float box_area(const float* b) {
-    float dx = fmaxf(b[3] - b[0], 0.f), dy = fmaxf(b[4] - b[1], 0.f), dz = fmaxf(b[5] - b[2], 0.f);
-    return dx * dy + dy * dz + dz * dx;
-}
-
-__device__ inline void bin_child(const BNode& nd, int c, int& ref, float* b) {
-    unpack_bnode(nd, c, b);
-    ref = c == 0 ? nd.d.x : nd.d.y;
-}
-
-__global__ void k_collapse(const BNode* bin, const int* frontier, int nf, BNode4* out, int* out_count,
-                           int* map, int* next, int* next_count) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nf) return;
-    int X = frontier[i];
-    int q = atomicAdd(out_count, 1);
-    map[X] = q;
-    int ref[4];
-    float bx[4][6];
-    BNode nd = bin[X];
-    bin_child(nd, 0, ref[0], bx[0]);
-    bin_child(nd, 1, ref[1], bx[1]);
-    int n = 2;
-    while (n < 4) {
-        int best = -1;
-        float bestA = -1.f;
-        for (int k = 0; k < n; ++k)
-            if (!ref_is_leaf(ref[k])) {
-                float A = box_area(bx[k]);
-                if (A > bestA) { bestA = A; best = k; }
-            }
-        if (best < 0) break;
-        BNode y = bin[ref[best]];
-        bin_child(y, 0, ref[best], bx[best]);
-        bin_child(y, 1, ref[n], bx[n]);
-        ++n;
-    }
-    BNode4 o;
-    float lo[3][4], hi[3][4];
-    int ch[4];
-    for (int k = 0; k < 4; ++k) {
-        for (int m = 0; m < 3; ++m) {
-            lo[m][k] = k < n ? bx[k][m] : INFINITY;
-            hi[m][k] = k < n ? bx[k][3 + m] : -INFINITY;
-        }
-        ch[k] = k < n ? ref[k] : EMPTY_REF;
-        if (k < n && !ref_is_leaf(ref[k])) next[atomicAdd(next_count, 1)] = ref[k];
-    }
-    o.lox = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
-    o.loy = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
-    o.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
-    o.hix = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
-    o.hiy = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
-    o.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
-    o.child = make_int4(ch[0], ch[1], ch[2], ch[3]);
-    o.pad = make_int4(0, 0, 0, 0);
-    out[q] = o;
-}
-
-// binary internal indices -> BVH4 indices
-__global__ void k_fix_refs(BNode4* out, int n4, const int* map) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n4) return;
-    int4 c = out[i].child;
-    int v[4] = {c.x, c.y, c.z, c.w};
-    for (int k = 0; k < 4; ++k)
-        if (v[k] != EMPTY_REF && !ref_is_leaf(v[k])) v[k] = map[v[k]];
-    out[i].child = make_int4(v[0], v[1], v[2], v[3]);
 }
 
 __global__ void k_sorted_tris(int n, const int* sorted_idx, const double* v0, const double* e1,

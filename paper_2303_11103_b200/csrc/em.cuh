@@ -165,7 +165,7 @@ __device__ inline void geom_from_points(d3 tx, const d3* pts, int k, d3 rx, cons
 // from a stored path table row (vertices + oriented normals + cosines)
 __device__ inline void geom_from_table(int k, const double* verts, const double* nrm,
                                        const double* cosv, const int* seq, const int* prim_mat,
-                                       double length, double delay, Geom& g) {
+                                       const int* imat, double length, double delay, Geom& g) {
     g.k = k;
     for (int j = 0; j <= k; ++j) {
         d3 s = sub(ld3(verts + 3 * (j + 1)), ld3(verts + 3 * j));
@@ -175,7 +175,7 @@ __device__ inline void geom_from_table(int k, const double* verts, const double*
     for (int j = 0; j < k; ++j) {
         g.nrm[j] = ld3(nrm + 3 * j);
         g.cosi[j] = cosv[j];
-        g.mat[j] = prim_mat[seq[j]];
+        g.mat[j] = imat ? imat[j] : prim_mat[seq[j]];
     }
     g.length = length;
     g.delay = delay;
@@ -212,14 +212,16 @@ __device__ inline d3 rx_field(const Geom& g, int rx_pat, double rx_slant, const 
     return element_field(rx_pat, rx_slant, Rrx, d3{karr.x * -1.0, karr.y * -1.0, karr.z * -1.0});
 }
 
-// Adjoint of a(eta) for one path and one element pair: accumulates
-// (dL/dRe eta_m, dL/dIm eta_m) for upstream G = dL/dRe a + j dL/dIm a.
+// Adjoint of a(eta) for one path and one element pair: writes interaction j's
+// contribution (dL/dRe eta_m, dL/dIm eta_m), m = its material, to contrib[j]
+// for upstream G = dL/dRe a + j dL/dIm a (the caller reduces per material in
+// a fixed order, so gradients are bit-reproducible).
 // Branch handling matches the reference tape: where Im(eta - sin^2) == 0 the
 // square root's imaginary-direction derivative is 0 (autodiff.py:373-377).
 __device__ inline void transfer_adjoint(const Geom& g, int tx_pat, double tx_slant,
                                         const double* Rtx, int rx_pat, double rx_slant,
                                         const double* Rrx, const double* eta, double wavelength,
-                                        double frequency, c2 G, double* grad_eta) {
+                                        double frequency, c2 G, double2* contrib) {
     if (g.k == 0) return;
     d3 ef = element_field(tx_pat, tx_slant, Rtx, g.dir[0]);
     c3 f = c3{c2{ef.x, 0.0}, c2{ef.y, 0.0}, c2{ef.z, 0.0}};
@@ -265,9 +267,7 @@ __device__ inline void transfer_adjoint(const Geom& g, int tx_pat, double tx_sla
         c2 dw_dim = arg_im == 0.0 ? c2{0.0, 0.0} : cmul(c2{0.0, 1.0}, dw_dre);
         c2 dre = cadd(da_de, cmul(da_dw, dw_dre));
         c2 dim = cadd(cmul(c2{0.0, 1.0}, da_de), cmul(da_dw, dw_dim));
-        int m = g.mat[j];
-        atomicAdd(grad_eta + 2 * m, cmul(Gc, dre).re);
-        atomicAdd(grad_eta + 2 * m + 1, cmul(Gc, dim).re);
+        contrib[j] = make_double2(cmul(Gc, dre).re, cmul(Gc, dim).re);
         // b <- R_j^T b = rte (b.ep) ep + rtm (b.epr) epi
         c2 gp = cmul(rte[j], b_ep), ga = cmul(rtm[j], b_epr);
         b.x = cadd(cscl(gp, B.ep.x), cscl(ga, B.epi.x));

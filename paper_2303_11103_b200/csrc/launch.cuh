@@ -216,97 +216,6 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
     }
 }
 
-// Persistent variant with dynamic ray fetch: a lane whose ray escaped or reached
-// max_depth immediately takes the next lattice slot (warp-aggregated atomic on
-// a global slot counter), so lanes stay busy instead of idling until the
-// warp's deepest ray finishes.  Same rays, same per-ray bounce sequence, same
-// trie inserts (keys carry the parent node, so mixed depths in a warp are fine).
-template <bool COUNT>
-__global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB)
-    k_launch_dyn(Bvh bvh, LaunchParams P, Trie T, unsigned long long* slot_counter) {
-    const unsigned FULL = 0xffffffffu;
-    int lane = threadIdx.x & 31;
-    unsigned long long my_bounces = 0, my_nodes = 0, my_tris = 0;
-    bool active = false, more = true;
-    const d3 tx = d3{P.tx, P.ty, P.tz};
-    d3 o = tx, d = d3{0, 0, 0};
-    int parent = 0, depth = 0;
-    while (true) {
-        // refill idle lanes from the global slot counter
-        unsigned need = __ballot_sync(FULL, !active) & (more ? FULL : 0u);
-        if (need) {
-            unsigned long long base = 0;
-            int leader = __ffs(need) - 1;
-            if (lane == leader) base = atomicAdd(slot_counter, (unsigned long long)__popc(need));
-            base = __shfl_sync(FULL, base, leader);
-            if (!active) {
-                long long slot = P.slot_begin + (long long)(base + __popc(need & ((1u << lane) - 1u)));
-                if (slot < P.slot_end) {
-                    long long i = slot;
-                    if (P.band > 0) {
-                        long long b = slot / P.band;
-                        if ((b + 1) * P.band <= P.n_rays) i = b * P.band + P.perm[slot - b * P.band];
-                    }
-                    d = P.dirs ? ld3(P.dirs + 3 * i) : fib_dir(i, P.n_rays);
-                    o = tx;
-                    parent = 0;
-                    depth = 0;
-                    active = true;
-                }
-            }
-            if (P.slot_begin + (long long)base + __popc(need) >= P.slot_end) more = false;
-        }
-        if (__ballot_sync(FULL, active) == 0) break;
-        int prim = -1;
-        double t = 0.0;
-        if (active) {
-            Ray r = make_ray(o, d);
-            if (COUNT) {
-                int nv = 0, nt = 0;
-                prim = trace_ray<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t,
-                                        &nv, &nt);
-                my_nodes += nv;
-                my_tris += nt;
-            } else {
-                prim = trace_ray<false>(bvh, r, RAY_EPS, __longlong_as_double(0x7ff0000000000000LL), &t);
-            }
-            ++my_bounces;
-            if (prim == -2) { atomicOr(P.error, 1); prim = -1; }
-            if (prim < 0) active = false;
-        }
-        unsigned hmask = __ballot_sync(FULL, active);
-        if (active) {
-            unsigned long long key = ((unsigned long long)(unsigned)parent << 32) | (unsigned)prim;
-            unsigned peers = __match_any_sync(hmask, key);
-            int leader = __ffs(peers) - 1;
-            int id = 0;
-            if (lane == leader) id = trie_insert(T, parent, prim);
-            id = __shfl_sync(peers, id, leader);
-            parent = id;
-            d3 n = ld3(P.normals + 3 * (long long)prim);
-            if (dot_blas(n, d) > 0.0) n = d3{-n.x, -n.y, -n.z};
-            d3 pt = d3{o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
-            double kk = 2.0 * dot_blas(d, n);
-            d = d3{d.x - kk * n.x, d.y - kk * n.y, d.z - kk * n.z};
-            o = pt;
-            ++depth;
-            if (id < 0 || depth >= P.max_depth) active = false;
-        }
-    }
-    for (int s = 16; s; s >>= 1) my_bounces += __shfl_xor_sync(FULL, my_bounces, s);
-    if (lane == 0 && my_bounces) atomicAdd(P.stats + 0, my_bounces);
-    if (COUNT) {
-        for (int s = 16; s; s >>= 1) {
-            my_nodes += __shfl_xor_sync(FULL, my_nodes, s);
-            my_tris += __shfl_xor_sync(FULL, my_tris, s);
-        }
-        if (lane == 0) {
-            atomicAdd(P.stats + 1, my_nodes);
-            atomicAdd(P.stats + 2, my_tris);
-        }
-    }
-}
-
 // ---- candidate materialization ----------------------------------------------------------
 
 // every occupied slot (a trie node) -> one padded sequence row (row order is

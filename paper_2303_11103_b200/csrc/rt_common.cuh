@@ -79,13 +79,6 @@ __host__ __device__ inline void unpack_bnode(const BNode& nd, int c, float* b) {
     }
 }
 
-// 4-wide node (collapsed from the binary tree): per-axis float4 of the four
-// children's bounds + refs; unused slots hold EMPTY_REF.
-struct __align__(16) BNode4 {
-    float4 lox, loy, loz, hix, hiy, hiz;
-    int4 child;
-    int4 pad;
-};
 constexpr int EMPTY_REF = 0x7fffffff;
 
 // triangle in sorted (BVH) order: FP64 v0, e1, e2 and the global prim id

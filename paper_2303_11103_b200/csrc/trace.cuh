@@ -7,15 +7,9 @@
 // t resolves to the lower global prim id (the reference's brute-force oracle,
 // tests/conftest.py:45-80).  Node boxes are conservative (inflated, rounded
 // outward to float) so the tree never culls a triangle the exact test accepts.
-//
-// RT_WIDE selects the node format walked: 0 = binary child-pair nodes (BNode),
-// 1 = 4-wide nodes (BNode4) collapsed from the same binary tree.
+
 #pragma once
 #include "rt_common.cuh"
-
-#ifndef RT_WIDE
-#define RT_WIDE 0
-#endif
 
 // The per-push stack bound check is compiled out when the builder verified
 // that the tree depth fits the stack (PLOC build: rt_bvh_build fails loudly
@@ -174,15 +168,12 @@ __device__ __forceinline__ bool mt_test(const Ray& r, const TriRec* __restrict__
 }
 
 struct Bvh {
-#if RT_WIDE
-    const BNode4* __restrict__ nodes;
-#else
     const BNode* __restrict__ nodes;
-#endif
     const TriRec* __restrict__ tris;
     const int* __restrict__ skip;   // origin skip table [2 * n_prims] (bvh_ploc.cuh) or null
     int n_prims;
     double origin_limit;   // |o_i| bound for the FP32 filter (else the FP64 one)
+    int* err;              // device error word: bit 0 = traversal stack overflow
 };
 
 // rays leaving a prim at |n.d| >= SKIP_MIN_COS: t_min |n.d| (5e-6 m) clears the
@@ -235,41 +226,6 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
     while (true) {
         if (!ref_is_leaf(cur)) {
             ++nv;
-#if RT_WIDE
-            const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
-            float4 lx = __ldg(np), ly = __ldg(np + 1), lz = __ldg(np + 2);
-            float4 hx = __ldg(np + 3), hy = __ldg(np + 4), hz = __ldg(np + 5);
-            int4 ch = __ldg(reinterpret_cast<const int4*>(np + 6));
-            float t0, t1, t2, t3;
-            bool h0 = box_hit(r, fast, make_float2(lx.x, hx.x), make_float2(ly.x, hy.x), make_float2(lz.x, hz.x),
-                              tmin, best_t, tmin_f, best_tf, t0);
-            bool h1 = box_hit(r, fast, make_float2(lx.y, hx.y), make_float2(ly.y, hy.y), make_float2(lz.y, hz.y),
-                              tmin, best_t, tmin_f, best_tf, t1);
-            bool h2 = box_hit(r, fast, make_float2(lx.z, hx.z), make_float2(ly.z, hy.z), make_float2(lz.z, hz.z),
-                              tmin, best_t, tmin_f, best_tf, t2);
-            bool h3 = box_hit(r, fast, make_float2(lx.w, hx.w), make_float2(ly.w, hy.w), make_float2(lz.w, hz.w),
-                              tmin, best_t, tmin_f, best_tf, t3);
-            const float INF = __int_as_float(0x7f800000);
-            int r0 = ch.x, r1 = ch.y, r2 = ch.z, r3 = ch.w;
-            if (!h0 || r0 == EMPTY_REF) t0 = INF;
-            if (!h1 || r1 == EMPTY_REF) t1 = INF;
-            if (!h2 || r2 == EMPTY_REF) t2 = INF;
-            if (!h3 || r3 == EMPTY_REF) t3 = INF;
-            int nh = (t0 != INF) + (t1 != INF) + (t2 != INF) + (t3 != INF);
-            if (nh > 0) {
-                cx(t0, r0, t1, r1);   // 5-comparator sorting network, nearest first
-                cx(t2, r2, t3, r3);
-                cx(t0, r0, t2, r2);
-                cx(t1, r1, t3, r3);
-                cx(t1, r1, t2, r2);
-                if (sp + 3 > STACK_SIZE) goto overflow;   // reported as an error
-                if (nh > 3) { stack[sp] = make_int2(r3, __float_as_int(t3)); ++sp; }
-                if (nh > 2) { stack[sp] = make_int2(r2, __float_as_int(t2)); ++sp; }
-                if (nh > 1) { stack[sp] = make_int2(r1, __float_as_int(t1)); ++sp; }
-                cur = r0;
-                continue;
-            }
-#else
             const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
             float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
             int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
@@ -296,7 +252,6 @@ __device__ int trace(const Bvh& bvh, const Ray& r, double tmin, double tmax, dou
                 cur = ch.y;
                 continue;
             }
-#endif
         } else {
             int first = leaf_first(cur), cnt = leaf_count(cur);
             nt += cnt;
@@ -338,7 +293,6 @@ overflow:
     return -2;
 }
 
-#if !RT_WIDE
 // "while-while" form of the binary traversal (Aila & Laine 2009): a lane
 // descends internal nodes until it reaches a leaf, then the warp runs leaf
 // tests together, instead of alternating node and FP64 triangle work per
@@ -431,7 +385,6 @@ overflow:
     *t_out = -1.0;
     return -2;
 }
-#endif
 
 // measured on C3: while-while wins for the any-hit occlusion queries (7.4 vs
 // 8.4 ms) and, since the origin skip table and the FFMA2 box filter, for the
@@ -454,19 +407,15 @@ __device__ __forceinline__ int trace_ray(const Bvh& bvh, const Ray& r, double tm
                                          int skip_end = EMPTY_REF) {
 #if RT_HOIST_FAST
     // one FP32-only and one FP64-only copy of the loop: no per-node filter test
-#if !RT_WIDE
     if ((ANY && RT_WW_ANY) || (!ANY && RT_WW_CLOSEST)) {
         if (ray_fast(bvh, r)) return trace_ww<ANY, 1>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos, skip, skip_end);
         return trace_ww<ANY, 2>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos, skip, skip_end);
     }
-#endif
     if (ray_fast(bvh, r)) return trace<ANY, 1>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos, skip, skip_end);
     return trace<ANY, 2>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos, skip, skip_end);
 #else
-#if !RT_WIDE
     if ((ANY && RT_WW_ANY) || (!ANY && RT_WW_CLOSEST))
         return trace_ww<ANY>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos, skip, skip_end);
-#endif
     return trace<ANY>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos, skip, skip_end);
 #endif
 }
@@ -499,7 +448,11 @@ __device__ inline int occluded(const Bvh& bvh, d3 p, d3 q, double eps = RAY_EPS,
     }
     double t;
     int h = trace_ray<true>(bvh, r, eps, dist - eps, &t, nullptr, nullptr, hit_pos, skip, skip_end);
-    return h >= 0 ? 1 : (h == -2 ? 1 : 0);
+    if (h == -2) {   // stack overflow: the answer is unknown, so the call fails (flag bit 0)
+        if (bvh.err) atomicOr(bvh.err, 1);
+        return 1;
+    }
+    return h >= 0 ? 1 : 0;
 }
 
 #ifndef RT_HINT_R

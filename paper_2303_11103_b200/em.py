@@ -164,7 +164,8 @@ def _launch_transfer(bvh, T: PathTable, tx_rows, rx_rows, tx_pat, rx_pat, st, sr
         stt = torch.tensor(st, dtype=torch.float64, device=bvh.device)
         srt = torch.tensor(sr, dtype=torch.float64, device=bvh.device)
     with torch.cuda.device(bvh.device):
-        bvh.ctx.call("rt_transfer", P, T.L, N.ptr(T.order), N.ptr(T.seq), N.ptr(T.verts),
+        bvh.ctx.call("rt_transfer", P, T.L, N.ptr(T.order), N.ptr(T.seq),
+                     N.ptr(getattr(T, "imat", None)), N.ptr(T.verts),
                      N.ptr(T.normals), N.ptr(T.cos), N.ptr(T.length), N.ptr(T.delay),
                      N.ptr(tx_rows), N.ptr(rx_rows), tx_pat, rx_pat, N.ptr(stt), len(st),
                      N.ptr(srt), len(sr), N.ptr(eta), eta.shape[0], float(wavelength),
@@ -199,7 +200,8 @@ class PathCoefficients(torch.autograd.Function):
             srt = torch.tensor(sr, dtype=torch.float64, device=bvh.device)
             with torch.cuda.device(bvh.device):
                 bvh.ctx.call("rt_transfer_bwd", T.n, T.L, N.ptr(T.order), N.ptr(T.seq),
-                             N.ptr(T.verts), N.ptr(T.normals), N.ptr(T.cos), N.ptr(T.length),
+                             N.ptr(getattr(T, "imat", None)), N.ptr(T.verts), N.ptr(T.normals),
+                             N.ptr(T.cos), N.ptr(T.length),
                              N.ptr(T.delay), N.ptr(tx_rows), N.ptr(rx_rows), tx_pat, rx_pat,
                              N.ptr(stt), len(st), N.ptr(srt), len(sr), N.ptr(eta), eta.shape[0],
                              float(wavelength), float(frequency), N.ptr(g), N.ptr(grad_eta),
@@ -293,23 +295,225 @@ def eta_from_params(eps_r, sigma, frequency_hz):
     return torch.stack([eps_r, sigma * (-eta_scale(frequency_hz))], dim=-1)
 
 
-def transfer(ctx: EvalContext, geom, materials, tx_dev, rx_dev, tx_pattern: str, rx_pattern: str,
-             tx_slant: float, rx_slant: float, bvh=None) -> complex:
-    """Complex gain of one path for one element pair (em.py:291-312).
+class DiffComplex(complex):
+    """Value type ``transfer`` returns: a Python complex that also carries the
+    accessors callers of the reference's DiffComplex use (E/autodiff.py:286-360:
+    ``to_complex``, ``abs2``, ``re``/``im``); arithmetic stays in this type."""
 
-    ``geom`` is a PropagationPath (the reference passes its PathGeometry,
-    which is derived from the same path); ``bvh`` supplies the device.
+    @staticmethod
+    def from_complex(z):
+        return DiffComplex(z)
+
+    @staticmethod
+    def expj(phase):
+        return DiffComplex(complex(math.cos(phase), math.sin(phase)))
+
+    def to_complex(self) -> complex:
+        return complex(self.real, self.imag)
+
+    @property
+    def re(self):
+        return self.real
+
+    @property
+    def im(self):
+        return self.imag
+
+    def abs2(self) -> float:
+        return self.real * self.real + self.imag * self.imag
+
+    def __add__(self, o): return DiffComplex(complex.__add__(self, o))
+    def __radd__(self, o): return DiffComplex(complex.__radd__(self, o))
+    def __sub__(self, o): return DiffComplex(complex.__sub__(self, o))
+    def __rsub__(self, o): return DiffComplex(complex.__rsub__(self, o))
+    def __mul__(self, o): return DiffComplex(complex.__mul__(self, o))
+    def __rmul__(self, o): return DiffComplex(complex.__rmul__(self, o))
+    def __truediv__(self, o): return DiffComplex(complex.__truediv__(self, o))
+    def __rtruediv__(self, o): return DiffComplex(complex.__rtruediv__(self, o))
+    def __neg__(self): return DiffComplex(complex.__neg__(self))
+
+
+@dataclass
+class PathGeometry:
+    """Geometry of one path ready for field transport (E/em.py:232-243)."""
+
+    vertices: list
+    seg_dirs: list
+    length: float
+    delay: float
+    k_dep: tuple
+    k_arr: tuple
+    normals: list
+    cos_incidence: list
+
+
+def _unit(v):
+    n = math.sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2])
+    return (v[0] / n, v[1] / n, v[2] / n)
+
+
+def _dirs(verts):
+    return [_unit((b[0] - a[0], b[1] - a[1], b[2] - a[2])) for a, b in zip(verts[:-1], verts[1:])]
+
+
+def geometry_from_path(path) -> PathGeometry:
+    """Frozen geometry of a traced path (E/em.py:246-255)."""
+    verts = [tuple(float(x) for x in v) for v in path.vertices]
+    dirs = _dirs(verts)
+    return PathGeometry(verts, dirs, float(path.length_m), float(path.delay_s), dirs[0], dirs[-1],
+                        [tuple(float(x) for x in n) for n in path.normals],
+                        [float(c) for c in path.cos_incidence])
+
+
+def _chain_points(tx, rx, planes):
+    """Interaction points of a reflection chain (the image construction of
+    E/tracer.py:71-102): images of tx through the planes in order, then from rx
+    backwards each point is where the line to the next image meets its plane.
+    None when a line runs parallel to its plane (|seg . n| < 1e-15)."""
+    dot = lambda a, b: a[0] * b[0] + a[1] * b[1] + a[2] * b[2]  # noqa: E731
+    img = [tx]
+    for n, c in planes:
+        p = img[-1]
+        k2 = 2.0 * (dot(p, n) - c)
+        img.append((p[0] - n[0] * k2, p[1] - n[1] * k2, p[2] - n[2] * k2))
+    pts = [None] * len(planes)
+    cur = rx
+    for k in reversed(range(len(planes))):
+        n, c = planes[k]
+        tgt = img[k + 1]
+        seg = (tgt[0] - cur[0], tgt[1] - cur[1], tgt[2] - cur[2])
+        den = dot(seg, n)
+        if abs(den) < 1e-15:
+            return None
+        f = (c - dot(cur, n)) / den
+        cur = (cur[0] + seg[0] * f, cur[1] + seg[1] * f, cur[2] + seg[2] * f)
+        pts[k] = cur
+    return pts
+
+
+def geometry_for_positions(path, tx_pos, rx_pos) -> PathGeometry:
+    """Geometry of the same topology for moved endpoints (E/em.py:258-282):
+    interaction points re-mirrored through the path's planes, with the plane
+    offset taken at the stored interaction vertex.  Host floats; gradients
+    w.r.t. positions go through ``path_coefficients_geo`` (rt_transfer_jvp)."""
+    normals = [tuple(float(x) for x in n) for n in path.normals]
+    planes = []
+    for k, n in enumerate(normals):
+        v = path.vertices[k + 1]
+        planes.append((n, n[0] * float(v[0]) + n[1] * float(v[1]) + n[2] * float(v[2])))
+    tx = tuple(float(x) for x in tx_pos)
+    rx = tuple(float(x) for x in rx_pos)
+    points = _chain_points(tx, rx, planes)
+    if points is None:
+        raise EmError("path geometry degenerated while differentiating positions")
+    verts = [tx] + [tuple(float(x) for x in p) for p in points] + [rx]
+    dirs = _dirs(verts)
+    length = 0.0
+    for a, b in zip(verts[:-1], verts[1:]):
+        d = (b[0] - a[0], b[1] - a[1], b[2] - a[2])
+        length = length + math.sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2])
+    cosines = [-(dirs[k][0] * n[0] + dirs[k][1] * n[1] + dirs[k][2] * n[2]) for k, n in enumerate(normals)]
+    return PathGeometry(verts, dirs, length, length / SPEED_OF_LIGHT, dirs[0], dirs[-1], normals, cosines)
+
+
+def path_geometry(ctx: EvalContext, path, tx_dev, rx_dev) -> PathGeometry:
+    """E/em.py:285-288: moved endpoints re-derive the geometry, else it is frozen."""
+    moved = [ctx.positions.get(d.name) for d in (tx_dev, rx_dev)]
+    if any(p is not None for p in moved):
+        tp = moved[0] if moved[0] is not None else tx_dev.position
+        rp = moved[1] if moved[1] is not None else rx_dev.position
+        return geometry_for_positions(path, [float(x) for x in tp], [float(x) for x in rp])
+    return geometry_from_path(path)
+
+
+class _DeviceHandle:
+    """The library context ``transfer`` runs on (no scene is needed: materials
+    arrive per interaction through rt_transfer's interaction_mat)."""
+
+    _by_device = {}
+
+    def __init__(self, device):
+        self.device = device
+        self.ctx = N.acquire_context(device)
+
+    @classmethod
+    def get(cls):
+        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+        if dev is None:
+            raise N.NativeError("no CUDA device: the B200 path has no CPU fallback")
+        h = cls._by_device.get(dev.index)
+        if h is None:
+            h = cls._by_device[dev.index] = cls(dev)
+        return h
+
+
+def transfer(ctx: EvalContext, geom, materials, tx_dev, rx_dev, tx_pattern: str, rx_pattern: str,
+             tx_slant: float, rx_slant: float):
+    """Complex gain of one path for one element pair — E/em.py:291-312's
+    signature and meaning: ``geom`` is the PathGeometry (``geometry_from_path``
+    / ``path_geometry``; a PropagationPath is accepted too) and ``materials``
+    the material name of each interaction (``path_materials``).
+
+    a = lambda/(4 pi L) * <rx field | prod_k R_k | tx field> * exp(-j 2 pi f tau),
+    one rt_transfer launch.  Returns a ``DiffComplex``; when a material value in
+    ``ctx.material_values`` is a tensor that requires grad, returns instead a
+    0-d complex128 tensor whose backward runs the adjoint (rt_transfer_bwd).
     """
-    if bvh is None:
-        raise EmError("transfer needs the Bvh of the scene (bvh=...)")
-    T = _table_from_paths([geom], bvh, [geom.tx], [geom.rx])
-    a = _launch_transfer(bvh, T, _rows_tensor([ctx.rotation_rows(tx_dev)], bvh.device),
-                         _rows_tensor([ctx.rotation_rows(rx_dev)], bvh.device),
-                         pattern_id(tx_pattern), pattern_id(rx_pattern), [float(tx_slant)],
-                         [float(rx_slant)], ctx.eta_table(bvh), ctx.scene.wavelength,
-                         ctx.scene.frequency_hz)
-    v = a[0, 0, 0].cpu().numpy()
-    return complex(v[0], v[1])
+    if hasattr(geom, "length_m"):
+        geom = geometry_from_path(geom)
+    mats = list(materials)
+    k = len(mats)
+    if k != len(geom.normals):
+        raise EmError("one material per interaction is required")
+    h = _DeviceHandle.get()
+    dev = h.device
+    scene = ctx.scene
+    names = list(dict.fromkeys(mats))
+    rows, track = [], False
+    for name in names:
+        m = scene.materials[name]
+        ov = ctx.material_values.get(name)
+        e, sg = material_params(m, scene.frequency_hz, None if ov is None else ov[0],
+                                None if ov is None else ov[1])
+        if isinstance(e, torch.Tensor) or isinstance(sg, torch.Tensor):
+            track = track or any(isinstance(v, torch.Tensor) and v.requires_grad for v in (e, sg))
+            e = torch.as_tensor(e, dtype=torch.float64, device=dev)
+            sg = torch.as_tensor(sg, dtype=torch.float64, device=dev)
+            rows.append(eta_from_params(e, sg, scene.frequency_hz))
+        else:
+            rows.append(torch.tensor([float(e), float(sg) * (-eta_scale(scene.frequency_hz))],
+                                     dtype=torch.float64, device=dev))
+    eta = torch.stack(rows) if rows else torch.tensor([[1.0, 0.0]], dtype=torch.float64, device=dev)
+    L = max(k, 1)
+    verts = np.zeros((1, L + 2, 3))
+    verts[0, :k + 2] = np.asarray(geom.vertices, dtype=np.float64).reshape(k + 2, 3)
+    nrm = np.zeros((1, L, 3))
+    cos = np.zeros((1, L))
+    imat = np.zeros((1, L), dtype=np.int32)
+    seq = np.full((1, L), -1, dtype=np.int32)
+    if k:
+        nrm[0, :k] = np.asarray(geom.normals, dtype=np.float64).reshape(k, 3)
+        cos[0, :k] = np.asarray(geom.cos_incidence, dtype=np.float64)
+        imat[0, :k] = [names.index(m) for m in mats]
+        seq[0, :k] = np.arange(k)
+    t = lambda a, dt=torch.float64: torch.as_tensor(a, dtype=dt, device=dev).contiguous()  # noqa: E731
+    z3 = t(np.zeros((1, 3)))
+    T = PathTable(L, [getattr(tx_dev, "name", "tx")], [getattr(rx_dev, "name", "rx")],
+                  tx=t([0], torch.int32), rx=t([0], torch.int32), cand=t([0], torch.int32),
+                  order=t([k], torch.int8), seq=t(seq, torch.int32), verts=t(verts),
+                  length=t([float(geom.length)]), delay=t([float(geom.delay)]), kdep=z3, karr=z3,
+                  normals=t(nrm), cos=t(cos))
+    T.imat = t(imat, torch.int32)
+    as_float = lambda r: tuple(tuple(float(x) for x in row) for row in r)  # noqa: E731
+    tx_rows = _rows_tensor([as_float(ctx.rotation_rows(tx_dev))], dev)
+    rx_rows = _rows_tensor([as_float(ctx.rotation_rows(rx_dev))], dev)
+    with torch.cuda.device(dev):
+        a = path_coefficients(h, T, eta, tx_rows, rx_rows, tx_pattern, rx_pattern, [tx_slant],
+                              [rx_slant], scene.wavelength, scene.frequency_hz)[0, 0, 0]
+    if track:
+        return a
+    v = torch.view_as_real(a.detach()).cpu().numpy()
+    return DiffComplex(complex(float(v[0]), float(v[1])))
 
 
 # -- channel gains for full arrays -----------------------------------------------------------

@@ -214,55 +214,89 @@ def nmse_loss(h_pred, h_true):
     return float(np.vdot(err, err).real) / norm2
 
 
-def _lr_for(leaf, config):
-    if leaf.endswith(":sigma"):
+_ANGLE_LEAVES = ("yaw", "pitch", "roll")
+
+
+def _leaf_kind(name):
+    return name.rsplit(":", 1)[-1]
+
+
+def _leaf_rate(name, config):
+    """Step size of one leaf: sigma and angle leaves have their own rates."""
+    kind = _leaf_kind(name)
+    if kind == "sigma":
         return config.lr_sigma
-    if leaf.split(":")[-1] in ("yaw", "pitch", "roll"):
-        return config.lr_angle
-    return config.lr
+    return config.lr_angle if kind in _ANGLE_LEAVES else config.lr
 
 
-def _project_materials(values):
-    for k in values:
-        if k.endswith(":eps_r") and values[k] < 1.0:
-            values[k] = 1.0
-        elif k.endswith(":sigma") and values[k] < 0.0:
-            values[k] = 0.0
+def _to_feasible(point):
+    """Clamp material leaves into their physical range in place: eps_r >= 1,
+    sigma >= 0 (the reference's projection, E/optim.py:195-200)."""
+    for name, v in point.items():
+        kind = _leaf_kind(name)
+        if kind == "eps_r" and v < 1.0:
+            point[name] = 1.0
+        elif kind == "sigma" and v < 0.0:
+            point[name] = 0.0
+    return point
 
 
-def _descend(values, loss0, grads, loss_fn, config, sign, scale=1.0):
-    """Armijo-backtracked step (optim.py:203-234); sign -1 descends, +1 ascends."""
-    direction = {k: _lr_for(k, config) * grads.get(k, 0.0) for k in values}
-    slope = sum(direction[k] * grads.get(k, 0.0) for k in values)
-    if slope == 0.0:
-        return dict(values), scale
+class ArmijoStep:
+    """Projected gradient step with backtracking (semantics of E/optim.py:203-234).
 
-    def stepped(s):
-        new = {k: values[k] + sign * s * direction[k] for k in values}
-        _project_materials(new)
-        return new
+    ``sign`` = -1 minimises, +1 maximises.  The trial scale starts at the
+    carried ``scale`` and halves until the objective improves by at least
+    1e-4 * scale * (d . g); a step accepted at its first trial doubles the
+    carried scale (capped at 1e9).  If no trial above 1e-10 is accepted, the
+    point is kept and the scale resets to 1.  Without line search a unit step
+    is taken unconditionally.
+    """
 
-    if not config.line_search:
-        return stepped(1.0), scale
-    first = True
-    while scale > 1e-10:
-        cand = stepped(scale)
-        f = float(loss_fn(cand))
-        if sign * (f - loss0) >= 1e-4 * scale * slope:
-            return cand, min(scale * 2.0, 1e9) if first else scale
-        scale *= 0.5
-        first = False
-    return dict(values), 1.0
+    ARMIJO_C = 1e-4
+    MIN_SCALE = 1e-10
+    MAX_SCALE = 1e9
+
+    def __init__(self, config, sign):
+        self.config = config
+        self.sign = sign
+
+    def __call__(self, point, f0, grads, objective, scale=1.0):
+        names = list(point)
+        g = [grads.get(n, 0.0) for n in names]
+        d = [_leaf_rate(n, self.config) * gi for n, gi in zip(names, g)]
+        slope = 0.0
+        for di, gi in zip(d, g):   # leaf order, left to right
+            slope += di * gi
+        if slope == 0.0:
+            return dict(point), scale
+
+        def trial(s):
+            step = self.sign * s
+            return _to_feasible({n: point[n] + step * di for n, di in zip(names, d)})
+
+        if not self.config.line_search:
+            return trial(1.0), scale
+        s, tries = scale, 0
+        while s > self.MIN_SCALE:
+            cand = trial(s)
+            gain = self.sign * (float(objective(cand)) - f0)
+            if gain >= self.ARMIJO_C * s * slope:
+                return cand, (min(2.0 * s, self.MAX_SCALE) if tries == 0 else s)
+            s *= 0.5
+            tries += 1
+        return dict(point), 1.0
 
 
-def _converged(losses, config):
+def _plateaued(history, config):
+    """True once the loss moved by less than rel_tol (relative) over the last
+    tol_window iterations."""
     w = config.tol_window
-    if len(losses) <= w:
+    if len(history) < w + 1:
         return False
-    ref = abs(losses[-w - 1])
-    if ref == 0.0:
-        return abs(losses[-1]) == 0.0
-    return abs(losses[-1] - losses[-w - 1]) / ref < config.rel_tol
+    then, now = history[-(w + 1)], history[-1]
+    if then == 0.0:
+        return now == 0.0
+    return abs(now - then) / abs(then) < config.rel_tol
 
 
 def generate_dataset(scene, positions=None, num_subcarriers=128, subcarrier_spacing_hz=30e3,
@@ -334,8 +368,8 @@ def learn_materials(scene, dataset: Dataset, config: OptimConfig | None = None,
             grads[f"mat:{n}:eps_r"] = float(e.grad) if e.grad is not None else 0.0
             grads[f"mat:{n}:sigma"] = float(s.grad) if s.grad is not None else 0.0
         log.append(it, loss_val, values)
-        values, scale = _descend(values, loss_val, grads, loss_fn, config, sign=-1.0, scale=scale)
-        if _converged(log.losses, config):
+        values, scale = ArmijoStep(config, -1.0)(values, loss_val, grads, loss_fn, scale)
+        if _plateaued(log.losses, config):
             break
     log.final_values = dict(values)
     return log
@@ -413,9 +447,8 @@ def optimize_orientation(scene, region, config: OptimConfig | None = None, tx_na
         torch.log(obj).backward()
         grads = dict(zip(keys, (float(g) for g in ypr.grad)))
         log.append(it, obj_val, values)
-        values, scale = _descend(values, math.log(obj_val), grads, log_objective, config,
-                                 sign=+1.0, scale=scale)
-        if _converged(log.losses, config):
+        values, scale = ArmijoStep(config, +1.0)(values, math.log(obj_val), grads, log_objective, scale)
+        if _plateaued(log.losses, config):
             break
     log.final_values = dict(values)
     return log

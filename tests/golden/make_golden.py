@@ -327,6 +327,53 @@ def artifacts_case():
     print("artifacts: done", flush=True)
 
 
+def transfer_case():
+    """The em.py:291-312 ``transfer`` boundary called exactly as the reference's
+    own callers do: optim._central_gains (optim.py:249-258: path_materials +
+    geometry_from_path + transfer with the arrays' first slants) and
+    channel.point_path_gain's probe loop (channel.py:214-232, path_geometry);
+    plus the Tape gradient of sum |a|^2 w.r.t. every material leaf."""
+    from emtrace.optim import _central_gains
+    from emtrace.channel import probe_receiver
+    from emtrace.em import EvalContext, path_geometry, path_materials, transfer
+    sc = to_ref(_canyon_small())
+    tree = accel.build(sc)
+    tx = sc.transmitters[0]
+    out = {"scene": np.array(scene_json(sc))}
+    seqs, central, probes = [], [], []
+    for ri, rx in enumerate(sc.receivers[:3]):
+        paths = E.compute_paths_between(sc, tree, tx, rx, 2, "exhaustive", 4096)
+        g = _central_gains(sc, tree, EvalContext(sc), tx, rx, paths)
+        for p, z in zip(paths, g):
+            seqs.append((ri,) + tuple(p.seq) + (-1,) * (2 - p.order))
+            central.append(z.to_complex())
+        probe = probe_receiver(np.asarray(rx.position) + np.array([0.5, -0.25, 0.0]))
+        ctx = EvalContext(sc)
+        ppaths = E.compute_paths_between(sc, tree, tx, probe, 2, "exhaustive", 4096)
+        for p in ppaths:
+            mats = path_materials(sc, tree, p)
+            geom = path_geometry(ctx, p, tx, probe)
+            for pat in ("_probe_theta", "_probe_phi"):
+                probes.append(transfer(ctx, geom, mats, tx, probe, sc.tx_array.pattern, pat,
+                                       sc.tx_array.slants[0], 0.0).to_complex())
+    tape = Tape()
+    names = sorted(sc.materials)
+    leaves = {n: (tape.leaf(float(sc.materials[n].eps_r), f"{n}:eps_r"),
+                  tape.leaf(float(sc.materials[n].sigma), f"{n}:sigma")) for n in names}
+    ctx = EvalContext(sc, material_values=leaves)
+    rx = sc.receivers[0]
+    paths = E.compute_paths_between(sc, tree, tx, rx, 2, "exhaustive", 4096)
+    loss = 0.0
+    for z in _central_gains(sc, tree, ctx, tx, rx, paths):
+        loss = loss + z.abs2()
+    grads = tape.gradient(loss)
+    out.update(seqs=np.array(seqs, dtype=np.int32), central=np.array(central),
+               probes=np.array(probes), loss=loss.value, grad_names=np.array(sorted(grads)),
+               grads=np.array([grads[k] for k in sorted(grads)]))
+    np.savez_compressed(os.path.join(HERE, "transfer.npz"), **out)
+    print("transfer: paths", len(central), "probe transfers", len(probes), flush=True)
+
+
 def main(which=None):
     cases = {
         "soup": soup_case,
@@ -356,6 +403,7 @@ def main(which=None):
         "drivers": drivers_case,
         "explicit": explicit_case,
         "artifacts": artifacts_case,
+        "transfer": transfer_case,
     }
     for k, fn in cases.items():
         if which and k not in which:

@@ -81,3 +81,21 @@ def test_coverage(golden, case):
         assert np.array_equal(got, g[f"cov{i}_gains"]), case
         i += 1
     assert i > 0
+
+
+def test_transfer_central_gains(golden):
+    """Oracle transfer vs the reference's optim._central_gains values."""
+    g = golden("transfer")
+    sc = golden_scene(g)
+    b = O.Bvh(O.SceneArrays(sc))
+    eta = b.sa.eta_table(sc, None)
+    tx = sc.transmitters[0]
+    got, seqs = [], []
+    for ri, rx in enumerate(sc.receivers[:3]):
+        for p in O.compute_paths_between(sc, b, tx, rx, 2, "exhaustive"):
+            seqs.append((ri,) + tuple(p.seq) + (-1,) * (2 - p.order))
+            got.append(O.transfer(b, eta, p, sc.tx_array.pattern, sc.tx_array.slants[0],
+                                  O.rotation_rows(*tx.orientation), sc.rx_array.pattern,
+                                  sc.rx_array.slants[0], O.rotation_rows(*rx.orientation)))
+    assert np.array_equal(np.array(seqs, dtype=np.int32), g["seqs"])
+    assert np.abs(np.array(got) - g["central"]).max() <= 1e-12 * np.abs(g["central"]).max()

@@ -1,5 +1,5 @@
 """Launch time / node visits of the C3 city for several transmitter positions
-(tree-quality A/B across libraries: B200RT_LIB=... python tools/tx_sweep.py)."""
+(tree-quality A/B across libraries: python tools/ab_run.py libb200rt_X.so tools/tx_sweep.py)."""
 import os
 import sys
 
@@ -34,7 +34,7 @@ def main():
         lib.rt_set_profiling(b.ctx.h, 0)
         out.append(round(float(ms[0]), 2))
         tot += float(ms[0])
-    print(os.environ.get("B200RT_LIB", "base"), "launch ms per tx:", out, "sum %.2f" % tot)
+    print(os.path.basename(P._native.LIB_PATH), "launch ms per tx:", out, "sum %.2f" % tot)
 
 
 if __name__ == "__main__":
