@@ -91,17 +91,25 @@ def workload_name(args):
             f"{args.cells}x{args.cells} cells @{args.cell_size:g}m")
 
 
-def l2_read_bandwidth(bvh):
-    """Measured L2-resident read bandwidth (GB/s): rt_l2_probe streams a 48 MB
-    buffer (fits the 126 MB L2) 64 times in one persistent kernel with 16-byte
-    loads; the traversal's working set (nodes + triangles) lives in L2."""
+MICROBENCH = (("fp32_tflops", 0), ("fp64_tflops", 1), ("issue_gwarp_inst_per_s", 2),
+              ("l1_read_gbs", 3), ("l2_read_gbs", 4))
+
+
+def measured_peaks(bvh):
+    """Roofline denominators measured live on this GPU (rt_microbench,
+    csrc/microbench.cuh): FP32 / FP64 FMA throughput, warp-instruction issue
+    rate (imm-form FFMA chains: one instruction per SMSP per cycle), L1- and
+    L2-resident read bandwidth.  HBM comes from MEASURED_PEAKS.json."""
     import ctypes
-    out = ctypes.c_double()
-    bvh.ctx.call("rt_l2_probe", ctypes.c_int64(48 << 20), 64, ctypes.byref(out), bvh.ctx.stream)
-    return out.value
+    out = {}
+    for name, kind in MICROBENCH:
+        v = ctypes.c_double()
+        bvh.ctx.call("rt_microbench", kind, ctypes.byref(v), bvh.ctx.stream)
+        out[name] = v.value
+    return out
 
 
-TRAFFIC_JSON = "profiles/r01_traffic.json"
+TRAFFIC_JSON = "profiles/r02_traffic.json"
 
 
 def committed_traffic(args, field="dram_bytes_per_launch"):
@@ -213,9 +221,12 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # rank count visible in the NCCL log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
@@ -291,21 +302,29 @@ def run_b200(args):
     if not args.no_e2e:
         e2e = run_e2e(args, sc, grid, rank, world, dev, flush)
 
+    peaks_live = measured_peaks(bvh)
+    c2 = c4 = None
+    if not args.no_c2:
+        c2 = c2_latency(args, rank, world)
+        c4 = c4_latency(args, rank, world)
     if rank != 0:
         return None
     import json as _json
     peaks = _json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    l2_bw = l2_read_bandwidth(bvh)
-    traffic = committed_traffic(args)
     launch_ms = stage_ms[0]
     bounces_per_launch = bounces_local / args.steps
-    alg_bytes = bounces_per_launch * (BYTES_PER_NODE * per_bounce_nodes + BYTES_PER_TRI * per_bounce_tris)
-    achieved = alg_bytes / (launch_ms / 1e3) / 1e9 if launch_ms > 0 else None
+    bytes_per_bounce = BYTES_PER_NODE * per_bounce_nodes + BYTES_PER_TRI * per_bounce_tris
+    t_launch = launch_ms / 1e3 if launch_ms > 0 else None
     names = ["launch", "cand_sort", "footprint", "solve", "validate", "rec_sort", "merge", "los",
              "trie_seq"]
     stage = {n: round(float(stage_ms[i]), 3) for i, n in enumerate(names)}
+    roof = roofline(args, peaks_live, hbm_peak, bounces_per_launch, bytes_per_bounce,
+                    per_bounce_nodes, per_bounce_tris, t_launch)
+    roof.update({"nodes_per_bounce": per_bounce_nodes, "tris_per_bounce": per_bounce_tris,
+                 "simd_efficiency": simd, "kernel_ms": launch_ms,
+                 "kernel_share": launch_ms / ms_per_step})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -319,93 +338,136 @@ def run_b200(args):
         "ray_bounces_per_step": bounces_all / args.steps,
         "stage_ms": stage,
         "stats": stats,
-        "roofline": {"bound": "hbm", "kernel": "k_launch",
-                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
-                     "traffic_source": TRAFFIC_JSON if traffic is not None else None,
-                     "bytes_per_bounce": BYTES_PER_NODE * per_bounce_nodes + BYTES_PER_TRI * per_bounce_tris,
-                     "nodes_per_bounce": per_bounce_nodes, "tris_per_bounce": per_bounce_tris,
-                     "simd_efficiency": simd,
-                     "kernel_ms": launch_ms, "kernel_share": launch_ms / ms_per_step,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
-                     "l2_peak_gbs": l2_bw, "l2_frac": (achieved / l2_bw) if achieved else None,
-                     "l2_peak_source": "measured in bench.py: rt_l2_probe streams a 48 MB "
-                                       "L2-resident buffer with 16-byte L2-only loads",
-                     "north_star_roofline": "T* = max(bytes/BW_L2, FP32 flops/peak); "
-                                            "frac = T*/T_kernel = l2_frac (L1 hits let it exceed 1)",
-                     "limiter": "instruction issue, not bandwidth: ncu (profiles/r01_ncu_full.md) shows "
-                                "~75% issue slots busy, L1 hit ~95%, DRAM ~0.01% of peak; "
-                                "DRAM traffic per launch (traffic) is ~1e-4 of the algorithmic bytes"},
+        "roofline": roof,
+        "peaks_measured": dict(peaks_live, hbm_gbs=hbm_peak,
+                               hbm_source="MEASURED_PEAKS.json" if peaks else "fallback"),
         "clocks": clocks.summary(),
         "gpu_launches": int(round(launches)),
     }
-    # the binding roofline of k_launch: warp-instruction issue (4 per SM per cycle)
-    insts = committed_traffic(args, "warp_instructions_per_launch")
-    if insts and launch_ms > 0:
-        import torch
-        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-        clk = line["clocks"].get("sm_mhz") or line["clocks"].get("sm_max_mhz") or 1965.0
-        peak = n_sm * 4 * float(clk) * 1e6
-        line["roofline"]["issue"] = {
-            "bound": "warp-instruction issue", "unit": "warp-instructions/s",
-            "achieved": insts / (launch_ms / 1e3), "peak": peak, "frac": insts / (launch_ms / 1e3) / peak,
-            "warp_instructions_per_launch": insts,
-            "warp_instructions_per_bounce": insts / max(bounces_per_launch, 1.0),
-            "source": TRAFFIC_JSON + " (ncu inst_executed of this workload); peak = SMs x 4 "
-                      "schedulers x SM clock under load"}
     if e2e:
         line["e2e"] = e2e
-    if not args.no_c2:
-        line["c2_paths_cir"] = c2_latency(args)
-        line["c4_material_grad"] = c4_latency(args)
+    if c2 is not None:
+        line["c2_paths_cir"] = c2
+        line["c4_material_grad"] = c4
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args, sc, tx, grid, samples=1)
     return line
 
 
-def c2_latency(args):
+def roofline(args, pk, hbm_peak, bounces, bytes_per_bounce, nodes_pb, tris_pb, t_launch):
+    """Roofline of the dominant kernel (k_launch).
+
+    Primary bound = warp-instruction issue, the one that binds:
+    achieved = ncu inst_executed of this workload (committed in TRAFFIC_JSON,
+    per bounce) x this run's bounces / this run's kernel time (CUDA events);
+    peak = the issue rate measured live by rt_microbench.  Secondary fractions:
+    L1 (algorithmic bytes / measured L1-resident read peak), L2 and DRAM (ncu
+    lts / dram bytes per launch, committed, / measured peaks), FP32 (box +
+    triangle flops / measured FP32 FMA peak) and the north-star traversal
+    roofline T* = max(bytes / BW_L2, flops / FP32 peak) / T_kernel."""
+    if not t_launch:
+        return {"bound": None}
+    alg = bounces * bytes_per_bounce
+    flops = bounces * (14.0 * nodes_pb * 2 + 40.0 * tris_pb)   # SURVEY 8d: 14 per box test, 2 boxes per node
+    insts = committed_traffic(args, "warp_instructions_per_launch")
+    lts = committed_traffic(args, "lts_bytes_per_launch")
+    dram = committed_traffic(args, "dram_bytes_per_launch")
+    out = {}
+    sec = {}
+    sec["l1"] = {"achieved": alg / t_launch / 1e9, "peak": pk["l1_read_gbs"], "unit": "GB/s",
+                 "frac": alg / t_launch / 1e9 / pk["l1_read_gbs"],
+                 "bytes": "algorithmic: 64 B per node visit + 80 B per triangle test"}
+    if lts is not None:
+        sec["l2"] = {"achieved": lts / t_launch / 1e9, "peak": pk["l2_read_gbs"], "unit": "GB/s",
+                     "frac": lts / t_launch / 1e9 / pk["l2_read_gbs"],
+                     "bytes": "ncu lts__t_bytes per launch (" + TRAFFIC_JSON + ")"}
+    if dram is not None:
+        sec["hbm"] = {"achieved": dram / t_launch / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": dram / t_launch / 1e9 / hbm_peak,
+                      "bytes": "ncu dram__bytes read+write per launch (" + TRAFFIC_JSON + ")"}
+    sec["fp32"] = {"achieved": flops / t_launch / 1e12, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
+                   "frac": flops / t_launch / 1e12 / pk["fp32_tflops"]}
+    t_star = max(alg / (pk["l2_read_gbs"] * 1e9), flops / (pk["fp32_tflops"] * 1e12))
+    sec["north_star_traversal"] = {"t_star_ms": 1e3 * t_star, "t_kernel_ms": 1e3 * t_launch,
+                                   "frac": t_star / t_launch,
+                                   "note": "T* = max(alg bytes / BW_L2, FP32 flops / peak); above 1 "
+                                           "because L1 serves ~98% of the node fetches"}
+    if insts is not None:
+        ach = insts / t_launch / 1e9
+        out = {"bound": "issue", "kernel": "k_launch", "achieved": ach,
+               "peak": pk["issue_gwarp_inst_per_s"], "unit": "Gwarp-inst/s",
+               "frac": ach / pk["issue_gwarp_inst_per_s"], "traffic": dram,
+               "warp_instructions_per_launch": insts,
+               "warp_instructions_per_bounce": insts / max(bounces, 1.0),
+               "achieved_source": TRAFFIC_JSON + " ncu inst_executed of this workload / this run's "
+                                                 "k_launch CUDA-event time",
+               "peak_source": "rt_microbench kind 2 measured in this run (imm-form FFMA chains)"}
+    else:   # no committed capture of this workload: the live L1-bytes bound
+        out = dict(sec["l1"], bound="l1", kernel="k_launch", traffic=dram,
+                   peak_source="rt_microbench kind 3 measured in this run")
+    out["traffic_source"] = TRAFFIC_JSON if dram is not None else None
+    out["bytes_per_bounce"] = bytes_per_bounce
+    out["secondary"] = sec
+    return out
+
+
+def c2_latency(args, rank=0, world=1):
     """BASELINE metric part 2: compute_paths + CIR latency at C2 (street canyon,
     2,002 tris, 8x8 tr38901 array, 256 rx, depth 3, 1e6 rays) through the public
-    API, host arrays in, host CIR out (wall clock, device synchronised)."""
+    API, host arrays in, host CIR out (wall clock, device synchronised).  With
+    N ranks: rays and receivers sharded, CIR rows all-gathered
+    (parallel.compute_paths_cir); the latency is the max over ranks."""
     import torch
     import paper_2303_11103_b200 as P
-    from paper_2303_11103_b200 import scenes
+    from paper_2303_11103_b200 import parallel, scenes
     sc = scenes.street_canyon(n_per_row=100)
     times = []
     out = None
     for i in range(args.warmup + args.steps):
+        parallel.barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         bvh = P.build(sc)
-        ps = P.compute_paths(sc, bvh, 3, method="fibonacci", num_rays=1_000_000)
-        cir = P.build_cir(P.compute_gains(sc, bvh, ps))
+        if world == 1:
+            ps = P.compute_paths(sc, bvh, 3, method="fibonacci", num_rays=1_000_000)
+            cir = P.build_cir(P.compute_gains(sc, bvh, ps))
+        else:
+            cir, ps = parallel.compute_paths_cir(sc, bvh, 3, "fibonacci", 1_000_000, rank, world)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         if i >= args.warmup:
             times.append(t1 - t0)
         out = (ps.table.n, list(cir.a.shape), bvh.num_prims)
-    return {"metric": "compute_paths+CIR latency", "value_ms": 1e3 * float(np.median(times)),
-            "unit": "ms", "higher_is_better": False, "paths": out[0], "cir_a_shape": out[1],
+    med = parallel.max_over_ranks(float(np.median(times)), world)
+    paths = int(parallel.sum_over_ranks(float(out[0]), world))
+    return {"metric": "compute_paths+CIR latency", "value_ms": 1e3 * med,
+            "unit": "ms", "higher_is_better": False, "paths": paths, "cir_a_shape": out[1],
             "triangles": out[2], "rx": 256, "tx_elements": 64, "num_rays": 1_000_000, "max_depth": 3,
-            "includes": "build(scene) H2D + launch + paths + gains + CIR D2H"}
+            "ranks": world,
+            "includes": "build(scene) H2D + launch + paths + gains + CIR D2H"
+                        + (" + candidate all_gather + CIR row all_gather" if world > 1 else "")}
 
 
-def c4_latency(args):
+def c4_latency(args, rank=0, world=1):
     """Config 4 (learning radio materials): one gradient step of the NMSE
     frequency-response loss w.r.t. (eps_r, sigma) of the 4 trainable materials
     through the hand-written adjoint — calib scene, 400 receivers, 128
-    subcarriers at 30 kHz, depth 2, paths frozen (optim.MaterialProblem)."""
+    subcarriers at 30 kHz, depth 2, paths frozen (optim.MaterialProblem).
+    With N ranks the records are sharded and [loss, grads] all-reduced
+    (parallel.material_loss_and_grad semantics, timed per step here)."""
     import torch
-    from paper_2303_11103_b200 import optim, scenes
+    from paper_2303_11103_b200 import optim, parallel, scenes
     truth, init = scenes.calib_scene(truth=True), scenes.calib_scene(truth=False)
     pos = np.array([d.position for d in truth.devices if d.kind == "rx"], dtype=np.float64)
     ds = optim.generate_dataset(truth, pos, 128, 30e3, max_depth=2)
     h = np.array([r.h for r in ds.records])
     keep = (np.abs(h) ** 2).sum(-1) > 0.0   # receivers inside buildings have no response
     pos, h = pos[keep], h[keep]
+    n_rec = len(pos)
+    mine = list(range(rank, n_rec, world))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    prob = optim.MaterialProblem(init, pos, h, 2, 128, 30e3)
+    prob = optim.MaterialProblem(init, pos[mine], h[mine], 2, 128, 30e3)
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
     times, grads, loss = [], {}, None
@@ -413,23 +475,32 @@ def c4_latency(args):
         vals = {n: tuple(torch.tensor(float(getattr(init.materials[n], k)), dtype=torch.float64,
                                       device=prob.bvh.device, requires_grad=True)
                          for k in ("eps_r", "sigma")) for n in prob.names}
+        parallel.barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        lo = prob.loss(vals)
+        lo = prob.loss(vals) * (len(mine) / n_rec)
         lo.backward()
-        grads = {f"{n}:{k}": float(v.grad) for n, pair in vals.items() for k, v in zip(("eps_r", "sigma"), pair)}
-        loss = float(lo.detach())
+        vec = torch.stack([lo.detach()] + [v.grad for pair in vals.values() for v in pair])
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(vec)
+        host = vec.tolist()
         t1 = time.perf_counter()
+        loss = host[0]
+        names = [f"{n}:{k}" for n in vals for k in ("eps_r", "sigma")]
+        grads = dict(zip(names, host[1:]))
         if i >= args.warmup:
             times.append(t1 - t0)
-    return {"metric": "material-gradient step latency", "value_ms": 1e3 * float(np.median(times)),
-            "unit": "ms", "higher_is_better": False, "setup_ms": 1e3 * setup, "records": len(pos),
-            "receivers_generated": int(len(keep)),
-            "materials": len(prob.names), "paths": int(prob.T.n), "subcarriers": 128, "max_depth": 2,
-            "loss": loss, "grads": grads,
-            "includes": "forward (rt_transfer + OFDM responses + NMSE) + backward (rt_transfer_bwd "
-                        "adjoint) + 8 gradient read-backs; setup = build + exhaustive candidates + path solve of "
-                        "the records (frozen topology)"}
+    med = parallel.max_over_ranks(float(np.median(times)), world)
+    return {"metric": "material-gradient step latency", "value_ms": 1e3 * med,
+            "unit": "ms", "higher_is_better": False, "setup_ms": 1e3 * setup, "records": n_rec,
+            "receivers_generated": int(len(keep)), "ranks": world,
+            "materials": len(prob.names), "paths_local": int(prob.T.n), "subcarriers": 128,
+            "max_depth": 2, "loss": loss, "grads": grads,
+            "includes": "forward (rt_transfer + rt_freq_nmse) + backward (rt_transfer_bwd adjoint) "
+                        "+ [loss, 8 grads] read-back" + (" after an all_reduce" if world > 1 else "")
+                        + "; setup = build + exhaustive candidates + path solve of the records "
+                          "(frozen topology)"}
 
 
 def _profile(bvh):
@@ -442,7 +513,10 @@ def _profile(bvh):
 
 
 def run_e2e(args, sc, grid, rank, world, dev, flush):
-    """Public-API step: build(scene) [H2D of the scene arrays] + coverage map [D2H gains]."""
+    """Public-API step: build(scene) [H2D of the scene arrays] + coverage map
+    [D2H gains].  One rank: the emtrace-signature call a drop-in caller makes,
+    coverage_map(scene, bvh, grid, max_depth, method, num_rays, cell_cap);
+    N ranks: parallel.coverage_map (rays and rows sharded)."""
     import torch
     import paper_2303_11103_b200 as P
     from paper_2303_11103_b200 import parallel
@@ -457,19 +531,27 @@ def run_e2e(args, sc, grid, rank, world, dev, flush):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         bvh = P.build(sc)
-        g, b = parallel.coverage_map(sc, bvh, grid, args.depth, int(args.rays), rank, world)
+        if world == 1:
+            cm = P.coverage_map(sc, bvh, grid, args.depth, method="fibonacci", num_rays=int(args.rays),
+                                cell_cap=grid.num_cells)
+            g, b = cm.gains, cm.stats["ray_bounces"]
+        else:
+            g, b = parallel.coverage_map(sc, bvh, grid, args.depth, int(args.rays), rank, world)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         parallel.barrier(world)
+        assert g.shape == (grid.ny, grid.nx)
         if i >= args.warmup:
             times.append(t1 - t0)
             bounces += b
         del bvh
     tot = parallel.max_over_ranks(sum(times), world)
     b_all = parallel.sum_over_ranks(float(bounces), world)
+    api = ("paper_2303_11103_b200.build + coverage_map(scene, bvh, grid, max_depth, method, num_rays, "
+           "cell_cap) (emtrace signature, E/channel.py:236)") if world == 1 else \
+        "paper_2303_11103_b200.build + parallel.coverage_map (rays + rows sharded, NCCL)"
     return {"value": b_all / tot, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * tot / args.steps,
-            "api": "paper_2303_11103_b200.build + parallel.coverage_map (public API, host arrays in/out)"}
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * tot / args.steps, "api": api}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -530,14 +612,31 @@ def run_reference(args):
                     "d2h_bytes_per_step": 0}}
 
 
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: start N ranks with torch.distributed.run
+    (127.0.0.1, one rank per GPU) and return their exit code."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     line = run_reference(args) if args.impl == "reference" else run_b200(args)
-    if line is not None:
-        print(json.dumps(line), flush=True)
     if args.impl != "reference" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    if line is not None:   # last, after NCCL's own log lines
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -252,7 +252,27 @@ int rt_set_profiling(rt_ctx* ctx, int flags);
  * streams a `bytes` buffer `iters` times with 16-byte L2-only loads (the
  * roofline denominator for the L2-resident traversal working set). */
 int rt_l2_probe(rt_ctx* ctx, int64_t bytes, int iters, double* gbs_out, void* stream);
+/* Measured peaks for the roofline denominators (csrc/microbench.cuh), timed
+ * with CUDA events on `stream` at the current clocks: kind 0 FP32 FMA TFLOP/s,
+ * 1 FP64 DFMA TFLOP/s, 2 warp-instruction issue rate (Gwarp-inst/s, imm-form
+ * FFMA chains), 3 L1-resident read GB/s, 4 L2-resident read GB/s (rt_l2_probe
+ * on 48 MB).  Synchronizes the stream. */
+int rt_microbench(rt_ctx* ctx, int kind, double* value_out, void* stream);
 int rt_get_profile(rt_ctx* ctx, double* ms_out, int64_t* counters_out);
+
+/* ---- OFDM responses and the calibration loss (channel.py:107-123,
+ * optim.py:158-177 _projected_sq_error, optim.py:305-372 learn_materials) ----
+ * Paths are grouped by record: record r owns rows rec_start[r] ..
+ * rec_start[r+1]-1 (device int64 [n_records+1]) of a [P*2] (complex) and
+ * tau [P]; freqs [n_sub] (device, n_sub <= 8192).
+ *   H_out [n_records*n_sub*2] (optional): H[r,k] = sum_i a_i e^{-j 2 pi f_k tau_i}
+ *   loss_out [n_records] (optional): scale * sum_k |H[r,k] - h[r,k]|^2 / norm2[r]
+ *   grad_a [P*2] (optional): dloss/da_i (dL/dRe + j dL/dIm) of sum_r loss_out[r]
+ * h [n_records*n_sub*2] and norm2 [n_records] are needed for loss / grad.
+ * Fixed summation order, no atomics: bit-reproducible. */
+int rt_freq_nmse(rt_ctx* ctx, int64_t n_records, int n_sub, const int64_t* rec_start, const double* a,
+                 const double* tau, const double* freqs, const double* h, const double* norm2,
+                 double scale, double* H_out, double* loss_out, double* grad_a, void* stream);
 
 #ifdef __cplusplus
 }

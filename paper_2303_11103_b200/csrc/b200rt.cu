@@ -18,6 +18,8 @@
 #include "bvh_sah.cuh"
 #include "cir.cuh"
 #include "em_jvp.cuh"
+#include "freq.cuh"
+#include "microbench.cuh"
 #include "launch.cuh"
 
 
@@ -1419,8 +1421,8 @@ int rt_transfer(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, 
                    delay, tx_rows, rx_rows, tx_pattern, rx_pattern, tx_slants, n_tx_slants,
                    rx_slants, n_rx_slants, eta, ctx->prim_mat.get<int>(), interaction_mat, wavelength,
                    frequency_hz};
-    if (!interaction_mat && ctx->n_prims == 0)
-        return fail(ctx, RT_EINVAL, "transfer needs interaction materials or an uploaded scene");
+    // without interaction_mat the materials come from the scene; a scene without
+    // primitives has only LOS paths, which read no material
     k_transfer<<<nblk(n_paths * n_tx_slants, 128), 128, 0, ST(stream)>>>(A, a_out);
     CKL();
     return RT_OK;
@@ -1441,8 +1443,8 @@ int rt_transfer_bwd(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* ord
                    delay, tx_rows, rx_rows, tx_pattern, rx_pattern, tx_slants, n_tx_slants,
                    rx_slants, n_rx_slants, eta, ctx->prim_mat.get<int>(), interaction_mat, wavelength,
                    frequency_hz};
-    if (!interaction_mat && ctx->n_prims == 0)
-        return fail(ctx, RT_EINVAL, "transfer needs interaction materials or an uploaded scene");
+    // without interaction_mat the materials come from the scene; a scene without
+    // primitives has only LOS paths, which read no material
     if (n_mat < 1) return fail(ctx, RT_EINVAL, "need n_mat >= 1");
     long long n = n_paths * n_tx_slants * n_rx_slants;
     CK(ctx->adj.reserve(sizeof(double2) * (size_t)n * max_len));
@@ -1604,6 +1606,46 @@ int rt_l2_probe(rt_ctx* ctx, int64_t bytes, int iters, double* gbs_out, void* st
     return RT_OK;
 }
 
+int rt_microbench(rt_ctx* ctx, int kind, double* value_out, void* stream) {
+    if (!ctx || !value_out || kind < RT_MB_FP32 || kind > RT_MB_L2)
+        return fail(ctx, RT_EINVAL, "bad microbenchmark arguments");
+    if (kind == RT_MB_L2) return rt_l2_probe(ctx, 48LL << 20, 64, value_out, stream);
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    const unsigned grid = (unsigned)ctx->n_sm * 8;   // 8 x 256 threads = 64 warps per SM
+    const long long threads = (long long)grid * 256;
+    CK(ctx->probe.reserve((size_t)grid * MB_L1_SLICE + 64));
+    float* sink = reinterpret_cast<float*>(ctx->probe.get<char>() + (size_t)grid * MB_L1_SLICE);
+    if (kind == RT_MB_L1) CK(cudaMemsetAsync(ctx->probe.p, 0, (size_t)grid * MB_L1_SLICE, st));
+    auto run = [&](int iters) {
+        if (kind == RT_MB_FP32) k_mb_ffma<<<grid, 256, 0, st>>>(iters, sink);
+        else if (kind == RT_MB_ISSUE) k_mb_issue<<<grid, 256, 0, st>>>(iters, sink);
+        else if (kind == RT_MB_FP64) k_mb_dfma<<<grid, 256, 0, st>>>(iters, reinterpret_cast<double*>(sink));
+        else k_mb_l1<<<grid, 256, 0, st>>>(ctx->probe.get<float4>(), iters, sink);
+    };
+    const int iters = kind == RT_MB_FP64 ? 400 : kind == RT_MB_L1 ? 2000 : 2000;
+    run(iters / 10);   // warm-up (clocks, L1 fill)
+    CKL();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, st));
+    run(iters);
+    CKL();
+    CK(cudaEventRecord(b, st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    double sec = ms * 1e-3;
+    double ops = (double)threads * iters * MB_UNROLL * MB_CHAINS;   // FMAs (or FFMA instructions)
+    if (kind == RT_MB_FP32 || kind == RT_MB_FP64) *value_out = 2.0 * ops / sec / 1e12;   // TFLOP/s
+    else if (kind == RT_MB_ISSUE) *value_out = ops / 32.0 / sec / 1e9;                    // Gwarp-inst/s
+    else *value_out = (double)grid * MB_L1_SLICE * iters / sec / 1e9;                     // GB/s
+    return RT_OK;
+}
+
 int rt_set_profiling(rt_ctx* ctx, int flags) {
     if (!ctx) return RT_EINVAL;
     ctx->prof = flags;
@@ -1711,6 +1753,26 @@ int rt_cir_scatter(rt_ctx* ctx, int64_t n_paths, const double* delay, int normal
                                                         ctx->cir_first.get<double>(), delay, normalize,
                                                         ctx->cir_ntx, n_rx_el, n_tx_el, n_t, n_path, a_in,
                                                         a_out, tau_out);
+    CKL();
+    return RT_OK;
+}
+
+int rt_freq_nmse(rt_ctx* ctx, int64_t n_records, int n_sub, const int64_t* rec_start, const double* a,
+                 const double* tau, const double* freqs, const double* h, const double* norm2, double scale,
+                 double* H_out, double* loss_out, double* grad_a, void* stream) {
+    if (!ctx || n_records < 0 || n_sub < 1 || n_sub > 8192 || !rec_start || !a || !tau || !freqs)
+        return fail(ctx, RT_EINVAL, "bad frequency-response arguments");
+    if ((loss_out || grad_a) && (!h || !norm2))
+        return fail(ctx, RT_EINVAL, "the NMSE needs targets and their norms");
+    if (n_records == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    size_t smem = sizeof(double2) * (size_t)n_sub;
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(k_freq_nmse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_freq_nmse<<<(unsigned)n_records, FREQ_BLOCK, smem, ST(stream)>>>(
+        n_sub, reinterpret_cast<const long long*>(rec_start), reinterpret_cast<const double2*>(a), tau, freqs,
+        reinterpret_cast<const double2*>(h), norm2, scale, reinterpret_cast<double2*>(H_out), loss_out,
+        reinterpret_cast<double2*>(grad_a));
     CKL();
     return RT_OK;
 }

@@ -322,6 +322,9 @@ class DiffComplex(complex):
     def abs2(self) -> float:
         return self.real * self.real + self.imag * self.imag
 
+    def conj(self):
+        return DiffComplex(complex.conjugate(self))
+
     def __add__(self, o): return DiffComplex(complex.__add__(self, o))
     def __radd__(self, o): return DiffComplex(complex.__radd__(self, o))
     def __sub__(self, o): return DiffComplex(complex.__sub__(self, o))
@@ -469,14 +472,16 @@ def transfer(ctx: EvalContext, geom, materials, tx_dev, rx_dev, tx_pattern: str,
     dev = h.device
     scene = ctx.scene
     names = list(dict.fromkeys(mats))
-    rows, track = [], False
+    # a context with autograd leaves returns tensors for every path (LOS too)
+    track = any(isinstance(v, torch.Tensor) and v.requires_grad
+                for pair in ctx.material_values.values() for v in pair)
+    rows = []
     for name in names:
         m = scene.materials[name]
         ov = ctx.material_values.get(name)
         e, sg = material_params(m, scene.frequency_hz, None if ov is None else ov[0],
                                 None if ov is None else ov[1])
         if isinstance(e, torch.Tensor) or isinstance(sg, torch.Tensor):
-            track = track or any(isinstance(v, torch.Tensor) and v.requires_grad for v in (e, sg))
             e = torch.as_tensor(e, dtype=torch.float64, device=dev)
             sg = torch.as_tensor(sg, dtype=torch.float64, device=dev)
             rows.append(eta_from_params(e, sg, scene.frequency_hz))

@@ -15,6 +15,7 @@ import math
 import numpy as np
 import torch
 
+from . import _native as N
 from .bvh import build
 from .em import eta_from_params, path_coefficients, rotation_entries
 from .scene import POLARIZATION_SLANTS, material_params
@@ -61,6 +62,14 @@ class MaterialProblem:
         self.tx_slant = POLARIZATION_SLANTS[scene.tx_array.polarization][0]
         self.rx_slant = POLARIZATION_SLANTS[scene.rx_array.polarization][0]
 
+        # rows of the path table are grouped by record (rt_paths: rx order): record r
+        # owns rows rec_start[r] .. rec_start[r + 1] - 1
+        counts = torch.bincount(self.T.rx.long(), minlength=self.R)
+        self.rec_start = torch.zeros(self.R + 1, dtype=torch.int64, device=dev)
+        self.rec_start[1:] = torch.cumsum(counts, 0)
+        self.freqs = f.contiguous()
+        self.h_ri = torch.view_as_real(self.h.contiguous()).contiguous()
+
     def eta(self, values):
         """eta table [n_mat, 2] with trainable entries taken from ``values`` (tensors)."""
         rows = []
@@ -82,20 +91,56 @@ class MaterialProblem:
                     torch.tensor(float(self.scene.materials[n].sigma), dtype=torch.float64, device=dev))
                 for n in self.names}
 
-    def responses(self, values):
-        """H_r(f_k) = sum over record r's paths of a_i e^{-j 2 pi f_k tau_i}  [R, N]."""
+    def coefficients(self, values):
+        """Central-element gains a_i of every frozen path (differentiable in eta)."""
         sc = self.scene
-        a = path_coefficients(self.bvh, self.T, self.eta(values), self.tx_rows, self.rx_rows,
-                              sc.tx_array.pattern, sc.rx_array.pattern, [self.tx_slant],
-                              [self.rx_slant], sc.wavelength, sc.frequency_hz)[:, 0, 0]
-        pred = torch.zeros((self.R, self.basis.shape[1]), dtype=torch.complex128,
-                           device=self.bvh.device)
-        return pred.index_add(0, self.T.rx.long(), a[:, None] * self.basis)
+        return path_coefficients(self.bvh, self.T, self.eta(values), self.tx_rows, self.rx_rows,
+                                 sc.tx_array.pattern, sc.rx_array.pattern, [self.tx_slant],
+                                 [self.rx_slant], sc.wavelength, sc.frequency_hz)[:, 0, 0]
+
+    def _freq_call(self, a, H=None, loss=None, grad=None, scale=1.0):
+        ar = torch.view_as_real(a.detach().contiguous()).contiguous()
+        with torch.cuda.device(self.bvh.device):
+            self.bvh.ctx.call("rt_freq_nmse", self.R, self.freqs.numel(), N.ptr(self.rec_start),
+                              N.ptr(ar), N.ptr(self.T.delay), N.ptr(self.freqs),
+                              N.ptr(self.h_ri) if loss is not None or grad is not None else None,
+                              N.ptr(self.norm2) if loss is not None or grad is not None else None,
+                              float(scale), N.ptr(H), N.ptr(loss), N.ptr(grad), self.bvh.ctx.stream)
+
+    def responses(self, values):
+        """H_r(f_k) = sum over record r's paths of a_i e^{-j 2 pi f_k tau_i}  [R, N]
+        (rt_freq_nmse, fixed summation order; not differentiable)."""
+        a = self.coefficients(values)
+        H = torch.empty((self.R, self.freqs.numel(), 2), dtype=torch.float64, device=self.bvh.device)
+        if self.R:
+            self._freq_call(a, H=H)
+        return torch.view_as_complex(H)
 
     def loss(self, values):
-        pred = self.responses(values)
-        err = ((pred - self.h).abs() ** 2).sum(-1) / self.norm2
-        return err.mean()
+        """mean_r ||H_r - h_r||^2 / ||h_r||^2, gradient through rt_freq_nmse + the adjoint."""
+        return _RecordNmse.apply(self.coefficients(values), self)
+
+
+class _RecordNmse(torch.autograd.Function):
+    """loss = sum_r (1/R) ||B_r a_r - h_r||^2 / ||h_r||^2 with dloss/da from the
+    same kernel launch (rt_freq_nmse); per-record losses are summed by torch's
+    fixed-order reduction."""
+
+    @staticmethod
+    def forward(ctx, a, prob):
+        dev = prob.bvh.device
+        loss_r = torch.zeros(prob.R, dtype=torch.float64, device=dev)
+        grad = torch.zeros((a.shape[0], 2), dtype=torch.float64, device=dev)
+        if prob.R:
+            prob._freq_call(a, loss=loss_r, grad=grad if a.requires_grad else None,
+                            scale=1.0 / prob.R)
+        ctx.save_for_backward(torch.view_as_complex(grad))
+        return loss_r.sum()
+
+    @staticmethod
+    def backward(ctx, g):
+        (grad,) = ctx.saved_tensors
+        return grad * g, None
 
 
 def material_loss_and_grad(scene, positions, h_targets, max_depth=2, num_subcarriers=128,

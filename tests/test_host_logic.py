@@ -195,3 +195,45 @@ def test_sionna_facade_compiles_to_emtrace_scene():
     tx = em.devices[0]
     assert abs(tx.orientation[0] - math.atan2(-17.0, 19.0)) < 1e-12
     assert sum(len(o.triangles) for o in em.objects) == 2 + 9 * 10
+
+
+def _gloo_rows_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2303_11103_b200 import parallel
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n_rx = 7
+        rows = parallel.rx_of_shard(n_rx, rank, world)
+        P = 2 + rank   # path-slot count differs per rank: padded to the maximum
+        x = torch.zeros((len(rows), 2, P), dtype=torch.complex128)
+        for j, r in enumerate(rows):
+            x[j, :, :P] = complex(r, -r) + torch.arange(P, dtype=torch.float64)[None, :]
+        full = parallel._gather_rows(x, rows, n_rx, world, pad_dims=(2,))
+        q.put((rank, torch.view_as_real(full).numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_cir_row_gather():
+    """Receiver rows r, r+W, ... of every rank land in receiver order, the path
+    dimension zero-padded to the largest rank's."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_rows_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = np.zeros((7, 2, 3), dtype=np.complex128)
+    for r in range(7):
+        P = 2 + (r % 2)
+        want[r, :, :P] = complex(r, -r) + np.arange(P)[None, :]
+    for _, full in out:
+        f = np.array(full)
+        assert np.array_equal(f[..., 0] + 1j * f[..., 1], want)
