@@ -78,9 +78,10 @@ __global__ void __launch_bounds__(256) k_mb_l1(const float4* __restrict__ buf, i
     const float4* p = buf + (long long)blockIdx.x * n4;
     float acc = 0.f;
     for (int it = 0; it < iters; ++it) {
+        // the slot rotates with `it`, so the loads cannot be hoisted out of the loop
 #pragma unroll 4
         for (int i = threadIdx.x; i < n4; i += 256) {
-            float4 v = __ldg(p + i);
+            float4 v = __ldg(p + ((i + it * 32) & (n4 - 1)));
             acc += (v.x + v.w);
         }
     }

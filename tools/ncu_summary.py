@@ -63,6 +63,7 @@ def full(path, out, traffic_json=None):
     dram = {}
     stalls = {}
     insts = {}
+    lts, l1 = {}, {}
     for r in rr[2:]:
         d = dict(zip(rh, r))
         k = (d.get("ID"), d.get("Kernel Name", "").split("(")[0])
@@ -70,6 +71,12 @@ def full(path, out, traffic_json=None):
             insts[k] = float(d["inst_executed"].replace(",", ""))
         except (KeyError, ValueError):
             pass
+        # 32-byte sectors through L2 (all sources) and the L1/TEX global loads
+        for name, dst in (("lts__t_sectors.sum", lts), ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", l1)):
+            try:
+                dst[k] = 32.0 * float(d[name].replace(",", ""))
+            except (KeyError, ValueError):
+                pass
         try:
             dram[k] = sum(float(d[m].replace(",", "")) * scale.get(units.get(m, "byte"), 1.0)
                           for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
@@ -99,15 +106,16 @@ def full(path, out, traffic_json=None):
                      ", ".join(f"{n} {100 * v / tot:.0f}%" for n, v in top) + "\n\n")
 
 
-    if traffic_json:   # traffic per kernel for bench.py's roofline "traffic" field
+    if traffic_json:   # per-kernel figures for bench.py's roofline
         import json
-        tr, ins = {}, {}
-        for k, v in dram.items():
-            tr.setdefault(k[1], []).append(v)
-        for k, v in insts.items():
-            ins.setdefault(k[1], []).append(v)
-        json.dump({"source": path, "dram_bytes_per_launch": {k: sum(v) / len(v) for k, v in tr.items()},
-                   "warp_instructions_per_launch": {k: sum(v) / len(v) for k, v in ins.items()}},
+        def per_kernel(m):
+            acc = {}
+            for k, v in m.items():
+                acc.setdefault(k[1], []).append(v)
+            return {k: sum(v) / len(v) for k, v in acc.items()}
+        json.dump({"source": path, "dram_bytes_per_launch": per_kernel(dram),
+                   "warp_instructions_per_launch": per_kernel(insts),
+                   "lts_bytes_per_launch": per_kernel(lts), "l1tex_bytes_per_launch": per_kernel(l1)},
                   open(traffic_json, "w"), indent=1)
 
 
