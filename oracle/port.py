@@ -77,6 +77,13 @@ def lib():
                                        i32, f64, P, P]
             L.orc_coverage.argtypes = [P, P, P, P, P, f64, f64, P, P, i32, P, P, i32, i32, P,
                                        P, i64, P, P, i64, i32, i32, P, P]
+            L.orc_pset_new.restype = P
+            L.orc_pset_new.argtypes = [i32]
+            L.orc_pset_free.argtypes = [P]
+            L.orc_pset_add.argtypes = [P, P, i64]
+            L.orc_pset_size.restype = i64
+            L.orc_pset_size.argtypes = [P]
+            L.orc_pset_export.argtypes = [P, P]
             _lib = L
     return _lib
 
@@ -136,11 +143,13 @@ def element_layout(arr, wavelength):
     return np.vstack([base] * len(sl)), np.repeat(sl, rows * cols)
 
 
-def fibonacci_directions(n: int) -> np.ndarray:
-    """Spherical Fibonacci lattice (geometry.py:62-76)."""
+def fibonacci_directions(n: int, begin: int = 0, end: int = None) -> np.ndarray:
+    """Spherical Fibonacci lattice (geometry.py:62-76); rows begin..end-1 of the
+    n-point lattice (the same elementwise numpy expressions, so a slice equals
+    the corresponding rows of the full array)."""
     if n < 1:
         raise OracleError("need at least one direction")
-    i = np.arange(n, dtype=np.float64)
+    i = np.arange(begin, n if end is None else end, dtype=np.float64)
     z = 1.0 - (2.0 * i + 1.0) / n
     phi = 2.0 * math.pi * i / _GOLDEN_SQ
     r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
@@ -270,6 +279,38 @@ def prefixes_from_sequences(seq: np.ndarray) -> set:
             for r in np.unique(rows, axis=0):
                 found.add(tuple(int(x) for x in r))
     return found
+
+
+def launch_candidate_rows(bvh: Bvh, tx_pos, max_depth: int, num_rays: int, chunk: int = 1 << 22):
+    """launch_candidates for launches too large for Python tuples (C3: 1e8 rays):
+    the lattice is traced in chunks of numpy directions and every prefix goes
+    into a C hash set.  Returns (rows [C, max_depth] int32 -1 padded, sorted by
+    (length, lexicographic), total intersect calls)."""
+    h = lib().orc_pset_new(int(max_depth))
+    bounces = 0
+    try:
+        for a in range(0, num_rays, chunk):
+            b = min(num_rays, a + chunk)
+            seq, nb = launch_sequences(bvh, tx_pos, max_depth, b - a,
+                                       dirs=fibonacci_directions(num_rays, a, b))
+            bounces += int(nb.sum())
+            lib().orc_pset_add(h, _p(np.ascontiguousarray(seq)), b - a)
+        n = lib().orc_pset_size(h)
+        rows = np.zeros((n, max_depth), dtype=np.int32)
+        lib().orc_pset_export(h, _p(rows))
+    finally:
+        lib().orc_pset_free(h)
+    return sort_candidate_rows(rows), bounces
+
+
+def sort_candidate_rows(rows):
+    """Rows (-1 padded) in (length, lexicographic) order."""
+    rows = np.asarray(rows, dtype=np.int32)
+    if not len(rows):
+        return rows
+    lens = (rows >= 0).sum(1)
+    keys = [rows[:, j] for j in range(rows.shape[1] - 1, -1, -1)] + [lens]
+    return rows[np.lexsort(keys)]
 
 
 def launch_candidates(bvh: Bvh, tx_pos, max_depth: int, num_rays: int = 4096, dirs=None):

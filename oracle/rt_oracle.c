@@ -710,3 +710,88 @@ void orc_coverage(void* h, const double* normals, const double* poff, const int3
         free(buf);
     }
 }
+
+/* ------------------------------------------------------------------------ */
+/* prefix set: the `found` set of tracer.py:232-243 (every prefix of every    */
+/* ray's hit history) for launches too large for Python tuples.  Keys are     */
+/* prefixes padded with -1 to L entries; open addressing, FNV-1a hash.        */
+
+typedef struct {
+    int L;
+    int64_t cap, n;
+    int32_t* keys;   /* cap * L; slot empty when keys[s*L] == INT32_MIN */
+} opset;
+
+static uint64_t pset_hash(const int32_t* k, int L) {
+    uint64_t h = 1469598103934665603ULL;
+    for (int i = 0; i < L; ++i) {
+        h ^= (uint32_t)k[i];
+        h *= 1099511628211ULL;
+    }
+    return h ^ (h >> 29);
+}
+
+static void pset_alloc(opset* s, int64_t cap) {
+    s->cap = cap;
+    s->keys = (int32_t*)malloc(sizeof(int32_t) * cap * s->L);
+    for (int64_t i = 0; i < cap; ++i) s->keys[i * s->L] = INT32_MIN;
+}
+
+static int pset_insert(opset* s, const int32_t* k) {
+    uint64_t m = (uint64_t)s->cap - 1, h = pset_hash(k, s->L) & m;
+    for (;;) {
+        int32_t* slot = s->keys + h * s->L;
+        if (slot[0] == INT32_MIN) {
+            memcpy(slot, k, sizeof(int32_t) * s->L);
+            s->n++;
+            return 1;
+        }
+        if (memcmp(slot, k, sizeof(int32_t) * s->L) == 0) return 0;
+        h = (h + 1) & m;
+    }
+}
+
+void* orc_pset_new(int L) {
+    opset* s = (opset*)calloc(1, sizeof(opset));
+    s->L = L;
+    pset_alloc(s, 1 << 16);
+    return s;
+}
+
+void orc_pset_free(void* h) {
+    opset* s = (opset*)h;
+    free(s->keys);
+    free(s);
+}
+
+/* add every prefix of each row of seq [n, L] (rows end at the first -1) */
+void orc_pset_add(void* h, const int32_t* seq, int64_t n) {
+    opset* s = (opset*)h;
+    int L = s->L;
+    int32_t key[16];
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t* r = seq + i * L;
+        for (int k = 0; k < L && r[k] >= 0; ++k) {
+            for (int j = 0; j < L; ++j) key[j] = j <= k ? r[j] : -1;
+            if (2 * (s->n + 1) > s->cap) {   /* grow: keep the load below 1/2 */
+                opset t = {L, 0, 0, NULL};
+                pset_alloc(&t, s->cap * 4);
+                for (int64_t q = 0; q < s->cap; ++q)
+                    if (s->keys[q * L] != INT32_MIN) pset_insert(&t, s->keys + q * L);
+                free(s->keys);
+                *s = t;
+            }
+            pset_insert(s, key);
+        }
+    }
+}
+
+int64_t orc_pset_size(void* h) { return ((opset*)h)->n; }
+
+/* the set's keys [n, L] in slot order (the caller sorts) */
+void orc_pset_export(void* h, int32_t* out) {
+    opset* s = (opset*)h;
+    int64_t w = 0;
+    for (int64_t q = 0; q < s->cap; ++q)
+        if (s->keys[q * s->L] != INT32_MIN) memcpy(out + (w++) * s->L, s->keys + q * s->L, sizeof(int32_t) * s->L);
+}
