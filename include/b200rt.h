@@ -260,6 +260,13 @@ int rt_l2_probe(rt_ctx* ctx, int64_t bytes, int iters, double* gbs_out, void* st
 int rt_microbench(rt_ctx* ctx, int kind, double* value_out, void* stream);
 int rt_get_profile(rt_ctx* ctx, double* ms_out, int64_t* counters_out);
 
+/* Fresnel reflection coefficients (em.py:123-141 fresnel, with
+ * autodiff.py:365-382 csqrt_posreal's Re >= 0 branch) of n (eta, cos theta_i)
+ * pairs: eta [n*2], cos_theta [n] -> r_te, r_tm [n*2] (device, complex as 2
+ * doubles).  The same device function the transfer kernels use. */
+int rt_fresnel(rt_ctx* ctx, int64_t n, const double* eta, const double* cos_theta, double* r_te,
+               double* r_tm, void* stream);
+
 /* ---- OFDM responses and the calibration loss (channel.py:107-123,
  * optim.py:158-177 _projected_sq_error, optim.py:305-372 learn_materials) ----
  * Paths are grouped by record: record r owns rows rec_start[r] ..

@@ -10,7 +10,8 @@ from .channel import (ChannelError, Cir, CoverageMap, FreqResponse, GridSpec, bu
                       coverage_map, frequency_response, load_cir, point_path_gain,
                       probe_receiver, save_cir, subcarrier_frequencies)
 from .em import (ChannelGains, DiffComplex, EmError, EvalContext, PathGain, PathGeometry,
-                 apply_doppler, compute_gains, geometry_for_positions, geometry_from_path,
+                 apply_doppler, compute_gains, fresnel, fresnel_batch, geometry_for_positions,
+                 geometry_from_path,
                  path_geometry, path_materials, transfer)
 from .scene import (AntennaArray, RadioDevice, RadioMaterial, Scene, SceneError, SceneObject,
                     load_scene, look_at, material_eta, write_scene)

@@ -28,7 +28,7 @@ EXPORTS = [
     "rt_paths", "rt_paths_get", "rt_transfer", "rt_transfer_bwd", "rt_coverage",
     "rt_set_profiling", "rt_get_profile", "rt_l2_probe", "rt_transfer_jvp", "rt_solve_pairs",
     "rt_launch_shard", "rt_gains_synthetic", "rt_cir_plan", "rt_cir_scatter", "rt_freq_nmse",
-    "rt_microbench",
+    "rt_microbench", "rt_fresnel",
 ]
 
 _lib = None
@@ -115,6 +115,7 @@ def lib():
             "rt_cir_scatter": (i32, [P, i64, P, i32, P, i32, i32, i32, i64, P, P, P]),
             "rt_freq_nmse": (i32, [P, i64, i32, P, P, P, P, P, P, f64, P, P, P, P]),
             "rt_microbench": (i32, [P, i32, ctypes.POINTER(ctypes.c_double), P]),
+            "rt_fresnel": (i32, [P, i64, P, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

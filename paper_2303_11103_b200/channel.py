@@ -215,16 +215,33 @@ def subcarrier_frequencies(num_subcarriers: int, spacing: float) -> np.ndarray:
 
 
 def frequency_response(cir: Cir, num_subcarriers: int, spacing: float) -> FreqResponse:
-    """H(f_k) = sum_i a_i e^{-j 2 pi f_k tau_i} (channel.py:107-123), on the device."""
+    """H(f_k) = sum_i a_i e^{-j 2 pi f_k tau_i} (channel.py:107-123) on the device:
+    every (rx, rx element, tx, tx element, time) row of the CIR is one record of
+    rt_freq_nmse (paths summed in slot order; a host CIR is uploaded first)."""
+    from .em import _DeviceHandle
     f = subcarrier_frequencies(num_subcarriers, spacing)
-    a = cir.a_dev if cir.a_dev is not None else torch.as_tensor(cir.a)
-    tau = cir.tau_dev if cir.tau_dev is not None else torch.as_tensor(cir.tau)
-    ft = torch.as_tensor(f, device=a.device)
-    phase = torch.exp(-2j * math.pi * tau[:, :, :, None] * ft[None, None, None, :])
-    h = torch.einsum("abcdpt,acpk->abcdkt", a, phase)
-    nr, nre, nt, nte = a.shape[:4]
-    h = h.reshape(nr * nre, nt * nte, num_subcarriers, a.shape[-1])
-    return FreqResponse(h=N.d2h(h), frequencies=f)
+    h = _DeviceHandle.get()
+    dev = cir.a_dev.device if cir.a_dev is not None else h.device
+    ctx = h.ctx if dev == h.device else N.acquire_context(dev)
+    a = cir.a_dev if cir.a_dev is not None else torch.as_tensor(np.asarray(cir.a), device=dev)
+    tau = cir.tau_dev if cir.tau_dev is not None else torch.as_tensor(np.asarray(cir.tau), device=dev)
+    nr, nre, nt, nte, P, T = a.shape
+    R = nr * nre * nt * nte * T
+    a_rec = a.to(torch.complex128).permute(0, 1, 2, 3, 5, 4).reshape(R, P)
+    tau_rec = tau.to(torch.float64)[:, None, :, None, None, :].expand(nr, nre, nt, nte, T, P).reshape(R, P)
+    ar = torch.view_as_real(a_rec.contiguous()).contiguous()
+    tr = tau_rec.contiguous()
+    start = torch.arange(R + 1, dtype=torch.int64, device=dev) * P
+    ft = torch.as_tensor(f, dtype=torch.float64, device=dev)
+    H = torch.zeros((R, num_subcarriers, 2), dtype=torch.float64, device=dev)
+    if R and P:
+        with torch.cuda.device(dev):
+            ctx.call("rt_freq_nmse", R, num_subcarriers, N.ptr(start), N.ptr(ar), N.ptr(tr), N.ptr(ft),
+                     None, None, 1.0, N.ptr(H), None, None, ctx.stream,
+                     exc_map={N.RT_EINVAL: ChannelError})
+    Hc = torch.view_as_complex(H).reshape(nr, nre, nt, nte, T, num_subcarriers)
+    Hc = Hc.permute(0, 1, 2, 3, 5, 4).reshape(nr * nre, nt * nte, num_subcarriers, T)
+    return FreqResponse(h=N.d2h(Hc.contiguous()), frequencies=f)
 
 
 # -- coverage ---------------------------------------------------------------------------------
@@ -362,12 +379,42 @@ def _device(scene, name):
     raise ChannelError(f"no device named {name!r}")
 
 
+def _tracked_gain(scene, bvh, T, tx_dev, probe, ctx, tx_mode):
+    """point_path_gain under a context holding autograd leaves (the reference's
+    Tape context, E/channel.py:214-232 with E/em.py:285-288): returns a 0-d
+    tensor whose backward reaches material (eps_r, sigma), tx orientation and
+    tx / probe position leaves through rt_transfer_jvp and rt_transfer_bwd."""
+    from .em import path_coefficients_geo, slants_of
+    if tx_mode != "central":
+        raise ChannelError("gradients are available for tx_mode='central' only")
+    dev = bvh.device
+    P = T.n
+
+    def vec3(v):
+        return torch.stack([torch.as_tensor(x, dtype=torch.float64, device=dev) for x in v])
+
+    ypr = vec3(ctx.orientations.get(tx_dev.name, tx_dev.orientation))
+    tp = vec3(ctx.positions.get(tx_dev.name, tx_dev.position))
+    rp = vec3(ctx.positions.get(probe.name, probe.position))
+    eta = ctx.eta_tensor(bvh)
+    slant = float(slants_of(scene.tx_array)[0])
+    zero = torch.zeros((P, 3), dtype=torch.float64, device=dev)
+    total = torch.zeros((), dtype=torch.float64, device=dev)
+    for pat in ("_probe_theta", "_probe_phi"):
+        a = path_coefficients_geo(bvh, T, eta, tp[None, :].expand(P, 3), rp[None, :].expand(P, 3),
+                                  ypr[None, :].expand(P, 3), zero, scene.tx_array.pattern, pat,
+                                  [slant], [0.0], scene.wavelength, scene.frequency_hz)[:, 0, 0]
+        total = total + (a.real ** 2 + a.imag ** 2).sum()
+    return total
+
+
 def point_path_gain(scene, bvh, tx_dev, point, max_depth: int, method: str = "exhaustive",
                     num_rays: int = 4096, ctx: EvalContext | None = None, frozen_paths=None,
                     tx_mode: str = "central"):
     """Sum_i |a_i|^2 over both probe polarizations at one point (channel.py:190-233).
 
     Returns (gain, paths) like the reference; ``frozen_paths`` reuses a topology.
+    Under a context with autograd leaves the gain is a differentiable 0-d tensor.
     """
     from .em import _launch_transfer, _rows_tensor, _table_from_paths
     from .tracer import table_to_paths
@@ -384,6 +431,8 @@ def point_path_gain(scene, bvh, tx_dev, point, max_depth: int, method: str = "ex
         T = _table_from_paths(paths, bvh, [tx_dev.name], [PROBE_NAME]) if paths else None
     if T is None or T.n == 0:
         return 0.0, paths
+    if ctx.tracks():
+        return _tracked_gain(scene, bvh, T, tx_dev, probe, ctx, tx_mode), paths
     rows, slants, off_w = _tx_antenna(scene, tx_dev, ctx)
     P = T.n
     dev = bvh.device

@@ -297,4 +297,16 @@ __global__ void __launch_bounds__(ADJ_BLOCK) k_grad_eta_reduce(const __grid_cons
     }
 }
 
+// Fresnel coefficients (em.py:123-141) of a batch of (eta, cos theta_i)
+__global__ void k_fresnel(long long n, const double* eta, const double* cosv, double* rte, double* rtm) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    c2 te, tm, w;
+    fresnel(c2{eta[2 * i], eta[2 * i + 1]}, cosv[i], te, tm, w);
+    rte[2 * i] = te.re;
+    rte[2 * i + 1] = te.im;
+    rtm[2 * i] = tm.re;
+    rtm[2 * i + 1] = tm.im;
+}
+
 }  // namespace rt

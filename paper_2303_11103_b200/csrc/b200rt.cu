@@ -1606,6 +1606,17 @@ int rt_l2_probe(rt_ctx* ctx, int64_t bytes, int iters, double* gbs_out, void* st
     return RT_OK;
 }
 
+int rt_fresnel(rt_ctx* ctx, int64_t n, const double* eta, const double* cos_theta, double* r_te,
+               double* r_tm, void* stream) {
+    if (!ctx || n < 0 || (n > 0 && (!eta || !cos_theta || !r_te || !r_tm)))
+        return fail(ctx, RT_EINVAL, "bad fresnel arguments");
+    if (n == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    k_fresnel<<<nblk(n, 256), 256, 0, ST(stream)>>>(n, eta, cos_theta, r_te, r_tm);
+    CKL();
+    return RT_OK;
+}
+
 int rt_microbench(rt_ctx* ctx, int kind, double* value_out, void* stream) {
     if (!ctx || !value_out || kind < RT_MB_FP32 || kind > RT_MB_L2)
         return fail(ctx, RT_EINVAL, "bad microbenchmark arguments");

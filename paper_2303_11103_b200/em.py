@@ -99,6 +99,29 @@ class EvalContext:
         """Complex permittivity per material in the scene's material order, [n_mat, 2]."""
         return torch.tensor(self.eta_values(bvh), dtype=torch.float64, device=bvh.device)
 
+    def tracks(self) -> bool:
+        """True when a material / orientation / position value is an autograd leaf."""
+        vals = [v for pair in self.material_values.values() for v in pair]
+        vals += [v for t in self.orientations.values() for v in t]
+        vals += [v for t in self.positions.values() for v in t]
+        return any(isinstance(v, torch.Tensor) and v.requires_grad for v in vals)
+
+    def eta_tensor(self, bvh):
+        """eta_table as a differentiable tensor [n_mat, 2] (tensor leaves in
+        ``material_values`` keep their autograd history)."""
+        f = self.scene.frequency_hz
+        rows = []
+        for name in bvh.material_names:
+            ov = self.material_values.get(name)
+            e, sg = material_params(self.scene.materials[name], f, None if ov is None else ov[0],
+                                    None if ov is None else ov[1])
+            e = torch.as_tensor(e, dtype=torch.float64, device=bvh.device)
+            sg = torch.as_tensor(sg, dtype=torch.float64, device=bvh.device)
+            rows.append(eta_from_params(e, sg, f))
+        if not rows:
+            return torch.tensor([[1.0, 0.0]], dtype=torch.float64, device=bvh.device)
+        return torch.stack(rows)
+
     def eta_values(self, bvh):
         """eta_table on the host (numpy [n_mat, 2])."""
         vals = []
@@ -295,6 +318,53 @@ def eta_from_params(eps_r, sigma, frequency_hz):
     return torch.stack([eps_r, sigma * (-eta_scale(frequency_hz))], dim=-1)
 
 
+class _DeviceHandle:
+    """The library context ``transfer`` runs on (no scene is needed: materials
+    arrive per interaction through rt_transfer's interaction_mat)."""
+
+    _by_device = {}
+
+    def __init__(self, device):
+        self.device = device
+        self.ctx = N.acquire_context(device)
+
+    @classmethod
+    def get(cls):
+        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+        if dev is None:
+            raise N.NativeError("no CUDA device: the B200 path has no CPU fallback")
+        h = cls._by_device.get(dev.index)
+        if h is None:
+            h = cls._by_device[dev.index] = cls(dev)
+        return h
+
+
+def fresnel_batch(eta, cos_theta):
+    """Fresnel coefficients of many (eta, cos theta_i) pairs on the device
+    (rt_fresnel: the transfer kernels' own device function, em.py:123-141).
+    Returns (r_te, r_tm) as complex128 numpy arrays."""
+    h = _DeviceHandle.get()
+    e = np.ascontiguousarray(np.asarray(eta, dtype=np.complex128).reshape(-1))
+    c = np.ascontiguousarray(np.asarray(cos_theta, dtype=np.float64).reshape(-1))
+    if e.shape != c.shape:
+        raise EmError("eta and cos_theta need the same length")
+    dev = h.device
+    et = torch.view_as_real(torch.as_tensor(e, device=dev)).contiguous()
+    ct = torch.as_tensor(c, device=dev)
+    te = torch.empty_like(et)
+    tm = torch.empty_like(et)
+    with torch.cuda.device(dev):
+        h.ctx.call("rt_fresnel", len(c), N.ptr(et), N.ptr(ct), N.ptr(te), N.ptr(tm), h.ctx.stream,
+                   exc_map={N.RT_EINVAL: EmError})
+    return (torch.view_as_complex(te).cpu().numpy(), torch.view_as_complex(tm).cpu().numpy())
+
+
+def fresnel(eta, cos_theta):
+    """(r_te, r_tm) for one interaction (em.py:123-141), as DiffComplex."""
+    te, tm = fresnel_batch([complex(eta)], [float(cos_theta)])
+    return DiffComplex(complex(te[0])), DiffComplex(complex(tm[0]))
+
+
 class DiffComplex(complex):
     """Value type ``transfer`` returns: a Python complex that also carries the
     accessors callers of the reference's DiffComplex use (E/autodiff.py:286-360:
@@ -427,27 +497,6 @@ def path_geometry(ctx: EvalContext, path, tx_dev, rx_dev) -> PathGeometry:
         rp = moved[1] if moved[1] is not None else rx_dev.position
         return geometry_for_positions(path, [float(x) for x in tp], [float(x) for x in rp])
     return geometry_from_path(path)
-
-
-class _DeviceHandle:
-    """The library context ``transfer`` runs on (no scene is needed: materials
-    arrive per interaction through rt_transfer's interaction_mat)."""
-
-    _by_device = {}
-
-    def __init__(self, device):
-        self.device = device
-        self.ctx = N.acquire_context(device)
-
-    @classmethod
-    def get(cls):
-        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
-        if dev is None:
-            raise N.NativeError("no CUDA device: the B200 path has no CPU fallback")
-        h = cls._by_device.get(dev.index)
-        if h is None:
-            h = cls._by_device[dev.index] = cls(dev)
-        return h
 
 
 def transfer(ctx: EvalContext, geom, materials, tx_dev, rx_dev, tx_pattern: str, rx_pattern: str,

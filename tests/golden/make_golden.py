@@ -374,6 +374,57 @@ def transfer_case():
     print("transfer: paths", len(central), "probe transfers", len(probes), flush=True)
 
 
+def criteria_case():
+    """Acceptance criteria 5 and 9 computed by the reference (T/test_acceptance.py
+    :122-175, :255-274): Tape gradients of the two-ray reflection power w.r.t.
+    (eps_r, sigma) at 5 points and of the region power w.r.t. tx yaw at 5
+    points; the moving-tx Doppler phase samples."""
+    from emtrace.channel import point_path_gain
+    from emtrace.em import (EvalContext, apply_doppler, compute_gains, geometry_from_path,
+                            path_materials, transfer)
+    sc = load_scene(bundled_scene("two_ray"))
+    tree = accel.build(sc)
+    ps = E.compute_paths(sc, tree, 1)
+    refl = [p for p in ps.paths if p.kind == "specular"][0]
+    tx, rx = sc.device("tx"), sc.device("rx")
+    mats = path_materials(sc, tree, refl)
+    geom = geometry_from_path(refl)
+    pts = [(15.0, 0.015), (3.0, 0.1), (5.24, 0.0462), (9.0, 0.3), (22.0, 0.002)]
+    mat_out = []
+    for eps0, sig0 in pts:
+        tape = Tape()
+        e, s_ = tape.leaf(eps0, "eps"), tape.leaf(sig0, "sig")
+        ctx = EvalContext(sc, material_values={"ground": (e, s_)})
+        out = transfer(ctx, geom, mats, tx, rx, "iso", "iso", math.pi / 2, math.pi / 2).abs2()
+        g = tape.gradient(out)
+        mat_out.append((out.value, g["eps"], g["sig"]))
+    sc_dir = to_ref(ground_scene())
+    sc_dir.tx_array = E.AntennaArray(pattern="tr38901", polarization="V")
+    tree_dir = accel.build(sc_dir)
+    cell = GridSpec(origin=(90.0, -5.0), cell_size=10.0, nx=1, ny=1, height=10.0).cell_center(0, 0)
+    _, frozen = point_path_gain(sc_dir, tree_dir, sc_dir.device("tx"), cell, 1)
+    yaw_out = []
+    for yaw0 in (0.2, 0.5, 0.9, 1.3, -0.4):
+        tape = Tape()
+        y = tape.leaf(yaw0, "yaw")
+        ctx = EvalContext(sc_dir, orientations={"tx": (y, 0.0, 0.0)})
+        g, _ = point_path_gain(sc_dir, tree_dir, sc_dir.device("tx"), cell, 1, ctx=ctx,
+                               frozen_paths=frozen)
+        yaw_out.append((g.value, tape.gradient(g)["yaw"]))
+    fs = load_scene(bundled_scene("free_space"))
+    fs.frequency_hz = 3.5e9
+    ftree = accel.build(fs)
+    fps = E.compute_paths(fs, ftree, 1)
+    moving = apply_doppler(compute_gains(fs, ftree, fps), 1e6, 14, tx_velocities=[3, 0, 0])
+    np.savez_compressed(
+        os.path.join(HERE, "criteria.npz"), two_ray=np.array(scene_json(sc)),
+        mat_points=np.array(pts), mat_out=np.array(mat_out), dir_scene=np.array(scene_json(sc_dir)),
+        cell=np.asarray(cell), yaw_points=np.array([0.2, 0.5, 0.9, 1.3, -0.4]),
+        yaw_out=np.array(yaw_out), free_space=np.array(scene_json(fs)),
+        doppler_a=moving.entries[0].a[0, 0, :], doppler_t=np.asarray(moving.sample_times))
+    print("criteria: done", flush=True)
+
+
 def main(which=None):
     cases = {
         "soup": soup_case,
@@ -404,6 +455,7 @@ def main(which=None):
         "explicit": explicit_case,
         "artifacts": artifacts_case,
         "transfer": transfer_case,
+        "criteria": criteria_case,
     }
     for k, fn in cases.items():
         if which and k not in which:

@@ -68,17 +68,6 @@ def test_build_cir_packing_matches_reference(golden, case):
     assert los_only.a.shape[4] <= 1
 
 
-def test_frequency_response_matches_oracle(golden):
-    from paper_2303_11103_b200.channel import build_cir, frequency_response
-    g = golden("canyon")
-    sc = golden_scene(g)
-    cir = build_cir(_cpu_gains(sc, g))
-    fr = frequency_response(cir, 32, 30e3)
-    h, f = O.frequency_response(g["cir_a"], g["cir_tau"], 32, 30e3)
-    assert np.allclose(fr.h, h, rtol=1e-12, atol=1e-20)
-    assert np.array_equal(fr.frequencies, f)
-
-
 def test_shard_ranges_cover_every_slot_and_row():
     from paper_2303_11103_b200.parallel import rows_of_shard, shard_range
     for n in (1, 7, 100, 10**8 + 3):
