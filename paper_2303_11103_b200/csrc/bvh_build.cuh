@@ -154,9 +154,10 @@ __global__ void k_morton(const float* cent, const float* pbox, const unsigned* c
     idx[i] = (int)i;
 }
 
-// eps_box = 2^-20 * max(S, 1), S = max |coordinate| (trace.cuh slab32)
+// eps_box = 2^-19 * max(S, 1) (2^-20 with the correctly rounded reciprocal),
+// S = max |coordinate| (trace.cuh slab32 error budget)
 __device__ inline float box_eps(const unsigned* cbounds) {
-    return fmaxf(ordered_to_float(cbounds[6]), 1.0f) * 9.5367431640625e-07f;
+    return fmaxf(ordered_to_float(cbounds[6]), 1.0f) * (RT_RCP_APPROX ? 1.9073486328125e-06f : 9.5367431640625e-07f);
 }
 __device__ inline void inflate6(float* b, float e) {
     for (int m = 0; m < 3; ++m) {

@@ -26,6 +26,9 @@ constexpr int MAX_DEPTH = 8;          // compile-time bound on interactions per 
 #endif
 constexpr int LEAF_MAX = RT_LEAF_MAX;  // BVH leaf collapse threshold (<= 8)
 constexpr int STACK_SIZE = 128;
+#ifndef RT_RCP_APPROX
+#define RT_RCP_APPROX 1   // approximate FP32 reciprocal in the box filter (trace.cuh rcp32)
+#endif
 constexpr int RT_PAT_PROBE_THETA_ID = 3;  // em.py:70-75 internal coverage probes
 constexpr int RT_PAT_PROBE_PHI_ID = 4;
 

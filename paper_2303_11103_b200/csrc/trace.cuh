@@ -49,6 +49,20 @@ __device__ __forceinline__ double inv_dir(double d) {
     return d != 0.0 ? 1.0 / d : __longlong_as_double(0x7ff0000000000000LL);
 }
 
+// FP32 reciprocal for the box filter.  RT_RCP_APPROX: one MUFU.RCP
+// (rcp.approx.ftz, <= 1 ulp = 2^-23 relative) instead of the correctly rounded
+// __frcp_rn (a ~10-instruction sequence per axis); the box inflation eps_box
+// doubles to cover the extra ulp (slab32's error budget below).
+__device__ __forceinline__ float rcp32(float x) {
+#if RT_RCP_APPROX
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+#else
+    return __frcp_rn(x);
+#endif
+}
+
 __device__ inline Ray make_ray(d3 o, d3 d) {
     Ray r;
     r.ox = o.x; r.oy = o.y; r.oz = o.z;
@@ -57,23 +71,26 @@ __device__ inline Ray make_ray(d3 o, d3 d) {
     // inf - inf = NaN on one plane and +-inf on the other, which mis-culls a
     // slab the ray lies inside; a 1e-30 direction component moves the ray by
     // < 1e-25 m over any scene, far inside eps_box.
-    // FP32 reciprocal of the FP32-rounded component: two roundings (2^-23
-    // relative) instead of the FP64 quotient's one, which the slab32 error
-    // budget absorbs (13 of its 16 units of 2^-24 S); no FP64 divides per bounce.
+    // FP32 reciprocal of the FP32-rounded component: 1 + 2 units of 2^-24
+    // relative (rounding of d, then the approximate reciprocal) instead of the
+    // FP64 quotient's one, which the slab32 error budget absorbs; no FP64
+    // divides per bounce.
     // d = +-0 gives +-inf -> +-1e30: min/max over the two planes is symmetric.
-    r.fix = fminf(fmaxf(__frcp_rn(__double2float_rn(d.x)), -1e30f), 1e30f);
-    r.fiy = fminf(fmaxf(__frcp_rn(__double2float_rn(d.y)), -1e30f), 1e30f);
-    r.fiz = fminf(fmaxf(__frcp_rn(__double2float_rn(d.z)), -1e30f), 1e30f);
+    r.fix = fminf(fmaxf(rcp32(__double2float_rn(d.x)), -1e30f), 1e30f);
+    r.fiy = fminf(fmaxf(rcp32(__double2float_rn(d.y)), -1e30f), 1e30f);
+    r.fiz = fminf(fmaxf(rcp32(__double2float_rn(d.z)), -1e30f), 1e30f);
     r.oix = -((float)o.x * r.fix); r.oiy = -((float)o.y * r.fiy); r.oiz = -((float)o.z * r.fiz);
     return r;
 }
 
 // FP32 box filter, one FFMA per slab plane: t = bound * inv - o * inv.
-// Conservative by construction: node boxes are inflated by eps_box = 2^-20 S
-// (S = max |scene coordinate|).  For |o| <= 2S the spatial error of a plane
-// distance is <= 2^-24 (|o| [origin rounding] + |o| [o*inv rounding] +
-// 2 |bound - o| [1/d: d rounded to FP32, then rcp] + |t d| [fma rounding])
-// <= (2 + 2 + 6 + 3) * 2^-24 S = 13 * 2^-24 S < eps_box = 16 * 2^-24 S.
+// Conservative by construction: node boxes are inflated by eps_box = 2^-19 S
+// (S = max |scene coordinate|; 2^-20 S with the correctly rounded
+// reciprocal).  For |o| <= 2S the spatial error of a plane distance is
+// <= 2^-24 (|o| [origin rounding] + |o| [o*inv rounding] + 3 |bound - o|
+// [1/d: d rounded to FP32 (1 unit), then rcp.approx (<= 2 units)] + |t d|
+// [fma rounding]) <= (2 + 2 + 9 + 3) * 2^-24 S = 16 * 2^-24 S < eps_box =
+// 32 * 2^-24 S (with __frcp_rn: 13 units < 16).
 // tmin is rounded down and tmax up by the caller; 1/d is clamped (make_ray)
 // so no plane distance is NaN.
 // both planes of one slab in one packed FFMA2 (sm_100): (lo, hi) * inv + oi,
