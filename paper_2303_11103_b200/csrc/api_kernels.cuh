@@ -297,6 +297,31 @@ __global__ void __launch_bounds__(ADJ_BLOCK) k_grad_eta_reduce(const __grid_cons
     }
 }
 
+// several device-to-device copies in one launch (blockIdx.y = segment):
+// rt_paths_get hands out the 11 path-table columns with one kernel instead
+// of 11 cudaMemcpyAsync calls
+struct CopySeg {
+    const unsigned char* src;
+    unsigned char* dst;
+    long long bytes;
+};
+struct CopyBatch {
+    CopySeg s[12];
+};
+__global__ void k_copy_batch(const __grid_constant__ CopyBatch B) {
+    const CopySeg& c = B.s[blockIdx.y];
+    if (!c.dst) return;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if ((c.bytes & 3) == 0 && (((unsigned long long)c.src | (unsigned long long)c.dst) & 3) == 0) {
+        const unsigned* a = reinterpret_cast<const unsigned*>(c.src);
+        unsigned* b = reinterpret_cast<unsigned*>(c.dst);
+        for (long long i = i0; i < c.bytes / 4; i += stride) b[i] = a[i];
+    } else {
+        for (long long i = i0; i < c.bytes; i += stride) c.dst[i] = c.src[i];
+    }
+}
+
 // Fresnel coefficients (em.py:123-141) of a batch of (eta, cos theta_i)
 __global__ void k_fresnel(long long n, const double* eta, const double* cosv, double* rte, double* rtm) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;

@@ -87,10 +87,9 @@ struct rt_ctx {
     bool bvh_ready = false;
     int bvh_depth = -1;           // deepest BNode (root 0); -1 = not measured
     bool tail_smem_set = false;   // k_ploc_tail's dynamic shared memory opt-in done
-    double origin_limit = 0.0;
     bool has_skip = false;        // origin skip table built with the tree (bvh_ploc.cuh)
     DevBuf tree_diag;             // [0] deepest BNode; doubles at +8: surface-area sums
-    int diag_root = -1;           // root id of the last PLOC/SAH tree for the SAH estimate
+    const int* diag_root_dev = nullptr;   // device root id of the last tree (SAH estimate)
     bool diag_pending = false;    // tree diagnostics not yet read back
     cudaEvent_t diag_ev = nullptr;  // end of the last build on the caller's stream
     // candidates
@@ -180,7 +179,7 @@ rt::Bvh bvh_dev(rt_ctx* ctx) {
     b.nodes = ctx->nodes.get<BNode>();
     b.tris = ctx->tris.get<TriRec>();
     b.n_prims = (int)ctx->n_prims;
-    b.origin_limit = ctx->origin_limit;
+    b.origin_limit = reinterpret_cast<const double*>(ctx->cbounds.get<char>() + 32);
     b.skip = ctx->has_skip ? ctx->skip_tab.get<int>() : nullptr;
     b.err = reinterpret_cast<int*>(ctx->dflag.get<long long>());
     return b;
@@ -256,30 +255,38 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st, boo
     }
     CK(ctx->s_perm.reserve(sizeof(int) * n));
     CK(ctx->s_perm_alt.reserve(sizeof(int) * n));
-    CK(ctx->s_keys.reserve(sizeof(unsigned) * n));
-    CK(ctx->s_keys_alt.reserve(sizeof(unsigned) * n));
+    CK(ctx->s_keys.reserve(sizeof(unsigned long long) * n));
+    CK(ctx->s_keys_alt.reserve(sizeof(unsigned long long) * n));
     CK(ctx->s_flag.reserve(sizeof(int) * (n + 1)));
     CK(ctx->s_pos.reserve(sizeof(int) * (n + 1)));
     int* perm = ctx->s_perm.get<int>();
     int* perm_alt = ctx->s_perm_alt.get<int>();
-    unsigned* keys = ctx->s_keys.get<unsigned>();
-    unsigned* keys_alt = ctx->s_keys_alt.get<unsigned>();
+    unsigned long long* keys = ctx->s_keys.get<unsigned long long>();
+    unsigned long long* keys_alt = ctx->s_keys_alt.get<unsigned long long>();
     const int* seq = ctx->s_seq.get<int>();
     const signed char* len = ctx->s_len.get<signed char>();
     k_iota<<<nblk(n, 256), 256, 0, st>>>(perm, n);
     CKL();
-    int W = bits_for(ctx->n_prims + 1);
-    // passes: digit L-1, ..., digit 0, length (most significant last)
-    for (int pass = 0; pass <= L; ++pass) {
-        int j = pass < L ? (L - 1 - pass) : L;
-        int end_bit = pass < L ? W : 4;
-        k_digit_column<<<nblk(n, 256), 256, 0, st>>>(n, seq, len, L, j, perm, keys);
+    // LSD over groups of digit columns packed into 64-bit keys (W bits per
+    // column, the row length above the most significant group): C3 (W = 18,
+    // L = 5) sorts twice instead of six times, the C2 canyon (W = 11, L = 3) once
+    const int W = bits_for(ctx->n_prims + 1);
+    const int per = std::max(1, 60 / W);
+    for (int hi = L - 1; hi >= -1;) {
+        int lo = std::max(0, hi - per + 1);
+        int ncol = hi >= 0 ? hi - lo + 1 : 0;
+        int with_len = (lo == 0 && ncol * W + 4 <= 64) || hi < 0;
+        if (hi < 0) lo = 0;
+        int end_bit = ncol * W + (with_len ? 4 : 0);
+        k_digit_columns<<<nblk(n, 256), 256, 0, st>>>(n, seq, len, L, lo, hi, W, with_len, perm, keys);
         CKL();
         RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
             return cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys_alt, perm, perm_alt,
                                                    (int)n, 0, end_bit, st);
         }));
         std::swap(perm, perm_alt);
+        if (with_len) break;
+        hi = lo == 0 ? -1 : lo - 1;
     }
     if (unique_in) {
         CK(ctx->cand_seq.reserve(sizeof(int) * n * L));
@@ -315,7 +322,7 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st, boo
     return RT_OK;
 }
 
-int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st);
+int finish_tree(rt_ctx* ctx, long long n, const int* root_p, cudaStream_t st);
 int tree_diagnostics(rt_ctx* ctx, cudaStream_t st);
 int build_morton(rt_ctx* ctx, long long n, cudaStream_t st);
 
@@ -371,14 +378,14 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     int* sidx = ctx->sorted_idx.get<int>();
     const float* pbox = ctx->pbox.get<float>();
     const float* cent = ctx->cent.get<float>();
-    // device ints: [0,1] big ranges (ping-pong), [2,3] their chunks, [4,5] medium
-    // ranges (ping-pong), [6] small ranges, [7] root
+    // device ints: [0,1] big ranges (ping-pong), [2,3] their chunks, [4,5,8] medium
+    // range counters (3-way rotation), [6] small ranges, [7] root
     int* dc = reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 16);
     k_iota<<<nblk(n, 256), 256, 0, st>>>(sidx, n);
     CKL();
     k_ploc_init<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, pbox, box, idx0, cnt, em);
     CKL();
-    int h[8] = {0, 0, 0, 0, 0, 0, 0, -1};
+    int h[12] = {0, 0, 0, 0, 0, 0, 0, -1, 0, 0, 0, 0};
     SahTask root_task{0, (int)n, -1, 0};
     if (n <= small_max) {
         h[6] = 1;
@@ -434,17 +441,21 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     // ranges of small_max < m <= SAH_BIG prims: SAH_MED_BATCH levels per host
     // round trip, each grid sized by the bound (ranges at most double per level;
     // CTAs past the live count exit at once)
-    const int SAH_MED_BATCH = 8;
-    int mcur = 0;
+    // small scenes take all their medium levels in one batch (one host sync)
+    const int SAH_MED_BATCH = n <= SAH_LATENCY_PRIMS ? 16 : 8;
+    // level k reads counter mc[k % 3], fills mc[(k + 1) % 3] and zeroes
+    // mc[(k + 2) % 3] for the level after it: no memset per level
+    int* mc[3] = {dc + 4, dc + 5, dc + 8};
+    int mcur = 0, lvl = 0;
     long long nmed = h[4];
     while (nmed > 0) {
         long long bound = nmed;
-        for (int b = 0; b < SAH_MED_BATCH; ++b) {
+        for (int b = 0; b < SAH_MED_BATCH; ++b, ++lvl) {
             int nx = mcur ^ 1;
-            SahOut O{small_max, small, dc + 6, med[nx], dc + 4 + nx, nullptr, nullptr, nullptr, nullptr, nullptr};
-            CK(cudaMemsetAsync(dc + 4 + nx, 0, 4, st));
-            k_sah_large<<<bound, SAH_BLOCK, 0, st>>>(med[mcur], dc + 4 + mcur, idx0, idx1, pbox, cent, (int)n,
-                                                     box, child, par, cnt, dc + 7, O);
+            SahOut O{small_max, small, dc + 6, med[nx], mc[(lvl + 1) % 3], nullptr, nullptr, nullptr, nullptr,
+                     nullptr};
+            k_sah_large<<<bound, SAH_BLOCK, 0, st>>>(med[mcur], mc[lvl % 3], mc[(lvl + 2) % 3], idx0, idx1, pbox,
+                                                     cent, (int)n, box, child, par, cnt, dc + 7, O);
             CKL();
             mcur = nx;
             ++levels;
@@ -452,7 +463,7 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
         }
         CK(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        nmed = h[4 + mcur];
+        nmed = h[lvl % 3 == 2 ? 8 : 4 + lvl % 3];
         if (levels > 4096) return fail(ctx, RT_ECUDA, "SAH build made no progress");
     }
     if (h[6] > 0) {
@@ -463,12 +474,10 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
     k_sah_emitted<<<nblk(n, 256), 256, 0, st>>>((int)n, par, child, cnt, em, ctx->flags.get<int>());
     CKL();
-    int root = -1;
-    CK(cudaMemcpyAsync(&root, dc + 7, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (root < (int)n) return fail(ctx, RT_ECUDA, "SAH build produced no root");
     ctx->counters[9] = levels;
-    return finish_tree(ctx, n, root, st);
+    // the root id stays on the device (dc[7], written by the split that had no
+    // parent): no host round trip
+    return finish_tree(ctx, n, dc + 7, st);
 }
 
 // PLOC hierarchy over the Morton-sorted prims (sorted_idx), then the
@@ -547,12 +556,15 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
         CK(cudaStreamSynchronize(st));
     }
     ctx->counters[9] = iters;
-    return finish_tree(ctx, n, root, st);
+    int* root_dev = reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 24);   // past dc[0..11]
+    CK(cudaMemcpyAsync(root_dev, &root, 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));   // `root` is a stack variable
+    return finish_tree(ctx, n, root_dev, st);
 }
 
 // depth-first child-pair layout + triangle records of a hierarchy in the PLOC
 // arrays (leaves [0, n) with sorted_idx, internal nodes [n, 2n-1), root id)
-int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st) {
+int finish_tree(rt_ctx* ctx, long long n, const int* root, cudaStream_t st) {
     int* em = ctx->pl_em.get<int>();
     float* box = ctx->pl_box.get<float>();
     int* cnt = ctx->pl_count.get<int>();
@@ -592,7 +604,7 @@ int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st) {
         CK(ctx->skip_tab.reserve(8ULL * n));
         CK(ctx->flags.reserve(4ULL * n));
         CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
-        CK(cudaMemsetAsync(par + root, 0xFF, 4, st));   // the refit climb stops at the root
+        k_root_parent<<<1, 1, 0, st>>>(root, par);   // the refit climb stops at the root
         k_dbox_refit<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, ctx->v0.get<double>(), ctx->e1.get<double>(),
                                                    ctx->e2.get<double>(), par, child, ctx->dbox.get<double>(),
                                                    ctx->flags.get<int>());
@@ -607,7 +619,7 @@ int finish_tree(rt_ctx* ctx, long long n, int root, cudaStream_t st) {
     CKL();
     // tree diagnostics (depth, surface-area estimate) are computed on demand by
     // rt_get_profile: no host round trip on the build path
-    ctx->diag_root = (n > 2 && dfs) ? root : -1;
+    ctx->diag_root_dev = (n > 2 && dfs) ? root : nullptr;
     ctx->diag_pending = n > 1;
     if (!ctx->diag_ev) CK(cudaEventCreateWithFlags(&ctx->diag_ev, cudaEventDisableTiming));
     CK(cudaEventRecord(ctx->diag_ev, st));
@@ -625,9 +637,12 @@ int tree_diagnostics(rt_ctx* ctx, cudaStream_t st) {
     CK(cudaStreamSynchronize(st));
     ctx->bvh_depth = h;
     ctx->counters[13] = h;
-    if (ctx->diag_root < 0) return RT_OK;
-    int n_nodes = 0;
-    CK(cudaMemcpyAsync(&n_nodes, ctx->pl_em.get<int>() + ctx->diag_root, 4, cudaMemcpyDeviceToHost, st));
+    if (!ctx->diag_root_dev) return RT_OK;
+    int root = -1, n_nodes = 0;
+    CK(cudaMemcpyAsync(&root, ctx->diag_root_dev, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (root < 0) return RT_OK;
+    CK(cudaMemcpyAsync(&n_nodes, ctx->pl_em.get<int>() + root, 4, cudaMemcpyDeviceToHost, st));
     double* sums = reinterpret_cast<double*>(ctx->tree_diag.get<int>() + 2);
     CK(cudaMemsetAsync(sums, 0, 24, st));
     CK(cudaStreamSynchronize(st));
@@ -704,8 +719,7 @@ int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
     CK(ctx->prim_mat.reserve(4 * n));
     CK(ctx->pbox.reserve(24 * n));
     CK(ctx->cent.reserve(12 * n));
-    CK(ctx->cbounds.reserve(32));
-    ctx->origin_limit = 0.0;
+    CK(ctx->cbounds.reserve(48));   // 7 ordered floats, then the FP32 filter's origin bound (double at +32)
     if (n_prims == 0) return RT_OK;
     CK(cudaMemcpyAsync(ctx->prim_mat.p, prim_material, 4 * n_prims, cudaMemcpyDeviceToDevice, st));
     // ordered-float bounds: mins start at 0xFFFFFFFF, maxima (and the scale) at 0
@@ -727,15 +741,11 @@ int rt_bvh_build(rt_ctx* ctx, void* stream) {
     ctx->bvh_ready = true;
     ctx->has_skip = false;
     if (n == 0) return RT_OK;
-    {   // scene scale S (ordered float in cbounds[6]) -> FP32 filter origin bound 2S
-        unsigned u = 0;
-        CK(cudaMemcpyAsync(&u, ctx->cbounds.get<unsigned>() + 6, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        unsigned v = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
-        float S;
-        memcpy(&S, &v, 4);
-        ctx->origin_limit = 2.0 * std::max((double)S, 1.0);
-    }
+    // scene scale S (ordered float in cbounds[6]) -> FP32 filter origin bound 2S,
+    // computed on the device (no host round trip)
+    k_origin_limit<<<1, 1, 0, st>>>(ctx->cbounds.get<unsigned>(),
+                                    reinterpret_cast<double*>(ctx->cbounds.get<char>() + 32));
+    CKL();
     CK(ctx->tris.reserve(sizeof(TriRec) * n));
     CK(ctx->sorted_idx.reserve(4 * n));
     CK(ctx->nodes.reserve(sizeof(BNode) * std::max<long long>(n - 1, 1)));
@@ -1387,20 +1397,21 @@ int rt_paths_get(rt_ctx* ctx, int32_t* rx_index, int32_t* cand, int8_t* order, i
     cudaStream_t st = ST(stream);
     size_t P = ctx->n_paths, L = ctx->path_L;
     if (!P) return RT_OK;
-    auto cp = [&](void* dst, const DevBuf& src, size_t bytes) -> cudaError_t {
-        return dst ? cudaMemcpyAsync(dst, src.p, bytes, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
-    };
-    CK(cp(rx_index, ctx->p_rx, 4 * P));
-    CK(cp(cand, ctx->p_cand, 4 * P));
-    CK(cp(order, ctx->p_order, P));
-    CK(cp(seq, ctx->p_seq, 4 * P * L));
-    CK(cp(vertices, ctx->p_verts, 24 * P * (L + 2)));
-    CK(cp(length, ctx->p_len, 8 * P));
-    CK(cp(delay, ctx->p_delay, 8 * P));
-    CK(cp(k_dep, ctx->p_kdep, 24 * P));
-    CK(cp(k_arr, ctx->p_karr, 24 * P));
-    CK(cp(normals, ctx->p_nrm, 24 * P * L));
-    CK(cp(cos_inc, ctx->p_cos, 8 * P * L));
+    void* dsts[11] = {rx_index, cand, order, seq, vertices, length, delay, k_dep, k_arr, normals, cos_inc};
+    const DevBuf* srcs[11] = {&ctx->p_rx, &ctx->p_cand, &ctx->p_order, &ctx->p_seq, &ctx->p_verts, &ctx->p_len,
+                              &ctx->p_delay, &ctx->p_kdep, &ctx->p_karr, &ctx->p_nrm, &ctx->p_cos};
+    const size_t bytes[11] = {4 * P, 4 * P, P, 4 * P * L, 24 * P * (L + 2), 8 * P, 8 * P, 24 * P, 24 * P,
+                              24 * P * L, 8 * P * L};
+    CopyBatch B{};
+    size_t most = 0;
+    for (int k = 0; k < 11; ++k) {
+        B.s[k] = CopySeg{srcs[k]->get<unsigned char>(), static_cast<unsigned char*>(dsts[k]), (long long)bytes[k]};
+        if (dsts[k]) most = std::max(most, bytes[k]);
+    }
+    if (!most) return RT_OK;
+    dim3 grid((unsigned)std::min<long long>(nblk((long long)(most + 3) / 4, 256), 4096), 11);
+    k_copy_batch<<<grid, 256, 0, st>>>(B);
+    CKL();
     return RT_OK;
 }
 

@@ -154,6 +154,11 @@ __global__ void k_morton(const float* cent, const float* pbox, const unsigned* c
     idx[i] = (int)i;
 }
 
+// FP32 box filter origin bound 2 max(S, 1) (trace.cuh ray_fast)
+__global__ void k_origin_limit(const unsigned* cbounds, double* out) {
+    *out = 2.0 * fmax((double)ordered_to_float(cbounds[6]), 1.0);
+}
+
 // eps_box = 2^-19 * max(S, 1) (2^-20 with the correctly rounded reciprocal),
 // S = max |coordinate| (trace.cuh slab32 error budget)
 __device__ inline float box_eps(const unsigned* cbounds) {

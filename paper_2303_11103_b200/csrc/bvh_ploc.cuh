@@ -227,10 +227,11 @@ __global__ void k_ploc_compact(const int* out, const int* valid, const int* pos,
 
 // depth-first triangle slot of every leaf: sum of left-sibling subtree sizes
 // over the ancestors where the path comes from the right child
-__global__ void k_ploc_slots(int n, const int* parent, const int* child, const int* count, int root,
+__global__ void k_ploc_slots(int n, const int* parent, const int* child, const int* count, const int* root_p,
                              int* slot) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
+    const int root = *root_p;
     int off = 0, node = k;
     while (node != root) {
         int p = parent[node];
@@ -257,10 +258,11 @@ __device__ inline int ploc_map(int id, int n, int root) {   // internal id -> BN
 // emitted nodes before it in preorder = its proper ancestors + the emitted
 // nodes of every left sibling subtree on the way up.  Parent and left child are
 // then adjacent in memory (same 128-byte line half the time).  -1 = collapsed.
-__global__ void k_ploc_dfs(int n, int root, const int* parent, const int* child, const int* count,
+__global__ void k_ploc_dfs(int n, const int* root_p, const int* parent, const int* child, const int* count,
                            const int* emitted, int* dfs, int* max_depth) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n - 1) return;
+    const int root = *root_p;
     int id = n + q;
     if (id != root && count[id] <= LEAF_MAX) { dfs[q] = -1; return; }
     int idx = 0, node = id, depth = 0;
@@ -276,10 +278,11 @@ __global__ void k_ploc_dfs(int n, int root, const int* parent, const int* child,
     atomicMax(max_depth, depth);   // BNode depth (root 0): bounds the traversal stack
 }
 
-__global__ void k_ploc_layout(int n, int root, const int* child, const int* count, const int* slot,
+__global__ void k_ploc_layout(int n, const int* root_p, const int* child, const int* count, const int* slot,
                               const float* nbox, const unsigned* cbounds, const int* dfs, BNode* out) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n - 1) return;
+    const int root = *root_p;
     int id = n + q;
     if (dfs && dfs[q] < 0) return;   // collapsed into a leaf of its parent
     float eps = box_eps(cbounds);
@@ -296,6 +299,9 @@ __global__ void k_ploc_layout(int n, int root, const int* child, const int* coun
     }
     out[dfs ? dfs[q] : ploc_map(id, n, root)] = pack_bnode(bx, ref[0], ref[1]);
 }
+
+// the root's parent is -1 (the refit and slot climbs stop there)
+__global__ void k_root_parent(const int* root_p, int* parent) { parent[*root_p] = -1; }
 
 // ---- origin skip table ------------------------------------------------------------------
 //
@@ -342,11 +348,12 @@ __global__ void k_dbox_refit(int n, const int* sorted_idx, const double* v0, con
 
 // one thread per leaf: skip[2 p + s] for prim p, s = 1 for rays leaving to the
 // side the stored normal points to, 0 for the other (EMPTY_REF = nothing)
-__global__ void k_skip_table(int n, int root, const int* sorted_idx, const int* parent, const int* child,
-                             const int* count, const int* slot, const int* dfs, const double* dbox,
-                             const double* nrm, const double* poff, int* skip) {
+__global__ void k_skip_table(int n, const int* root_p, const int* sorted_idx, const int* parent,
+                             const int* child, const int* count, const int* slot, const int* dfs,
+                             const double* dbox, const double* nrm, const double* poff, int* skip) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
+    const int root = *root_p;
     int p = sorted_idx[k];
     double nx = nrm[3 * (long long)p], ny = nrm[3 * (long long)p + 1], nz = nrm[3 * (long long)p + 2];
     double c = poff[p];

@@ -274,10 +274,14 @@ __device__ void sah_emit(const SahTask& T, const float box[6], const int* sp, in
 // ---- ranges of small_max < m <= SAH_BIG prims: one CTA each ----------------------------
 
 __global__ void __launch_bounds__(SAH_BLOCK) k_sah_large(const SahTask* __restrict__ tasks, const int* d_ntask,
-                                                        int* idx0, int* idx1, const float* __restrict__ pbox,
+                                                        int* zero_after_next, int* idx0, int* idx1,
+                                                        const float* __restrict__ pbox,
                                                         const float* __restrict__ cent, int n, float* nbox,
                                                         int* child, int* parent, int* count, int* root_out,
                                                         SahOut O) {
+    // the counter the level after next fills: nobody reads or writes it during
+    // this level (the caller's 3-way rotation), so clear it here
+    if (blockIdx.x == 0 && threadIdx.x == 0 && zero_after_next) *zero_after_next = 0;
     if ((int)blockIdx.x >= *d_ntask) return;
     const SahTask T = tasks[blockIdx.x];
     const int* src = (T.side >> 1) & 1 ? idx1 : idx0;

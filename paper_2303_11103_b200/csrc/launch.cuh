@@ -246,17 +246,23 @@ __global__ void k_trie_sequences(long long cap, const unsigned long long* keys, 
 
 // LSD radix passes over the digit columns: key of row perm[r] at column j
 // (prim + 1, 0 = padding) or, for j == max_len, the sequence length.
-__global__ void k_digit_column(long long n, const int* seq, const signed char* len, int max_len,
-                               int j, const int* perm, unsigned* keys) {
+// key of row perm[r] over digit columns j_lo..j_hi (j_lo most significant),
+// W bits each (prim + 1, 0 past the row's length), with the row length above
+// them when with_len: several LSD digits in one 64-bit radix sort
+__global__ void k_digit_columns(long long n, const int* seq, const signed char* len, int max_len,
+                                int j_lo, int j_hi, int W, int with_len, const int* perm,
+                                unsigned long long* keys) {
     long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (r >= n) return;
     long long row = perm[r];
-    unsigned v;
-    if (j == max_len) v = (unsigned)len[row];
-    else {
+    int ln = len[row];
+    unsigned long long v = 0;
+    for (int j = j_lo; j <= j_hi; ++j) {
         int p = seq[row * max_len + j];
-        v = (j < len[row] && p >= 0) ? (unsigned)(p + 1) : 0u;
+        unsigned d = (j < ln && p >= 0) ? (unsigned)(p + 1) : 0u;
+        v = (v << W) | d;
     }
+    if (with_len) v |= (unsigned long long)ln << (W * (j_hi - j_lo + 1));
     keys[r] = v;
 }
 

@@ -189,7 +189,7 @@ struct Bvh {
     const TriRec* __restrict__ tris;
     const int* __restrict__ skip;   // origin skip table [2 * n_prims] (bvh_ploc.cuh) or null
     int n_prims;
-    double origin_limit;   // |o_i| bound for the FP32 filter (else the FP64 one)
+    const double* origin_limit;   // device: |o_i| bound for the FP32 filter (else the FP64 one)
     int* err;              // device error word: bit 0 = traversal stack overflow
 };
 
@@ -205,7 +205,7 @@ __device__ __forceinline__ int origin_skip(const Bvh& bvh, int prim, double n_do
 
 // the FP32 filter is valid for origins within origin_limit (slab32)
 __device__ __forceinline__ bool ray_fast(const Bvh& bvh, const Ray& r) {
-    return fmax(fmax(fabs(r.ox), fabs(r.oy)), fabs(r.oz)) <= bvh.origin_limit;
+    return fmax(fmax(fabs(r.ox), fabs(r.oy)), fabs(r.oz)) <= __ldg(bvh.origin_limit);
 }
 
 // FP32 lower bound of t_min for the box filter.  The common t_min = RAY_EPS is
