@@ -113,21 +113,23 @@ TRAFFIC_JSON = "profiles/r02_traffic.json"
 
 
 def committed_traffic(args, field="dram_bytes_per_launch"):
-    """Per-launch k_launch figure (DRAM bytes, or warp instructions executed with
-    field="warp_instructions_per_launch") from the committed `ncu --set full`
-    capture of this same workload (tools/ncu_summary.py full ... <json>); None if
-    absent or the capture was of another configuration."""
+    """Per-launch k_launch figure (DRAM / L2 / L1 bytes, or warp instructions
+    executed with field="warp_instructions_per_launch") from the committed
+    `ncu --set full` capture of this same workload (TRAFFIC_JSON holds one
+    capture per workload, written by tools/ncu_summary.py full ... <json>);
+    None when no capture of this configuration is committed."""
     import json as _json
     path = os.path.join(REPO, TRAFFIC_JSON)
     if not os.path.exists(path):
         return None
     d = _json.load(open(path))
-    if d.get("workload") != workload_name(args) or float(d.get("num_rays", -1)) != float(args.rays) \
-            or int(d.get("max_depth", -1)) != int(args.depth):
-        return None
-    for k, v in d.get(field, {}).items():
-        if "k_launch" in k:
-            return float(v)
+    for cap in d.get("captures", [d]):
+        if cap.get("workload") != workload_name(args) or float(cap.get("num_rays", -1)) != float(args.rays) \
+                or int(cap.get("max_depth", -1)) != int(args.depth):
+            continue
+        for k, v in cap.get(field, {}).items():
+            if "k_launch" in k:
+                return float(v)
     return None
 
 
@@ -374,9 +376,14 @@ def roofline(args, pk, hbm_peak, bounces, bytes_per_bounce, nodes_pb, tris_pb, t
     dram = committed_traffic(args, "dram_bytes_per_launch")
     out = {}
     sec = {}
-    sec["l1"] = {"achieved": alg / t_launch / 1e9, "peak": pk["l1_read_gbs"], "unit": "GB/s",
-                 "frac": alg / t_launch / 1e9 / pk["l1_read_gbs"],
-                 "bytes": "algorithmic: 64 B per node visit + 80 B per triangle test"}
+    l1 = committed_traffic(args, "l1tex_bytes_per_launch")
+    if l1 is not None:
+        sec["l1"] = {"achieved": l1 / t_launch / 1e9, "peak": pk["l1_read_gbs"], "unit": "GB/s",
+                     "frac": l1 / t_launch / 1e9 / pk["l1_read_gbs"],
+                     "bytes": "ncu l1tex global-load sectors x 32 B per launch (" + TRAFFIC_JSON + ")"}
+    sec["lane_bytes"] = {"achieved": alg / t_launch / 1e9, "unit": "GB/s",
+                         "bytes": "algorithmic, per lane: 64 B per node visit + 80 B per triangle test; "
+                                  "coherent lanes share each L1 line, so this exceeds any cache bandwidth"}
     if lts is not None:
         sec["l2"] = {"achieved": lts / t_launch / 1e9, "peak": pk["l2_read_gbs"], "unit": "GB/s",
                      "frac": lts / t_launch / 1e9 / pk["l2_read_gbs"],
@@ -402,9 +409,9 @@ def roofline(args, pk, hbm_peak, bounces, bytes_per_bounce, nodes_pb, tris_pb, t
                "achieved_source": TRAFFIC_JSON + " ncu inst_executed of this workload / this run's "
                                                  "k_launch CUDA-event time",
                "peak_source": "rt_microbench kind 2 measured in this run (imm-form FFMA chains)"}
-    else:   # no committed capture of this workload: the live L1-bytes bound
-        out = dict(sec["l1"], bound="l1", kernel="k_launch", traffic=dram,
-                   peak_source="rt_microbench kind 3 measured in this run")
+    else:   # no committed capture of this workload: FP32 work vs the measured FP32 peak
+        out = dict(sec["fp32"], bound="fp32 (no committed ncu capture of this workload)",
+                   kernel="k_launch", traffic=dram, peak_source="rt_microbench kind 0 measured in this run")
     out["traffic_source"] = TRAFFIC_JSON if dram is not None else None
     out["bytes_per_bounce"] = bytes_per_bounce
     out["secondary"] = sec

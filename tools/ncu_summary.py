@@ -1,7 +1,9 @@
 """Summarise ncu outputs into profiles/ (launch list shares + per-kernel metrics).
 
 usage: python tools/ncu_summary.py launches <launches.csv> <out.md>
-       python tools/ncu_summary.py full <report.ncu-rep> <out.md>
+       python tools/ncu_summary.py full <report.ncu-rep> <out.md> [<traffic.json> <bench args...>]
+The traffic JSON keeps one capture per bench workload (bench.py committed_traffic);
+the bench args (e.g. --config c5) name the workload the capture was taken of.
 """
 import csv
 import io
@@ -43,7 +45,7 @@ KEYS = ["Duration", "Compute (SM) Throughput", "Memory Throughput", "DRAM Throug
         "Warp Cycles Per Issued Instruction", "Branch Efficiency", "Executed Instructions"]
 
 
-def full(path, out, traffic_json=None):
+def full(path, out, traffic_json=None, *bench_args):
     txt = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
@@ -113,10 +115,19 @@ def full(path, out, traffic_json=None):
             for k, v in m.items():
                 acc.setdefault(k[1], []).append(v)
             return {k: sum(v) / len(v) for k, v in acc.items()}
-        json.dump({"source": path, "dram_bytes_per_launch": per_kernel(dram),
-                   "warp_instructions_per_launch": per_kernel(insts),
-                   "lts_bytes_per_launch": per_kernel(lts), "l1tex_bytes_per_launch": per_kernel(l1)},
-                  open(traffic_json, "w"), indent=1)
+        import os
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        args = bench.parse(list(bench_args))
+        cap = {"source": path, "workload": bench.workload_name(args), "num_rays": int(args.rays),
+               "max_depth": args.depth,
+               "dram_bytes_per_launch": per_kernel(dram), "warp_instructions_per_launch": per_kernel(insts),
+               "lts_bytes_per_launch": per_kernel(lts), "l1tex_bytes_per_launch": per_kernel(l1)}
+        caps = []
+        if os.path.exists(traffic_json):
+            old = json.load(open(traffic_json))
+            caps = [c for c in old.get("captures", [old]) if c.get("workload") != cap["workload"]]
+        json.dump({"captures": caps + [cap]}, open(traffic_json, "w"), indent=1)
 
 
 if __name__ == "__main__":
