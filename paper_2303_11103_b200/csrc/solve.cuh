@@ -519,6 +519,9 @@ __device__ inline void probe_powers(const Geom& g, const EmParams& E, double& pt
     pp = ap.re * ap.re + ap.im * ap.im;
 }
 
+#ifndef RT_VAL_PREFETCH
+#define RT_VAL_PREFETCH 1
+#endif
 #ifndef RT_VAL_MINB
 #define RT_VAL_MINB 8   // 64 registers: C3 validate 3.60 ms vs 4.65 (minB 1, 110 regs), 3.84 (minB 6)
 #endif
@@ -536,6 +539,10 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_validate(Cands C, SceneDev
         long long i = it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
         bool ok = false;
         Rec rec;
+#if RT_VAL_PREFETCH
+        // the next iteration's item streams from HBM: start pulling it into L2 now
+        if (i + stride < n_pend) asm volatile("prefetch.global.L2 [%0];" ::"l"(pend + i + stride));
+#endif
         if (i < n_pend) {
             Pending pd = pend[i];
             d3 rx = receiver_pos(R, pd.rx);
