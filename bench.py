@@ -225,11 +225,20 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    # BENCH_DIST_BACKEND=gloo is a plumbing check of the sharded legs on a box
+    # with fewer GPUs than ranks (ranks share devices round-robin); measurements
+    # use NCCL with one GPU per rank
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        os.environ.setdefault("NCCL_DEBUG", "INFO")   # rank count visible in the NCCL log
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")   # rank count visible in the NCCL log
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
 
 
@@ -490,7 +499,9 @@ def c4_latency(args, rank=0, world=1):
         vec = torch.stack([lo.detach()] + [v.grad for pair in vals.values() for v in pair])
         if world > 1:
             import torch.distributed as dist
-            dist.all_reduce(vec)
+            w = parallel._wire(dist, vec)
+            dist.all_reduce(w)
+            vec = w
         host = vec.tolist()
         t1 = time.perf_counter()
         loss = host[0]
@@ -605,6 +616,9 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
+    # torchrun sets OMP_NUM_THREADS=1 for every rank; the reference arm runs on
+    # rank 0 alone and uses all host cores (read when the oracle's libgomp loads)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
     sc, tx, grid = make_workload(args)
     cb = cpu_baseline(args, sc, tx, grid, steps=args.warmup + args.steps)
     return {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
