@@ -206,12 +206,23 @@ int clear_flags(rt_ctx* ctx, cudaStream_t st) {
     return RT_OK;
 }
 
-int check_flags(rt_ctx* ctx, cudaStream_t st) {
-    RC(fetch(ctx, ctx->dflag.p, 1, st));
-    long long f = ctx->hpin[0];
+int flags_status(rt_ctx* ctx, long long f) {
     if (f & 1) return fail(ctx, RT_ECUDA, "BVH traversal stack overflow");
     if (f & 4) return fail(ctx, RT_ECOINCIDE, "transmitter and probe/receiver coincide");
     return RT_OK;
+}
+
+int check_flags(rt_ctx* ctx, cudaStream_t st) {
+    RC(fetch(ctx, ctx->dflag.p, 1, st));
+    return flags_status(ctx, ctx->hpin[0]);
+}
+
+// n 8-byte words -> hpin[0..n) and the error word -> hpin[n], one host sync
+int fetch_and_flags(rt_ctx* ctx, const void* dev, int n, cudaStream_t st) {
+    CK(cudaMemcpyAsync(ctx->hpin, dev, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ctx->hpin + n, ctx->dflag.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return flags_status(ctx, ctx->hpin[n]);
 }
 
 void prof_mark(rt_ctx* ctx, int stage, int end, cudaStream_t st) {
@@ -975,7 +986,7 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
             CKL();
         }
         PROF_END(ST_LAUNCH);
-        RC(fetch(ctx, ctr, 9, st));
+        RC(fetch_and_flags(ctx, ctr, 9, st));   // counters + the error word, one round trip
         ctx->counters[1] = ctx->hpin[3];
         ctx->counters[2] = ctx->hpin[4];
         ctx->counters[10] = ctx->hpin[6];
@@ -984,7 +995,6 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
         long long nodes = (long long)(int)(ctx->hpin[0] & 0xffffffff);
         bool overflow = (int)(ctx->hpin[1] & 0xffffffff) != 0;
         long long bounces = ctx->hpin[2];
-        RC(check_flags(ctx, st));
         if (overflow) {   // a probe chain ran out of slots: results incomplete, relaunch
             ctx->trie_cap *= 4;
             continue;
@@ -1230,7 +1240,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         cudaMemcpyToSymbol(g_vstats, z, sizeof(z));
     }
 #endif
-    RC(fetch(ctx, nr, 1, st));
+    RC(fetch_and_flags(ctx, nr, 1, st));   // record count + the validation's error word
     long long n_rec = ctx->hpin[0];
     if (power && n_rec > 0) {
         k_rec_powers<<<nblk(n_rec, 128), 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, E,
@@ -1239,7 +1249,6 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     }
     PROF_END(ST_VALIDATE);
     ctx->counters[6] = n_rec;
-    RC(check_flags(ctx, st));
     if (stats) stats[2] = n_rec;
     if (n_rec == 0) return RT_OK;
     PROF_BEGIN(ST_REC_SORT);
