@@ -242,6 +242,23 @@ def h2d(array, device):
     return out
 
 
+def d2h_many(tensors):
+    """d2h of several device tensors with one stream synchronisation."""
+    outs = []
+    dev = None
+    for t in tensors:
+        if t.device.type != "cuda" or t.numel() == 0:
+            outs.append(t.cpu().numpy())
+            continue
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+        dev = t.device
+    if dev is not None:
+        torch.cuda.current_stream(dev).synchronize()
+    return [o.numpy() if isinstance(o, torch.Tensor) else o for o in outs]
+
+
 def d2h(t):
     """Host numpy copy of a device tensor through page-locked memory.
 

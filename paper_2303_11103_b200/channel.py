@@ -149,8 +149,7 @@ def _build_cir_device(gains, T, a_all, delay, rx_names, tx_names, n_rx_el, n_tx_
     cir = Cir(a=None, tau=None, rx_names=rx_names, tx_names=tx_names, sample_times=gains.sample_times,
               a_dev=a, tau_dev=tau)
     if to_host:
-        cir.a = N.d2h(a)
-        cir.tau = N.d2h(tau)
+        cir.a, cir.tau = N.d2h_many([a, tau])
     return cir
 
 

@@ -235,6 +235,12 @@ class PathCoefficients(torch.autograd.Function):
 def path_coefficients(bvh, T: PathTable, eta, tx_rows, rx_rows, tx_pattern, rx_pattern,
                       tx_slants, rx_slants, wavelength, frequency, slants_dev=None):
     """Differentiable a[p, s, r] (complex128) for a device path table."""
+    if not (torch.is_grad_enabled() and eta.requires_grad):   # no autograd node needed
+        st = tuple(float(s) for s in tx_slants)
+        sr = tuple(float(s) for s in rx_slants)
+        a = _launch_transfer(bvh, T, tx_rows, rx_rows, pattern_id(tx_pattern), pattern_id(rx_pattern),
+                             st, sr, eta.detach().contiguous(), wavelength, frequency, slants_dev)
+        return torch.view_as_complex(a)
     return PathCoefficients.apply(eta, bvh, T, tx_rows, rx_rows, pattern_id(tx_pattern),
                                   pattern_id(rx_pattern), tuple(float(s) for s in tx_slants),
                                   tuple(float(s) for s in rx_slants), float(wavelength),
@@ -722,12 +728,18 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
     off_rx_w = np.einsum("ek,dmk->dem", np.asarray(off_rx, dtype=np.float64), rows_r)
     eta_host = ctx.eta_values(bvh) if eta is None else np.zeros((0, 2))
     parts = [rows_t.reshape(-1), rows_r.reshape(-1), off_tx_w.reshape(-1), off_rx_w.reshape(-1),
-             np.array([st.index(float(x)) for x in sl_tx], dtype=np.float64),
-             np.array([sr.index(float(x)) for x in sl_rx], dtype=np.float64),
+             np.zeros(0), np.zeros(0),
              np.asarray(st, dtype=np.float64), np.asarray(sr, dtype=np.float64), eta_host.reshape(-1)]
     cuts = np.cumsum([0] + [len(x) for x in parts])
-    allp = N.h2d(np.concatenate(parts), dev)
+    # slant indices as int32 behind the doubles: one pinned upload, typed device views
+    s_idx = np.array([st.index(float(x)) for x in sl_tx], dtype=np.int32)
+    r_idx = np.array([sr.index(float(x)) for x in sl_rx], dtype=np.int32)
+    f64 = np.concatenate(parts)
+    blob = N.h2d(np.concatenate([f64.view(np.uint8), s_idx.view(np.uint8), r_idx.view(np.uint8)]), dev)
+    allp = blob[:8 * len(f64)].view(torch.float64)
+    ints = blob[8 * len(f64):].view(torch.int32)
     seg = [allp[cuts[i]:cuts[i + 1]] for i in range(len(parts))]
+    seg[4], seg[5] = ints[:len(s_idx)], ints[len(s_idx):]
     Rt, Rr = seg[0].reshape(n_td, 3, 3), seg[1].reshape(n_rd, 3, 3)
     offw_t, offw_r = seg[2].reshape(n_td, n_tx_el, 3), seg[3].reshape(n_rd, n_rx_el, 3)
     tx_rows = Rt.reshape(n_td, 9)[tx_idx].contiguous()
@@ -740,8 +752,7 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
         _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows_dev, rx_rows_dev)
     if not base.requires_grad:   # one kernel: element phasors x slant coefficients
         a = torch.empty((T.n, n_rx_el, n_tx_el), dtype=torch.complex128, device=dev)
-        si = seg[4].to(torch.int32)
-        ri = seg[5].to(torch.int32)
+        si, ri = seg[4], seg[5]
         with torch.cuda.device(dev):
             bvh.ctx.call("rt_gains_synthetic", T.n, len(st), len(sr), N.ptr(base), N.ptr(T.tx),
                          N.ptr(T.rx), N.ptr(T.kdep), N.ptr(T.karr), n_tx_el, N.ptr(offw_t), N.ptr(si),
