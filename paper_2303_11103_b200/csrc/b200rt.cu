@@ -116,6 +116,7 @@ struct rt_ctx {
     // error flags + pinned host staging
     DevBuf dflag, probe;
     DevBuf adj;   // adjoint contributions [items * L] (rt_transfer_bwd)
+    DevBuf deferred;   // k_validate's deferred items (RT_VAL_DEFER)
     // PLOC builder scratch
     DevBuf pl_box, pl_count, pl_parent, pl_ca, pl_cb, pl_nn, pl_out, pl_valid, pl_pos, pl_slot, pl_em, pl_dfs;
     DevBuf sah_tasks;
@@ -1226,10 +1227,30 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         hints = ctx->occ_hint.get<int>();
         CK(cudaMemsetAsync(hints, 0xFF, 4ULL * nC * (MAX_DEPTH + 1), st));
     }
-    k_validate<false><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
-                                                         bvh_dev(ctx), ctx->pending.get<Pending>(),
-                                                         n_pend, E, ctx->recs.get<Rec>(), nr, hints);
-    CKL();
+    if (RT_VAL_DEFER > 0 && hints) {
+        CK(ctx->deferred.reserve(4ULL * n_pend));
+        unsigned long long* nd = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>()) + 2;
+        k_validate<false><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
+                                                             bvh_dev(ctx), ctx->pending.get<Pending>(),
+                                                             n_pend, E, ctx->recs.get<Rec>(), nr, hints,
+                                                             nullptr, RT_VAL_DEFER, ctx->deferred.get<int>(), nd);
+        CKL();
+        RC(fetch(ctx, nd, 1, st));
+        long long n_def = ctx->hpin[0];
+        if (n_def > 0) {
+            long long b2 = std::min<long long>((n_def + 127) / 128, (long long)ctx->n_sm * 32);
+            k_validate<false><<<(unsigned)b2, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
+                                                            bvh_dev(ctx), ctx->pending.get<Pending>(),
+                                                            n_def, E, ctx->recs.get<Rec>(), nr, hints,
+                                                            ctx->deferred.get<int>());
+            CKL();
+        }
+    } else {
+        k_validate<false><<<(unsigned)vblocks, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
+                                                             bvh_dev(ctx), ctx->pending.get<Pending>(),
+                                                             n_pend, E, ctx->recs.get<Rec>(), nr, hints);
+        CKL();
+    }
 #ifdef RT_VALIDATE_STATS
     {
         unsigned long long hv[8];
