@@ -561,7 +561,7 @@ def run_e2e(args, sc, grid, rank, world, dev, flush):
     from paper_2303_11103_b200 import parallel
     from paper_2303_11103_b200.bvh import gather_meshes
     verts, tris, _, _, pmat, _ = gather_meshes(sc)
-    h2d = verts.nbytes + tris.nbytes + pmat.nbytes
+    h2d = verts.nbytes + 4 * tris.size + pmat.nbytes   # vertex ids travel as int32
     d2h = grid.num_cells * 8
     times, bounces = [], 0
     for i in range(args.warmup + args.steps):

@@ -52,12 +52,12 @@ int rt_destroy(rt_ctx* ctx);
 const char* rt_last_error(const rt_ctx* ctx);
 
 /* ---- scene ingest + acceleration (bvh.py:33-79,180-202: Bvh.__init__, _gather, build) ----
- * vertices: device [n_vertices*3] f64; tri_vertex: device [n_prims*3] i64 global
- * vertex ids in _gather order (object order, then triangle order);
+ * vertices: device [n_vertices*3] f64; tri_vertex: device [n_prims*3] i32 global
+ * vertex ids (< 2^31) in _gather order (object order, then triangle order);
  * prim_material: device [n_prims] i32.  Computes v0/e1/e2, unit normals and
  * plane offsets bit-identically to the reference's numpy calls. */
 int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
-                    const int64_t* tri_vertex, const int32_t* prim_material, int64_t n_prims,
+                    const int32_t* tri_vertex, const int32_t* prim_material, int64_t n_prims,
                     void* stream);
 /* BVH over the uploaded primitives (replaces Bvh._build, bvh.py:59-79):
  * top-down binned SAH on the device, depth-first child-pair layout with

@@ -43,7 +43,7 @@ class _PinnedStaging:
         n = int(np.prod(shape)) if len(shape) else 1
         tdt = {np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32}[dtype]
         b = self.bufs.get(name)
-        if b is None or b.numel() < n:
+        if b is None or b.numel() < n or b.dtype != tdt:
             b = torch.empty(max(n, 1), dtype=tdt, pin_memory=True)
             self.bufs[name] = b
         return b[:n].numpy().reshape(shape)
@@ -62,7 +62,7 @@ def _staging_for(device):
     return st
 
 
-def _gather_geometry(scene, alloc=None):
+def _gather_geometry(scene, alloc=None, tri_dtype=np.int64):
     """One pass over the objects into preallocated arrays: (vertices [V,3] f64,
     tri_vertex [N,3] i64 with global vertex ids, prim_material [N] i32,
     material_names, object index of each non-empty object, its triangle count).
@@ -82,15 +82,17 @@ def _gather_geometry(scene, alloc=None):
     if alloc is None:
         def alloc(name, shape, dtype):
             return np.empty(shape, dtype=dtype)
+    if nv >= 2 ** 31:
+        raise ValueError("scene has 2^31 or more vertices (vertex ids are 32-bit on the device)")
     verts = alloc("verts", (nv, 3), np.float64)
-    tris = alloc("tris", (nt, 3), np.int64)
+    tris = alloc("tris", (nt, 3), tri_dtype)
     pmat = alloc("pmat", (nt,), np.int32)
     obj_ids = np.empty(len(objs), dtype=np.int64)
     counts = np.empty(len(objs), dtype=np.int64)
     vb = tb = 0
     for k, (oi, v, t) in enumerate(objs):
         verts[vb:vb + len(v)] = v
-        np.add(t, vb, out=tris[tb:tb + len(t)])
+        np.add(t, vb, out=tris[tb:tb + len(t)], casting="unsafe")
         pmat[tb:tb + len(t)] = mindex.get(scene.objects[oi].material, -1)
         obj_ids[k] = oi
         counts[k] = len(t)
@@ -124,7 +126,7 @@ class Bvh:
         self.device = self.ctx.device
         staging = _staging_for(self.device)
         verts, tris, prim_mat, self.material_names, self._obj_ids, self._obj_counts = \
-            _gather_geometry(scene, staging.get)
+            _gather_geometry(scene, staging.get, tri_dtype=np.int32)   # 32-bit vertex ids on the device
         self._prim_ids = None
         self.num_prims = len(tris)
         self.frequency_hz = float(scene.frequency_hz)

@@ -712,7 +712,7 @@ int64_t rt_num_candidates(const rt_ctx* ctx) { return ctx ? ctx->n_cand : 0; }
 int rt_candidates_max_len(const rt_ctx* ctx) { return ctx ? ctx->cand_max_len : 1; }
 
 int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
-                    const int64_t* tri_vertex, const int32_t* prim_material, int64_t n_prims,
+                    const int32_t* tri_vertex, const int32_t* prim_material, int64_t n_prims,
                     void* stream) {
     if (!ctx || n_prims < 0 || n_vertices < 0) return fail(ctx, RT_EINVAL, "bad scene arguments");
     if (n_prims > (1 << 27)) return fail(ctx, RT_EINVAL, "too many primitives (max 2^27)");

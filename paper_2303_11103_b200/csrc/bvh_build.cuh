@@ -29,7 +29,7 @@ __device__ inline float hi_f(double x) { return __double2float_ru(x + (1e-9 + 1e
 
 // v0/e1/e2 gather (bvh.py:180-197), normals + plane offsets (bvh.py:39-44),
 // prim boxes and centroids; cbounds accumulates the centroid AABB.
-__global__ void k_gather(const double* __restrict__ V, const int64_t* __restrict__ T, int64_t n,
+__global__ void k_gather(const double* __restrict__ V, const int32_t* __restrict__ T, int64_t n,
                          double* v0, double* e1, double* e2, double* nrm, double* poff,
                          float* box /*[n*6]*/, float* cent /*[n*3]*/, unsigned* cbounds) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
