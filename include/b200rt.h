@@ -50,11 +50,18 @@ int rt_version(void);
 int rt_create(int device, rt_ctx** out);
 int rt_destroy(rt_ctx* ctx);
 const char* rt_last_error(const rt_ctx* ctx);
+/* Host -> device copy of a small parameter block through the library's
+ * page-locked staging ring, asynchronous on `stream` of `device`; the host
+ * buffer may be reused as soon as the call returns (plumbing for the
+ * per-call parameter uploads of the Python layer). */
+int rt_h2d(int device, void* dst, const void* src, int64_t bytes, void* stream);
 
 /* ---- scene ingest + acceleration (bvh.py:33-79,180-202: Bvh.__init__, _gather, build) ----
- * vertices: device [n_vertices*3] f64; tri_vertex: device [n_prims*3] i32 global
+ * vertices: [n_vertices*3] f64; tri_vertex: [n_prims*3] i32 global
  * vertex ids (< 2^31) in _gather order (object order, then triangle order);
- * prim_material: device [n_prims] i32.  Computes v0/e1/e2, unit normals and
+ * prim_material: [n_prims] i32 — device memory, or host memory that the call
+ * copies in on `stream` (host buffers may be refilled once rt_bvh_build has
+ * returned: it waits for those copies).  Computes v0/e1/e2, unit normals and
  * plane offsets bit-identically to the reference's numpy calls. */
 int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
                     const int32_t* tri_vertex, const int32_t* prim_material, int64_t n_prims,
@@ -172,11 +179,47 @@ int rt_gains_synthetic(rt_ctx* ctx, int64_t n_paths, int n_tx_slants, int n_rx_s
                        const double* off_tx_w, const int32_t* tx_slant_index, int n_rx_el,
                        const double* off_rx_w, const int32_t* rx_slant_index, double wavelength,
                        double* a_out, void* stream);
+/* rt_gains (em.py:359-422, compute_gains with a synthetic array, no autograd):
+ * rt_transfer followed by rt_gains_synthetic in one call.  Rotation rows are
+ * per DEVICE (tx_rows [n_tx_dev*9], rx_rows [n_rx_dev*9], row-major 3x3)
+ * and picked per path through tx_dev / rx_dev [P]; the per-(path, slant
+ * pair) coefficients stay in library scratch.  Other arguments as in
+ * rt_transfer / rt_gains_synthetic; out a [P*Er*Et*2] (device). */
+int rt_gains(rt_ctx* ctx, int64_t n_paths, int max_len, const int32_t* tx_dev, const int32_t* rx_dev,
+             const int8_t* order, const int32_t* seq, const int32_t* interaction_mat,
+             const double* vertices, const double* normals, const double* cos_inc,
+             const double* length, const double* delay, const double* k_dep, const double* k_arr,
+             const double* tx_rows, const double* rx_rows, int tx_pattern, int rx_pattern,
+             const double* tx_slants, int n_tx_slants, const double* rx_slants, int n_rx_slants,
+             const double* eta, int n_mat, int n_tx_el, const double* off_tx_w,
+             const int32_t* tx_slant_index, int n_rx_el, const double* off_rx_w,
+             const int32_t* rx_slant_index, double wavelength, double frequency_hz, double* a_out,
+             void* stream);
+/* rt_gains_h: compute_gains (em.py:359-422, synthetic arrays, no autograd) as
+ * one call with the per-device parameters on the HOST: orientations tx_ypr
+ * [n_tx_dev*3] / rx_ypr [n_rx_dev*3] (yaw, pitch, roll -> rows as
+ * geometry.py:50-59), array-frame element offsets off_tx [Et*3] / off_rx
+ * [Er*3] and slants sl_tx [Et] / sl_rx [Er] (scene.py:138-154), eta
+ * [n_mat*2].  The library forms the rows, the world-frame offsets and the
+ * distinct slant sets, uploads them with one copy and runs the rt_gains
+ * kernels.  With tx_pos / rx_pos (host [n_dev*3]) and near_field given,
+ * *near_field = 1 when some (tx, rx) pair is closer than the Fraunhofer
+ * distance 2 D^2 / lambda of its larger aperture D (em.py:344-356's
+ * pre-check: the caller then inspects the paths themselves). */
+int rt_gains_h(rt_ctx* ctx, int64_t n_paths, int max_len, const int32_t* tx_dev, const int32_t* rx_dev,
+               const int8_t* order, const int32_t* seq, const int32_t* interaction_mat,
+               const double* vertices, const double* normals, const double* cos_inc,
+               const double* length, const double* delay, const double* k_dep, const double* k_arr,
+               int n_tx_dev, const double* tx_ypr, const double* tx_pos, int n_rx_dev,
+               const double* rx_ypr, const double* rx_pos, int tx_pattern, int n_tx_el,
+               const double* off_tx, const double* sl_tx, int rx_pattern, int n_rx_el,
+               const double* off_rx, const double* sl_rx, const double* eta, int n_mat,
+               double wavelength, double frequency_hz, double* a_out, int* near_field, void* stream);
 /* build_cir (channel.py:40-72), two calls.  rt_cir_plan keeps LOS and/or
  * specular paths, buckets them by scene (rx, tx) pair (rx_of/tx_of [P]
  * device) and orders every bucket by (delay, kind, sequence); *n_path_out =
  * the largest bucket (host sync).  rt_cir_scatter then writes a_in [P*Er*
- * Et*n_t*2] into the caller-zeroed a_out [n_rx*Er*n_tx*Et*n_path*n_t*2] and
+ * Et*n_t*2] into a_out (zero-filled by the call) [n_rx*Er*n_tx*Et*n_path*n_t*2] and
  * tau_out [n_rx*n_tx*n_path] (delays minus the pair's first arrival when
  * normalize != 0). */
 int rt_cir_plan(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, const int32_t* seq,

@@ -28,7 +28,7 @@ EXPORTS = [
     "rt_paths", "rt_paths_get", "rt_transfer", "rt_transfer_bwd", "rt_coverage",
     "rt_set_profiling", "rt_get_profile", "rt_l2_probe", "rt_transfer_jvp", "rt_solve_pairs",
     "rt_launch_shard", "rt_gains_synthetic", "rt_cir_plan", "rt_cir_scatter", "rt_freq_nmse",
-    "rt_microbench", "rt_fresnel",
+    "rt_microbench", "rt_fresnel", "rt_gains", "rt_h2d", "rt_gains_h",
 ]
 
 _lib = None
@@ -111,6 +111,11 @@ def lib():
             "rt_solve_pairs": (i32, [P, i64, i32] + [P] * 15),
             "rt_gains_synthetic": (i32, [P, i64, i32, i32, P, P, P, P, P, i32, P, P, i32, P, P, f64,
                                          P, P]),
+            "rt_gains": (i32, [P, i64, i32] + [P] * 14 + [i32, i32, P, i32, P, i32, P, i32, i32, P, P,
+                                                        i32, P, P, f64, f64, P, P]),
+            "rt_h2d": (i32, [i32, P, P, i64, P]),
+            "rt_gains_h": (i32, [P, i64, i32] + [P] * 12 + [i32, P, P, i32, P, P, i32, i32, P, P, i32, i32,
+                                                          P, P, P, i32, f64, f64, P, P, P]),
             "rt_cir_plan": (i32, [P, i64, i32, P, P, P, P, P, i32, i32, i32, i32, pi64, P]),
             "rt_cir_scatter": (i32, [P, i64, P, i32, P, i32, i32, i32, i64, P, P, P]),
             "rt_freq_nmse": (i32, [P, i64, i32, P, P, P, P, P, P, f64, P, P, P, P]),
@@ -131,14 +136,14 @@ def ptr(t):
         return None
     if isinstance(t, torch.Tensor):
         return ctypes.c_void_p(t.data_ptr())
-    if isinstance(t, np.ndarray):
-        return t.ctypes.data_as(ctypes.c_void_p)
+    if isinstance(t, np.ndarray):   # (ndarray.ctypes builds a helper object: ~10x slower)
+        return ctypes.c_void_p(t.__array_interface__["data"][0])
     raise TypeError(type(t))
 
 
 def host_doubles(values):
     arr = np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(-1))
-    return arr, arr.ctypes.data_as(ctypes.c_void_p)
+    return arr, ctypes.c_void_p(arr.__array_interface__["data"][0])
 
 
 class Context:
@@ -205,40 +210,24 @@ def release_context(ctx: Context):
         _pool.setdefault(ctx.device.index, []).append(ctx)
 
 
-class _SmallH2D:
-    """Per-device pinned ring for small parameter uploads: one page-locked
-    buffer, refilled only after the previous copy out of it completed."""
-
-    CAP = 1 << 20
-
-    def __init__(self):
-        self.buf = torch.empty(self.CAP, dtype=torch.uint8, pin_memory=True)
-        self.ready = None
-
-
-_SMALL = {}
+_TORCH_DTYPES = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+                 np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32,
+                 np.dtype(np.int8): torch.int8, np.dtype(np.uint8): torch.uint8,
+                 np.dtype(np.complex128): torch.complex128, np.dtype(np.bool_): torch.bool}
 
 
 def h2d(array, device):
-    """Device copy of a small host array via reusable pinned memory (async on
-    the current stream; falls back to a plain copy above 1 MiB)."""
+    """Device copy of a small host array (async on the device's current stream):
+    rt_h2d stages it through the library's page-locked ring, so the host array
+    may change as soon as this returns."""
     a = np.ascontiguousarray(array)
-    if a.nbytes == 0 or a.nbytes > _SmallH2D.CAP:
-        return torch.as_tensor(a, device=device)
     device = torch.device(device)
-    st = _SMALL.get(device)
-    if st is None:
-        st = _SMALL[device] = _SmallH2D()
-    if st.ready is not None:
-        st.ready.synchronize()
-    view = st.buf[:a.nbytes].numpy().view(a.dtype).reshape(a.shape)
-    view[...] = a
-    with torch.cuda.device(device):
-        out = torch.from_numpy(view).to(device, non_blocking=True)
-        # the copy runs on the destination device's current stream: the buffer
-        # may be refilled only after that stream passed this point
-        st.ready = torch.cuda.Event()
-        st.ready.record(torch.cuda.current_stream(device))
+    out = torch.empty(a.shape, dtype=_TORCH_DTYPES[a.dtype], device=device)
+    if a.nbytes:
+        rc = lib().rt_h2d(device.index or 0, out.data_ptr(), a.__array_interface__["data"][0], a.nbytes,
+                          torch.cuda.current_stream(device).cuda_stream)
+        if rc != RT_OK:
+            raise NativeError(f"rt_h2d failed ({rc})")
     return out
 
 

@@ -32,12 +32,11 @@ class Hit:
 
 class _PinnedStaging:
     """Reusable page-locked host buffers for the scene upload: no page faults on
-    refill and truly asynchronous H2D copies.  `ready` is recorded after the
-    copies are enqueued; a refill waits for it first."""
+    refill and truly asynchronous H2D copies (rt_bvh_build returns only after
+    the upload has consumed them)."""
 
     def __init__(self):
         self.bufs = {}
-        self.ready = None
 
     def get(self, name, shape, dtype):
         n = int(np.prod(shape)) if len(shape) else 1
@@ -56,9 +55,6 @@ def _staging_for(device):
     st = _STAGING.get(device)
     if st is None:
         st = _STAGING[device] = _PinnedStaging()
-    if st.ready is not None:
-        st.ready.synchronize()
-        st.ready = None
     return st
 
 
@@ -132,15 +128,11 @@ class Bvh:
         self.frequency_hz = float(scene.frequency_hz)
         dev = self.device
         with torch.cuda.device(dev):
-            # pinned staging -> device on the current stream (the library's stream)
-            self._verts = torch.from_numpy(verts).to(dev, non_blocking=True)
-            self._tris = torch.from_numpy(tris).to(dev, non_blocking=True)
-            self._pmat = torch.from_numpy(prim_mat).to(dev, non_blocking=True)
-            staging.ready = torch.cuda.Event()
-            staging.ready.record()
+            # rt_scene_upload copies the pinned staging in on the library's stream;
+            # rt_bvh_build returns only after those copies, so the staging may be refilled
             s = self.ctx.stream
-            self.ctx.call("rt_scene_upload", N.ptr(self._verts), len(verts), N.ptr(self._tris),
-                          N.ptr(self._pmat), self.num_prims, s)
+            self.ctx.call("rt_scene_upload", N.ptr(verts), len(verts), N.ptr(tris), N.ptr(prim_mat),
+                          self.num_prims, s)
             self.ctx.call("rt_bvh_build", s)
         self._arrays = None
 

@@ -141,9 +141,10 @@ def _build_cir_device(gains, T, a_all, delay, rx_names, tx_names, n_rx_el, n_tx_
                  N.ptr(tx_of), len(rx_names), len(tx_names), int(bool(los)), int(bool(reflection)),
                  ctypes.byref(n), ctx.stream, exc_map={N.RT_EINVAL: ChannelError})
         n_path = int(n.value)
-        a = torch.zeros((len(rx_names), n_rx_el, len(tx_names), n_tx_el, n_path, n_t),
+        # zero-filled by rt_cir_scatter
+        a = torch.empty((len(rx_names), n_rx_el, len(tx_names), n_tx_el, n_path, n_t),
                         dtype=torch.complex128, device=dev)
-        tau = torch.zeros((len(rx_names), len(tx_names), n_path), dtype=torch.float64, device=dev)
+        tau = torch.empty((len(rx_names), len(tx_names), n_path), dtype=torch.float64, device=dev)
         ctx.call("rt_cir_scatter", T.n, N.ptr(delay), int(bool(normalize_delays)), N.ptr(a_in), n_rx_el,
                  n_tx_el, n_t, n_path, N.ptr(a), N.ptr(tau), ctx.stream, exc_map={N.RT_EINVAL: ChannelError})
     cir = Cir(a=None, tau=None, rx_names=rx_names, tx_names=tx_names, sample_times=gains.sample_times,

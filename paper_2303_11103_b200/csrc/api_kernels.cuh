@@ -108,24 +108,41 @@ __device__ void emit_row(const PathTable& T, long long row, long long rx_i, int 
     st3(T.karr + 3 * row, g.dir[K]);
 }
 
-// LOS first, then kept records in (order, candidate) order (tracer.py:294)
+// LOS first, then kept records in (order, candidate) order (tracer.py:294).
+// One warp per receiver: lanes take 32 consecutive sorted records at a time
+// and place their rows with a ballot prefix (a receiver's records are
+// contiguous, so a lane past the run ends it).
 __global__ void k_emit_paths(Cands C, SceneDev S, const double* images, Receivers R, d3 tx,
                              const Rec* recs, const int* order, const unsigned long long* keys,
                              long long n_rec, const unsigned char* keep, const unsigned char* los,
                              const int* heads, const int* offsets, PathTable T) {
-    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (r >= R.n) return;
+    const unsigned FULL = 0xffffffffu;
+    long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (r >= R.n) return;   // whole warps
     long long row = offsets[r];
     d3 rx = receiver_pos(R, r);
-    if (los[r]) emit_row(T, row++, r, -1, 0, nullptr, tx, nullptr, rx, S);
+    if (los[r]) {
+        if (lane == 0) emit_row(T, row, r, -1, 0, nullptr, tx, nullptr, rx, S);
+        ++row;
+    }
     int h = heads[r];
     if (h < 0) return;
-    for (long long i = h; i < n_rec && (long long)(keys[i] >> 36) == r; ++i) {
-        if (!keep[i]) continue;
-        const Rec& a = recs[order[i]];
-        d3 pts[MAX_DEPTH];
-        solve_geometric(C, S, images, a.cand, tx, rx, pts);
-        emit_row(T, row++, r, a.cand, a.order, C.seq + (long long)a.cand * C.max_len, tx, pts, rx, S);
+    for (long long b = h;; b += 32) {
+        long long i = b + lane;
+        bool in = i < n_rec && (long long)(keys[i] >> 36) == r;
+        bool k = in && keep[i];
+        unsigned m_in = __ballot_sync(FULL, in);
+        unsigned m = __ballot_sync(FULL, k);
+        if (k) {
+            const Rec& a = recs[order[i]];
+            d3 pts[MAX_DEPTH];
+            solve_geometric(C, S, images, a.cand, tx, rx, pts);
+            emit_row(T, row + __popc(m & ((1u << lane) - 1u)), r, a.cand, a.order,
+                     C.seq + (long long)a.cand * C.max_len, tx, pts, rx, S);
+        }
+        row += __popc(m);
+        if (m_in != FULL) break;
     }
 }
 
@@ -211,7 +228,18 @@ struct TransferArgs {
     const int* prim_mat;
     const int* imat;   // [P*L] material per interaction, or null (prim_mat[seq])
     double wavelength, frequency;
+    // rotation rows per device (rt_gains): row block of path p = tx_rows[tx_ridx[p]];
+    // null = one row block per path (rt_transfer)
+    const int* tx_ridx;
+    const int* rx_ridx;
 };
+
+__device__ __forceinline__ const double* tx_rows_of(const TransferArgs& A, long long p) {
+    return A.tx_rows + 9 * (A.tx_ridx ? (long long)A.tx_ridx[p] : p);
+}
+__device__ __forceinline__ const double* rx_rows_of(const TransferArgs& A, long long p) {
+    return A.rx_rows + 9 * (A.rx_ridx ? (long long)A.rx_ridx[p] : p);
+}
 
 __device__ inline void table_geom(const TransferArgs& A, long long p, Geom& g) {
     int K = A.order[p];
@@ -232,9 +260,9 @@ __global__ void k_transfer(const __grid_constant__ TransferArgs A, double* a_out
     int s = (int)(i - p * A.n_st);
     Geom g;
     table_geom(A, p, g);
-    c3 f = transport(g, A.tx_pat, A.tx_slants[s], A.tx_rows + 9 * p, A.eta);
+    c3 f = transport(g, A.tx_pat, A.tx_slants[s], tx_rows_of(A, p), A.eta);
     for (int r = 0; r < A.n_sr; ++r) {
-        d3 rf = rx_field(g, A.rx_pat, A.rx_slants[r], A.rx_rows + 9 * p);
+        d3 rf = rx_field(g, A.rx_pat, A.rx_slants[r], rx_rows_of(A, p));
         c2 a = finish(f, rf, g, A.wavelength, A.frequency);
         long long o = ((p * A.n_st + s) * A.n_sr + r) * 2;
         a_out[o] = a.re;
@@ -257,8 +285,8 @@ __global__ void k_transfer_bwd(const __grid_constant__ TransferArgs A, const dou
     if (G.re == 0.0 && G.im == 0.0) return;
     Geom g;
     table_geom(A, p, g);
-    transfer_adjoint(g, A.tx_pat, A.tx_slants[s], A.tx_rows + 9 * p, A.rx_pat, A.rx_slants[r],
-                     A.rx_rows + 9 * p, A.eta, A.wavelength, A.frequency, G, out);
+    transfer_adjoint(g, A.tx_pat, A.tx_slants[s], tx_rows_of(A, p), A.rx_pat, A.rx_slants[r],
+                     rx_rows_of(A, p), A.eta, A.wavelength, A.frequency, G, out);
 }
 
 // grad_eta[m] += sum of the contributions of material m, in a fixed order: one

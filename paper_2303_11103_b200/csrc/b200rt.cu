@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -43,6 +44,7 @@
 #define RT_OCC_HINTS 1   // occluder cache in k_validate (solve.cuh segments_clear_hinted)
 #endif
 #include "solve.cuh"
+#include "sort_small.cuh"
 
 using namespace rt;
 
@@ -82,6 +84,9 @@ struct rt_ctx {
     // scene (global gather order)
     int64_t n_prims = 0;
     DevBuf v0, e1, e2, nrm, poff, prim_mat, pbox, cent, cbounds;
+    DevBuf up_verts, up_tris;          // device copies of host scene inputs (rt_scene_upload)
+    cudaEvent_t up_ev = nullptr;       // host scene inputs consumed (waited for by rt_bvh_build)
+    bool up_pending = false;
     // bvh
     DevBuf nodes, dbox, skip_tab, tris, sorted_idx, morton, morton_alt, idx_alt, child, flags;
     bool bvh_ready = false;
@@ -116,6 +121,8 @@ struct rt_ctx {
     // error flags + pinned host staging
     DevBuf dflag, probe;
     DevBuf adj;   // adjoint contributions [items * L] (rt_transfer_bwd)
+    DevBuf gbase;   // rt_gains' per-(path, slant pair) coefficients [P*S*R*2]
+    DevBuf gparam;  // rt_gains_h's uploaded parameter block
     DevBuf deferred;   // k_validate's deferred items (RT_VAL_DEFER)
     // PLOC builder scratch
     DevBuf pl_box, pl_count, pl_parent, pl_ca, pl_cb, pl_nn, pl_out, pl_valid, pl_pos, pl_slot, pl_em, pl_dfs;
@@ -123,7 +130,7 @@ struct rt_ctx {
     // CIR packing scratch (rt_cir_plan -> rt_cir_scatter)
     DevBuf cir_pair, cir_count, cir_off, cir_fill, cir_bucket, cir_slot, cir_first;
     int64_t cir_n = 0;
-    int cir_ntx = 0;
+    int cir_ntx = 0, cir_nrx = 0;
     long long* hpin = nullptr;
     // profiling: per-stage CUDA events on the caller's stream + counters
     int prof = 0;
@@ -252,6 +259,27 @@ int cub_call(rt_ctx* ctx, F&& f) {
     return RT_OK;
 }
 
+// Stable (key, value) radix sort over key bits [begin_bit, end_bit): one CTA
+// (k_sort_small) up to SORT_SMALL_MAX pairs, cub::DeviceRadixSort above.
+int sort_pairs(rt_ctx* ctx, const unsigned long long* kin, unsigned long long* kout, const int* vin, int* vout,
+               long long n, int begin_bit, int end_bit, cudaStream_t st) {
+    if (n <= 0) return RT_OK;
+    if (n <= SORT_SMALL_MAX) {
+        static bool attr_set[64] = {};
+        size_t smem = sizeof(typename SmallSort::TempStorage);
+        if (ctx->device < 64 && !attr_set[ctx->device]) {
+            CK(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set[ctx->device] = true;
+        }
+        k_sort_small<<<1, SORT_SMALL_THREADS, smem, st>>>(kin, kout, vin, vout, (int)n, begin_bit, end_bit);
+        CKL();
+        return RT_OK;
+    }
+    return cub_call(ctx, [&](void* tmp, size_t& bytes) {
+        return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, begin_bit, end_bit, st);
+    });
+}
+
 // Sort rows (s_seq/s_len, n rows, width L) by (length, lexicographic) and
 // drop duplicates into cand_seq/cand_len (LSD radix over digit columns).
 // unique_in: the rows are known to be distinct (one launch's trie): the
@@ -292,10 +320,7 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st, boo
         int end_bit = ncol * W + (with_len ? 4 : 0);
         k_digit_columns<<<nblk(n, 256), 256, 0, st>>>(n, seq, len, L, lo, hi, W, with_len, perm, keys);
         CKL();
-        RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
-            return cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys_alt, perm, perm_alt,
-                                                   (int)n, 0, end_bit, st);
-        }));
+        RC(sort_pairs(ctx, keys, keys_alt, perm, perm_alt, n, 0, end_bit, st));
         std::swap(perm, perm_alt);
         if (with_len) break;
         hi = lo == 0 ? -1 : lo - 1;
@@ -674,6 +699,58 @@ extern "C" {
 
 int rt_version(void) { return 1; }
 
+// rt_h2d: per-device ring of page-locked slots; a slot is refilled only after
+// the copy out of it has completed (its event)
+namespace {
+constexpr int H2D_SLOTS = 8;
+constexpr size_t H2D_SLOT_BYTES = 1 << 20;
+struct H2DRing {
+    void* host[H2D_SLOTS] = {};
+    cudaEvent_t ev[H2D_SLOTS] = {};
+    bool used[H2D_SLOTS] = {};
+    int next = 0;
+};
+std::mutex g_h2d_mu;
+H2DRing g_h2d[64];
+}  // namespace
+
+namespace {
+int h2d_staged(int device, void* dst, const void* src, int64_t bytes, cudaStream_t st) {
+    if (device < 0 || device >= 64 || bytes < 0 || (bytes > 0 && (!dst || !src))) return RT_EINVAL;
+    if (bytes == 0) return RT_OK;
+    std::lock_guard<std::mutex> lock(g_h2d_mu);
+    if (cudaSetDevice(device) != cudaSuccess) return RT_ECUDA;
+    H2DRing& R = g_h2d[device];
+    const char* p = static_cast<const char*>(src);
+    char* d = static_cast<char*>(dst);
+    while (bytes > 0) {
+        int k = R.next;
+        R.next = (k + 1) % H2D_SLOTS;
+        if (!R.host[k]) {
+            if (cudaMallocHost(&R.host[k], H2D_SLOT_BYTES) != cudaSuccess) return RT_ENOMEM;
+            if (cudaEventCreateWithFlags(&R.ev[k], cudaEventDisableTiming) != cudaSuccess) return RT_ECUDA;
+        } else if (R.used[k] && cudaEventSynchronize(R.ev[k]) != cudaSuccess) {
+            return RT_ECUDA;
+        }
+        size_t n = std::min<size_t>((size_t)bytes, H2D_SLOT_BYTES);
+        std::memcpy(R.host[k], p, n);
+        if (cudaMemcpyAsync(d, R.host[k], n, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaEventRecord(R.ev[k], st) != cudaSuccess)
+            return RT_ECUDA;
+        R.used[k] = true;
+        p += n;
+        d += n;
+        bytes -= (int64_t)n;
+    }
+    return RT_OK;
+}
+}  // namespace
+
+int rt_h2d(int device, void* dst, const void* src, int64_t bytes, void* stream) {
+    return h2d_staged(device, dst, src, bytes, ST(stream));
+}
+
+
 int rt_create(int device, rt_ctx** out) {
     rt_ctx* ctx = nullptr;
     if (!out) return RT_EINVAL;
@@ -698,6 +775,7 @@ int rt_destroy(rt_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->hpin) cudaFreeHost(ctx->hpin);
     if (ctx->diag_ev) cudaEventDestroy(ctx->diag_ev);
+    if (ctx->up_ev) cudaEventDestroy(ctx->up_ev);
     for (auto& pair : ctx->ev)
         for (cudaEvent_t e : pair)
             if (e) cudaEventDestroy(e);
@@ -733,7 +811,23 @@ int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
     CK(ctx->cent.reserve(12 * n));
     CK(ctx->cbounds.reserve(48));   // 7 ordered floats, then the FP32 filter's origin bound (double at +32)
     if (n_prims == 0) return RT_OK;
-    CK(cudaMemcpyAsync(ctx->prim_mat.p, prim_material, 4 * n_prims, cudaMemcpyDeviceToDevice, st));
+    // inputs in host memory (page-locked or pageable) are copied in on the stream;
+    // device inputs are read in place
+    cudaPointerAttributes at{};
+    bool host_in = cudaPointerGetAttributes(&at, vertices) != cudaSuccess || at.type != cudaMemoryTypeDevice;
+    cudaGetLastError();   // clear a pageable-pointer query error
+    if (host_in) {
+        CK(ctx->up_verts.reserve(24ULL * std::max<int64_t>(n_vertices, 1)));
+        CK(ctx->up_tris.reserve(12ULL * n_prims));
+        CK(cudaMemcpyAsync(ctx->up_verts.p, vertices, 24ULL * n_vertices, cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(ctx->up_tris.p, tri_vertex, 12ULL * n_prims, cudaMemcpyDefault, st));
+        vertices = ctx->up_verts.get<double>();
+        tri_vertex = ctx->up_tris.get<int32_t>();
+    }
+    CK(cudaMemcpyAsync(ctx->prim_mat.p, prim_material, 4 * n_prims, cudaMemcpyDefault, st));
+    if (!ctx->up_ev) CK(cudaEventCreateWithFlags(&ctx->up_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->up_ev, st));
+    ctx->up_pending = true;
     // ordered-float bounds: mins start at 0xFFFFFFFF, maxima (and the scale) at 0
     CK(cudaMemsetAsync(ctx->cbounds.p, 0xFF, 3 * sizeof(unsigned), st));
     CK(cudaMemsetAsync(ctx->cbounds.get<unsigned>() + 3, 0, 4 * sizeof(unsigned), st));
@@ -745,8 +839,19 @@ int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
     return RT_OK;
 }
 
+static int bvh_build_impl(rt_ctx* ctx, void* stream);
+
 int rt_bvh_build(rt_ctx* ctx, void* stream) {
     if (!ctx) return RT_EINVAL;
+    int rc = bvh_build_impl(ctx, stream);
+    if (ctx->up_pending) {   // the caller may refill its host scene buffers after this returns
+        ctx->up_pending = false;
+        CK(cudaEventSynchronize(ctx->up_ev));
+    }
+    return rc;
+}
+
+static int bvh_build_impl(rt_ctx* ctx, void* stream) {
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ST(stream);
     long long n = ctx->n_prims;
@@ -1285,10 +1390,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     int* vin = ctx->ridx_alt.get<int>();
     int* vout = ctx->ridx.get<int>();
     int end_bit = 36 + bits_for(R.n);
-    RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
-        return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n_rec, 0,
-                                               std::min(end_bit, 64), st);
-    }));
+    RC(sort_pairs(ctx, kin, kout, vin, vout, n_rec, 0, std::min(end_bit, 64), st));
     PROF_END(ST_REC_SORT);
     *n_rec_out = n_rec;
     return RT_OK;
@@ -1407,7 +1509,7 @@ int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx, int6
     PT.cosv = ctx->p_cos.get<double>();
     PT.L = L;
     if (P > 0) {
-        k_emit_paths<<<nblk(n_rx, 64), 64, 0, st>>>(cands_dev(ctx), scene_dev(ctx), ctx->images.get<double>(), R, T,
+        k_emit_paths<<<nblk(32 * n_rx, 128), 128, 0, st>>>(cands_dev(ctx), scene_dev(ctx), ctx->images.get<double>(), R, T,
                                                      ctx->recs.get<Rec>(), ctx->ridx.get<int>(),
                                                      ctx->rkeys.get<unsigned long long>(), n_rec,
                                                      ctx->keep.get<unsigned char>(), ctx->losbuf.get<unsigned char>(),
@@ -1746,6 +1848,164 @@ int rt_gains_synthetic(rt_ctx* ctx, int64_t n_paths, int n_tx_slants, int n_rx_s
     return RT_OK;
 }
 
+int rt_gains(rt_ctx* ctx, int64_t n_paths, int max_len, const int32_t* tx_dev, const int32_t* rx_dev,
+             const int8_t* order, const int32_t* seq, const int32_t* interaction_mat,
+             const double* vertices, const double* normals, const double* cos_inc, const double* length,
+             const double* delay, const double* k_dep, const double* k_arr, const double* tx_rows,
+             const double* rx_rows, int tx_pattern, int rx_pattern, const double* tx_slants,
+             int n_tx_slants, const double* rx_slants, int n_rx_slants, const double* eta, int n_mat,
+             int n_tx_el, const double* off_tx_w, const int32_t* tx_slant_index, int n_rx_el,
+             const double* off_rx_w, const int32_t* rx_slant_index, double wavelength,
+             double frequency_hz, double* a_out, void* stream) {
+    if (!ctx || n_paths < 0 || max_len < 1 || n_tx_slants < 1 || n_rx_slants < 1 || n_tx_el < 1 ||
+        n_rx_el < 1 || !(wavelength > 0.0) || !tx_dev || !rx_dev)
+        return fail(ctx, RT_EINVAL, "bad gains arguments");
+    if (tx_pattern < 0 || tx_pattern > 4 || rx_pattern < 0 || rx_pattern > 4)
+        return fail(ctx, RT_EINVAL, "unknown antenna pattern");
+    if (n_paths == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    (void)n_mat;
+    cudaStream_t st = ST(stream);
+    CK(ctx->gbase.reserve(16ULL * n_paths * n_tx_slants * n_rx_slants));
+    double* base = ctx->gbase.get<double>();
+    TransferArgs A{n_paths, max_len, (const signed char*)order, seq, vertices, normals, cos_inc, length,
+                   delay, tx_rows, rx_rows, tx_pattern, rx_pattern, tx_slants, n_tx_slants,
+                   rx_slants, n_rx_slants, eta, ctx->prim_mat.get<int>(), interaction_mat, wavelength,
+                   frequency_hz, tx_dev, rx_dev};
+    k_transfer<<<nblk(n_paths * n_tx_slants, 128), 128, 0, st>>>(A, base);
+    CKL();
+    long long n = (long long)n_paths * n_tx_el * n_rx_el;
+    k_gains_synth<<<nblk(n, 256), 256, 0, st>>>(n_paths, n_tx_slants, n_rx_slants, base, tx_dev, rx_dev,
+                                                k_dep, k_arr, n_tx_el, off_tx_w, tx_slant_index,
+                                                n_rx_el, off_rx_w, rx_slant_index, wavelength, a_out);
+    CKL();
+    return RT_OK;
+}
+
+namespace {
+// rotation_entries (em.py:33-40 / geometry.py:50-59): same libm calls and
+// operation order as the Python restatement
+void rotation_rows(const double* ypr, double* r) {
+    double cy = cos(ypr[0]), sy = sin(ypr[0]), cp = cos(ypr[1]), sp = sin(ypr[1]);
+    double cr = cos(ypr[2]), sr = sin(ypr[2]);
+    r[0] = cy * cp; r[1] = cy * sp * sr - sy * cr; r[2] = cy * sp * cr + sy * sr;
+    r[3] = sy * cp; r[4] = sy * sp * sr + cy * cr; r[5] = sy * sp * cr - cy * sr;
+    r[6] = -sp;     r[7] = cp * sr;                r[8] = cp * cr;
+}
+
+// per device: rows [9], world-frame element offsets w[e] = R off[e] (em.py:372-379)
+// and the aperture |max_e w - min_e w| (em.py:344-356); a device whose
+// orientation equals its predecessor's reuses that device's values
+void device_frames(int n_dev, const double* ypr, int n_el, const double* off, double* rows,
+                   double* offw, double* aperture) {
+    for (int d = 0; d < n_dev; ++d) {
+        const double* o = ypr + 3 * d;
+        if (d > 0 && o[0] == o[-3] && o[1] == o[-2] && o[2] == o[-1]) {
+            std::memcpy(rows + 9 * d, rows + 9 * (d - 1), 9 * sizeof(double));
+            std::memcpy(offw + 3 * (size_t)n_el * d, offw + 3 * (size_t)n_el * (d - 1), 3 * n_el * sizeof(double));
+            aperture[d] = aperture[d - 1];
+            continue;
+        }
+        double* r = rows + 9 * d;
+        rotation_rows(o, r);
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int e = 0; e < n_el; ++e) {
+            const double* x = off + 3 * e;
+            double* w = offw + 3 * ((size_t)n_el * d + e);
+            for (int m = 0; m < 3; ++m) {
+                w[m] = x[0] * r[3 * m] + x[1] * r[3 * m + 1] + x[2] * r[3 * m + 2];
+                lo[m] = std::min(lo[m], w[m]);
+                hi[m] = std::max(hi[m], w[m]);
+            }
+        }
+        double ex = hi[0] - lo[0], ey = hi[1] - lo[1], ez = hi[2] - lo[2];
+        aperture[d] = n_el > 1 ? sqrt(ex * ex + ey * ey + ez * ez) : 0.0;
+    }
+}
+
+// distinct slants in ascending order + each element's index into them
+int slant_sets(int n_el, const double* sl, double* distinct, int32_t* idx) {
+    int n = 0;
+    for (int e = 0; e < n_el; ++e) {
+        bool seen = false;
+        for (int k = 0; k < n; ++k) seen |= distinct[k] == sl[e];
+        if (!seen) distinct[n++] = sl[e];
+    }
+    std::sort(distinct, distinct + n);
+    for (int e = 0; e < n_el; ++e)
+        for (int k = 0; k < n; ++k)
+            if (distinct[k] == sl[e]) idx[e] = k;
+    return n;
+}
+}  // namespace
+
+int rt_gains_h(rt_ctx* ctx, int64_t n_paths, int max_len, const int32_t* tx_dev, const int32_t* rx_dev,
+               const int8_t* order, const int32_t* seq, const int32_t* interaction_mat,
+               const double* vertices, const double* normals, const double* cos_inc, const double* length,
+               const double* delay, const double* k_dep, const double* k_arr, int n_tx_dev,
+               const double* tx_ypr, const double* tx_pos, int n_rx_dev, const double* rx_ypr,
+               const double* rx_pos, int tx_pattern, int n_tx_el, const double* off_tx,
+               const double* sl_tx, int rx_pattern, int n_rx_el, const double* off_rx,
+               const double* sl_rx, const double* eta, int n_mat, double wavelength,
+               double frequency_hz, double* a_out, int* near_field, void* stream) {
+    if (!ctx || n_paths < 0 || max_len < 1 || n_tx_dev < 1 || n_rx_dev < 1 || n_tx_el < 1 ||
+        n_rx_el < 1 || n_mat < 1 || !(wavelength > 0.0) || !tx_ypr || !rx_ypr || !off_tx || !sl_tx ||
+        !off_rx || !sl_rx || !eta)
+        return fail(ctx, RT_EINVAL, "bad gains arguments");
+    if (tx_pattern < 0 || tx_pattern > 4 || rx_pattern < 0 || rx_pattern > 4)
+        return fail(ctx, RT_EINVAL, "unknown antenna pattern");
+    if (near_field) *near_field = 0;
+    // host parameter block: rows_t | rows_r | offw_t | offw_r | st | sr | eta | (int32) s_idx | r_idx
+    size_t o_rt = 0, o_rr = o_rt + 9 * (size_t)n_tx_dev, o_wt = o_rr + 9 * (size_t)n_rx_dev;
+    size_t o_wr = o_wt + 3 * (size_t)n_tx_dev * n_tx_el, o_st = o_wr + 3 * (size_t)n_rx_dev * n_rx_el;
+    size_t o_sr = o_st + n_tx_el, o_eta = o_sr + n_rx_el, n_dbl = o_eta + 2 * (size_t)n_mat;
+    size_t bytes = 8 * n_dbl + 4 * (size_t)(n_tx_el + n_rx_el);
+    std::vector<double> hb((bytes + 7) / 8);
+    double* h = hb.data();
+    std::vector<double> ap_t(n_tx_dev), ap_r(n_rx_dev);
+    device_frames(n_tx_dev, tx_ypr, n_tx_el, off_tx, h + o_rt, h + o_wt, ap_t.data());
+    device_frames(n_rx_dev, rx_ypr, n_rx_el, off_rx, h + o_rr, h + o_wr, ap_r.data());
+    int32_t* si = reinterpret_cast<int32_t*>(h + n_dbl);
+    int32_t* ri = si + n_tx_el;
+    int S = slant_sets(n_tx_el, sl_tx, h + o_st, si);
+    int R = slant_sets(n_rx_el, sl_rx, h + o_sr, ri);
+    std::memcpy(h + o_eta, eta, 16 * (size_t)n_mat);
+    if (near_field && tx_pos && rx_pos) {
+        // every path is at least as long as the straight tx-rx distance (em.py:344-356 pre-check)
+        for (int t = 0; t < n_tx_dev && !*near_field; ++t)
+            for (int r = 0; r < n_rx_dev; ++r) {
+                double a = std::max(ap_t[t], ap_r[r]);
+                if (a <= 0.0) continue;
+                double dx = tx_pos[3 * t] - rx_pos[3 * r], dy = tx_pos[3 * t + 1] - rx_pos[3 * r + 1];
+                double dz = tx_pos[3 * t + 2] - rx_pos[3 * r + 2];
+                if (sqrt(dx * dx + dy * dy + dz * dz) < 2.0 * a * a / wavelength * (1.0 + 1e-9)) {
+                    *near_field = 1;
+                    break;
+                }
+            }
+    }
+    if (n_paths == 0) return RT_OK;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ST(stream);
+    CK(ctx->gparam.reserve(bytes));
+    RC(h2d_staged(ctx->device, ctx->gparam.p, h, (int64_t)bytes, st));
+    const double* d = ctx->gparam.get<double>();
+    const int32_t* dsi = reinterpret_cast<const int32_t*>(d + n_dbl);
+    CK(ctx->gbase.reserve(16ULL * n_paths * S * R));
+    double* base = ctx->gbase.get<double>();
+    TransferArgs A{n_paths, max_len, (const signed char*)order, seq, vertices, normals, cos_inc, length,
+                   delay, d + o_rt, d + o_rr, tx_pattern, rx_pattern, d + o_st, S, d + o_sr, R, d + o_eta,
+                   ctx->prim_mat.get<int>(), interaction_mat, wavelength, frequency_hz, tx_dev, rx_dev};
+    k_transfer<<<nblk(n_paths * S, 128), 128, 0, st>>>(A, base);
+    CKL();
+    long long n = (long long)n_paths * n_tx_el * n_rx_el;
+    k_gains_synth<<<nblk(n, 256), 256, 0, st>>>(n_paths, S, R, base, tx_dev, rx_dev, k_dep, k_arr, n_tx_el,
+                                                d + o_wt, dsi, n_rx_el, d + o_wr, dsi + n_tx_el, wavelength,
+                                                a_out);
+    CKL();
+    return RT_OK;
+}
+
 int rt_cir_plan(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, const int32_t* seq,
                 const double* delay, const int32_t* rx_of, const int32_t* tx_of, int n_rx, int n_tx,
                 int los, int reflection, int64_t* n_path_out, void* stream) {
@@ -1754,6 +2014,7 @@ int rt_cir_plan(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, 
     *n_path_out = 0;
     ctx->cir_n = n_paths;
     ctx->cir_ntx = n_tx;
+    ctx->cir_nrx = n_rx;
     if (n_paths == 0) return RT_OK;
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ST(stream);
@@ -1786,10 +2047,9 @@ int rt_cir_plan(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, 
                                                    (const signed char*)order, seq, max_len,
                                                    ctx->cir_slot.get<int>(), ctx->cir_first.get<double>());
     CKL();
-    int h = 0;
-    CK(cudaMemcpyAsync(&h, dmax, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ctx->hpin, dmax, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    *n_path_out = h;
+    *n_path_out = reinterpret_cast<int*>(ctx->hpin)[0];
     return RT_OK;
 }
 
@@ -1801,6 +2061,10 @@ int rt_cir_scatter(rt_ctx* ctx, int64_t n_paths, const double* delay, int normal
     long long n = (long long)n_paths * n_rx_el * n_tx_el * n_t;
     if (n == 0 || n_path == 0) return RT_OK;
     CK(cudaSetDevice(ctx->device));
+    // the outputs need not be zeroed by the caller: slots past a pair's paths are 0
+    long long n_pairs = (long long)ctx->cir_nrx * ctx->cir_ntx;
+    CK(cudaMemsetAsync(a_out, 0, 16ULL * n_pairs * n_rx_el * n_tx_el * n_path * n_t, ST(stream)));
+    CK(cudaMemsetAsync(tau_out, 0, 8ULL * n_pairs * n_path, ST(stream)));
     k_cir_scatter<<<nblk(n, 256), 256, 0, ST(stream)>>>(n_paths, ctx->cir_pair.get<int>(), ctx->cir_slot.get<int>(),
                                                         ctx->cir_first.get<double>(), delay, normalize,
                                                         ctx->cir_ntx, n_rx_el, n_tx_el, n_t, n_path, a_in,

@@ -11,6 +11,7 @@ kernel rt_transfer_bwd) — this replaces the reference's scalar Tape.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import warnings
 from dataclasses import dataclass
@@ -641,41 +642,54 @@ def _rows_array(rows):
     return np.asarray(rows, dtype=np.float64).reshape(len(rows), 3, 3)
 
 
+_APERTURE_MEMO = {}
+
+
 def _aperture(off, rows):
+    """Largest world-frame extent of an array's element offsets (em.py:344-356);
+    memoised on (offset array, rotation values): the layouts are shared
+    read-only arrays (scene.element_layout) and most devices share one row."""
     if len(off) <= 1:
         return 0.0
-    w = off @ np.asarray(rows, dtype=np.float64).T
-    return float(np.linalg.norm(w.max(axis=0) - w.min(axis=0)))
+    key = (id(off), tuple(float(x) for x in np.asarray(rows, dtype=np.float64).reshape(-1)))
+    hit = _APERTURE_MEMO.get(key)
+    if hit is not None and hit[0] is off:
+        return hit[1]
+    w = off @ np.asarray(rows, dtype=np.float64).reshape(3, 3).T
+    v = float(np.linalg.norm(w.max(axis=0) - w.min(axis=0)))
+    if len(_APERTURE_MEMO) > 4096:
+        _APERTURE_MEMO.clear()
+    _APERTURE_MEMO[key] = (off, v)
+    return v
+
+
+def _device_positions(scene, T):
+    """[n_tx, 3], [n_rx, 3] positions of the table's devices (the arrays
+    compute_paths traced with, else looked up by name)."""
+    tp, rp = getattr(T, "tx_pos", None), getattr(T, "rx_pos", None)
+    if tp is None or rp is None:
+        devs = {d.name: d for d in scene.devices}
+        tp = np.array([devs[n].position for n in T.tx_names], dtype=np.float64).reshape(-1, 3)
+        rp = np.array([devs[n].position for n in T.rx_names], dtype=np.float64).reshape(-1, 3)
+    return tp, rp
 
 
 def _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows, rx_rows):
     """em.py:344-356 for every (tx, rx) pair, vectorized over the path table."""
-    memo = {}   # rows are shared tuples (EvalContext.rotation_rows memo): one aperture each
-
-    def ap(off, r, tag):
-        k = (tag, id(r)) if isinstance(r, tuple) else None   # shared row tuples: by identity
-        if k is None:
-            return _aperture(off, r)
-        v = memo.get(k)
-        if v is None:
-            v = memo[k] = _aperture(off, r)
-        return v
-    def aps(off, rows, tag):   # shared row tuples: one aperture per distinct object
+    def aps(off, rows):   # devices sharing one row object: one aperture
         if rows and all(r is rows[0] for r in rows):
-            return [ap(off, rows[0], tag)] * len(rows)
-        return [ap(off, r, tag) for r in rows]
-    ap_t = aps(off_tx, tx_rows, 0)
-    ap_r = aps(off_rx, rx_rows, 1)
-    if max(ap_t + ap_r + [0.0]) == 0.0:
+            return np.full(len(rows), _aperture(off, rows[0]))
+        return np.array([_aperture(off, r) for r in rows])
+    ap_t = aps(off_tx, tx_rows)
+    ap_r = aps(off_rx, rx_rows)
+    if not (ap_t.any() or ap_r.any()):
         return
     n_rx = len(T.rx_names)
-    a_pair = np.maximum(np.asarray(ap_t)[:, None], np.asarray(ap_r)[None, :]).reshape(-1)
+    a_pair = np.maximum(ap_t[:, None], ap_r[None, :]).reshape(-1)
     fr_pair = 2.0 * a_pair * a_pair / scene.wavelength
     # every path is at least as long as the straight tx-rx distance: when that
     # already clears the Fraunhofer distance no path can warn (no read-back)
-    devs = {d.name: d for d in scene.devices}
-    tp = np.array([devs[n].position for n in T.tx_names], dtype=np.float64).reshape(-1, 3)
-    rp = np.array([devs[n].position for n in T.rx_names], dtype=np.float64).reshape(-1, 3)
+    tp, rp = _device_positions(scene, T)
     dist = np.linalg.norm(tp[:, None, :] - rp[None, :, :], axis=-1).reshape(-1)
     if not np.any((a_pair > 0.0) & (dist < fr_pair)):
         return
@@ -689,6 +703,23 @@ def _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows, rx_rows):
         warnings.warn(f"path {T.tx_names[ti]}->{T.rx_names[ri]} at {mins[k]:.1f} m is inside "
                       f"the Fraunhofer distance {fr_pair[k]:.1f} m; the plane-wave synthetic-array "
                       "assumption degrades here", stacklevel=3)
+
+
+_SLANT_MEMO = {}
+
+
+def _slant_sets(sl):
+    """(distinct slants sorted, int32 index of every element's slant) of a
+    memoised element_layout slant array."""
+    hit = _SLANT_MEMO.get(id(sl))
+    if hit is not None and hit[0] is sl:
+        return hit[1], hit[2]
+    u = sorted(set(float(s) for s in sl))
+    idx = np.array([u.index(float(x)) for x in sl], dtype=np.int32)
+    if len(_SLANT_MEMO) > 64:
+        _SLANT_MEMO.clear()
+    _SLANT_MEMO[id(sl)] = (sl, u, idx)
+    return u, idx
 
 
 def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=None) -> ChannelGains:
@@ -709,16 +740,17 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
     if T is None or T.n == 0:
         empty = torch.zeros((0, n_rx_el, n_tx_el, 1), dtype=torch.complex128, device=dev)
         return ChannelGains(scene, T, empty, np.zeros(1))
+    if (scene.synthetic_array and eta is None and T.rx_ypr is not None and T.tx_ypr is not None
+            and not ctx.orientations):
+        return _gains_synthetic_native(scene, bvh, T, ctx, off_tx, sl_tx, off_rx, sl_rx)
     devs = {d.name: d for d in scene.devices}
     tx_rows_dev = ctx.rotation_rows_many([devs[n] for n in T.tx_names])
     rx_rows_dev = ctx.rotation_rows_many([devs[n] for n in T.rx_names])
     if not scene.synthetic_array:
         return _gains_explicit(scene, bvh, T, ctx, off_tx, sl_tx, off_rx, sl_rx, tx_rows_dev,
                                rx_rows_dev, devs, eta)
-    tx_idx = T.tx.long()
-    rx_idx = T.rx.long()
-    st = sorted(set(float(s) for s in sl_tx))
-    sr = sorted(set(float(s) for s in sl_rx))
+    st, s_idx = _slant_sets(sl_tx)
+    sr, r_idx = _slant_sets(sl_rx)
     # every small host-side parameter in one pinned upload
     n_td, n_rd = len(tx_rows_dev), len(rx_rows_dev)
     # world-frame element offsets per device (em.py:372-379), on the host
@@ -728,42 +760,71 @@ def compute_gains(scene, bvh, pathset: PathSet, ctx: EvalContext = None, eta=Non
     off_rx_w = np.einsum("ek,dmk->dem", np.asarray(off_rx, dtype=np.float64), rows_r)
     eta_host = ctx.eta_values(bvh) if eta is None else np.zeros((0, 2))
     parts = [rows_t.reshape(-1), rows_r.reshape(-1), off_tx_w.reshape(-1), off_rx_w.reshape(-1),
-             np.zeros(0), np.zeros(0),
              np.asarray(st, dtype=np.float64), np.asarray(sr, dtype=np.float64), eta_host.reshape(-1)]
     cuts = np.cumsum([0] + [len(x) for x in parts])
     # slant indices as int32 behind the doubles: one pinned upload, typed device views
-    s_idx = np.array([st.index(float(x)) for x in sl_tx], dtype=np.int32)
-    r_idx = np.array([sr.index(float(x)) for x in sl_rx], dtype=np.int32)
     f64 = np.concatenate(parts)
     blob = N.h2d(np.concatenate([f64.view(np.uint8), s_idx.view(np.uint8), r_idx.view(np.uint8)]), dev)
     allp = blob[:8 * len(f64)].view(torch.float64)
     ints = blob[8 * len(f64):].view(torch.int32)
     seg = [allp[cuts[i]:cuts[i + 1]] for i in range(len(parts))]
-    seg[4], seg[5] = ints[:len(s_idx)], ints[len(s_idx):]
-    Rt, Rr = seg[0].reshape(n_td, 3, 3), seg[1].reshape(n_rd, 3, 3)
-    offw_t, offw_r = seg[2].reshape(n_td, n_tx_el, 3), seg[3].reshape(n_rd, n_rx_el, 3)
-    tx_rows = Rt.reshape(n_td, 9)[tx_idx].contiguous()
-    rx_rows = Rr.reshape(n_rd, 9)[rx_idx].contiguous()
+    si, ri = ints[:len(s_idx)], ints[len(s_idx):]
+    _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows_dev, rx_rows_dev)
     if eta is None:
-        eta = seg[8].reshape(-1, 2)
-    base = path_coefficients(bvh, T, eta, tx_rows, rx_rows, tx_arr.pattern, rx_arr.pattern, st, sr,
-                             lam, scene.frequency_hz, slants_dev=(seg[6], seg[7]))  # [P, S, R]
-    if scene.synthetic_array:
-        _fraunhofer_warnings(scene, T, off_tx, off_rx, tx_rows_dev, rx_rows_dev)
-    if not base.requires_grad:   # one kernel: element phasors x slant coefficients
+        eta = seg[6].reshape(-1, 2)
+    if not (torch.is_grad_enabled() and eta.requires_grad):
+        # rt_gains: transfer + element phasors in one call, rows picked per path
+        # on the device (no per-path row gather)
+        eta_c = eta.detach().contiguous()
         a = torch.empty((T.n, n_rx_el, n_tx_el), dtype=torch.complex128, device=dev)
-        si, ri = seg[4], seg[5]
         with torch.cuda.device(dev):
-            bvh.ctx.call("rt_gains_synthetic", T.n, len(st), len(sr), N.ptr(base), N.ptr(T.tx),
-                         N.ptr(T.rx), N.ptr(T.kdep), N.ptr(T.karr), n_tx_el, N.ptr(offw_t), N.ptr(si),
-                         n_rx_el, N.ptr(offw_r), N.ptr(ri), float(lam), N.ptr(a), bvh.ctx.stream,
+            bvh.ctx.call("rt_gains", T.n, T.L, N.ptr(T.tx), N.ptr(T.rx), N.ptr(T.order), N.ptr(T.seq),
+                         N.ptr(getattr(T, "imat", None)), N.ptr(T.verts), N.ptr(T.normals), N.ptr(T.cos),
+                         N.ptr(T.length), N.ptr(T.delay), N.ptr(T.kdep), N.ptr(T.karr), N.ptr(seg[0]),
+                         N.ptr(seg[1]), pattern_id(tx_arr.pattern), pattern_id(rx_arr.pattern),
+                         N.ptr(seg[4]), len(st), N.ptr(seg[5]), len(sr), N.ptr(eta_c), eta_c.shape[0],
+                         n_tx_el, N.ptr(seg[2]), N.ptr(si), n_rx_el, N.ptr(seg[3]), N.ptr(ri), float(lam),
+                         float(scene.frequency_hz), N.ptr(a), bvh.ctx.stream,
                          exc_map={N.RT_EINVAL: EmError})
         return ChannelGains(scene, T, a[..., None], np.zeros(1), ctx=bvh.ctx)
-    s_index, r_index = seg[4].long(), seg[5].long()
+    # differentiable w.r.t. eta: per-path rows, autograd node over rt_transfer
+    tx_idx = T.tx.long()
+    rx_idx = T.rx.long()
+    Rt, Rr = seg[0].reshape(n_td, 9), seg[1].reshape(n_rd, 9)
+    offw_t, offw_r = seg[2].reshape(n_td, n_tx_el, 3), seg[3].reshape(n_rd, n_rx_el, 3)
+    tx_rows = Rt[tx_idx].contiguous()
+    rx_rows = Rr[rx_idx].contiguous()
+    base = path_coefficients(bvh, T, eta, tx_rows, rx_rows, tx_arr.pattern, rx_arr.pattern, st, sr,
+                             lam, scene.frequency_hz, slants_dev=(seg[4], seg[5]))  # [P, S, R]
+    s_index, r_index = si.long(), ri.long()
     ph_tx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", offw_t[tx_idx], T.kdep) / lam)
     ph_rx = torch.exp(1j * TWO_PI * torch.einsum("pem,pm->pe", offw_r[rx_idx], -T.karr) / lam)
     b = base[:, s_index][:, :, r_index].transpose(1, 2)                       # [P, rx_el, tx_el]
     a = b * ph_rx[:, :, None] * ph_tx[:, None, :]
+    return ChannelGains(scene, T, a[..., None], np.zeros(1), ctx=bvh.ctx)
+
+
+def _gains_synthetic_native(scene, bvh, T, ctx, off_tx, sl_tx, off_rx, sl_rx):
+    """compute_gains for a synthetic array as one rt_gains_h call: the device
+    orientations / positions compute_paths traced with, the memoised element
+    layouts and the material table go in as host arrays; rows, world-frame
+    offsets and slant sets are formed and uploaded by the library."""
+    tx_arr, rx_arr = scene.tx_array, scene.rx_array
+    eta_h = np.ascontiguousarray(ctx.eta_values(bvh))
+    a = torch.empty((T.n, len(off_rx), len(off_tx)), dtype=torch.complex128, device=bvh.device)
+    near = ctypes.c_int(0)
+    with torch.cuda.device(bvh.device):
+        bvh.ctx.call("rt_gains_h", T.n, T.L, N.ptr(T.tx), N.ptr(T.rx), N.ptr(T.order), N.ptr(T.seq),
+                     N.ptr(getattr(T, "imat", None)), N.ptr(T.verts), N.ptr(T.normals), N.ptr(T.cos),
+                     N.ptr(T.length), N.ptr(T.delay), N.ptr(T.kdep), N.ptr(T.karr),
+                     len(T.tx_ypr), N.ptr(T.tx_ypr), N.ptr(T.tx_pos), len(T.rx_ypr), N.ptr(T.rx_ypr),
+                     N.ptr(T.rx_pos), pattern_id(tx_arr.pattern), len(off_tx), N.ptr(off_tx), N.ptr(sl_tx),
+                     pattern_id(rx_arr.pattern), len(off_rx), N.ptr(off_rx), N.ptr(sl_rx), N.ptr(eta_h),
+                     len(eta_h), float(scene.wavelength), float(scene.frequency_hz), N.ptr(a),
+                     ctypes.byref(near), bvh.ctx.stream, exc_map={N.RT_EINVAL: EmError})
+    if near.value:   # some pair inside the Fraunhofer distance: check the paths themselves
+        _fraunhofer_warnings(scene, T, off_tx, off_rx, [rotation_entries(*y) for y in T.tx_ypr],
+                             [rotation_entries(*y) for y in T.rx_ypr])
     return ChannelGains(scene, T, a[..., None], np.zeros(1), ctx=bvh.ctx)
 
 

@@ -70,6 +70,12 @@ class PathTable:
 
     FIELDS = ("tx", "rx", "cand", "order", "seq", "verts", "length", "delay", "kdep", "karr",
               "normals", "cos")
+    # host positions of the devices the table was traced for ([n_tx, 3], [n_rx, 3]),
+    # set by compute_paths; None = look them up by name
+    tx_pos = None
+    rx_pos = None
+    tx_ypr = None   # orientations (yaw, pitch, roll) of the same devices
+    rx_ypr = None
 
     def __init__(self, L, tx_names, rx_names, **cols):
         self.L = L
@@ -318,6 +324,10 @@ def compute_paths(scene, bvh: Bvh, max_depth: int, method: str = "exhaustive",
     T = PathTable.cat(tables) if len(tables) > 1 else tables[0]
     T.tx_names = [t.name for t in txs]
     T.rx_names = [r.name for r in rxs]
+    T.tx_pos = np.array([t.position for t in txs], dtype=np.float64).reshape(-1, 3)
+    T.rx_pos = rx_pos
+    T.tx_ypr = np.array([t.orientation for t in txs], dtype=np.float64).reshape(-1, 3)
+    T.rx_ypr = np.array([r.orientation for r in rxs], dtype=np.float64).reshape(-1, 3)
     return PathSet(scene=scene, max_depth=max_depth, method=method, table=T)
 
 

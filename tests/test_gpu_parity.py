@@ -781,6 +781,11 @@ def test_degenerate_arguments_fail_loudly(P):
     assert L.rt_cir_scatter(h, 5, None, 0, None, 1, 1, 1, 1, None, None, None) == N.RT_EINVAL   # != planned count
     assert L.rt_gains_synthetic(h, 1, 1, 1, None, None, None, None, None, 1, None, None, 1, None, None,
                                 0.0, None, None) == N.RT_EINVAL   # wavelength <= 0
+    nul = [None] * 14
+    assert L.rt_gains(h, 1, 1, *nul, 0, 0, None, 1, None, 1, None, 1, 1, None, None, 1, None, None,
+                      0.0, 1e9, None, None) == N.RT_EINVAL   # wavelength <= 0, no device indices
+    assert L.rt_gains(h, 0, 1, ctypes.c_void_p(8), ctypes.c_void_p(8), *nul[2:], 0, 7, None, 1, None, 1,
+                      None, 1, 1, None, None, 1, None, None, 0.1, 1e9, None, None) == N.RT_EINVAL   # pattern
 
 
 @pytest.mark.parametrize("case", ["box", "canyon", "two_ray"])
