@@ -388,9 +388,9 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     const int small_max = n < SAH_LATENCY_PRIMS ? SAH_SMALL_LATENCY : SAH_SMALL;
     const long long cap_med = n / (small_max + 1) + 2, cap_small = n + 2;
     const long long cap_big = 2 * (n / SAH_BIG) + 2, cap_chunk = n / SAH_CHUNK + cap_big + 2;
-    size_t bytes = sizeof(SahTask) * (2 * cap_med + cap_small + 2 * cap_big) + sizeof(int2) * 2 * cap_big +
+    size_t bytes = sizeof(SahTask) * (3 * cap_med + cap_small + 2 * cap_big) + sizeof(int2) * 2 * cap_big +
                    sizeof(int) * 3 * cap_chunk + sizeof(unsigned) * 2 * cap_big * SAH_RB +
-                   16 * 16;   // alignment of the 12 sub-buffers
+                   16 * 16;   // alignment of the 13 sub-buffers
     CK(ctx->sah_tasks.reserve(bytes));
     CK(ctx->flags.reserve(4 * n));
     char* q = ctx->sah_tasks.get<char>();
@@ -401,6 +401,11 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     int2* bigc[2] = {(int2*)take(sizeof(int2) * cap_big), (int2*)take(sizeof(int2) * cap_big)};
     int* ctask[2] = {(int*)take(sizeof(int) * cap_chunk), (int*)take(sizeof(int) * cap_chunk)};
     int* cleft = (int*)take(sizeof(int) * cap_chunk);
+    // warp subtrees pay off with many ranges in flight (C3: build 1.83 -> 1.62 ms);
+    // a small scene has a handful, whose serial warps are slower than CTA levels
+    // (C2 canyon: 0.40 -> 0.70 ms), so it keeps the CTA levels to the bottom
+    SahTask* wlist = (SahTask*)take(sizeof(SahTask) * cap_med);
+    SahTask* wl = n >= SAH_LATENCY_PRIMS ? wlist : nullptr;
     unsigned* rb[2] = {(unsigned*)take(sizeof(unsigned) * cap_big * SAH_RB),
                        (unsigned*)take(sizeof(unsigned) * cap_big * SAH_RB)};
     if ((size_t)(q - ctx->sah_tasks.get<char>()) > ctx->sah_tasks.bytes)
@@ -416,7 +421,7 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     const float* pbox = ctx->pbox.get<float>();
     const float* cent = ctx->cent.get<float>();
     // device ints: [0,1] big ranges (ping-pong), [2,3] their chunks, [4,5,8] medium
-    // range counters (3-way rotation), [6] small ranges, [7] root
+    // range counters (3-way rotation), [6] small ranges, [7] root, [9] warp ranges
     int* dc = reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 16);
     k_iota<<<nblk(n, 256), 256, 0, st>>>(sidx, n);
     CKL();
@@ -427,6 +432,9 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     if (n <= small_max) {
         h[6] = 1;
         CK(cudaMemcpyAsync(small, &root_task, sizeof(SahTask), cudaMemcpyHostToDevice, st));
+    } else if (wl && n <= SAH_WARP_MAX) {
+        h[9] = 1;
+        CK(cudaMemcpyAsync(wlist, &root_task, sizeof(SahTask), cudaMemcpyHostToDevice, st));
     } else if (n <= SAH_BIG) {
         h[4] = 1;
         CK(cudaMemcpyAsync(med[0], &root_task, sizeof(SahTask), cudaMemcpyHostToDevice, st));
@@ -450,7 +458,8 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
         long long bb = nbig, bc = nchunk;
         for (int bt = 0; bt < SAH_BIG_BATCH; ++bt) {
             int nx = cur ^ 1;
-            SahOut O{small_max, small, dc + 6, med[0], dc + 4, big[nx], bigc[nx], dc + nx, ctask[nx], dc + 2 + nx};
+            SahOut O{small_max, small, dc + 6, med[0], dc + 4, big[nx], bigc[nx], dc + nx, ctask[nx], dc + 2 + nx,
+                     wl, dc + 9};
             CK(cudaMemsetAsync(dc + nx, 0, 4, st));
             CK(cudaMemsetAsync(dc + 2 + nx, 0, 4, st));
             k_sahb_init<<<bb, 128, 0, st>>>(dc + cur, rb[cur]);
@@ -490,7 +499,7 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
         for (int b = 0; b < SAH_MED_BATCH; ++b, ++lvl) {
             int nx = mcur ^ 1;
             SahOut O{small_max, small, dc + 6, med[nx], mc[(lvl + 1) % 3], nullptr, nullptr, nullptr, nullptr,
-                     nullptr};
+                     nullptr, wl, dc + 9};
             k_sah_large<<<bound, SAH_BLOCK, 0, st>>>(med[mcur], mc[lvl % 3], mc[(lvl + 2) % 3], idx0, idx1, pbox,
                                                      cent, (int)n, box, child, par, cnt, dc + 7, O);
             CKL();
@@ -502,6 +511,12 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
         CK(cudaStreamSynchronize(st));
         nmed = h[lvl % 3 == 2 ? 8 : 4 + lvl % 3];
         if (levels > 4096) return fail(ctx, RT_ECUDA, "SAH build made no progress");
+    }
+    if (h[9] > 0) {   // every range of small_max < m <= SAH_WARP_MAX: one warp per subtree
+        k_sah_warp<<<(unsigned)((h[9] + SAHW_WARPS - 1) / SAHW_WARPS), 32 * SAHW_WARPS, 0, st>>>(
+            wlist, dc + 9, idx0, idx1, pbox, cent, (int)n, box, child, par, cnt, dc + 7, small_max, small, dc + 6);
+        CKL();
+        h[6] = (int)(n / 2 + 1);   // the warps add small ranges (>= 2 prims each): grid by the bound
     }
     if (h[6] > 0) {
         k_sah_small<<<nblk(h[6], 128), 128, 0, st>>>(small, dc + 6, idx0, idx1, pbox, cent, (int)n, box, child,

@@ -46,8 +46,17 @@ constexpr int SAH_BLOCK = 256;
 constexpr int SAH_BIG = RT_SAH_BIG;       // ranges above this: several CTAs (SAH_CHUNK prims each)
 constexpr int SAH_CHUNK = 2048;
 constexpr int SAH_NCAND = 3 * (SAH_BINS - 1);
+static_assert(SAH_BINS == 32, "k_sah_warp keeps one bin per lane");
 constexpr int SAH_NB = 3 * SAH_BINS * 7;   // bins per range: count + 6 ordered bounds, 3 axes
 constexpr int SAH_NW = SAH_BLOCK / 32;
+// ranges of small_max < m <= SAH_WARP_MAX: one warp builds the whole subtree
+// (k_sah_warp) instead of one CTA per range and level
+#ifndef RT_SAH_WARP_MAX
+#define RT_SAH_WARP_MAX 128
+#endif
+constexpr int SAH_WARP_MAX = RT_SAH_WARP_MAX;
+constexpr int SAHW_WARPS = 4;                  // warps per CTA
+constexpr int SAHW_STACK = SAH_WARP_MAX;       // pending ranges per warp (<= subtree depth)
 
 // a primitive range [begin, end) whose node hangs off `parent` as child
 // `side & 1`; bit 1 of side names the index buffer holding the range
@@ -130,47 +139,73 @@ __device__ __forceinline__ void sah_bin_warp(bool valid, int p, const float* __r
     }
 }
 
-// Cheapest split from the bins (all threads call; s_cost: SAH_NCAND floats of
-// shared scratch).  out = {axis, last left bin, left count}; axis -1 when every
-// centroid coincides (split the range in the middle).
-__device__ void sah_choose(const unsigned* bins, const float scale[3], int m, float* s_cost, int* out) {
-    int tid = threadIdx.x;
-    for (int cand = tid; cand < SAH_NCAND; cand += blockDim.x) {   // any block size
-        float cost = INFINITY;
-        int a = cand / (SAH_BINS - 1), s = cand % (SAH_BINS - 1);
-        if (scale[a] != 0.f) {
-            float l[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            float r[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            int nl = 0, nr = 0;
-            for (int b = 0; b < SAH_BINS; ++b) {
-                int c = (int)bins[sah_cnt(a, b)];
-                if (!c) continue;
-                float* q = b <= s ? l : r;
-                if (b <= s) nl += c; else nr += c;
-                for (int k = 0; k < 3; ++k) {
-                    q[k] = fminf(q[k], ordered_to_float(bins[sah_bnd(a, b, k)]));
-                    q[3 + k] = fmaxf(q[3 + k], ordered_to_float(bins[sah_bnd(a, b, 3 + k)]));
-                }
+// Cheapest split from the bins, computed by one warp (all 32 lanes call; every
+// lane gets the result).  Candidate (axis a, last left bin s) costs
+// area(left) * n_left + area(right) * n_right (INFINITY when the axis is flat
+// or a side is empty); ties go to the lowest (a, s).  Lane b holds bin b: a
+// prefix scan gives the left side of split b, a suffix scan the right side
+// (empty bins are the identity of min / max).  axis -1 when every centroid
+// coincides (split the range in the middle).
+__device__ void sah_choose_warp(const unsigned* bins, const float scale[3], int m, int& axis, int& split,
+                                int& nl) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    float bc = INFINITY;
+    int bi = SAH_NCAND;
+    for (int a = 0; a < 3; ++a) {
+        if (scale[a] == 0.f) continue;
+        int cnt = (int)bins[sah_cnt(a, lane)];
+        float q[6];
+        for (int k = 0; k < 3; ++k) {
+            q[k] = cnt ? ordered_to_float(bins[sah_bnd(a, lane, k)]) : INFINITY;
+            q[3 + k] = cnt ? ordered_to_float(bins[sah_bnd(a, lane, 3 + k)]) : -INFINITY;
+        }
+        float l[6], r[6];
+        int nl_ = cnt, nr_ = cnt;
+        for (int k = 0; k < 6; ++k) { l[k] = q[k]; r[k] = q[k]; }
+        for (int o = 1; o < 32; o <<= 1) {
+            int cu = __shfl_up_sync(FULL, nl_, o), cd = __shfl_down_sync(FULL, nr_, o);
+            if (lane >= o) nl_ += cu;
+            if (lane + o < 32) nr_ += cd;
+            for (int k = 0; k < 6; ++k) {
+                float u = __shfl_up_sync(FULL, l[k], o), d = __shfl_down_sync(FULL, r[k], o);
+                if (lane >= o) l[k] = k < 3 ? fminf(l[k], u) : fmaxf(l[k], u);
+                if (lane + o < 32) r[k] = k < 3 ? fminf(r[k], d) : fmaxf(r[k], d);
             }
-            if (nl > 0 && nr > 0)
-                cost = box_area(l[0], l[1], l[2], l[3], l[4], l[5]) * (float)nl +
-                       box_area(r[0], r[1], r[2], r[3], r[4], r[5]) * (float)nr;
         }
-        s_cost[cand] = cost;
+        // split s = lane: left = prefix[lane], right = suffix[lane + 1]
+        int nr_s = __shfl_down_sync(FULL, nr_, 1);
+        float rs[6];
+        for (int k = 0; k < 6; ++k) rs[k] = __shfl_down_sync(FULL, r[k], 1);
+        if (lane < SAH_BINS - 1 && nl_ > 0 && nr_s > 0) {
+            float c = box_area(l[0], l[1], l[2], l[3], l[4], l[5]) * (float)nl_ +
+                      box_area(rs[0], rs[1], rs[2], rs[3], rs[4], rs[5]) * (float)nr_s;
+            int cand = a * (SAH_BINS - 1) + lane;
+            if (c < bc) { bc = c; bi = cand; }
+        }
     }
-    __syncthreads();
-    if (tid == 0) {
-        int best = -1;
-        float bc = INFINITY;
-        for (int t = 0; t < SAH_NCAND; ++t)
-            if (s_cost[t] < bc) { bc = s_cost[t]; best = t; }   // ties: lowest axis, lowest bin
-        if (best >= 0) {
-            int a = best / (SAH_BINS - 1), s = best % (SAH_BINS - 1), nl = 0;
-            for (int b = 0; b <= s; ++b) nl += (int)bins[sah_cnt(a, b)];
-            out[0] = a; out[1] = s; out[2] = nl;
-        } else {
-            out[0] = -1; out[1] = 0; out[2] = m / 2;
-        }
+    for (int o = 16; o; o >>= 1) {
+        float oc = __shfl_xor_sync(FULL, bc, o);
+        int oi = __shfl_xor_sync(FULL, bi, o);
+        if (oc < bc || (oc == bc && oi < bi)) { bc = oc; bi = oi; }
+    }
+    axis = -1; split = 0; nl = m / 2;
+    if (bc < INFINITY) {
+        axis = bi / (SAH_BINS - 1);
+        split = bi % (SAH_BINS - 1);
+        int c = lane <= split ? (int)bins[sah_cnt(axis, lane)] : 0;
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+        nl = c;
+    }
+}
+
+// sah_choose_warp for a CTA (all threads call; warp 0 computes).  out = {axis,
+// last left bin, left count}.
+__device__ void sah_choose(const unsigned* bins, const float scale[3], int m, int* out) {
+    if (threadIdx.x < 32) {
+        int axis, split, nl;
+        sah_choose_warp(bins, scale, m, axis, split, nl);
+        if (threadIdx.x == 0) { out[0] = axis; out[1] = split; out[2] = nl; }
     }
     __syncthreads();
 }
@@ -237,6 +272,7 @@ struct SahOut {
     SahTask* small; int* n_small;
     SahTask* med; int* n_med;
     SahTask* big; int2* big_chunks; int* n_big; int* chunk_task; int* n_chunk;
+    SahTask* warp; int* n_warp;   // small_max < m <= SAH_WARP_MAX: k_sah_warp (null: med)
 };
 
 __device__ void sah_emit(const SahTask& T, const float box[6], const int* sp, int n, const int* dst,
@@ -258,6 +294,8 @@ __device__ void sah_emit(const SahTask& T, const float box[6], const int* sp, in
             parent[p] = id;
         } else if (sz <= O.small_max) {
             O.small[atomicAdd(O.n_small, 1)] = ct;
+        } else if (O.warp && sz <= SAH_WARP_MAX) {
+            O.warp[atomicAdd(O.n_warp, 1)] = ct;
         } else if (sz <= SAH_BIG) {
             O.med[atomicAdd(O.n_med, 1)] = ct;
         } else {
@@ -291,7 +329,6 @@ __global__ void __launch_bounds__(SAH_BLOCK) k_sah_large(const SahTask* __restri
     __shared__ float red[12][SAH_NW];
     __shared__ float s_lo[3], s_scale[3], s_box[6];
     __shared__ unsigned s_bins[SAH_NB];
-    __shared__ float s_cost[SAH_NCAND];
     __shared__ int s_sp[3];
     __shared__ int s_wl[SAH_NW], s_wr[SAH_NW];
 
@@ -342,9 +379,119 @@ __global__ void __launch_bounds__(SAH_BLOCK) k_sah_large(const SahTask* __restri
         sah_bin_warp(valid, valid ? src[i] : 0, pbox, cent, lo, scale, s_bins);
     }
     __syncthreads();
-    sah_choose(s_bins, scale, T.end - T.begin, s_cost, s_sp);
+    sah_choose(s_bins, scale, T.end - T.begin, s_sp);
     sah_partition(T, T.begin, T.end, src, dst, cent, s_sp, lo, scale, 0, 0, s_wl, s_wr);
     if (tid == 0) sah_emit(T, s_box, s_sp, n, dst, true, nbox, child, parent, count, root_out, O);
+}
+
+// ---- ranges of small_max < m <= SAH_WARP_MAX prims: one warp per range, whole subtree ----
+//
+// The same binned SAH as k_sah_large (bins, candidate costs, ties to the
+// lowest (axis, bin), stable partition into the other index buffer), with the
+// warp walking its subtree depth-first from a shared-memory stack: one launch
+// for every level below SAH_WARP_MAX instead of one CTA per range and level.
+__global__ void __launch_bounds__(32 * SAHW_WARPS) k_sah_warp(const SahTask* __restrict__ tasks, const int* d_ntask,
+                                                            int* idx0, int* idx1, const float* __restrict__ pbox,
+                                                            const float* __restrict__ cent, int n, float* nbox,
+                                                            int* child, int* parent, int* count, int* root_out,
+                                                            int small_max, SahTask* small, int* n_small) {
+    const unsigned FULL = 0xffffffffu;
+    __shared__ unsigned s_bins[SAHW_WARPS][SAH_NB];
+    __shared__ SahTask s_stack[SAHW_WARPS][SAHW_STACK];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int t = blockIdx.x * SAHW_WARPS + w;
+    if (t >= *d_ntask) return;   // whole warps
+    unsigned* bins = s_bins[w];
+    SahTask* stk = s_stack[w];
+    if (lane == 0) stk[0] = tasks[t];
+    int sp = 1;
+    __syncwarp();
+    while (sp > 0) {
+        const SahTask T = stk[--sp];
+        __syncwarp();
+        const int* src = (T.side >> 1) & 1 ? idx1 : idx0;
+        int* dst = (T.side >> 1) & 1 ? idx0 : idx1;
+        const int m = T.end - T.begin;
+        // centroid bounds and the node's box (every lane ends with the totals)
+        float v[12];
+        for (int k = 0; k < 3; ++k) {
+            v[k] = INFINITY; v[3 + k] = -INFINITY; v[6 + k] = INFINITY; v[9 + k] = -INFINITY;
+        }
+        for (int i = T.begin + lane; i < T.end; i += 32) {
+            int p = src[i];
+            for (int k = 0; k < 3; ++k) {
+                float c = __ldg(cent + 3 * (long long)p + k);
+                v[k] = fminf(v[k], c);
+                v[3 + k] = fmaxf(v[3 + k], c);
+                v[6 + k] = fminf(v[6 + k], __ldg(pbox + 6 * (long long)p + k));
+                v[9 + k] = fmaxf(v[9 + k], __ldg(pbox + 6 * (long long)p + 3 + k));
+            }
+        }
+        for (int k = 0; k < 12; ++k) {
+            bool mx = (k / 3) & 1;
+            for (int o = 16; o; o >>= 1) {
+                float y = __shfl_xor_sync(FULL, v[k], o);
+                v[k] = mx ? fmaxf(v[k], y) : fminf(v[k], y);
+            }
+        }
+        float lo[3], scale[3];
+        {
+            float cmin[3] = {v[0], v[1], v[2]}, cmax[3] = {v[3], v[4], v[5]};
+            sah_frame(cmin, cmax, lo, scale);
+        }
+        sah_bins_clear(bins, lane, 32);
+        __syncwarp();
+        for (int c0 = T.begin; c0 < T.end; c0 += 32) {
+            int i = c0 + lane;
+            bool valid = i < T.end;
+            sah_bin_warp(valid, valid ? src[i] : 0, pbox, cent, lo, scale, bins);
+        }
+        __syncwarp();
+        int axis, split, nl;
+        sah_choose_warp(bins, scale, m, axis, split, nl);
+        // stable partition
+        const unsigned below = (1u << lane) - 1u;
+        int lb = 0, rb = 0;
+        for (int c0 = T.begin; c0 < T.end; c0 += 32) {
+            int i = c0 + lane;
+            bool valid = i < T.end;
+            int p = valid ? src[i] : 0;
+            bool left = valid && sah_left(p, i - T.begin, cent, axis, split, nl, lo, scale);
+            unsigned bl = __ballot_sync(FULL, left), br = __ballot_sync(FULL, valid && !left);
+            if (valid) dst[left ? T.begin + lb + __popc(bl & below) : T.begin + nl + rb + __popc(br & below)] = p;
+            lb += __popc(bl);
+            rb += __popc(br);
+        }
+        __syncwarp();   // the children read what other lanes wrote
+        // the node and its children
+        const int s = T.begin + nl, id = n + s - 1, buf = ((T.side >> 1) & 1) ^ 1;
+        float bxv = v[6];
+#pragma unroll
+        for (int k = 1; k < 6; ++k)
+            if (lane == k) bxv = v[6 + k];
+        if (lane < 6) nbox[6 * (long long)id + lane] = bxv;
+        if (lane == 0) {
+            count[id] = m;
+            sah_link(id, T.parent, T.side & 1, n, child, parent, root_out);
+        }
+        for (int c = 0; c < 2; ++c) {
+            int cb = c ? s : T.begin, ce = c ? T.end : s, sz = ce - cb;
+            SahTask ct{cb, ce, id, c | (buf << 1)};
+            if (sz == 1) {
+                if (lane == 0) {
+                    int p = dst[cb];
+                    child[2 * (long long)(id - n) + c] = p;
+                    parent[p] = id;
+                }
+            } else if (sz <= small_max) {
+                if (lane == 0) small[atomicAdd(n_small, 1)] = ct;
+            } else {
+                if (lane == 0) stk[sp] = ct;
+                ++sp;
+            }
+        }
+        __syncwarp();
+    }
 }
 
 // ---- ranges of > SAH_BIG prims: one CTA per SAH_CHUNK-prim chunk -----------------------
@@ -467,11 +614,10 @@ __global__ void __launch_bounds__(64) k_sahb_split(const SahTask* __restrict__ t
     if (t >= *d_ntask) return;
     const SahTask T = tasks[t];
     unsigned* r = rb + (long long)t * SAH_RB;
-    __shared__ float s_cost[SAH_NCAND];
     __shared__ int s_sp[3];
     float lo[3], scale[3];
     sahb_frame(r, lo, scale);
-    sah_choose(r + 12, scale, T.end - T.begin, s_cost, s_sp);
+    sah_choose(r + 12, scale, T.end - T.begin, s_sp);
     if (threadIdx.x == 0) {
         int* sp = reinterpret_cast<int*>(r + 12 + SAH_NB);
         sp[0] = s_sp[0]; sp[1] = s_sp[1]; sp[2] = s_sp[2];
