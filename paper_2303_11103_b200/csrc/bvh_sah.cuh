@@ -6,11 +6,15 @@
 // depth 5: the surface-area estimate drops 27.9 -> 22.7).  The Manhattan grid
 // defeats the Morton-order neighbourhood PLOC merges within.
 //
-// Level-synchronous: every range of > small_max primitives is one CTA
-// (k_sah_large): centroid bounds, SAH_BINS bins per axis in shared memory,
-// the cheapest split, a stable partition into the other index buffer.
-// Ranges of 2..small_max (16, or 4 for small scenes) primitives go to a list that k_sah_small finishes
-// one thread per range with the exact sweep SAH.  The tree is split all the
+// Level-synchronous: every range of > SAH_BIG primitives is split by CTAs
+// over chunks (k_sahb_*), every range of > SAH_WARP_MAX (large scenes) or >
+// small_max (small scenes) primitives by one CTA (k_sah_large): centroid
+// bounds, SAH_BINS bins per axis in shared memory, the cheapest split, a
+// stable partition into the other index buffer.  In large scenes a range of
+// small_max < m <= SAH_WARP_MAX primitives is finished, whole subtree, by one
+// warp (k_sah_warp).  Ranges of 2..small_max (8, or 4 for small scenes)
+// primitives go to a list that k_sah_small finishes one thread per range with
+// the exact sweep SAH.  The tree is split all the
 // way to single primitives; the PLOC layout path then collapses subtrees of
 // <= LEAF_MAX primitives into leaves.
 //
@@ -29,7 +33,7 @@ namespace rt {
 #endif
 constexpr int SAH_BINS = RT_SAH_BINS;
 #ifndef RT_SAH_SMALL
-#define RT_SAH_SMALL 16
+#define RT_SAH_SMALL 8   // with k_sah_warp below: C3 build 1.53 -> 1.47 ms (16: the per-thread sweeps dominate, 4: more warp nodes)
 #endif
 #ifndef RT_SAH_BIG
 #define RT_SAH_BIG 8192
