@@ -42,6 +42,9 @@
 #endif
 #ifndef RT_OCC_HINTS
 #define RT_OCC_HINTS 1   // occluder cache in k_validate (solve.cuh segments_clear_hinted)
+#ifndef RT_FUSED_SV
+#define RT_FUSED_SV 1    // solve + validation in one pass (solve.cuh k_solve_validate)
+#endif
 #endif
 #include "solve.cuh"
 #include "sort_small.cuh"
@@ -114,6 +117,7 @@ struct rt_ctx {
     DevBuf images, fp, counts, scan, pending, recs, rkeys, rkeys_alt, ridx, ridx_alt, keep,
         losbuf, heads, pcounts, poffs, em_small, ctrs;
     uint64_t pending_cap = 0;
+    uint64_t rec_cap = 0;     // record list capacity of the fused solve + validation
     // path table
     int64_t n_paths = 0;
     int path_L = 1;
@@ -1309,9 +1313,63 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     ctx->counters[4] = W;
     if (stats) stats[0] = W;
     if (W == 0) return RT_OK;
-    // geometric solve with compaction; grow and retry when the buffer is short
     if (ctx->pending_cap == 0) ctx->pending_cap = 1 << 20;
+    if (ctx->rec_cap == 0) ctx->rec_cap = 1 << 20;
+    unsigned long long* nr = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>()) + 1;
+    // occluder cache: one TriRec index per (candidate, segment), -1 = none yet
+    CK(ctx->occ_hint.reserve(4ULL * nC * (MAX_DEPTH + 1)));
+    int* hints = RT_OCC_HINTS ? ctx->occ_hint.get<int>() : nullptr;
     long long n_pend = 0;
+    if (RT_FUSED_SV && hints) {
+        // solve + validation in one pass, thin warps' open items deferred to a
+        // k_validate pass over that list; grow and rerun when a list is short
+        PROF_BEGIN(ST_SOLVE);
+        long long n_def = 0;
+        for (int attempt = 0; attempt < 8; ++attempt) {
+            CK(ctx->pending.reserve(sizeof(Pending) * ctx->pending_cap));
+            CK(ctx->recs.reserve(sizeof(Rec) * ctx->rec_cap));
+            CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
+            CK(cudaMemsetAsync(hints, 0xFF, 4ULL * nC * (MAX_DEPTH + 1), st));
+            RC(clear_flags(ctx, st));
+            unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>());
+            long long blocks = std::min<long long>((W + 127) / 128, (long long)ctx->n_sm * 32);
+            if (grid)
+                k_solve_validate<true><<<(unsigned)blocks, 128, 0, st>>>(
+                    C, SD, ctx->images.get<double>(), R, tx, W, G, bvh_dev(ctx), hints, RT_VAL_DEFER,
+                    ctx->recs.get<Rec>(), ctx->rec_cap, ctx->pending.get<Pending>(), ctx->pending_cap, ctr);
+            else
+                k_solve_validate<false><<<(unsigned)blocks, 128, 0, st>>>(
+                    C, SD, ctx->images.get<double>(), R, tx, W, G, bvh_dev(ctx), hints, RT_VAL_DEFER,
+                    ctx->recs.get<Rec>(), ctx->rec_cap, ctx->pending.get<Pending>(), ctx->pending_cap, ctr);
+            CKL();
+            RC(fetch(ctx, ctr, 3, st));
+            n_pend = ctx->hpin[0];
+            long long n_rec1 = ctx->hpin[1];
+            n_def = ctx->hpin[2];
+            bool grow = false;
+            if ((unsigned long long)n_def > ctx->pending_cap) {
+                while (ctx->pending_cap < (unsigned long long)n_def) ctx->pending_cap *= 2;
+                grow = true;
+            }
+            if ((unsigned long long)(n_rec1 + n_def) > ctx->rec_cap) {
+                while (ctx->rec_cap < (unsigned long long)(n_rec1 + n_def)) ctx->rec_cap *= 2;
+                grow = true;
+            }
+            if (!grow) break;
+        }
+        PROF_END(ST_SOLVE);
+        PROF_BEGIN(ST_VALIDATE);
+        if (n_def > 0) {
+            long long b2 = std::min<long long>((n_def + 127) / 128, (long long)ctx->n_sm * 32);
+            k_validate<false><<<(unsigned)b2, 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx,
+                                                            bvh_dev(ctx), ctx->pending.get<Pending>(),
+                                                            n_def, E, ctx->recs.get<Rec>(), nr, hints);
+            CKL();
+        }
+        if (stats) stats[1] = n_pend;
+        ctx->counters[5] = n_pend;
+    } else {
+    // geometric solve with compaction; grow and retry when the buffer is short
     for (int attempt = 0; attempt < 8; ++attempt) {
         CK(ctx->pending.reserve(sizeof(Pending) * ctx->pending_cap));
         CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
@@ -1336,17 +1394,10 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     if (n_pend == 0) return RT_OK;
     CK(ctx->recs.reserve(sizeof(Rec) * n_pend));
     CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
-    unsigned long long* nr = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>()) + 1;
     RC(clear_flags(ctx, st));
     long long vblocks = std::min<long long>((n_pend + 127) / 128, (long long)ctx->n_sm * 32);
-    // occluder cache: one TriRec index per (candidate, segment), -1 = none yet
-    CK(ctx->occ_hint.reserve(4ULL * nC * (MAX_DEPTH + 1)));
     PROF_BEGIN(ST_VALIDATE);
-    int* hints = nullptr;
-    if (RT_OCC_HINTS) {
-        hints = ctx->occ_hint.get<int>();
-        CK(cudaMemsetAsync(hints, 0xFF, 4ULL * nC * (MAX_DEPTH + 1), st));
-    }
+    if (hints) CK(cudaMemsetAsync(hints, 0xFF, 4ULL * nC * (MAX_DEPTH + 1), st));
     if (RT_VAL_DEFER > 0 && hints) {
         CK(ctx->deferred.reserve(4ULL * n_pend));
         unsigned long long* nd = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>()) + 2;
@@ -1370,6 +1421,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
                                                              bvh_dev(ctx), ctx->pending.get<Pending>(),
                                                              n_pend, E, ctx->recs.get<Rec>(), nr, hints);
         CKL();
+    }
     }
 #ifdef RT_VALIDATE_STATS
     {

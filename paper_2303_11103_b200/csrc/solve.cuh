@@ -618,6 +618,103 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_validate(Cands C, SceneDev
     }
 }
 
+// Solve and validation in one pass (RT_FUSED_SV): each item is solved; a
+// geometric survivor is first tried against the receiver-side occluder hint
+// of its candidate (the common exit), and the warp's remaining open items
+// are validated in place when at least defer_min of them are open, otherwise
+// deferred as Pending records for a k_validate pass over the deferred list
+// (full warps, warm occluder cache).  No Pending record per survivor, no
+// re-solve of the items validated here.  Capacity overflow of the record or
+// deferred list is counted (the host grows the buffers and reruns).
+// ctr: [0] survivors, [1] records, [2] deferred.
+template <bool GRID>
+__global__ void __launch_bounds__(128, RT_VAL_MINB) k_solve_validate(Cands C, SceneDev S, const double* images,
+                                                        Receivers R, d3 tx, long long W, Segs G, Bvh bvh,
+                                                        int* hints, int defer_min, Rec* recs,
+                                                        unsigned long long rec_cap, Pending* deferred,
+                                                        unsigned long long def_cap, unsigned long long* ctr) {
+    const unsigned FULL = 0xffffffffu;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    long long iters = (W + stride - 1) / stride;
+    int lane = threadIdx.x & 31;
+    for (long long it = 0; it < iters; ++it) {
+        long long w = it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+        long long rxi = 0;
+        int c = 0;
+        if (GRID) {
+            long long w0 = w - lane;
+            long long s0 = w0 < W ? G.chunk_seg[w0 >> 5] : 0;
+            if (w < W) {
+                long long sg = s0;
+                while (G.item_off[sg + 1] <= w) ++sg;
+                c = G.cand[sg];
+                long long iy = G.iy[sg], ix = G.ix0[sg] + (w - G.item_off[sg]);
+                rxi = iy * R.nx + ix;
+            }
+        } else if (w < W) {
+            c = (int)(w % C.n);
+            rxi = w / C.n;
+        }
+        d3 pts[MAX_DEPTH];
+        d3 rx = d3{0, 0, 0};
+        int K = 0;
+        bool geo = false;
+        if (w < W) {
+            rx = receiver_pos(R, rxi);
+            geo = solve_geometric(C, S, images, c, tx, rx, pts);
+            K = C.len[c];
+        }
+        unsigned gm = __ballot_sync(FULL, geo);
+        if (gm && lane == __ffs(gm) - 1) atomicAdd(ctr, (unsigned long long)__popc(gm));
+        int* hc = hints + (long long)c * (MAX_DEPTH + 1);
+        bool open_ = false;
+        if (geo) {
+            int hK = __ldcg(hc + K);
+            open_ = !(hK >= 0 && hint_blocks(bvh, hK, pts[K - 1], rx));
+        }
+        unsigned om = __ballot_sync(FULL, open_);
+        if (om && __popc(om) < defer_min) {   // too few to fill the warp's traversals: later
+            unsigned long long base = 0;
+            int leader = __ffs(om) - 1;
+            if (lane == leader) base = atomicAdd(ctr + 2, (unsigned long long)__popc(om));
+            base = __shfl_sync(FULL, base, leader);
+            if (open_) {
+                unsigned long long slot = base + __popc(om & ((1u << lane) - 1u));
+                if (slot < def_cap) {
+                    Pending q;
+                    q.rx = rxi; q.cand = c; q.order = K;
+                    q.lx = pts[K - 1].x; q.ly = pts[K - 1].y; q.lz = pts[K - 1].z;
+                    deferred[slot] = q;
+                }
+            }
+            open_ = false;
+        }
+        bool ok = false;
+        if (open_)
+            ok = segments_clear_hinted(bvh, tx, pts, K, rx, hc, C.seq + (long long)c * C.max_len, S.nrm, K);
+        unsigned m = __ballot_sync(FULL, ok);
+        if (m) {
+            unsigned long long base = 0;
+            int leader = __ffs(m) - 1;
+            if (lane == leader) base = atomicAdd(ctr + 1, (unsigned long long)__popc(m));
+            base = __shfl_sync(FULL, base, leader);
+            if (ok) {
+                unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
+                if (slot < rec_cap) {
+                    Rec rec;
+                    rec.rx = rxi;
+                    rec.cand = c;
+                    rec.order = K;
+                    rec.p0x = pts[0].x; rec.p0y = pts[0].y; rec.p0z = pts[0].z;
+                    rec.p_theta = 0.0;
+                    rec.p_phi = 0.0;
+                    recs[slot] = rec;
+                }
+            }
+        }
+    }
+}
+
 // probe powers of the surviving records (split from k_validate so the
 // occlusion kernel stays light on registers)
 __global__ void __launch_bounds__(128) k_rec_powers(Cands C, SceneDev S, const double* images,
