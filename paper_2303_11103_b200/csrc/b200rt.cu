@@ -17,6 +17,7 @@
 #include "bvh_build.cuh"
 #include "bvh_ploc.cuh"
 #include "bvh_sah.cuh"
+#include "bvh_finish.cuh"
 #include "cir.cuh"
 #include "em_jvp.cuh"
 #include "freq.cuh"
@@ -88,6 +89,7 @@ struct rt_ctx {
     int64_t n_prims = 0;
     DevBuf v0, e1, e2, nrm, poff, prim_mat, pbox, cent, cbounds;
     DevBuf up_verts, up_tris;          // device copies of host scene inputs (rt_scene_upload)
+    DevBuf rx_up;                      // rt_paths' receivers when given in host memory
     cudaEvent_t up_ev = nullptr;       // host scene inputs consumed (waited for by rt_bvh_build)
     bool up_pending = false;
     // bvh
@@ -364,6 +366,7 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st, boo
 }
 
 int finish_tree(rt_ctx* ctx, long long n, const int* root_p, cudaStream_t st);
+int finish_small(rt_ctx* ctx, long long n, const int* root, cudaStream_t st);
 int tree_diagnostics(rt_ctx* ctx, cudaStream_t st);
 int build_morton(rt_ctx* ctx, long long n, cudaStream_t st);
 
@@ -504,8 +507,15 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
             int nx = mcur ^ 1;
             SahOut O{small_max, small, dc + 6, med[nx], mc[(lvl + 1) % 3], nullptr, nullptr, nullptr, nullptr,
                      nullptr, wl, dc + 9};
-            k_sah_large<<<bound, SAH_BLOCK, 0, st>>>(med[mcur], mc[lvl % 3], mc[(lvl + 2) % 3], idx0, idx1, pbox,
-                                                     cent, (int)n, box, child, par, cnt, dc + 7, O);
+            // the top levels of a small scene are a few ranges of ~n / 2^lvl prims on as
+            // many SMs: wide CTAs shorten their latency chain (C2 canyon: 2 levels)
+            if (n <= SAH_LATENCY_PRIMS && (n >> lvl) > 2 * SAH_BLOCK)
+                k_sah_large<1024><<<bound, 1024, 0, st>>>(med[mcur], mc[lvl % 3], mc[(lvl + 2) % 3], idx0, idx1,
+                                                          pbox, cent, (int)n, box, child, par, cnt, dc + 7, O);
+            else
+                k_sah_large<SAH_BLOCK><<<bound, SAH_BLOCK, 0, st>>>(med[mcur], mc[lvl % 3], mc[(lvl + 2) % 3], idx0,
+                                                                    idx1, pbox, cent, (int)n, box, child, par, cnt,
+                                                                    dc + 7, O);
             CKL();
             mcur = nx;
             ++levels;
@@ -527,10 +537,12 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
                                                      par, cnt, dc + 7);
         CKL();
     }
+    ctx->counters[9] = levels;
+    if (RT_DFS_LAYOUT && RT_ORIGIN_SKIP && RT_STACK_CHECK && n <= FIN_MAX)
+        return finish_small(ctx, n, dc + 7, st);   // the passes below in one CTA
     CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
     k_sah_emitted<<<nblk(n, 256), 256, 0, st>>>((int)n, par, child, cnt, em, ctx->flags.get<int>());
     CKL();
-    ctx->counters[9] = levels;
     // the root id stays on the device (dc[7], written by the split that had no
     // parent): no host round trip
     return finish_tree(ctx, n, dc + 7, st);
@@ -677,6 +689,35 @@ int finish_tree(rt_ctx* ctx, long long n, const int* root, cudaStream_t st) {
     // rt_get_profile: no host round trip on the build path
     ctx->diag_root_dev = (n > 2 && dfs) ? root : nullptr;
     ctx->diag_pending = n > 1;
+    if (!ctx->diag_ev) CK(cudaEventCreateWithFlags(&ctx->diag_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->diag_ev, st));
+    return RT_OK;
+}
+
+// finish_tree + the SAH emitted counts for a small SAH tree (2 <= n <= FIN_MAX):
+// one CTA, tree links in shared memory (bvh_finish.cuh), same outputs
+int finish_small(rt_ctx* ctx, long long n, const int* root, cudaStream_t st) {
+    CK(ctx->nodes.reserve(sizeof(BNode) * std::max<long long>(n - 1, 1)));
+    CK(ctx->tree_diag.reserve(64));
+    CK(ctx->dbox.reserve(48ULL * (2 * n - 1)));
+    CK(ctx->skip_tab.reserve(8ULL * n));
+    size_t smem = fin_smem_bytes((int)n);
+    static bool attr_set[64] = {};
+    if (ctx->device < 64 && !attr_set[ctx->device]) {
+        CK(cudaFuncSetAttribute(k_finish_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fin_smem_bytes(FIN_MAX)));
+        attr_set[ctx->device] = true;
+    }
+    k_finish_small<<<1, FIN_THREADS, smem, st>>>(
+        (int)n, root, ctx->sorted_idx.get<int>(), ctx->pl_parent.get<int>(), ctx->child.get<int>(),
+        ctx->pl_count.get<int>(), ctx->pl_em.get<int>(), ctx->pl_slot.get<int>(), ctx->pl_dfs.get<int>(),
+        ctx->tree_diag.get<int>(), ctx->pl_box.get<float>(), ctx->cbounds.get<unsigned>(), ctx->nodes.get<BNode>(),
+        ctx->dbox.get<double>(), ctx->v0.get<double>(), ctx->e1.get<double>(), ctx->e2.get<double>(),
+        ctx->nrm.get<double>(), ctx->poff.get<double>(), ctx->skip_tab.get<int>(), ctx->tris.get<TriRec>());
+    CKL();
+    ctx->has_skip = true;
+    ctx->diag_root_dev = n > 2 ? root : nullptr;
+    ctx->diag_pending = true;
     if (!ctx->diag_ev) CK(cudaEventCreateWithFlags(&ctx->diag_ev, cudaEventDisableTiming));
     CK(cudaEventRecord(ctx->diag_ev, st));
     return RT_OK;
@@ -1494,6 +1535,17 @@ int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx, int6
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ST(stream);
     d3 T = d3{tx[0], tx[1], tx[2]};
+    if (n_rx > 0 && !rx) return fail(ctx, RT_EINVAL, "bad path arguments");
+    if (n_rx > 0) {   // host receiver positions: staged in on the stream
+        cudaPointerAttributes at{};
+        bool host_in = cudaPointerGetAttributes(&at, rx) != cudaSuccess || at.type != cudaMemoryTypeDevice;
+        cudaGetLastError();
+        if (host_in) {
+            CK(ctx->rx_up.reserve(24ULL * n_rx));
+            RC(h2d_staged(ctx->device, ctx->rx_up.p, rx, 24LL * n_rx, st));
+            rx = ctx->rx_up.get<double>();
+        }
+    }
     Receivers R;
     R.pts = rx;
     R.ox = R.oy = R.cell = R.height = 0.0;

@@ -222,14 +222,15 @@ __device__ __forceinline__ bool sah_left(int p, int pos_in_range, const float* _
 
 // Stable partition of src[b0, e0) (a piece of range T starting at T.begin):
 // left prims go to dst[T.begin + lbase ...], right ones to dst[T.begin + nl +
-// rbase ...].  All threads call; s_wl / s_wr: SAH_NW ints of shared scratch.
+// rbase ...].  All BLOCK threads call; s_wl / s_wr: BLOCK / 32 ints of shared scratch.
+template <int BLOCK = SAH_BLOCK>
 __device__ void sah_partition(const SahTask& T, int b0, int e0, const int* src, int* dst,
                               const float* __restrict__ cent, const int* sp /*axis, split, nl*/,
                               const float lo[3], const float scale[3], int lbase, int rbase, int* s_wl,
                               int* s_wr) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int axis = sp[0], split = sp[1], nl = sp[2];
-    for (int c0 = b0; c0 < e0; c0 += SAH_BLOCK) {
+    for (int c0 = b0; c0 < e0; c0 += BLOCK) {
         int i = c0 + tid;
         bool valid = i < e0;
         int p = valid ? src[i] : 0;
@@ -239,7 +240,7 @@ __device__ void sah_partition(const SahTask& T, int b0, int e0, const int* src, 
         if (lane == 0) { s_wl[wid] = __popc(bl); s_wr[wid] = __popc(br); }
         __syncthreads();
         int ol = 0, or_ = 0, tl = 0, tr = 0;
-        for (int w = 0; w < SAH_NW; ++w) {
+        for (int w = 0; w < BLOCK / 32; ++w) {
             if (w < wid) { ol += s_wl[w]; or_ += s_wr[w]; }
             tl += s_wl[w];
             tr += s_wr[w];
@@ -315,7 +316,8 @@ __device__ void sah_emit(const SahTask& T, const float box[6], const int* sp, in
 
 // ---- ranges of small_max < m <= SAH_BIG prims: one CTA each ----------------------------
 
-__global__ void __launch_bounds__(SAH_BLOCK) k_sah_large(const SahTask* __restrict__ tasks, const int* d_ntask,
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_sah_large(const SahTask* __restrict__ tasks, const int* d_ntask,
                                                         int* zero_after_next, int* idx0, int* idx1,
                                                         const float* __restrict__ pbox,
                                                         const float* __restrict__ cent, int n, float* nbox,
@@ -330,18 +332,18 @@ __global__ void __launch_bounds__(SAH_BLOCK) k_sah_large(const SahTask* __restri
     int* dst = (T.side >> 1) & 1 ? idx0 : idx1;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
-    __shared__ float red[12][SAH_NW];
+    __shared__ float red[12][BLOCK / 32];
     __shared__ float s_lo[3], s_scale[3], s_box[6];
     __shared__ unsigned s_bins[SAH_NB];
     __shared__ int s_sp[3];
-    __shared__ int s_wl[SAH_NW], s_wr[SAH_NW];
+    __shared__ int s_wl[BLOCK / 32], s_wr[BLOCK / 32];
 
     // centroid bounds and the node's box
     float v[12];
     for (int k = 0; k < 3; ++k) {
         v[k] = INFINITY; v[3 + k] = -INFINITY; v[6 + k] = INFINITY; v[9 + k] = -INFINITY;
     }
-    for (int i = T.begin + tid; i < T.end; i += SAH_BLOCK) {
+    for (int i = T.begin + tid; i < T.end; i += BLOCK) {
         int p = src[i];
         for (int k = 0; k < 3; ++k) {
             float c = __ldg(cent + 3 * (long long)p + k);
@@ -360,12 +362,12 @@ __global__ void __launch_bounds__(SAH_BLOCK) k_sah_large(const SahTask* __restri
         }
         if (lane == 0) red[k][wid] = x;
     }
-    sah_bins_clear(s_bins, tid, SAH_BLOCK);
+    sah_bins_clear(s_bins, tid, BLOCK);
     __syncthreads();
     if (tid < 12) {
         bool mx = (tid / 3) & 1;
         float x = red[tid][0];
-        for (int w = 1; w < SAH_NW; ++w) x = mx ? fmaxf(x, red[tid][w]) : fminf(x, red[tid][w]);
+        for (int w = 1; w < BLOCK / 32; ++w) x = mx ? fmaxf(x, red[tid][w]) : fminf(x, red[tid][w]);
         red[tid][0] = x;
     }
     __syncthreads();
@@ -377,14 +379,14 @@ __global__ void __launch_bounds__(SAH_BLOCK) k_sah_large(const SahTask* __restri
     __syncthreads();
     float lo[3] = {s_lo[0], s_lo[1], s_lo[2]}, scale[3] = {s_scale[0], s_scale[1], s_scale[2]};
 
-    for (int c0 = T.begin; c0 < T.end; c0 += SAH_BLOCK) {   // warp-uniform trip count
+    for (int c0 = T.begin; c0 < T.end; c0 += BLOCK) {   // warp-uniform trip count
         int i = c0 + tid;
         bool valid = i < T.end;
         sah_bin_warp(valid, valid ? src[i] : 0, pbox, cent, lo, scale, s_bins);
     }
     __syncthreads();
     sah_choose(s_bins, scale, T.end - T.begin, s_sp);
-    sah_partition(T, T.begin, T.end, src, dst, cent, s_sp, lo, scale, 0, 0, s_wl, s_wr);
+    sah_partition<BLOCK>(T, T.begin, T.end, src, dst, cent, s_sp, lo, scale, 0, 0, s_wl, s_wr);
     if (tid == 0) sah_emit(T, s_box, s_sp, n, dst, true, nbox, child, parent, count, root_out, O);
 }
 

@@ -273,7 +273,7 @@ def prepare_candidates(bvh: Bvh, tx_pos, max_depth, method, num_rays):
 def paths_to_receivers(bvh: Bvh, tx_pos, rx_pos, tx_index=0) -> PathTable:
     """rt_paths for the current candidate set; returns the device path table."""
     dev = bvh.device
-    rx = N.h2d(np.asarray(rx_pos, dtype=np.float64).reshape(-1, 3), dev)   # pinned, async
+    rx = np.ascontiguousarray(np.asarray(rx_pos, dtype=np.float64).reshape(-1, 3))   # staged in by rt_paths
     n = ctypes.c_int64()
     txh = _pos3(tx_pos)
     with torch.cuda.device(dev):
@@ -326,9 +326,18 @@ def compute_paths(scene, bvh: Bvh, max_depth: int, method: str = "exhaustive",
     T.rx_names = [r.name for r in rxs]
     T.tx_pos = np.array([t.position for t in txs], dtype=np.float64).reshape(-1, 3)
     T.rx_pos = rx_pos
-    T.tx_ypr = np.array([t.orientation for t in txs], dtype=np.float64).reshape(-1, 3)
-    T.rx_ypr = np.array([r.orientation for r in rxs], dtype=np.float64).reshape(-1, 3)
+    T.tx_ypr = _orientations(txs)
+    T.rx_ypr = _orientations(rxs)
     return PathSet(scene=scene, max_depth=max_depth, method=method, table=T)
+
+
+def _orientations(devs):
+    """[n, 3] (yaw, pitch, roll); devices sharing one orientation object (the
+    dataclass default) cost one conversion."""
+    o0 = devs[0].orientation
+    if all(d.orientation is o0 for d in devs):
+        return np.tile(np.asarray(o0, dtype=np.float64).reshape(1, 3), (len(devs), 1))
+    return np.array([d.orientation for d in devs], dtype=np.float64).reshape(-1, 3)
 
 
 def solve_pairs(bvh: Bvh, tx_pos, rx_pos, seqs, lens):
