@@ -267,20 +267,31 @@ int cub_call(rt_ctx* ctx, F&& f) {
 
 // Stable (key, value) radix sort over key bits [begin_bit, end_bit): one CTA
 // (k_sort_small) up to SORT_SMALL_MAX pairs, cub::DeviceRadixSort above.
-int sort_pairs(rt_ctx* ctx, const unsigned long long* kin, unsigned long long* kout, const int* vin, int* vout,
-               long long n, int begin_bit, int end_bit, cudaStream_t st) {
-    if (n <= 0) return RT_OK;
-    if (n <= SORT_SMALL_MAX) {
-        static bool attr_set[64] = {};
-        size_t smem = sizeof(typename SmallSort::TempStorage);
-        if (ctx->device < 64 && !attr_set[ctx->device]) {
-            CK(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr_set[ctx->device] = true;
-        }
-        k_sort_small<<<1, SORT_SMALL_THREADS, smem, st>>>(kin, kout, vin, vout, (int)n, begin_bit, end_bit);
-        CKL();
-        return RT_OK;
+template <int ITEMS>
+int sort_small_launch(rt_ctx* ctx, const unsigned long long* kin, unsigned long long* kout, const int* vin,
+                      int* vout, long long n, int begin_bit, int end_bit, int expand_cb, cudaStream_t st) {
+    static bool attr_set[64] = {};
+    size_t smem = sizeof(typename SmallSort<ITEMS>::TempStorage);
+    if (ctx->device < 64 && !attr_set[ctx->device]) {
+        CK(cudaFuncSetAttribute(k_sort_small<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set[ctx->device] = true;
     }
+    k_sort_small<ITEMS><<<1, SORT_SMALL_THREADS, smem, st>>>(kin, kout, vin, vout, (int)n, begin_bit, end_bit,
+                                                             expand_cb);
+    CKL();
+    return RT_OK;
+}
+
+int sort_pairs(rt_ctx* ctx, const unsigned long long* kin, unsigned long long* kout, const int* vin, int* vout,
+               long long n, int begin_bit, int end_bit, cudaStream_t st, int expand_cb = 0) {
+    if (n <= 0) return RT_OK;
+    if (n <= SORT_SMALL_THREADS * 4)
+        return sort_small_launch<4>(ctx, kin, kout, vin, vout, n, begin_bit, end_bit, expand_cb, st);
+    if (n <= SORT_SMALL_THREADS * 8)
+        return sort_small_launch<8>(ctx, kin, kout, vin, vout, n, begin_bit, end_bit, expand_cb, st);
+    if (n <= SORT_SMALL_MAX)
+        return sort_small_launch<16>(ctx, kin, kout, vin, vout, n, begin_bit, end_bit, expand_cb, st);
+    if (expand_cb > 0) return fail(ctx, RT_ECUDA, "compact record keys above the one-CTA sort size");
     return cub_call(ctx, [&](void* tmp, size_t& bytes) {
         return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, begin_bit, end_bit, st);
     });
@@ -786,12 +797,16 @@ int h2d_staged(int device, void* dst, const void* src, int64_t bytes, cudaStream
     while (bytes > 0) {
         int k = R.next;
         R.next = (k + 1) % H2D_SLOTS;
-        if (!R.host[k]) {
-            if (cudaMallocHost(&R.host[k], H2D_SLOT_BYTES) != cudaSuccess) return RT_ENOMEM;
-            if (cudaEventCreateWithFlags(&R.ev[k], cudaEventDisableTiming) != cudaSuccess) return RT_ECUDA;
-        } else if (R.used[k] && cudaEventSynchronize(R.ev[k]) != cudaSuccess) {
-            return RT_ECUDA;
+        if (!R.host[0]) {   // the whole ring at once: no page-locking (~2 ms a slot) on later calls
+            char* block = nullptr;
+            if (cudaMallocHost(reinterpret_cast<void**>(&block), H2D_SLOTS * H2D_SLOT_BYTES) != cudaSuccess)
+                return RT_ENOMEM;
+            for (int q = 0; q < H2D_SLOTS; ++q) {
+                R.host[q] = block + q * H2D_SLOT_BYTES;
+                if (cudaEventCreateWithFlags(&R.ev[q], cudaEventDisableTiming) != cudaSuccess) return RT_ECUDA;
+            }
         }
+        if (R.used[k] && cudaEventSynchronize(R.ev[k]) != cudaSuccess) return RT_ECUDA;
         size_t n = std::min<size_t>((size_t)bytes, H2D_SLOT_BYTES);
         std::memcpy(R.host[k], p, n);
         if (cudaMemcpyAsync(d, R.host[k], n, cudaMemcpyHostToDevice, st) != cudaSuccess ||
@@ -1490,15 +1505,17 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     CK(ctx->rkeys_alt.reserve(8 * n_rec));
     CK(ctx->ridx.reserve(4 * n_rec));
     CK(ctx->ridx_alt.reserve(4 * n_rec));
+    // a one-CTA sort takes compact keys (fewer radix passes) and expands them
+    int cb = n_rec <= SORT_SMALL_MAX ? bits_for(nC) : 0;
     k_rec_keys<<<nblk(n_rec, 256), 256, 0, st>>>(ctx->recs.get<Rec>(), n_rec, ctx->rkeys_alt.get<unsigned long long>(),
-                                                ctx->ridx_alt.get<int>());
+                                                ctx->ridx_alt.get<int>(), cb);
     CKL();
     unsigned long long* kin = ctx->rkeys_alt.get<unsigned long long>();
     unsigned long long* kout = ctx->rkeys.get<unsigned long long>();
     int* vin = ctx->ridx_alt.get<int>();
     int* vout = ctx->ridx.get<int>();
-    int end_bit = 36 + bits_for(R.n);
-    RC(sort_pairs(ctx, kin, kout, vin, vout, n_rec, 0, std::min(end_bit, 64), st));
+    int end_bit = (cb > 0 ? cb + 4 : 36) + bits_for(R.n);
+    RC(sort_pairs(ctx, kin, kout, vin, vout, n_rec, 0, std::min(end_bit, 64), st, cb));
     PROF_END(ST_REC_SORT);
     *n_rec_out = n_rec;
     return RT_OK;

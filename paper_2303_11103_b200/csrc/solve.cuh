@@ -733,11 +733,14 @@ __global__ void __launch_bounds__(128) k_rec_powers(Cands C, SceneDev S, const d
     recs[i].p_phi = r.p_phi;
 }
 
-__global__ void k_rec_keys(const Rec* recs, long long n, unsigned long long* keys, int* idx) {
+// record sort keys (rx, order, candidate rank): rx << 36 | order << 32 | cand,
+// or with cb > 0 the compact rx << (cb + 4) | order << cb | cand (cand < 2^cb)
+__global__ void k_rec_keys(const Rec* recs, long long n, unsigned long long* keys, int* idx, int cb) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const Rec& r = recs[i];
-    keys[i] = ((unsigned long long)r.rx << 36) | ((unsigned long long)r.order << 32) | (unsigned)r.cand;
+    int sh = cb > 0 ? cb : 32;
+    keys[i] = ((unsigned long long)r.rx << (sh + 4)) | ((unsigned long long)r.order << sh) | (unsigned)r.cand;
     idx[i] = (int)i;
 }
 
