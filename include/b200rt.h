@@ -132,6 +132,9 @@ int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx,
              int64_t* n_paths_out, void* stream);
 /* copy the path table (device outputs; any may be NULL); rows are grouped by
  * receiver in rx order.  max_len = rt_candidates_max_len (>=1). */
+/* the most paths of one receiver in the last rt_paths (its per-receiver
+ * counts come with the path count: no extra round trip) */
+int64_t rt_paths_max_per_receiver(const rt_ctx* ctx);
 int rt_paths_get(rt_ctx* ctx, int32_t* rx_index, int32_t* cand, int8_t* order, int32_t* seq,
                  double* vertices, double* length, double* delay, double* k_dep,
                  double* k_arr, double* normals, double* cos_inc, void* stream);
@@ -218,7 +221,10 @@ int rt_gains_h(rt_ctx* ctx, int64_t n_paths, int max_len, const int32_t* tx_dev,
 /* build_cir (channel.py:40-72), two calls.  rt_cir_plan keeps LOS and/or
  * specular paths, buckets them by scene (rx, tx) pair (rx_of/tx_of [P]
  * device) and orders every bucket by (delay, kind, sequence); *n_path_out =
- * the largest bucket (host sync).  rt_cir_scatter then writes a_in [P*Er*
+ * the largest bucket (host sync).  A caller that knows the largest bucket
+ * passes it in *n_path_out (>= 0; e.g. rt_paths_max_per_receiver for a
+ * table of one rt_paths call with LOS and specular kept): no host sync;
+ * -1 = compute it.  rt_cir_scatter then writes a_in [P*Er*
  * Et*n_t*2] into a_out (zero-filled by the call) [n_rx*Er*n_tx*Et*n_path*n_t*2] and
  * tau_out [n_rx*n_tx*n_path] (delays minus the pair's first arrival when
  * normalize != 0). */

@@ -28,7 +28,7 @@ EXPORTS = [
     "rt_paths", "rt_paths_get", "rt_transfer", "rt_transfer_bwd", "rt_coverage",
     "rt_set_profiling", "rt_get_profile", "rt_l2_probe", "rt_transfer_jvp", "rt_solve_pairs",
     "rt_launch_shard", "rt_gains_synthetic", "rt_cir_plan", "rt_cir_scatter", "rt_freq_nmse",
-    "rt_microbench", "rt_fresnel", "rt_gains", "rt_h2d", "rt_gains_h",
+    "rt_microbench", "rt_fresnel", "rt_gains", "rt_h2d", "rt_gains_h", "rt_paths_max_per_receiver",
 ]
 
 _lib = None
@@ -95,6 +95,7 @@ def lib():
             "rt_candidates_get": (i32, [P, P, P, i32, P]),
             "rt_num_candidates": (i64, [P]),
             "rt_candidates_max_len": (i32, [P]),
+            "rt_paths_max_per_receiver": (i64, [P]),
             "rt_paths": (i32, [P, P, P, i64, pi64, P]),
             "rt_paths_get": (i32, [P] + [P] * 11 + [P]),
             "rt_transfer": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P, i32,

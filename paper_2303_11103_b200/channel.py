@@ -135,7 +135,10 @@ def _build_cir_device(gains, T, a_all, delay, rx_names, tx_names, n_rx_el, n_tx_
     rx_of, tx_of = rx_of.to(torch.int32).contiguous(), tx_of.to(torch.int32).contiguous()
     delay = delay.to(torch.float64).contiguous()
     a_in = a_all.contiguous()
-    n = ctypes.c_int64()
+    # the largest (rx, tx) bucket is known when every path is kept and the table
+    # is compute_paths' own (rt_paths counted them): no host round trip
+    known = T.max_per_rx if (los and reflection and T.max_per_rx is not None) else -1
+    n = ctypes.c_int64(known)
     with torch.cuda.device(dev):
         ctx.call("rt_cir_plan", T.n, int(T.L), N.ptr(T.order), N.ptr(T.seq), N.ptr(delay), N.ptr(rx_of),
                  N.ptr(tx_of), len(rx_names), len(tx_names), int(bool(los)), int(bool(reflection)),

@@ -58,9 +58,10 @@ __global__ void k_seg_heads(const unsigned long long* keys, long long n, int* he
     if (i == 0 || (long long)(keys[i - 1] >> 36) != rx) heads[rx] = (int)i;
 }
 
+// paths per receiver (LOS + kept records) and their maximum (*max_count, zeroed by the caller)
 __global__ void k_path_counts(long long n_rx, const int* heads, const unsigned long long* keys,
                               long long n_rec, const unsigned char* keep,
-                              const unsigned char* los, int* counts) {
+                              const unsigned char* los, int* counts, int* max_count) {
     long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (r >= n_rx) return;
     int c = los[r];
@@ -68,6 +69,7 @@ __global__ void k_path_counts(long long n_rx, const int* heads, const unsigned l
     if (h >= 0)
         for (long long i = h; i < n_rec && (long long)(keys[i] >> 36) == r; ++i) c += keep[i];
     counts[r] = c;
+    if (c) atomicMax(max_count, c);
 }
 
 struct PathTable {

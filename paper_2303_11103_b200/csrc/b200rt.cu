@@ -123,6 +123,7 @@ struct rt_ctx {
     // path table
     int64_t n_paths = 0;
     int path_L = 1;
+    int64_t paths_max_rx = 0;   // most paths of one receiver in the last rt_paths
     DevBuf p_rx, p_cand, p_order, p_seq, p_verts, p_len, p_delay, p_kdep, p_karr, p_nrm, p_cos;
     // error flags + pinned host staging
     DevBuf dflag, probe;
@@ -863,6 +864,7 @@ const char* rt_last_error(const rt_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 int64_t rt_num_prims(const rt_ctx* ctx) { return ctx ? ctx->n_prims : 0; }
 int64_t rt_num_candidates(const rt_ctx* ctx) { return ctx ? ctx->n_cand : 0; }
 int rt_candidates_max_len(const rt_ctx* ctx) { return ctx ? ctx->cand_max_len : 1; }
+int64_t rt_paths_max_per_receiver(const rt_ctx* ctx) { return ctx ? ctx->paths_max_rx : 0; }
 
 int rt_scene_upload(rt_ctx* ctx, const double* vertices, int64_t n_vertices,
                     const int32_t* tri_vertex, const int32_t* prim_material, int64_t n_prims,
@@ -1569,6 +1571,7 @@ int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx, int6
     R.nx = R.ny = 0;
     R.n = n_rx;
     ctx->n_paths = 0;
+    ctx->paths_max_rx = 0;
     ctx->path_L = ctx->cand_max_len;
     if (n_rx == 0) {
         if (n_paths_out) *n_paths_out = 0;
@@ -1603,15 +1606,20 @@ int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx, int6
     int* cnt = ctx->pcounts.get<int>();
     int* off = ctx->poffs.get<int>();
     CK(cudaMemsetAsync(cnt + n_rx, 0, 4, st));
+    int* dmax = reinterpret_cast<int*>(ctx->ctrs.get<long long>() + 26);
+    CK(cudaMemsetAsync(dmax, 0, 4, st));
     k_path_counts<<<nblk(n_rx, 128), 128, 0, st>>>(n_rx, ctx->heads.get<int>(), ctx->rkeys.get<unsigned long long>(),
                                                    n_rec, ctx->keep.get<unsigned char>(),
-                                                   ctx->losbuf.get<unsigned char>(), cnt);
+                                                   ctx->losbuf.get<unsigned char>(), cnt, dmax);
     CKL();
     RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
         return cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, off, (int)(n_rx + 1), st);
     }));
+    // path count, (flags at hpin[1]), the largest per-receiver count: one host sync
     CK(cudaMemcpyAsync(ctx->hpin, off + n_rx, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ctx->hpin + 2, dmax, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    ctx->paths_max_rx = reinterpret_cast<int*>(ctx->hpin + 2)[0];
     {
         long long f = ctx->hpin[1];
         if (f & 1) return fail(ctx, RT_ECUDA, "BVH traversal stack overflow");
@@ -2147,6 +2155,7 @@ int rt_cir_plan(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, 
                 int los, int reflection, int64_t* n_path_out, void* stream) {
     if (!ctx || n_paths < 0 || max_len < 1 || n_rx < 1 || n_tx < 1 || !n_path_out)
         return fail(ctx, RT_EINVAL, "bad CIR arguments");
+    const int64_t hint = *n_path_out;   // >= 0: the caller knows the largest bucket
     *n_path_out = 0;
     ctx->cir_n = n_paths;
     ctx->cir_ntx = n_tx;
@@ -2183,6 +2192,10 @@ int rt_cir_plan(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* order, 
                                                    (const signed char*)order, seq, max_len,
                                                    ctx->cir_slot.get<int>(), ctx->cir_first.get<double>());
     CKL();
+    if (hint >= 0) {   // no host round trip
+        *n_path_out = hint;
+        return RT_OK;
+    }
     CK(cudaMemcpyAsync(ctx->hpin, dmax, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     *n_path_out = reinterpret_cast<int*>(ctx->hpin)[0];

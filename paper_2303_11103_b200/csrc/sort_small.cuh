@@ -14,8 +14,11 @@ namespace rt {
 constexpr int SORT_SMALL_THREADS = 512;
 constexpr int SORT_SMALL_MAX = SORT_SMALL_THREADS * 16;   // 8192 pairs
 
+#ifndef RT_SORT_RADIX_BITS
+#define RT_SORT_RADIX_BITS 4
+#endif
 template <int ITEMS>
-using SmallSort = cub::BlockRadixSort<unsigned long long, SORT_SMALL_THREADS, ITEMS, int>;
+using SmallSort = cub::BlockRadixSort<unsigned long long, SORT_SMALL_THREADS, ITEMS, int, RT_SORT_RADIX_BITS>;
 
 // expand_cb > 0: the keys are the compact path-record keys (rx << (cb + 4) |
 // order << cb | cand, cb = candidate bits) and leave in the library's record

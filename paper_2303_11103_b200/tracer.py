@@ -76,6 +76,7 @@ class PathTable:
     rx_pos = None
     tx_ypr = None   # orientations (yaw, pitch, roll) of the same devices
     rx_ypr = None
+    max_per_rx = None   # most paths of one (rx, tx) pair (rt_paths); None = unknown
 
     def __init__(self, L, tx_names, rx_names, **cols):
         self.L = L
@@ -101,7 +102,10 @@ class PathTable:
                     v = _pad_L(f, v, L, t.L)
                 parts.append(v)
             cols[f] = torch.cat(parts, 0)
-        return PathTable(L, tables[0].tx_names, tables[0].rx_names, **cols)
+        T = PathTable(L, tables[0].tx_names, tables[0].rx_names, **cols)
+        if all(t.max_per_rx is not None for t in tables):   # one transmitter per part
+            T.max_per_rx = max(t.max_per_rx for t in tables)
+        return T
 
     def host(self):
         return {f: getattr(self, f).cpu().numpy() for f in self.FIELDS}
@@ -295,7 +299,9 @@ def paths_to_receivers(bvh: Bvh, tx_pos, rx_pos, tx_index=0) -> PathTable:
                                            ("rx", "cand", "order", "seq", "verts", "length", "delay",
                                             "kdep", "karr", "normals", "cos")], bvh.ctx.stream)
         cols["tx"] = torch.full((P,), tx_index, dtype=torch.int32, device=dev)
-    return PathTable(L, [], [], **cols)
+    T = PathTable(L, [], [], **cols)
+    T.max_per_rx = int(bvh.ctx.lib.rt_paths_max_per_receiver(bvh.ctx.h))
+    return T
 
 
 def compute_paths_between(scene, bvh: Bvh, tx_dev, rx_dev, max_depth: int,
