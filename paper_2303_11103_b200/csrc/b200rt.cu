@@ -43,6 +43,9 @@
 #endif
 #ifndef RT_OCC_HINTS
 #define RT_OCC_HINTS 1   // occluder cache in k_validate (solve.cuh segments_clear_hinted)
+#ifndef RT_DEFER_MIN_ITEMS
+#define RT_DEFER_MIN_ITEMS (1LL << 23)   // fused solve + validation defers thin warps from this many items
+#endif
 #ifndef RT_FUSED_SV
 #define RT_FUSED_SV 1    // solve + validation in one pass (solve.cuh k_solve_validate)
 #endif
@@ -1383,6 +1386,9 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         // k_validate pass over that list; grow and rerun when a list is short
         PROF_BEGIN(ST_SOLVE);
         long long n_def = 0;
+        // deferral pays on long passes (C3: 37.5M items, solve + validate 4.73 -> 4.46 ms);
+        // a short one is better off in one pass (C2 canyon: 1.4M items, 141 -> 114 us)
+        const int defer_min = W >= RT_DEFER_MIN_ITEMS ? RT_VAL_DEFER : 0;
         for (int attempt = 0; attempt < 8; ++attempt) {
             CK(ctx->pending.reserve(sizeof(Pending) * ctx->pending_cap));
             CK(ctx->recs.reserve(sizeof(Rec) * ctx->rec_cap));
@@ -1393,11 +1399,11 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
             long long blocks = std::min<long long>((W + 127) / 128, (long long)ctx->n_sm * 32);
             if (grid)
                 k_solve_validate<true><<<(unsigned)blocks, 128, 0, st>>>(
-                    C, SD, ctx->images.get<double>(), R, tx, W, G, bvh_dev(ctx), hints, RT_VAL_DEFER,
+                    C, SD, ctx->images.get<double>(), R, tx, W, G, bvh_dev(ctx), hints, defer_min,
                     ctx->recs.get<Rec>(), ctx->rec_cap, ctx->pending.get<Pending>(), ctx->pending_cap, ctr);
             else
                 k_solve_validate<false><<<(unsigned)blocks, 128, 0, st>>>(
-                    C, SD, ctx->images.get<double>(), R, tx, W, G, bvh_dev(ctx), hints, RT_VAL_DEFER,
+                    C, SD, ctx->images.get<double>(), R, tx, W, G, bvh_dev(ctx), hints, defer_min,
                     ctx->recs.get<Rec>(), ctx->rec_cap, ctx->pending.get<Pending>(), ctx->pending_cap, ctr);
             CKL();
             RC(fetch(ctx, ctr, 3, st));
