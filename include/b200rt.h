@@ -132,6 +132,13 @@ int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx,
              int64_t* n_paths_out, void* stream);
 /* copy the path table (device outputs; any may be NULL); rows are grouped by
  * receiver in rx order.  max_len = rt_candidates_max_len (>=1). */
+/* compute_paths_between for one transmitter with method "fibonacci"
+ * (tracer.py:268-295): rt_launch over the whole n_rays lattice, then rt_paths
+ * to the n_rx receivers, in one call (no host round trip between them).  A
+ * scene without primitives gives LOS paths only. */
+int rt_paths_fibonacci(rt_ctx* ctx, const double* tx, int64_t n_rays, int max_depth, const double* rx,
+                       int64_t n_rx, int64_t* n_cand_out, int64_t* n_bounces_out, int64_t* n_paths_out,
+                       void* stream);
 /* the most paths of one receiver in the last rt_paths (its per-receiver
  * counts come with the path count: no extra round trip) */
 int64_t rt_paths_max_per_receiver(const rt_ctx* ctx);

@@ -29,6 +29,7 @@ EXPORTS = [
     "rt_set_profiling", "rt_get_profile", "rt_l2_probe", "rt_transfer_jvp", "rt_solve_pairs",
     "rt_launch_shard", "rt_gains_synthetic", "rt_cir_plan", "rt_cir_scatter", "rt_freq_nmse",
     "rt_microbench", "rt_fresnel", "rt_gains", "rt_h2d", "rt_gains_h", "rt_paths_max_per_receiver",
+    "rt_paths_fibonacci",
 ]
 
 _lib = None
@@ -98,6 +99,7 @@ def lib():
             "rt_paths_max_per_receiver": (i64, [P]),
             "rt_paths": (i32, [P, P, P, i64, pi64, P]),
             "rt_paths_get": (i32, [P] + [P] * 11 + [P]),
+            "rt_paths_fibonacci": (i32, [P, P, i64, i32, P, i64, pi64, pi64, pi64, P]),
             "rt_transfer": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P, i32,
                                   P, i32, f64, f64, P, P]),
             "rt_transfer_bwd": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P,

@@ -1671,6 +1671,22 @@ int rt_paths(rt_ctx* ctx, const double* tx, const double* rx, int64_t n_rx, int6
     return RT_OK;
 }
 
+int rt_paths_fibonacci(rt_ctx* ctx, const double* tx, int64_t n_rays, int max_depth, const double* rx,
+                       int64_t n_rx, int64_t* n_cand_out, int64_t* n_bounces_out, int64_t* n_paths_out,
+                       void* stream) {
+    if (!ctx || !tx || n_rays < 1 || max_depth < 1)
+        return fail(ctx, RT_EINVAL, "need num_rays >= 1 and max_depth >= 1");
+    if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
+    if (ctx->n_prims == 0) {   // no geometry: LOS only (tracer.prepare_candidates' empty set)
+        RC(sort_unique_candidates(ctx, 0, 1, ST(stream)));
+        if (n_cand_out) *n_cand_out = 0;
+        if (n_bounces_out) *n_bounces_out = 0;
+    } else {
+        RC(launch_impl(ctx, tx, n_rays, 0, n_rays, 0, 1, max_depth, nullptr, n_cand_out, n_bounces_out, stream));
+    }
+    return rt_paths(ctx, tx, rx, n_rx, n_paths_out, stream);
+}
+
 int rt_paths_get(rt_ctx* ctx, int32_t* rx_index, int32_t* cand, int8_t* order, int32_t* seq,
                  double* vertices, double* length, double* delay, double* k_dep, double* k_arr,
                  double* normals, double* cos_inc, void* stream) {

@@ -276,29 +276,47 @@ def prepare_candidates(bvh: Bvh, tx_pos, max_depth, method, num_rays):
 
 def paths_to_receivers(bvh: Bvh, tx_pos, rx_pos, tx_index=0) -> PathTable:
     """rt_paths for the current candidate set; returns the device path table."""
-    dev = bvh.device
     rx = np.ascontiguousarray(np.asarray(rx_pos, dtype=np.float64).reshape(-1, 3))   # staged in by rt_paths
     n = ctypes.c_int64()
     txh = _pos3(tx_pos)
-    with torch.cuda.device(dev):
+    with torch.cuda.device(bvh.device):
         bvh.ctx.call("rt_paths", N.ptr(txh), N.ptr(rx), rx.shape[0], ctypes.byref(n), bvh.ctx.stream,
                      exc_map=_TRACER_ERRORS)
-        P = n.value
-        L = bvh.ctx.lib.rt_candidates_max_len(bvh.ctx.h)
-        f64 = dict(dtype=torch.float64, device=dev)
-        cols = dict(rx=torch.empty(P, dtype=torch.int32, device=dev),
-                    cand=torch.empty(P, dtype=torch.int32, device=dev),
-                    order=torch.empty(P, dtype=torch.int8, device=dev),
-                    seq=torch.empty((P, L), dtype=torch.int32, device=dev),
-                    verts=torch.empty((P, L + 2, 3), **f64), length=torch.empty(P, **f64),
-                    delay=torch.empty(P, **f64), kdep=torch.empty((P, 3), **f64),
-                    karr=torch.empty((P, 3), **f64), normals=torch.empty((P, L, 3), **f64),
-                    cos=torch.empty((P, L), **f64))
-        if P:
-            bvh.ctx.call("rt_paths_get", *[N.ptr(cols[k]) for k in
-                                           ("rx", "cand", "order", "seq", "verts", "length", "delay",
-                                            "kdep", "karr", "normals", "cos")], bvh.ctx.stream)
-        cols["tx"] = torch.full((P,), tx_index, dtype=torch.int32, device=dev)
+        return _path_table(bvh, n.value, tx_index)
+
+
+def paths_fibonacci(bvh: Bvh, tx_pos, rx_pos, max_depth, num_rays, tx_index=0) -> PathTable:
+    """prepare_candidates("fibonacci") + paths_to_receivers as one library call
+    (rt_paths_fibonacci: no host round trip between the launch and the paths)."""
+    if num_rays < 1 or max_depth < 1:
+        raise TracerError("need num_rays >= 1 and max_depth >= 1")
+    rx = np.ascontiguousarray(np.asarray(rx_pos, dtype=np.float64).reshape(-1, 3))
+    nc, nb, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    txh = _pos3(tx_pos)
+    with torch.cuda.device(bvh.device):
+        bvh.ctx.call("rt_paths_fibonacci", N.ptr(txh), int(num_rays), int(max_depth), N.ptr(rx), rx.shape[0],
+                     ctypes.byref(nc), ctypes.byref(nb), ctypes.byref(n), bvh.ctx.stream, exc_map=_TRACER_ERRORS)
+        return _path_table(bvh, n.value, tx_index)
+
+
+def _path_table(bvh: Bvh, P, tx_index) -> PathTable:
+    """The library's current path table (P rows) as device tensors."""
+    dev = bvh.device
+    L = bvh.ctx.lib.rt_candidates_max_len(bvh.ctx.h)
+    f64 = dict(dtype=torch.float64, device=dev)
+    cols = dict(rx=torch.empty(P, dtype=torch.int32, device=dev),
+                cand=torch.empty(P, dtype=torch.int32, device=dev),
+                order=torch.empty(P, dtype=torch.int8, device=dev),
+                seq=torch.empty((P, L), dtype=torch.int32, device=dev),
+                verts=torch.empty((P, L + 2, 3), **f64), length=torch.empty(P, **f64),
+                delay=torch.empty(P, **f64), kdep=torch.empty((P, 3), **f64),
+                karr=torch.empty((P, 3), **f64), normals=torch.empty((P, L, 3), **f64),
+                cos=torch.empty((P, L), **f64))
+    if P:
+        bvh.ctx.call("rt_paths_get", *[N.ptr(cols[k]) for k in
+                                       ("rx", "cand", "order", "seq", "verts", "length", "delay",
+                                        "kdep", "karr", "normals", "cos")], bvh.ctx.stream)
+    cols["tx"] = torch.full((P,), tx_index, dtype=torch.int32, device=dev)
     T = PathTable(L, [], [], **cols)
     T.max_per_rx = int(bvh.ctx.lib.rt_paths_max_per_receiver(bvh.ctx.h))
     return T
@@ -325,8 +343,11 @@ def compute_paths(scene, bvh: Bvh, max_depth: int, method: str = "exhaustive",
     rx_pos = np.array([r.position for r in rxs], dtype=np.float64).reshape(-1, 3)
     tables = []
     for ti, tx in enumerate(txs):
-        prepare_candidates(bvh, tx.position, max_depth, method, num_rays)
-        tables.append(paths_to_receivers(bvh, tx.position, rx_pos, tx_index=ti))
+        if method == "fibonacci" and max_depth >= 1:
+            tables.append(paths_fibonacci(bvh, tx.position, rx_pos, max_depth, num_rays, tx_index=ti))
+        else:
+            prepare_candidates(bvh, tx.position, max_depth, method, num_rays)
+            tables.append(paths_to_receivers(bvh, tx.position, rx_pos, tx_index=ti))
     T = PathTable.cat(tables) if len(tables) > 1 else tables[0]
     T.tx_names = [t.name for t in txs]
     T.rx_names = [r.name for r in rxs]
