@@ -116,6 +116,24 @@ __device__ __forceinline__ bool slab32(const Ray& r, float2 x, float2 y, float2 
     return n <= f;
 }
 
+// slab32 for a ray whose direction signs are fixed at compile time (bit a of
+// OCT set: 1/d_a < 0, so the hi plane is the entry plane of axis a): the six
+// per-axis min / max of slab32 become register choices.  Same result bits:
+// fma(b, inv, oi) is monotonic in b, so min / max pick exactly these planes.
+template <int OCT>
+__device__ __forceinline__ bool slab32_oct(const Ray& r, float2 x, float2 y, float2 z, float tmin, float tmax,
+                                           float& tnear) {
+    float2 tx = slab_planes(x, r.fix, r.oix), ty = slab_planes(y, r.fiy, r.oiy),
+           tz = slab_planes(z, r.fiz, r.oiz);
+    float nx = (OCT & 1) ? tx.y : tx.x, fx = (OCT & 1) ? tx.x : tx.y;
+    float ny = (OCT & 2) ? ty.y : ty.x, fy = (OCT & 2) ? ty.x : ty.y;
+    float nz = (OCT & 4) ? tz.y : tz.x, fz = (OCT & 4) ? tz.x : tz.y;
+    float n = fmaxf(fmaxf(nx, ny), fmaxf(nz, tmin));
+    float f = fminf(fminf(fx, fy), fminf(fz, tmax));
+    tnear = n;
+    return n <= f;
+}
+
 // FP64 slab test (origins beyond the FP32 filter's range); NaN never culls.
 __device__ __forceinline__ bool slab(const Ray& r, float lx, float ly, float lz, float hx,
                                      float hy, float hz, double tmin, double tmax,
@@ -314,6 +332,70 @@ overflow:
 // descends internal nodes until it reaches a leaf, then the warp runs leaf
 // tests together, instead of alternating node and FP64 triangle work per
 // iteration.  Same visit order and results as trace<>.
+#ifndef RT_OCTANT
+#define RT_OCTANT 1
+#endif
+
+// The descent of trace_ww: a lane walks internal nodes until it reaches a leaf
+// (cur) or its stack runs empty (returns false).  OCT >= 0: FP32 filter with
+// the ray's octant fixed at compile time (slab32_oct); OCT < 0: box_hit.
+template <bool ANY, int OCT>
+__device__ __forceinline__ bool ww_descend(const Bvh& bvh, const Ray& r, bool fast, double tmin, double best_t,
+                                           float tmin_f, float best_tf, int& cur, int2* stack, int& sp, int& nv,
+                                           bool& overflow, int skip, int skip_end) {
+    while (!ref_is_leaf(cur)) {
+        ++nv;
+        const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
+        float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
+        int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
+        float tn0, tn1;
+        bool h0, h1;
+        if (OCT >= 0) {
+            h0 = slab32_oct<(OCT < 0 ? 0 : OCT)>(r, make_float2(a.x, a.y), make_float2(a.z, a.w),
+                                                 make_float2(b.x, b.y), tmin_f, best_tf, tn0) &&
+                 !RT_SKIPPED(ch.x);
+            h1 = slab32_oct<(OCT < 0 ? 0 : OCT)>(r, make_float2(b.z, b.w), make_float2(c.x, c.y),
+                                                 make_float2(c.z, c.w), tmin_f, best_tf, tn1) &&
+                 !RT_SKIPPED(ch.y);
+        } else {
+            h0 = box_hit(r, fast, make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(b.x, b.y), tmin,
+                         best_t, tmin_f, best_tf, tn0) &&
+                 !RT_SKIPPED(ch.x);   // the subtree behind the ray's own wall (origin skip table)
+            h1 = box_hit(r, fast, make_float2(b.z, b.w), make_float2(c.x, c.y), make_float2(c.z, c.w), tmin,
+                         best_t, tmin_f, best_tf, tn1) &&
+                 !RT_SKIPPED(ch.y);
+        }
+        if (h0 && h1) {
+            int nearc = ch.x, farc = ch.y;
+            float tf = tn1;
+            if (tn1 < tn0) { nearc = ch.y; farc = ch.x; tf = tn0; }
+            if (RT_STACK_CHECK && sp >= STACK_SIZE) { overflow = true; return false; }   // reported as an error
+            stack[sp] = make_int2(farc, __float_as_int(tf));
+            ++sp;
+            cur = nearc;
+        } else if (h0) {
+            cur = ch.x;
+        } else if (h1) {
+            cur = ch.y;
+        } else {
+            bool found = false;
+            while (sp > 0) {
+                --sp;
+                int2 e = stack[sp];
+                if (__int_as_float(e.y) <= best_tf) { cur = e.x; found = true; break; }
+            }
+            if (!found) return false;
+        }
+    }
+    return true;
+}
+
+// "while-while" form of the binary traversal (Aila & Laine 2009): a lane
+// descends internal nodes until it reaches a leaf, then the warp runs leaf
+// tests together, instead of alternating node and FP64 triangle work per
+// iteration.  Same visit order and results as trace<>.  With RT_OCTANT the
+// descent of an FP32-filtered ray runs in the copy specialised for its
+// octant (one switch per leaf visit; coherent warps share one copy).
 template <bool ANY, int MODE = 0>
 __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, double* t_out,
                         int* visits = nullptr, int* tests = nullptr, int* hit_pos = nullptr,
@@ -325,46 +407,29 @@ __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, 
     float best_tf = __double2float_ru(tmax);
     const float tmin_f = ray_tmin_f(tmin);
     const bool fast = MODE == 1 ? true : MODE == 2 ? false : ray_fast(bvh, r);
+    const int oct = (RT_OCTANT && fast) ? ((r.fix < 0.f) | ((r.fiy < 0.f) << 1) | ((r.fiz < 0.f) << 2)) : -1;
     int best_prim = -1;
     int cur = 0;
     int nv = 0, nt = 0;
-    bool alive = true;
-    while (alive) {
-        while (!ref_is_leaf(cur)) {
-            ++nv;
-            const float4* np = reinterpret_cast<const float4*>(bvh.nodes + cur);
-            float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
-            int4 ch = __ldg(reinterpret_cast<const int4*>(np + 3));
-            float tn0, tn1;
-            bool h0 = box_hit(r, fast, make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(b.x, b.y), tmin,
-                              best_t, tmin_f, best_tf, tn0) &&
-                      !RT_SKIPPED(ch.x);   // the subtree behind the ray's own wall (origin skip table)
-            bool h1 = box_hit(r, fast, make_float2(b.z, b.w), make_float2(c.x, c.y), make_float2(c.z, c.w), tmin,
-                              best_t, tmin_f, best_tf, tn1) &&
-                      !RT_SKIPPED(ch.y);
-            if (h0 && h1) {
-                int nearc = ch.x, farc = ch.y;
-                float tf = tn1;
-                if (tn1 < tn0) { nearc = ch.y; farc = ch.x; tf = tn0; }
-                if (RT_STACK_CHECK && sp >= STACK_SIZE) goto overflow;   // reported as an error
-                stack[sp] = make_int2(farc, __float_as_int(tf));
-                ++sp;
-                cur = nearc;
-            } else if (h0) {
-                cur = ch.x;
-            } else if (h1) {
-                cur = ch.y;
-            } else {
-                bool found = false;
-                while (sp > 0) {
-                    --sp;
-                    int2 e = stack[sp];
-                    if (__int_as_float(e.y) <= best_tf) { cur = e.x; found = true; break; }
-                }
-                if (!found) { alive = false; break; }
-            }
+    bool overflow = false;
+    for (;;) {
+        bool more;
+#define RT_WW_DESCEND(O) ww_descend<ANY, O>(bvh, r, fast, tmin, best_t, tmin_f, best_tf, cur, stack, sp, nv, \
+                                            overflow, skip, skip_end)
+        switch (oct) {
+            case 0: more = RT_WW_DESCEND(0); break;
+            case 1: more = RT_WW_DESCEND(1); break;
+            case 2: more = RT_WW_DESCEND(2); break;
+            case 3: more = RT_WW_DESCEND(3); break;
+            case 4: more = RT_WW_DESCEND(4); break;
+            case 5: more = RT_WW_DESCEND(5); break;
+            case 6: more = RT_WW_DESCEND(6); break;
+            case 7: more = RT_WW_DESCEND(7); break;
+            default: more = RT_WW_DESCEND(-1); break;
         }
-        if (!alive) break;
+#undef RT_WW_DESCEND
+        if (overflow) goto overflow;
+        if (!more) break;
         int first = leaf_first(cur), cnt = leaf_count(cur);
         nt += cnt;
         for (int k = 0; k < cnt; ++k) {
@@ -390,7 +455,7 @@ __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, 
         while (sp > 0) {
             --sp;
             int2 e = stack[sp];
-                    if (__int_as_float(e.y) <= best_tf) { cur = e.x; found = true; break; }
+            if (__int_as_float(e.y) <= best_tf) { cur = e.x; found = true; break; }
         }
         if (!found) break;
     }
