@@ -46,6 +46,9 @@
 #ifndef RT_DEFER_MIN_ITEMS
 #define RT_DEFER_MIN_ITEMS (1LL << 23)   // fused solve + validation defers thin warps from this many items
 #endif
+#ifndef RT_SAH_WIDE_MIN
+#define RT_SAH_WIDE_MIN 1024   // large scenes: medium SAH levels with ranges above ~this many prims use 1024-thread CTAs (C3 build 1.50 -> 1.43 ms)
+#endif
 #ifndef RT_FUSED_SV
 #define RT_FUSED_SV 1    // solve + validation in one pass (solve.cuh k_solve_validate)
 #endif
@@ -380,7 +383,7 @@ int sort_unique_candidates(rt_ctx* ctx, long long n, int L, cudaStream_t st, boo
     return RT_OK;
 }
 
-int finish_tree(rt_ctx* ctx, long long n, const int* root_p, cudaStream_t st);
+int finish_tree(rt_ctx* ctx, long long n, const int* root_p, cudaStream_t st, bool dbox_ready = false);
 int finish_small(rt_ctx* ctx, long long n, const int* root, cudaStream_t st);
 int tree_diagnostics(rt_ctx* ctx, cudaStream_t st);
 int build_morton(rt_ctx* ctx, long long n, cudaStream_t st);
@@ -523,8 +526,11 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
             SahOut O{small_max, small, dc + 6, med[nx], mc[(lvl + 1) % 3], nullptr, nullptr, nullptr, nullptr,
                      nullptr, wl, dc + 9};
             // the top levels of a small scene are a few ranges of ~n / 2^lvl prims on as
-            // many SMs: wide CTAs shorten their latency chain (C2 canyon: 2 levels)
-            if (n <= SAH_LATENCY_PRIMS && (n >> lvl) > 2 * SAH_BLOCK)
+            // many SMs: wide CTAs shorten their latency chain (C2 canyon: 2 levels); in a
+            // large scene the first medium levels hold ranges of up to SAH_BIG prims
+            const bool wide = n <= SAH_LATENCY_PRIMS ? (n >> lvl) > 2 * SAH_BLOCK
+                                                     : (n / std::max<long long>(nmed, 1) >> b) > RT_SAH_WIDE_MIN;
+            if (wide)
                 k_sah_large<1024><<<bound, 1024, 0, st>>>(med[mcur], mc[lvl % 3], mc[(lvl + 2) % 3], idx0, idx1,
                                                           pbox, cent, (int)n, box, child, par, cnt, dc + 7, O);
             else
@@ -556,6 +562,14 @@ int build_sah(rt_ctx* ctx, long long n, cudaStream_t st) {
     if (RT_DFS_LAYOUT && RT_ORIGIN_SKIP && RT_STACK_CHECK && n <= FIN_MAX)
         return finish_small(ctx, n, dc + 7, st);   // the passes below in one CTA
     CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
+    if (RT_ORIGIN_SKIP) {   // emitted counts + the exact FP64 boxes in one climb (finish_tree skips its refit)
+        CK(ctx->dbox.reserve(48ULL * (2 * n - 1)));
+        k_sah_climb<<<nblk(n, 256), 256, 0, st>>>((int)n, par, child, cnt, em, ctx->flags.get<int>(),
+                                                  ctx->v0.get<double>(), ctx->e1.get<double>(), ctx->e2.get<double>(),
+                                                  ctx->dbox.get<double>());
+        CKL();
+        return finish_tree(ctx, n, dc + 7, st, true);
+    }
     k_sah_emitted<<<nblk(n, 256), 256, 0, st>>>((int)n, par, child, cnt, em, ctx->flags.get<int>());
     CKL();
     // the root id stays on the device (dc[7], written by the split that had no
@@ -647,7 +661,7 @@ int build_ploc(rt_ctx* ctx, long long n, cudaStream_t st) {
 
 // depth-first child-pair layout + triangle records of a hierarchy in the PLOC
 // arrays (leaves [0, n) with sorted_idx, internal nodes [n, 2n-1), root id)
-int finish_tree(rt_ctx* ctx, long long n, const int* root, cudaStream_t st) {
+int finish_tree(rt_ctx* ctx, long long n, const int* root, cudaStream_t st, bool dbox_ready) {
     int* em = ctx->pl_em.get<int>();
     float* box = ctx->pl_box.get<float>();
     int* cnt = ctx->pl_count.get<int>();
@@ -685,12 +699,14 @@ int finish_tree(rt_ctx* ctx, long long n, const int* root, cudaStream_t st) {
     if (RT_ORIGIN_SKIP && n > 1 && dfs) {   // exact FP64 boxes -> per-prim origin skip refs
         CK(ctx->dbox.reserve(48ULL * (2 * n - 1)));
         CK(ctx->skip_tab.reserve(8ULL * n));
-        CK(ctx->flags.reserve(4ULL * n));
-        CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
-        k_root_parent<<<1, 1, 0, st>>>(root, par);   // the refit climb stops at the root
-        k_dbox_refit<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, ctx->v0.get<double>(), ctx->e1.get<double>(),
-                                                   ctx->e2.get<double>(), par, child, ctx->dbox.get<double>(),
-                                                   ctx->flags.get<int>());
+        if (!dbox_ready) {
+            CK(ctx->flags.reserve(4ULL * n));
+            CK(cudaMemsetAsync(ctx->flags.p, 0, 4 * n, st));
+            k_root_parent<<<1, 1, 0, st>>>(root, par);   // the refit climb stops at the root
+            k_dbox_refit<<<nblk(n, 256), 256, 0, st>>>((int)n, sidx, ctx->v0.get<double>(), ctx->e1.get<double>(),
+                                                       ctx->e2.get<double>(), par, child, ctx->dbox.get<double>(),
+                                                       ctx->flags.get<int>());
+        }
         k_skip_table<<<nblk(n, 256), 256, 0, st>>>((int)n, root, sidx, par, child, cnt, slot, dfs,
                                                    ctx->dbox.get<double>(), ctx->nrm.get<double>(),
                                                    ctx->poff.get<double>(), ctx->skip_tab.get<int>());

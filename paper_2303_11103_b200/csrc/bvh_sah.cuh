@@ -793,4 +793,35 @@ __global__ void k_sah_emitted(int n, const int* parent, const int* child, const 
     }
 }
 
+// k_sah_emitted and the exact FP64 refit (bvh_ploc.cuh k_dbox_refit) in one
+// climb: the second child to arrive at a node computes both its emitted-node
+// count and its FP64 box (leaf k is prim k in the SAH order)
+__global__ void k_sah_climb(int n, const int* parent, const int* child, const int* count, int* em, int* flags,
+                            const double* v0, const double* e1, const double* e2, double* dbox) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double* o = dbox + 6 * (long long)k;
+    for (int a = 0; a < 3; ++a) {
+        double x0 = v0[3 * (long long)k + a];
+        double x1 = x0 + e1[3 * (long long)k + a], x2 = x0 + e2[3 * (long long)k + a];
+        o[a] = fmin(x0, fmin(x1, x2));
+        o[3 + a] = fmax(x0, fmax(x1, x2));
+    }
+    int node = parent[k];
+    while (node >= 0) {
+        __threadfence();
+        if (atomicAdd(&flags[node - n], 1) == 0) return;
+        int a = child[2 * (long long)(node - n)], b = child[2 * (long long)(node - n) + 1];
+        em[node] = __ldcg(em + a) + __ldcg(em + b) + (count[node] > LEAF_MAX ? 1 : 0);
+        const double* ca = dbox + 6 * (long long)a;
+        const double* cb = dbox + 6 * (long long)b;
+        double* q = dbox + 6 * (long long)node;
+        for (int m = 0; m < 3; ++m) {
+            q[m] = fmin(__ldcg(ca + m), __ldcg(cb + m));
+            q[3 + m] = fmax(__ldcg(ca + 3 + m), __ldcg(cb + 3 + m));
+        }
+        node = parent[node];
+    }
+}
+
 }  // namespace rt
