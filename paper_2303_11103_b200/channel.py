@@ -334,8 +334,8 @@ def coverage_from_candidates(scene, bvh, tx_dev, grid: GridSpec, tx_mode="centra
     sl_h, _ = N.host_doubles(slants)
     off_h, _ = N.host_doubles(off_w)
     tx_h, _ = N.host_doubles([float(x) for x in tx_dev.position])
-    eta = ctx.eta_table(bvh)
     dev = bvh.device
+    eta = N.h2d(ctx.eta_values(bvh), dev)   # staged: no blocking pageable copy
     g = out if out is not None else torch.empty((grid.ny, grid.nx), dtype=torch.float64, device=dev)
     stats = np.zeros(8, dtype=np.int64)
     with torch.cuda.device(dev):

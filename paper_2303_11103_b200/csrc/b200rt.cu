@@ -1322,9 +1322,11 @@ namespace {
 
 // stage 1-4 of the solve pipeline for either receiver kind; leaves sorted
 // records in recs/ridx/rkeys and returns their count
+// keep_flags: the caller cleared the error word before kernels whose errors
+// this call's final read-back reports with its own (no host sync of their own)
 int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power, const EmParams& E,
                   int shard_index, int shard_count, long long* n_rec_out, long long* stats,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool keep_flags = false) {
     Cands C = cands_dev(ctx);
     SceneDev SD = scene_dev(ctx);
     long long nC = C.n;
@@ -1410,7 +1412,8 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
             CK(ctx->recs.reserve(sizeof(Rec) * ctx->rec_cap));
             CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
             CK(cudaMemsetAsync(hints, 0xFF, 4ULL * nC * (MAX_DEPTH + 1), st));
-            RC(clear_flags(ctx, st));
+            // error bits are sticky across a capacity rerun: an error of any attempt fails the call
+            if (attempt == 0 && !keep_flags) RC(clear_flags(ctx, st));
             unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>());
             long long blocks = std::min<long long>((W + 127) / 128, (long long)ctx->n_sm * 32);
             if (grid)
@@ -1474,7 +1477,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     if (n_pend == 0) return RT_OK;
     CK(ctx->recs.reserve(sizeof(Rec) * n_pend));
     CK(cudaMemsetAsync(ctx->ctrs.p, 0, 64, st));
-    RC(clear_flags(ctx, st));
+    if (!keep_flags) RC(clear_flags(ctx, st));
     long long vblocks = std::min<long long>((n_pend + 127) / 128, (long long)ctx->n_sm * 32);
     PROF_BEGIN(ST_VALIDATE);
     if (hints) CK(cudaMemsetAsync(hints, 0xFF, 4ULL * nC * (MAX_DEPTH + 1), st));
@@ -1555,8 +1558,7 @@ int em_upload(rt_ctx* ctx, const double* tx_rows, const double* probe_rows, cons
     for (int e = 0; e < n_el; ++e) h[18 + e] = slants ? slants[e] : 0.0;
     for (int e = 0; e < 3 * n_el; ++e) h[18 + n_el + e] = offsets_w ? offsets_w[e] : 0.0;
     CK(ctx->em_small.reserve(8 * n));
-    CK(cudaMemcpyAsync(ctx->em_small.p, h.data(), 8 * n, cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));
+    RC(h2d_staged(ctx->device, ctx->em_small.p, h.data(), (int64_t)(8 * n), st));   // no host sync
     double* b = ctx->em_small.get<double>();
     *d_tx = b;
     *d_probe = b + 9;
@@ -1830,9 +1832,9 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
                                                 reinterpret_cast<int*>(ctx->dflag.get<long long>()));
     CKL();
     PROF_END(ST_LOS);
-    RC(check_flags(ctx, st));
+    // the LOS kernel's error bits are reported with solve_records' read-back (no sync here)
     long long n_rec = 0;
-    RC(solve_records(ctx, T, R, true, true, E, shard_index, shard_count, &n_rec, stats, st));
+    RC(solve_records(ctx, T, R, true, true, E, shard_index, shard_count, &n_rec, stats, st, true));
     if (n_rec > 0) {
         CK(ctx->keep.reserve((size_t)n_rec));
         PROF_BEGIN(ST_MERGE);
