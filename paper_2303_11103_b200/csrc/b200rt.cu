@@ -49,6 +49,9 @@
 #ifndef RT_SAH_WIDE_MIN
 #define RT_SAH_WIDE_MIN 1024   // large scenes: medium SAH levels with ranges above ~this many prims use 1024-thread CTAs (C3 build 1.50 -> 1.43 ms)
 #endif
+#ifndef RT_SV_GRID
+#define RT_SV_GRID 32   // fused solve + validation grid: blocks per SM (grid-stride loop)
+#endif
 #ifndef RT_FUSED_SV
 #define RT_FUSED_SV 1    // solve + validation in one pass (solve.cuh k_solve_validate)
 #endif
@@ -1415,7 +1418,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
             // error bits are sticky across a capacity rerun: an error of any attempt fails the call
             if (attempt == 0 && !keep_flags) RC(clear_flags(ctx, st));
             unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ctx->ctrs.get<long long>());
-            long long blocks = std::min<long long>((W + 127) / 128, (long long)ctx->n_sm * 32);
+            long long blocks = std::min<long long>((W + 127) / 128, (long long)ctx->n_sm * RT_SV_GRID);
             if (grid)
                 k_solve_validate<true><<<(unsigned)blocks, 128, 0, st>>>(
                     C, SD, ctx->images.get<double>(), R, tx, W, G, bvh_dev(ctx), hints, defer_min,
