@@ -1407,6 +1407,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         // k_validate pass over that list; grow and rerun when a list is short
         PROF_BEGIN(ST_SOLVE);
         long long n_def = 0;
+        bool fits = false;
         // deferral pays on long passes (C3: 37.5M items, solve + validate 4.73 -> 4.46 ms);
         // a short one is better off in one pass (C2 canyon: 1.4M items, 141 -> 114 us)
         const int defer_min = W >= RT_DEFER_MIN_ITEMS ? RT_VAL_DEFER : 0;
@@ -1441,8 +1442,9 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
                 while (ctx->rec_cap < (unsigned long long)(n_rec1 + n_def)) ctx->rec_cap *= 2;
                 grow = true;
             }
-            if (!grow) break;
+            if (!grow) { fits = true; break; }
         }
+        if (!fits) return fail(ctx, RT_ENOMEM, "record / deferred lists still short after 8 regrowths");
         PROF_END(ST_SOLVE);
         PROF_BEGIN(ST_VALIDATE);
         if (n_def > 0) {
@@ -1475,6 +1477,8 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         if ((unsigned long long)n_pend <= ctx->pending_cap) break;
         while (ctx->pending_cap < (unsigned long long)n_pend) ctx->pending_cap *= 2;
     }
+    if ((unsigned long long)n_pend > ctx->pending_cap)
+        return fail(ctx, RT_ENOMEM, "pending list still short after 8 regrowths");
     if (stats) stats[1] = n_pend;
     ctx->counters[5] = n_pend;
     if (n_pend == 0) return RT_OK;
