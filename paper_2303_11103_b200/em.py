@@ -211,6 +211,7 @@ class PathCoefficients(torch.autograd.Function):
                              frequency, slants_dev)
         ctx.save_for_backward(eta_c)
         ctx.args = (bvh, T, tx_rows, rx_rows, tx_pat, rx_pat, st, sr, wavelength, frequency)
+        ctx.slants_dev = slants_dev
         return torch.view_as_complex(a)
 
     @staticmethod
@@ -220,8 +221,11 @@ class PathCoefficients(torch.autograd.Function):
         g = torch.view_as_real(grad_a.contiguous().to(torch.complex128)).contiguous()
         grad_eta = torch.zeros_like(eta)
         if T.n:
-            stt = torch.tensor(st, dtype=torch.float64, device=bvh.device)
-            srt = torch.tensor(sr, dtype=torch.float64, device=bvh.device)
+            if getattr(ctx, "slants_dev", None) is not None:   # already on the device
+                stt, srt = ctx.slants_dev
+            else:
+                stt = torch.tensor(st, dtype=torch.float64, device=bvh.device)
+                srt = torch.tensor(sr, dtype=torch.float64, device=bvh.device)
             with torch.cuda.device(bvh.device):
                 bvh.ctx.call("rt_transfer_bwd", T.n, T.L, N.ptr(T.order), N.ptr(T.seq),
                              N.ptr(getattr(T, "imat", None)), N.ptr(T.verts), N.ptr(T.normals),

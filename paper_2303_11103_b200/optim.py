@@ -17,8 +17,8 @@ import torch
 
 from . import _native as N
 from .bvh import build
-from .em import eta_from_params, path_coefficients, rotation_entries
-from .scene import POLARIZATION_SLANTS, material_params
+from .em import _launch_transfer, eta_from_params, path_coefficients, pattern_id, rotation_entries
+from .scene import POLARIZATION_SLANTS, eta_scale, material_params
 from .tracer import paths_to_receivers, prepare_candidates
 
 _EPS_KEY = "{}:eps_r"
@@ -69,20 +69,33 @@ class MaterialProblem:
         self.rec_start[1:] = torch.cumsum(counts, 0)
         self.freqs = f.contiguous()
         self.h_ri = torch.view_as_real(self.h.contiguous()).contiguous()
+        # the eta table at the scene's own values (device, once) and the slants as
+        # device tensors: a step then uploads nothing
+        f_c = scene.frequency_hz
+        self._eta_base = torch.tensor([[float(x) for x in eta_from_params(
+            *[torch.tensor(float(v), dtype=torch.float64) for v in material_params(scene.materials[n], f_c)], f_c)]
+            for n in self.bvh.material_names] or [[1.0, 0.0]], dtype=torch.float64, device=dev)
+        self._eta_row = {n: i for i, n in enumerate(self.bvh.material_names)}
+        self._eta_mul = torch.tensor([1.0, -eta_scale(f_c)], dtype=torch.float64, device=dev)
+        self._index_cache = {}
+        self._slants_dev = (torch.tensor([float(self.tx_slant)], dtype=torch.float64, device=dev),
+                            torch.tensor([float(self.rx_slant)], dtype=torch.float64, device=dev))
 
     def eta(self, values):
-        """eta table [n_mat, 2] with trainable entries taken from ``values`` (tensors)."""
-        rows = []
-        f = self.scene.frequency_hz
-        for name in self.bvh.material_names:
-            if name in values:
-                e, s = values[name]
-            else:
-                e0, s0 = material_params(self.scene.materials[name], f)
-                e = torch.tensor(float(e0), dtype=torch.float64, device=self.bvh.device)
-                s = torch.tensor(float(s0), dtype=torch.float64, device=self.bvh.device)
-            rows.append(eta_from_params(e, s, f))
-        return torch.stack(rows)
+        """eta table [n_mat, 2] with the entries of ``values`` (material -> (eps_r,
+        sigma), tensors or floats) replacing the scene's; differentiable in the
+        tensors.  Same numbers as eta_from_params per row: (eps_r, sigma * -scale)."""
+        keys = tuple(n for n in self.bvh.material_names if n in values)
+        if not keys:
+            return self._eta_base
+        dev = self.bvh.device
+        pairs = [torch.stack([torch.as_tensor(values[n][0], dtype=torch.float64, device=dev),
+                              torch.as_tensor(values[n][1], dtype=torch.float64, device=dev)]) for n in keys]
+        upd = torch.stack(pairs) * self._eta_mul                                     # [k, 2]
+        idx = self._index_cache.get(keys)
+        if idx is None:
+            idx = self._index_cache[keys] = torch.tensor([self._eta_row[n] for n in keys], device=dev)
+        return self._eta_base.index_put((idx,), upd)
 
     def default_values(self):
         """The scene's own (eps_r, sigma) of every trainable material as tensors."""
@@ -96,7 +109,8 @@ class MaterialProblem:
         sc = self.scene
         return path_coefficients(self.bvh, self.T, self.eta(values), self.tx_rows, self.rx_rows,
                                  sc.tx_array.pattern, sc.rx_array.pattern, [self.tx_slant],
-                                 [self.rx_slant], sc.wavelength, sc.frequency_hz)[:, 0, 0]
+                                 [self.rx_slant], sc.wavelength, sc.frequency_hz,
+                                 slants_dev=self._slants_dev)[:, 0, 0]
 
     def _freq_call(self, a, H=None, loss=None, grad=None, scale=1.0):
         ar = torch.view_as_real(a.detach().contiguous()).contiguous()
@@ -117,30 +131,71 @@ class MaterialProblem:
         return torch.view_as_complex(H)
 
     def loss(self, values):
-        """mean_r ||H_r - h_r||^2 / ||h_r||^2, gradient through rt_freq_nmse + the adjoint."""
-        return _RecordNmse.apply(self.coefficients(values), self)
+        """mean_r ||H_r - h_r||^2 / ||h_r||^2, differentiable in the tensors of
+        ``values`` (material -> (eps_r, sigma)): one autograd node whose forward is
+        rt_transfer + rt_freq_nmse (loss and dL/da in one launch) and whose backward
+        is the hand-written adjoint rt_transfer_bwd."""
+        keys = tuple(n for n in self.bvh.material_names if n in values)
+        dev = self.bvh.device
+        if not keys:
+            return _MaterialLoss.apply(torch.zeros((0, 2), dtype=torch.float64, device=dev), self, keys)
+        params = torch.stack([torch.as_tensor(x, dtype=torch.float64, device=dev)
+                              for n in keys for x in values[n]]).view(-1, 2)
+        return _MaterialLoss.apply(params, self, keys)
 
 
-class _RecordNmse(torch.autograd.Function):
-    """loss = sum_r (1/R) ||B_r a_r - h_r||^2 / ||h_r||^2 with dloss/da from the
-    same kernel launch (rt_freq_nmse); per-record losses are summed by torch's
-    fixed-order reduction."""
+class _MaterialLoss(torch.autograd.Function):
+    """loss = sum_r (1/R) ||B_r a_r - h_r||^2 / ||h_r||^2 of params [k, 2] =
+    (eps_r, sigma) of the materials ``keys``.  forward: eta table (the scene's
+    rows with those entries replaced, eta_from_params' arithmetic), rt_transfer,
+    rt_freq_nmse (per-record losses + dL/da); the per-record losses are summed by
+    torch's fixed-order reduction.  backward: rt_transfer_bwd of dL/da (dL/d eta
+    per material, deterministic), then d eta / d (eps_r, sigma) = (1, -scale)."""
 
     @staticmethod
-    def forward(ctx, a, prob):
+    def forward(ctx, params, prob, keys):
         dev = prob.bvh.device
-        loss_r = torch.zeros(prob.R, dtype=torch.float64, device=dev)
-        grad = torch.zeros((a.shape[0], 2), dtype=torch.float64, device=dev)
-        if prob.R:
-            prob._freq_call(a, loss=loss_r, grad=grad if a.requires_grad else None,
-                            scale=1.0 / prob.R)
-        ctx.save_for_backward(torch.view_as_complex(grad))
+        sc = prob.scene
+        if keys:
+            idx = prob._index_cache.get(keys)
+            if idx is None:
+                idx = prob._index_cache[keys] = torch.tensor([prob._eta_row[n] for n in keys], device=dev)
+            eta = prob._eta_base.index_put((idx,), params.detach() * prob._eta_mul)
+        else:
+            idx, eta = None, prob._eta_base
+        st, sr = (float(prob.tx_slant),), (float(prob.rx_slant),)
+        a = _launch_transfer(prob.bvh, prob.T, prob.tx_rows, prob.rx_rows, pattern_id(sc.tx_array.pattern),
+                             pattern_id(sc.rx_array.pattern), st, sr, eta, sc.wavelength, sc.frequency_hz,
+                             prob._slants_dev)
+        loss_r = torch.empty(prob.R, dtype=torch.float64, device=dev)
+        grad = torch.empty((prob.T.n, 2), dtype=torch.float64, device=dev)
+        if prob.R:   # rt_freq_nmse writes every record's loss and every path's dL/da
+            prob._freq_call(torch.view_as_complex(a[:, 0, 0]), loss=loss_r, grad=grad, scale=1.0 / prob.R)
+        ctx.prob, ctx.idx, ctx.st, ctx.sr = prob, idx, st, sr
+        ctx.save_for_backward(grad, eta)
         return loss_r.sum()
 
     @staticmethod
     def backward(ctx, g):
-        (grad,) = ctx.saved_tensors
-        return grad * g, None
+        grad, eta = ctx.saved_tensors
+        prob, idx = ctx.prob, ctx.idx
+        if idx is None:
+            return None, None, None
+        sc = prob.scene
+        T = prob.T
+        ga = (grad * g).contiguous()            # dL/da as (re, im) pairs = [P, S=1, R=1, 2]
+        grad_eta = torch.zeros_like(eta)
+        if T.n:
+            stt, srt = prob._slants_dev
+            with torch.cuda.device(prob.bvh.device):
+                prob.bvh.ctx.call("rt_transfer_bwd", T.n, T.L, N.ptr(T.order), N.ptr(T.seq),
+                                  N.ptr(getattr(T, "imat", None)), N.ptr(T.verts), N.ptr(T.normals),
+                                  N.ptr(T.cos), N.ptr(T.length), N.ptr(T.delay), N.ptr(prob.tx_rows),
+                                  N.ptr(prob.rx_rows), pattern_id(sc.tx_array.pattern),
+                                  pattern_id(sc.rx_array.pattern), N.ptr(stt), 1, N.ptr(srt), 1, N.ptr(eta),
+                                  eta.shape[0], float(sc.wavelength), float(sc.frequency_hz), N.ptr(ga),
+                                  N.ptr(grad_eta), prob.bvh.ctx.stream)
+        return grad_eta[idx] * prob._eta_mul, None, None
 
 
 def material_loss_and_grad(scene, positions, h_targets, max_depth=2, num_subcarriers=128,
