@@ -345,6 +345,8 @@ def coverage_from_candidates(scene, bvh, tx_dev, grid: GridSpec, tx_mode="centra
                      N.ptr(off_h), len(slants), mode, N.ptr(eta), eta.shape[0], scene.wavelength,
                      scene.frequency_hz, int(shard_index), int(shard_count), N.ptr(g),
                      N.ptr(stats), bvh.ctx.stream, exc_map=_COV_ERRORS)
+    # geometric_pairs: (cell, candidate) pairs that passed the image solve and were not
+    # stopped by the receiver-side occluder hint (the fused pass exits there early)
     keys = ("work_items", "geometric_pairs", "valid_paths", "cells", "candidates")
     return g, {k: int(stats[i]) for i, k in enumerate(keys)}
 

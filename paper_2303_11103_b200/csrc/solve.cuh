@@ -61,8 +61,15 @@ __global__ void k_images(Cands C, SceneDev S, d3 tx, double* images /*[n*max_len
 // solve_points back-substitution (tracer.py:88-102) + the geometric part of
 // image_solve (tracer.py:164-180).  Returns true when every test passes; the
 // interaction points land in pts[0..K).
+//
+// rx_hint (optional): the candidate's receiver-side occluder-cache slot.  The
+// back-substitution yields the last interaction point first; when the cached
+// occluder blocks the segment from it to the receiver, the path cannot be
+// valid whatever the remaining levels give (image_solve's conjunction,
+// tracer.py:164-182), so the solve stops there and returns false.
 __device__ inline bool solve_geometric(const Cands& C, const SceneDev& S, const double* images,
-                                       long long c, d3 tx, d3 rx, d3* pts) {
+                                       long long c, d3 tx, d3 rx, d3* pts, const Bvh* bvh = nullptr,
+                                       const int* rx_hint = nullptr) {
     int K = C.len[c];
     const int* seq = C.seq + c * C.max_len;
     d3 cur = rx;
@@ -92,6 +99,10 @@ __device__ inline bool solve_geometric(const Cands& C, const SceneDev& S, const 
         }
         pts[j] = p;
         cur = p;
+        if (rx_hint && j == K - 1) {
+            int h = __ldcg(rx_hint);
+            if (h >= 0 && hint_blocks(*bvh, h, p, rx)) return false;
+        }
     }
     for (int j = 0; j < K; ++j) {   // same-side reflection (tracer.py:170-176)
         int prim = seq[j];
@@ -659,19 +670,18 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_solve_validate(Cands C, Sc
         d3 rx = d3{0, 0, 0};
         int K = 0;
         bool geo = false;
+        int* hc = hints + (long long)c * (MAX_DEPTH + 1);
         if (w < W) {
             rx = receiver_pos(R, rxi);
-            geo = solve_geometric(C, S, images, c, tx, rx, pts);
             K = C.len[c];
+            // the receiver-side occluder hint is tried as soon as the solve has the
+            // last interaction point: a blocked item skips the remaining levels
+            geo = solve_geometric(C, S, images, c, tx, rx, pts, &bvh, hc + K);
         }
+        // geometric survivors not blocked by the receiver-side hint
         unsigned gm = __ballot_sync(FULL, geo);
         if (gm && lane == __ffs(gm) - 1) atomicAdd(ctr, (unsigned long long)__popc(gm));
-        int* hc = hints + (long long)c * (MAX_DEPTH + 1);
-        bool open_ = false;
-        if (geo) {
-            int hK = __ldcg(hc + K);
-            open_ = !(hK >= 0 && hint_blocks(bvh, hK, pts[K - 1], rx));
-        }
+        bool open_ = geo;
         unsigned om = __ballot_sync(FULL, open_);
         if (om && __popc(om) < defer_min) {   // too few to fill the warp's traversals: later
             unsigned long long base = 0;
