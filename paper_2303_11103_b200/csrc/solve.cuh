@@ -117,7 +117,10 @@ __device__ inline bool solve_geometric(const Cands& C, const SceneDev& S, const 
     for (int j = 0; j <= K; ++j) {   // minimum segment length (tracer.py:178-180)
         d3 b = j < K ? pts[j] : rx;
         double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
-        if (sqrt(dx * dx + dy * dy + dz * dz) <= 2 * RAY_EPS) return false;
+        // the square root only near the threshold: above (2 eps)^2 (1 + 1e-9) the
+        // correctly rounded root exceeds 2 eps (a 5e-10 relative gap >> 1 ulp)
+        double d2 = dx * dx + dy * dy + dz * dz;
+        if (d2 <= (2 * RAY_EPS) * (2 * RAY_EPS) * (1.0 + 1e-9) && sqrt(d2) <= 2 * RAY_EPS) return false;
         a = b;
     }
     return true;
