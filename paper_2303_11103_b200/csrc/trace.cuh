@@ -223,7 +223,9 @@ __device__ __forceinline__ int origin_skip(const Bvh& bvh, int prim, double n_do
 
 // the FP32 filter is valid for origins within origin_limit (slab32)
 __device__ __forceinline__ bool ray_fast(const Bvh& bvh, const Ray& r) {
-    return fmax(fmax(fabs(r.ox), fabs(r.oy)), fabs(r.oz)) <= __ldg(bvh.origin_limit);
+    // max |o_i| <= L as three compares (sm_100 has no FP64 min / max instruction)
+    const double L = __ldg(bvh.origin_limit);
+    return fabs(r.ox) <= L && fabs(r.oy) <= L && fabs(r.oz) <= L;
 }
 
 // FP32 lower bound of t_min for the box filter.  The common t_min = RAY_EPS is
