@@ -1171,11 +1171,15 @@ int launch_impl(rt_ctx* ctx, const double* tx, int64_t n_rays, int64_t slot_begi
         P.n_rays = n_rays;
         P.slot_begin = slot_begin;
         P.slot_end = slot_end;
-        P.shard_unit = unit;
+        P.shard_unit = unit;   // B or 4096: a power of two
+        P.shard_shift = 0;
+        while ((1LL << P.shard_shift) < unit) ++P.shard_shift;
         P.shard_index = shard_index;
         P.shard_count = shard_count;
         P.max_depth = max_depth;
         P.band = B;
+        P.band_shift = 0;
+        while (B > 0 && (1 << P.band_shift) < B) ++P.band_shift;
         P.perm = ctx->perm_band.get<int>();
         P.dirs = dirs;
         P.normals = ctx->nrm.get<double>();

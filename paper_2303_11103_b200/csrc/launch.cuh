@@ -77,9 +77,12 @@ struct LaunchParams {
     double tx, ty, tz;
     long long n_rays, slot_begin, slot_end;
     long long shard_unit;     // sharded launch: local slot l -> global unit (l/unit)*count+index
+                              // (a power of two: shard_shift = log2 unit)
     int shard_index, shard_count;
     int max_depth;
-    int band;                 // B; 0 disables the permutation
+    int band;                 // B (a power of two); 0 disables the permutation
+    int band_shift;           // log2 B
+    int shard_shift;
     const int* perm;          // [B]
     const double* dirs;       // optional [n_rays*3]
     const double* normals;    // [n_prims*3] global order
@@ -124,16 +127,16 @@ __global__ void __launch_bounds__(RT_LAUNCH_BLOCK, RT_LAUNCH_MINB) k_launch(Bvh 
         long long slot = P.slot_begin + it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
         bool active = slot < P.slot_end;
         if (P.shard_count > 1) {   // band-interleaved shard (rt_launch_shard)
-            long long lu = slot / P.shard_unit;
-            slot = (lu * P.shard_count + P.shard_index) * P.shard_unit + (slot - lu * P.shard_unit);
+            long long lu = slot >> P.shard_shift;
+            slot = ((lu * P.shard_count + P.shard_index) << P.shard_shift) + (slot & (P.shard_unit - 1));
             active = active && slot < P.n_rays;
         }
         d3 o = tx, d = d3{0, 0, 0};
         if (active) {
             long long i = slot;
-            if (P.band > 0) {
-                long long b = slot / P.band;
-                if ((b + 1) * P.band <= P.n_rays) i = b * P.band + P.perm[slot - b * P.band];
+            if (P.band > 0) {   // B is a power of two: shift and mask, no 64-bit division
+                long long b = slot >> P.band_shift;
+                if ((b + 1) * P.band <= P.n_rays) i = (b << P.band_shift) + P.perm[slot & (P.band - 1)];
             }
             d = P.dirs ? ld3(P.dirs + 3 * i) : fib_dir(i, P.n_rays);
         }
