@@ -655,6 +655,7 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_solve_validate(Cands C, Sc
         long long w = it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
         long long rxi = 0;
         int c = 0;
+        d3 rx = d3{0, 0, 0};
         if (GRID) {
             long long w0 = w - lane;
             long long s0 = w0 < W ? G.chunk_seg[w0 >> 5] : 0;
@@ -664,18 +665,20 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_solve_validate(Cands C, Sc
                 c = G.cand[sg];
                 long long iy = G.iy[sg], ix = G.ix0[sg] + (w - G.item_off[sg]);
                 rxi = iy * R.nx + ix;
+                // GridSpec.cell_center from (ix, iy) directly (receiver_pos's arithmetic,
+                // without dividing the flat index back)
+                rx = d3{R.ox + ((double)ix + 0.5) * R.cell, R.oy + ((double)iy + 0.5) * R.cell, R.height};
             }
         } else if (w < W) {
             c = (int)(w % C.n);
             rxi = w / C.n;
+            rx = receiver_pos(R, rxi);
         }
         d3 pts[MAX_DEPTH];
-        d3 rx = d3{0, 0, 0};
         int K = 0;
         bool geo = false;
         int* hc = hints + (long long)c * (MAX_DEPTH + 1);
         if (w < W) {
-            rx = receiver_pos(R, rxi);
             K = C.len[c];
             // the receiver-side occluder hint is tried as soon as the solve has the
             // last interaction point: a blocked item skips the remaining levels
