@@ -242,6 +242,16 @@ int rt_cir_scatter(rt_ctx* ctx, int64_t n_paths, const double* delay, int normal
                    const double* a_in, int n_rx_el, int n_tx_el, int n_t, int64_t n_path,
                    double* a_out, double* tau_out, void* stream);
 
+/* coverage_map (channel.py:236-253) with method "fibonacci" on one device: rt_launch
+ * over the whole n_rays lattice, then rt_coverage (shard 0 of 1), in one call (no
+ * host round trip between them).  *n_bounces_out = the launch's ray-bounces. */
+int rt_coverage_fibonacci(rt_ctx* ctx, const double* tx, int64_t n_rays, int max_depth, double origin_x,
+                          double origin_y, double cell_size, int64_t nx, int64_t ny, double height,
+                          const double* tx_rows, const double* probe_rows, int tx_pattern, const double* slants,
+                          const double* offsets_w, int n_el, int tx_mode, const double* eta, int n_mat,
+                          double wavelength, double frequency_hz, double* gains_out, int64_t* stats_out,
+                          int64_t* n_bounces_out, void* stream);
+
 /* Batched image_solve of independent (tx, rx, sequence) triples (tracer.py:
  * 150-183; order-0 rows are LOS visibility checks, tracer.py:190) — the
  * explicit-array gains (em.py:425-459) and single image_solve queries.

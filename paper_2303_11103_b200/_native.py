@@ -29,7 +29,7 @@ EXPORTS = [
     "rt_set_profiling", "rt_get_profile", "rt_l2_probe", "rt_transfer_jvp", "rt_solve_pairs",
     "rt_launch_shard", "rt_gains_synthetic", "rt_cir_plan", "rt_cir_scatter", "rt_freq_nmse",
     "rt_microbench", "rt_fresnel", "rt_gains", "rt_h2d", "rt_gains_h", "rt_paths_max_per_receiver",
-    "rt_paths_fibonacci",
+    "rt_paths_fibonacci", "rt_coverage_fibonacci",
 ]
 
 _lib = None
@@ -104,6 +104,8 @@ def lib():
                                   P, i32, f64, f64, P, P]),
             "rt_transfer_bwd": (i32, [P, i64, i32, P, P, P, P, P, P, P, P, P, P, i32, i32, P, i32, P,
                                       i32, P, i32, f64, f64, P, P, P]),
+            "rt_coverage_fibonacci": (i32, [P, P, i64, i32, f64, f64, f64, i64, i64, f64, P, P, i32, P, P, i32,
+                                            i32, P, i32, f64, f64, P, P, pi64, P]),
             "rt_coverage": (i32, [P, P, f64, f64, f64, i64, i64, f64, P, P, i32, P, P, i32, i32, P,
                                   i32, f64, f64, i32, i32, P, P, P]),
             "rt_set_profiling": (i32, [P, i32]),

@@ -320,9 +320,8 @@ def _tx_antenna(scene, tx_dev, ctx):
 _COV_ERRORS = {N.RT_EINVAL: ChannelError, N.RT_ECOINCIDE: TracerError, N.RT_ECAP: ChannelError}
 
 
-def coverage_from_candidates(scene, bvh, tx_dev, grid: GridSpec, tx_mode="central", ctx=None,
-                             shard_index=0, shard_count=1, out=None):
-    """rt_coverage over the context's current candidate set; returns (gains_dev, stats)."""
+def _coverage_params(scene, bvh, tx_dev, tx_mode, ctx):
+    """Host-side antenna / material parameters of rt_coverage (eta staged to the device)."""
     if ctx is None:
         ctx = EvalContext(scene)
     mode = {"central": 0, "array": 1}.get(tx_mode)
@@ -334,21 +333,52 @@ def coverage_from_candidates(scene, bvh, tx_dev, grid: GridSpec, tx_mode="centra
     sl_h, _ = N.host_doubles(slants)
     off_h, _ = N.host_doubles(off_w)
     tx_h, _ = N.host_doubles([float(x) for x in tx_dev.position])
+    eta = N.h2d(ctx.eta_values(bvh), bvh.device)   # staged: no blocking pageable copy
+    return tx_h, rows_h, probe_h, sl_h, off_h, len(slants), mode, eta
+
+
+_COV_KEYS = ("work_items", "geometric_pairs", "valid_paths", "cells", "candidates")
+
+
+def coverage_from_candidates(scene, bvh, tx_dev, grid: GridSpec, tx_mode="central", ctx=None,
+                             shard_index=0, shard_count=1, out=None):
+    """rt_coverage over the context's current candidate set; returns (gains_dev, stats)."""
+    tx_h, rows_h, probe_h, sl_h, off_h, n_el, mode, eta = _coverage_params(scene, bvh, tx_dev, tx_mode, ctx)
     dev = bvh.device
-    eta = N.h2d(ctx.eta_values(bvh), dev)   # staged: no blocking pageable copy
     g = out if out is not None else torch.empty((grid.ny, grid.nx), dtype=torch.float64, device=dev)
     stats = np.zeros(8, dtype=np.int64)
     with torch.cuda.device(dev):
         bvh.ctx.call("rt_coverage", N.ptr(tx_h), float(grid.origin[0]), float(grid.origin[1]),
                      float(grid.cell_size), int(grid.nx), int(grid.ny), float(grid.height),
                      N.ptr(rows_h), N.ptr(probe_h), pattern_id(scene.tx_array.pattern), N.ptr(sl_h),
-                     N.ptr(off_h), len(slants), mode, N.ptr(eta), eta.shape[0], scene.wavelength,
+                     N.ptr(off_h), n_el, mode, N.ptr(eta), eta.shape[0], scene.wavelength,
                      scene.frequency_hz, int(shard_index), int(shard_count), N.ptr(g),
                      N.ptr(stats), bvh.ctx.stream, exc_map=_COV_ERRORS)
     # geometric_pairs: (cell, candidate) pairs that passed the image solve and were not
     # stopped by the receiver-side occluder hint (the fused pass exits there early)
-    keys = ("work_items", "geometric_pairs", "valid_paths", "cells", "candidates")
-    return g, {k: int(stats[i]) for i, k in enumerate(keys)}
+    return g, {k: int(stats[i]) for i, k in enumerate(_COV_KEYS)}
+
+
+def coverage_fibonacci(scene, bvh, tx_dev, grid: GridSpec, max_depth: int, num_rays: int,
+                       tx_mode="central", ctx=None, out=None):
+    """launch_candidates (fibonacci) + rt_coverage as one library call
+    (rt_coverage_fibonacci: no host round trip between the launch and the map).
+    Returns (gains_dev, stats, ray_bounces)."""
+    if num_rays < 1 or max_depth < 1:
+        raise TracerError("need num_rays >= 1 and max_depth >= 1")
+    tx_h, rows_h, probe_h, sl_h, off_h, n_el, mode, eta = _coverage_params(scene, bvh, tx_dev, tx_mode, ctx)
+    dev = bvh.device
+    g = out if out is not None else torch.empty((grid.ny, grid.nx), dtype=torch.float64, device=dev)
+    stats = np.zeros(8, dtype=np.int64)
+    nb = ctypes.c_int64()
+    with torch.cuda.device(dev):
+        bvh.ctx.call("rt_coverage_fibonacci", N.ptr(tx_h), int(num_rays), int(max_depth),
+                     float(grid.origin[0]), float(grid.origin[1]), float(grid.cell_size), int(grid.nx),
+                     int(grid.ny), float(grid.height), N.ptr(rows_h), N.ptr(probe_h),
+                     pattern_id(scene.tx_array.pattern), N.ptr(sl_h), N.ptr(off_h), n_el, mode, N.ptr(eta),
+                     eta.shape[0], scene.wavelength, scene.frequency_hz, N.ptr(g), N.ptr(stats),
+                     ctypes.byref(nb), bvh.ctx.stream, exc_map=_COV_ERRORS)
+    return g, {k: int(stats[i]) for i, k in enumerate(_COV_KEYS)}, int(nb.value)
 
 
 def coverage_map(scene, bvh, grid: GridSpec, max_depth: int, method: str = "exhaustive",
@@ -362,6 +392,11 @@ def coverage_map(scene, bvh, grid: GridSpec, max_depth: int, method: str = "exha
         raise ChannelError("scene has no transmitter")
     tx_dev = _device(scene, tx_name) if tx_name else txs[0]
     bounces = 0
+    if method == "fibonacci" and max_depth >= 1 and bvh.num_prims:   # one library call
+        g, stats, bounces = coverage_fibonacci(scene, bvh, tx_dev, grid, max_depth, num_rays, tx_mode)
+        stats["ray_bounces"] = int(bounces)
+        return CoverageMap(grid=grid, gains=N.d2h(g), frequency_hz=scene.frequency_hz,
+                           stats=stats, gains_dev=g)
     if max_depth >= 1 and bvh.num_prims:
         if method == "exhaustive":
             run_enumerate(bvh, max_depth)

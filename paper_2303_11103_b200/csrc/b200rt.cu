@@ -1860,6 +1860,26 @@ int rt_coverage(rt_ctx* ctx, const double* tx, double origin_x, double origin_y,
     return RT_OK;
 }
 
+int rt_coverage_fibonacci(rt_ctx* ctx, const double* tx, int64_t n_rays, int max_depth, double origin_x,
+                          double origin_y, double cell_size, int64_t nx, int64_t ny, double height,
+                          const double* tx_rows, const double* probe_rows, int tx_pattern, const double* slants,
+                          const double* offsets_w, int n_el, int tx_mode, const double* eta, int n_mat,
+                          double wavelength, double frequency_hz, double* gains_out, int64_t* stats_out,
+                          int64_t* n_bounces_out, void* stream) {
+    if (!ctx || !tx || n_rays < 1 || max_depth < 1)
+        return fail(ctx, RT_EINVAL, "need num_rays >= 1 and max_depth >= 1");
+    if (!ctx->bvh_ready) return fail(ctx, RT_ESTATE, "rt_bvh_build has not run");
+    if (n_bounces_out) *n_bounces_out = 0;
+    if (ctx->n_prims == 0) {   // no geometry: LOS only
+        RC(sort_unique_candidates(ctx, 0, 1, ST(stream)));
+    } else {
+        RC(launch_impl(ctx, tx, n_rays, 0, n_rays, 0, 1, max_depth, nullptr, nullptr, n_bounces_out, stream));
+    }
+    return rt_coverage(ctx, tx, origin_x, origin_y, cell_size, nx, ny, height, tx_rows, probe_rows, tx_pattern,
+                       slants, offsets_w, n_el, tx_mode, eta, n_mat, wavelength, frequency_hz, 0, 1, gains_out,
+                       stats_out, stream);
+}
+
 int rt_solve_pairs(rt_ctx* ctx, int64_t n, int max_len, const double* tx_pos,
                    const double* rx_pos, const int32_t* seq, const int8_t* len, uint8_t* valid,
                    double* vertices, double* length, double* delay, double* k_dep, double* k_arr,

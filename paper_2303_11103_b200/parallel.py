@@ -152,6 +152,11 @@ def coverage_step(scene, bvh, tx_dev, grid, max_depth, num_rays, rank=0, world=1
     """One sharded coverage map with device-resident inputs.
 
     Returns (local ray-bounces, stats, gains tensor [ny, nx] on the device)."""
+    if world == 1 and max_depth >= 1 and bvh.num_prims:   # launch + map in one library call
+        from .channel import coverage_fibonacci
+        g, stats, bounces = coverage_fibonacci(scene, bvh, tx_dev, grid, max_depth, num_rays, tx_mode, out=out)
+        stats["ray_bounces_local"] = bounces
+        return bounces, stats, g
     _, bounces = run_launch(bvh, tx_dev.position, max_depth, num_rays, shard=(rank, world))
     if world > 1:
         seq, ln = get_candidates(bvh)
