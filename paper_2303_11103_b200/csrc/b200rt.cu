@@ -301,10 +301,14 @@ int sort_pairs(rt_ctx* ctx, const unsigned long long* kin, unsigned long long* k
         return sort_small_launch<8>(ctx, kin, kout, vin, vout, n, begin_bit, end_bit, expand_cb, st);
     if (n <= SORT_SMALL_MAX)
         return sort_small_launch<16>(ctx, kin, kout, vin, vout, n, begin_bit, end_bit, expand_cb, st);
-    if (expand_cb > 0) return fail(ctx, RT_ECUDA, "compact record keys above the one-CTA sort size");
-    return cub_call(ctx, [&](void* tmp, size_t& bytes) {
+    RC(cub_call(ctx, [&](void* tmp, size_t& bytes) {
         return cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, begin_bit, end_bit, st);
-    });
+    }));
+    if (expand_cb > 0) {   // compact record keys back to the library's layout
+        k_rec_keys_expand<<<nblk(n, 256), 256, 0, st>>>(kout, n, expand_cb);
+        CKL();
+    }
+    return RT_OK;
 }
 
 // Sort rows (s_seq/s_len, n rows, width L) by (length, lexicographic) and
@@ -1544,7 +1548,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     CK(ctx->ridx.reserve(4 * n_rec));
     CK(ctx->ridx_alt.reserve(4 * n_rec));
     // a one-CTA sort takes compact keys (fewer radix passes) and expands them
-    int cb = n_rec <= SORT_SMALL_MAX ? bits_for(nC) : 0;
+    int cb = bits_for(nC);   // compact keys: (rx, order, cand) in fewer radix passes
     k_rec_keys<<<nblk(n_rec, 256), 256, 0, st>>>(ctx->recs.get<Rec>(), n_rec, ctx->rkeys_alt.get<unsigned long long>(),
                                                 ctx->ridx_alt.get<int>(), cb);
     CKL();

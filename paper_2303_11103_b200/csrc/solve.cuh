@@ -760,6 +760,14 @@ __global__ void k_rec_keys(const Rec* recs, long long n, unsigned long long* key
     idx[i] = (int)i;
 }
 
+// compact record keys (k_rec_keys with cb > 0) -> rx << 36 | order << 32 | cand
+__global__ void k_rec_keys_expand(unsigned long long* keys, long long n, int cb) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long x = keys[i];
+    keys[i] = ((x >> (cb + 4)) << 36) | (((x >> cb) & 0xFULL) << 32) | (x & ((1ULL << cb) - 1));
+}
+
 // Greedy coincident merge of one receiver's records (tracer.py:247-265):
 // records are visited in (order, candidate) order; a record is dropped when
 // an earlier KEPT record of the same order has every vertex within 1e-6.
