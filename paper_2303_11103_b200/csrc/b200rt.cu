@@ -1410,6 +1410,8 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
     CK(ctx->occ_hint.reserve(4ULL * nC * (MAX_DEPTH + 1)));
     int* hints = RT_OCC_HINTS ? ctx->occ_hint.get<int>() : nullptr;
     long long n_pend = 0;
+    long long fused_flags = 0;
+    long long n_rec_known = -1;   // set when the fused pass's read-back already holds the final count
     if (RT_FUSED_SV && hints) {
         // solve + validation in one pass, thin warps' open items deferred to a
         // k_validate pass over that list; grow and rerun when a list is short
@@ -1437,10 +1439,14 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
                     C, SD, ctx->images.get<double>(), R, tx, W, G, bvh_dev(ctx), hints, defer_min,
                     ctx->recs.get<Rec>(), ctx->rec_cap, ctx->pending.get<Pending>(), ctx->pending_cap, ctr);
             CKL();
-            RC(fetch(ctx, ctr, 3, st));
+            // the three counters and the error word in one read-back
+            CK(cudaMemcpyAsync(ctx->hpin, ctr, 3 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(ctx->hpin + 3, ctx->dflag.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
             n_pend = ctx->hpin[0];
             long long n_rec1 = ctx->hpin[1];
             n_def = ctx->hpin[2];
+            fused_flags = ctx->hpin[3];
             bool grow = false;
             if ((unsigned long long)n_def > ctx->pending_cap) {
                 while (ctx->pending_cap < (unsigned long long)n_def) ctx->pending_cap *= 2;
@@ -1461,6 +1467,9 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
                                                             bvh_dev(ctx), ctx->pending.get<Pending>(),
                                                             n_def, E, ctx->recs.get<Rec>(), nr, hints);
             CKL();
+        } else {   // nothing deferred: the read-back above is final (no second host sync)
+            RC(flags_status(ctx, fused_flags));
+            n_rec_known = ctx->hpin[1];
         }
         if (stats) stats[1] = n_pend;
         ctx->counters[5] = n_pend;
@@ -1531,8 +1540,11 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         cudaMemcpyToSymbol(g_vstats, z, sizeof(z));
     }
 #endif
-    RC(fetch_and_flags(ctx, nr, 1, st));   // record count + the validation's error word
-    long long n_rec = ctx->hpin[0];
+    long long n_rec = n_rec_known;
+    if (n_rec < 0) {
+        RC(fetch_and_flags(ctx, nr, 1, st));   // record count + the validation's error word
+        n_rec = ctx->hpin[0];
+    }
     if (power && n_rec > 0) {
         k_rec_powers<<<nblk(n_rec, 128), 128, 0, st>>>(C, SD, ctx->images.get<double>(), R, tx, E,
                                                        ctx->recs.get<Rec>(), n_rec);
