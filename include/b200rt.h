@@ -282,8 +282,8 @@ int rt_transfer_jvp(rt_ctx* ctx, int64_t n_paths, int max_len, const int8_t* ord
  * receives sum_paths sum_{theta,phi probes} |a|^2 over the current candidate
  * set, with per-cell merge; tx_mode 0 = central element (slants[0]), 1 =
  * coherent sum over n_el elements with world offsets offsets_w [n_el*3] and
- * slants [n_el] (host arrays).  Rows with (iy / 8) % shard_count == shard_index
- * (8-row blocks, round-robin) are computed; other cells are written 0
+ * slants [n_el] (host arrays).  Rows with iy % shard_count == shard_index
+ * (round-robin rows) are computed; other cells are written 0
  * (sum-allreduce the shards).
  * gains_out: device [ny*nx] f64.  stats_out (host [8], may be NULL):
  * work items, geometric pairs, valid paths, cells, candidates. */
