@@ -105,3 +105,22 @@ def test_staged_uploads_round_trip(P):
     b = np.arange(12, dtype=np.int32).reshape(3, 4)
     tb = N.h2d(b, dev)
     assert tb.dtype == torch.int32 and tb.shape == (3, 4) and np.array_equal(tb.cpu().numpy(), b)
+
+
+def test_fused_entry_points_without_geometry(P, golden):
+    """A scene without primitives: rt_paths_fibonacci takes the empty candidate
+    set (LOS only, as prepare_candidates does) and coverage_map (fibonacci)
+    keeps the launch-free route."""
+    from conftest import golden_scene
+    fs = golden_scene(golden("criteria"), "free_space")
+    bvh = P.build(fs)
+    assert bvh.num_prims == 0
+    fib = P.compute_paths(fs, bvh, 2, method="fibonacci", num_rays=4096)
+    exh = P.compute_paths(fs, bvh, 2, method="exhaustive")
+    assert [(p.rx, p.kind, p.seq) for p in fib.paths] == [(p.rx, p.kind, p.seq) for p in exh.paths]
+    assert all(p.kind == "los" for p in fib.paths) and len(fib.paths) > 0
+    tx = [d for d in fs.devices if d.kind == "tx"][0]
+    grid = P.GridSpec((float(tx.position[0]) + 5.0, float(tx.position[1]) - 8.0), 2.0, 8, 8, 1.5)
+    a = P.coverage_map(fs, bvh, grid, 2, method="fibonacci", num_rays=4096)
+    b = P.coverage_map(fs, bvh, grid, 2, method="exhaustive")
+    assert np.array_equal(a.gains, b.gains) and (a.gains > 0).all()
