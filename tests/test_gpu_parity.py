@@ -814,3 +814,45 @@ def test_device_cir_packing_matches_reference(P, golden, case):
         got = P.build_cir(dev_gains(), **kw)
         assert np.array_equal(got.a, want.a) and np.array_equal(got.tau, want.tau), kw
 
+
+
+def _edge_scene():
+    """Floor quad [0,10]^2 and a 40 m wall at x = 20 under a transmitter at
+    (5,5,10); receivers at z = 30 on integer cell centers.  The floor's image
+    cone meets z = 30 exactly on the lines x, y = -15 and 25, and the wall's
+    top-corner edge passes exactly through the cell (5,15): footprint edges
+    through cell centers."""
+    from paper_2303_11103_b200 import scenes
+    from paper_2303_11103_b200.scene import AntennaArray, RadioDevice, RadioMaterial, Scene, SceneObject
+    gv, gt = scenes.quad([(0, 0, 0), (10, 0, 0), (10, 10, 0), (0, 10, 0)])
+    wv, wt = scenes.quad([(20, -10, 0), (20, 10, 0), (20, 10, 40), (20, -10, 40)])
+    arr = AntennaArray(pattern="iso", polarization="V")
+    sc = Scene(3.5e9, [SceneObject("floor", "m", gv, gt), SceneObject("wall", "m", wv, wt)],
+               {"m": RadioMaterial("m", "constant", 5.0, 0.05)}, arr, arr,
+               [RadioDevice("tx", "tx", np.array([5.0, 5.0, 10.0])),
+                RadioDevice("rx", "rx", np.array([-3.0, 2.0, 10.0]))])
+    sc.validate()
+    return sc
+
+
+@pytest.mark.parametrize("method", ["exhaustive", "fibonacci"])
+def test_coverage_footprint_edges_through_cell_centers(P, method):
+    """Cells whose centers lie exactly on a reflection footprint's boundary:
+    the oracle accepts those paths (edge hits within the barycentric
+    tolerance), so the unpadded footprint enumeration must still visit them."""
+    import oracle as O
+    sc = _edge_scene()
+    b = _bvh(P, sc)
+    ob = O.Bvh(O.SceneArrays(sc))
+    grid = P.GridSpec((-30.5, -30.5), 1.0, 70, 70, 30.0)
+    want = O.coverage_map(sc, ob, grid.origin, grid.cell_size, grid.nx, grid.ny, grid.height, 2,
+                          method=method, num_rays=50_000)
+    los = O.coverage_map(sc, ob, grid.origin, grid.cell_size, grid.nx, grid.ny, grid.height, 0,
+                         method="exhaustive")
+    # the fixture exercises the edges: reflections present on the boundary cells
+    for x, y in ((-15, 5), (5, -15), (-15, -15), (5, 15)):
+        assert want[y + 30, x + 30] > los[y + 30, x + 30] * 1.05
+    cm = P.coverage_map(sc, b, grid, 2, method=method, num_rays=50_000)
+    assert np.array_equal(cm.gains == 0.0, want == 0.0)
+    nz = want > 0
+    assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz])
