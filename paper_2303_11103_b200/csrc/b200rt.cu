@@ -1535,7 +1535,7 @@ int solve_records(rt_ctx* ctx, d3 tx, const Receivers& R, bool grid, bool power,
         unsigned long long hv[8];
         cudaMemcpyFromSymbol(hv, g_vstats, sizeof(hv));
         fprintf(stderr, "validate stats: items %llu rx-hint hits %llu other hint hits %llu traversals %llu "
-                "blocked %llu\n", hv[0], hv[1], hv[4], hv[2], hv[3]);
+                "blocked %llu fused items %llu survivors %llu\n", hv[0], hv[1], hv[4], hv[2], hv[3], hv[5], hv[6]);
         unsigned long long z[8] = {};
         cudaMemcpyToSymbol(g_vstats, z, sizeof(z));
     }

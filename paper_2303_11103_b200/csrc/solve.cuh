@@ -677,6 +677,9 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_validate(Cands C, SceneDev
 // re-solve of the items validated here.  Capacity overflow of the record or
 // deferred list is counted (the host grows the buffers and reruns).
 // ctr: [0] survivors, [1] records, [2] deferred.
+#ifndef RT_SV_CHUNK
+#define RT_SV_CHUNK 8
+#endif
 template <bool GRID>
 __global__ void __launch_bounds__(128, RT_VAL_MINB) k_solve_validate(Cands C, SceneDev S, const double* images,
                                                         Receivers R, d3 tx, long long W, Segs G, Bvh bvh,
@@ -684,11 +687,8 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_solve_validate(Cands C, Sc
                                                         unsigned long long rec_cap, Pending* deferred,
                                                         unsigned long long def_cap, unsigned long long* ctr) {
     const unsigned FULL = 0xffffffffu;
-    long long stride = (long long)gridDim.x * blockDim.x;
-    long long iters = (W + stride - 1) / stride;
     int lane = threadIdx.x & 31;
-    for (long long it = 0; it < iters; ++it) {
-        long long w = it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    auto item = [&](long long w) {
         long long rxi = 0;
         int c = 0;
         d3 rx = d3{0, 0, 0};
@@ -719,6 +719,8 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_solve_validate(Cands C, Sc
             // the receiver-side occluder hint is tried as soon as the solve has the
             // last interaction point: a blocked item skips the remaining levels
             geo = solve_geometric(C, S, images, c, tx, rx, pts, &bvh, hc + K);
+            VSTAT(5);
+            if (geo) VSTAT(6);
         }
         // geometric survivors not blocked by the receiver-side hint
         unsigned gm = __ballot_sync(FULL, geo);
@@ -764,7 +766,22 @@ __global__ void __launch_bounds__(128, RT_VAL_MINB) k_solve_validate(Cands C, Sc
                 }
             }
         }
+    };
+#if RT_SV_CHUNK > 0
+    // each warp takes RT_SV_CHUNK x 32 consecutive items at a time: the next
+    // 32 cells of a row segment see the occluders the previous 32 found
+    for (;;) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(ctr + 4, (unsigned long long)(RT_SV_CHUNK * 32));
+        base = __shfl_sync(FULL, base, 0);
+        if ((long long)base >= W) break;
+        for (int t = 0; t < RT_SV_CHUNK && (long long)base + t * 32 < W; ++t) item((long long)base + t * 32 + lane);
     }
+#else
+    long long stride = (long long)gridDim.x * blockDim.x;
+    long long iters = (W + stride - 1) / stride;
+    for (long long it = 0; it < iters; ++it) item(it * stride + blockIdx.x * (long long)blockDim.x + threadIdx.x);
+#endif
 }
 
 // probe powers of the surviving records (split from k_validate so the
