@@ -334,6 +334,13 @@ overflow:
 // descends internal nodes until it reaches a leaf, then the warp runs leaf
 // tests together, instead of alternating node and FP64 triangle work per
 // iteration.  Same visit order and results as trace<>.
+// The octant copies only for the closest-hit traversal (k_launch): in the
+// occlusion kernels the eight extra descents overflow the instruction cache
+// (k_solve_validate: 20 % of stall samples "no_instructions"); C3 fused pass
+// 2.52 -> 2.22 ms with the generic descent there.
+#ifndef RT_OCTANT_ANY
+#define RT_OCTANT_ANY 0
+#endif
 #ifndef RT_OCTANT
 #define RT_OCTANT 1
 #endif
@@ -409,7 +416,8 @@ __device__ int trace_ww(const Bvh& bvh, const Ray& r, double tmin, double tmax, 
     float best_tf = __double2float_ru(tmax);
     const float tmin_f = ray_tmin_f(tmin);
     const bool fast = MODE == 1 ? true : MODE == 2 ? false : ray_fast(bvh, r);
-    const int oct = (RT_OCTANT && fast) ? ((r.fix < 0.f) | ((r.fiy < 0.f) << 1) | ((r.fiz < 0.f) << 2)) : -1;
+    const int oct = (RT_OCTANT && (!ANY || RT_OCTANT_ANY) && fast)
+                        ? ((r.fix < 0.f) | ((r.fiy < 0.f) << 1) | ((r.fiz < 0.f) << 2)) : -1;
     int best_prim = -1;
     int cur = 0;
     int nv = 0, nt = 0;
@@ -479,6 +487,9 @@ overflow:
 #ifndef RT_WW_CLOSEST
 #define RT_WW_CLOSEST 1
 #endif
+#ifndef RT_HOIST_FAST_ANY
+#define RT_HOIST_FAST_ANY 1   // 0: one any-hit loop with a per-node FP32 / FP64 choice (C3 fused pass 2.22 -> 2.51 ms)
+#endif
 #ifndef RT_HOIST_FAST
 #define RT_HOIST_FAST 1   // measured on C3: launch 25.8 vs 26.8 ms, validate 5.5 vs 6.3 ms
 #endif
@@ -491,6 +502,8 @@ __device__ __forceinline__ int trace_ray(const Bvh& bvh, const Ray& r, double tm
                                          int skip_end = EMPTY_REF) {
 #if RT_HOIST_FAST
     // one FP32-only and one FP64-only copy of the loop: no per-node filter test
+    if (ANY && !RT_HOIST_FAST_ANY && RT_WW_ANY)
+        return trace_ww<ANY>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos, skip, skip_end);
     if ((ANY && RT_WW_ANY) || (!ANY && RT_WW_CLOSEST)) {
         if (ray_fast(bvh, r)) return trace_ww<ANY, 1>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos, skip, skip_end);
         return trace_ww<ANY, 2>(bvh, r, tmin, tmax, t_out, visits, tests, hit_pos, skip, skip_end);
