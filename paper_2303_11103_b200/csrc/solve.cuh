@@ -207,7 +207,12 @@ __device__ inline d3 receiver_pos(const Receivers& R, long long r) {
 
 constexpr int HP_PER_TRI = 4;
 constexpr int HP_MAX = HP_PER_TRI * MAX_DEPTH;
-constexpr int POLY_MAX = 4 + HP_MAX;
+#ifndef RT_POLY_CAP
+#define RT_POLY_CAP 12
+#endif
+#ifndef RT_POLY_SMEM
+#define RT_POLY_SMEM 1
+#endif
 
 // Half-plane a x + b y + c >= 0 on the grid plane (c widened by the rounding
 // margin), stored in cell-index row form for row_interval: at the center of
@@ -238,18 +243,21 @@ __device__ inline void hp_line(const double* hp, double& a, double& b, double& c
     else { a = 0.0; b = hp[1]; c = hp[2]; }
 }
 
-// clip a convex polygon by a x + b y + c >= 0 (Sutherland-Hodgman)
+// clip a convex polygon by a x + b y + c >= 0 (Sutherland-Hodgman); vertex k
+// at [k * PS]; the output has at most n + 1 vertices
+template <int PS>
 __device__ inline int clip_poly(const double* px, const double* py, int n, double a, double b,
                                 double c, double* qx, double* qy) {
     int m = 0;
     for (int i = 0; i < n; ++i) {
-        int j = (i + 1) % n;
-        double fi = a * px[i] + b * py[i] + c, fj = a * px[j] + b * py[j] + c;
-        if (fi >= 0.0) { qx[m] = px[i]; qy[m] = py[i]; ++m; }
+        int j = i + 1 == n ? 0 : i + 1;
+        double xi = px[i * PS], yi = py[i * PS], xj = px[j * PS], yj = py[j * PS];
+        double fi = a * xi + b * yi + c, fj = a * xj + b * yj + c;
+        if (fi >= 0.0) { qx[m * PS] = xi; qy[m * PS] = yi; ++m; }
         if ((fi >= 0.0) != (fj >= 0.0)) {
             double t = fi / (fi - fj);
-            qx[m] = px[i] + t * (px[j] - px[i]);
-            qy[m] = py[i] + t * (py[j] - py[i]);
+            qx[m * PS] = xi + t * (xj - xi);
+            qy[m * PS] = yi + t * (yj - yi);
             ++m;
         }
     }
@@ -331,20 +339,37 @@ __global__ void k_halfplanes(Cands C, SceneDev S, const double* images, Receiver
     }
     nhp[c] = m;
     // clip the grid rectangle, padded one cell, in cell-index space (u, iy)
-    double px[POLY_MAX], py[POLY_MAX], qx[POLY_MAX], qy[POLY_MAX];
+    // The polygon only bounds the rows (row_interval applies every half-plane
+    // per row), so clipping may stop early: a polygon about to outgrow
+    // RT_POLY_CAP vertices keeps its current, larger, shape.  The vertex lists
+    // live in shared memory (RT_POLY_SMEM): as per-thread local arrays they
+    // outgrow L1 and the clip loop waits on L2.
+#if RT_POLY_SMEM
+    __shared__ double sbuf[4][RT_POLY_CAP][128];
+    double* px = &sbuf[0][0][threadIdx.x];
+    double* py = &sbuf[1][0][threadIdx.x];
+    double* qx = &sbuf[2][0][threadIdx.x];
+    double* qy = &sbuf[3][0][threadIdx.x];
+    constexpr int PS = 128;   // element stride
+#else
+    double bx[2][RT_POLY_CAP], by[2][RT_POLY_CAP];
+    double *px = bx[0], *py = by[0], *qx = bx[1], *qy = by[1];
+    constexpr int PS = 1;
+#endif
     double x0 = -1.5, x1 = R.nx + 0.5, y0 = -1.5, y1 = R.ny + 0.5;
-    px[0] = x0; py[0] = y0; px[1] = x1; py[1] = y0; px[2] = x1; py[2] = y1; px[3] = x0; py[3] = y1;
+    px[0] = x0; py[0] = y0; px[PS] = x1; py[PS] = y0; px[2 * PS] = x1; py[2 * PS] = y1; px[3 * PS] = x0; py[3 * PS] = y1;
     int n = 4;
-    for (int i = 0; i < m && n > 0; ++i) {
+    for (int i = 0; i < m && n > 0 && n < RT_POLY_CAP; ++i) {
         double la, lb, lc;
         hp_line(hp + 3 * i, la, lb, lc);
-        n = clip_poly(px, py, n, la, lb, lc, qx, qy);
-        for (int k = 0; k < n; ++k) { px[k] = qx[k]; py[k] = qy[k]; }
+        n = clip_poly<PS>(px, py, n, la, lb, lc, qx, qy);
+        double* t = px; px = qx; qx = t;
+        t = py; py = qy; qy = t;
     }
     long long rows = 0, first = 0;
     if (n > 0) {
         double ylo = py[0], yhi = py[0];
-        for (int k = 1; k < n; ++k) { ylo = fmin(ylo, py[k]); yhi = fmax(yhi, py[k]); }
+        for (int k = 1; k < n; ++k) { ylo = fmin(ylo, py[k * PS]); yhi = fmax(yhi, py[k * PS]); }
         long long iy0 = (long long)fmax(floor(ylo) - 1.0, 0.0);
         long long iy1 = (long long)fmin(ceil(yhi) + 1.0, (double)(R.ny - 1));
         if (iy0 <= iy1) {

@@ -13,7 +13,7 @@ from paper_2303_11103_b200.bvh import gather_meshes  # noqa: E402
 
 
 def main():
-    args = bench.parse([])
+    args = bench.parse(sys.argv[1:])
     sc, _, grid = bench.make_workload(args)
     rows = []
     for i in range(6):
