@@ -37,6 +37,20 @@ def test_gather_order_matches_reference_prim_ids(golden):
     assert np.array_equal(pmat, sa.prim_material)
 
 
+def test_threaded_gather_equals_serial(monkeypatch):
+    """Large scenes gather in row chunks on host threads: same arrays as one pass
+    (forced here on a small multi-object scene with uneven chunk boundaries)."""
+    from paper_2303_11103_b200 import bvh as B, scenes
+    sc = scenes.street_canyon(n_per_row=13, seed=2)
+    monkeypatch.setattr(B, "_GATHER_PARALLEL_MIN", 1 << 40)
+    serial = B._gather_geometry(sc, tri_dtype=np.int32)
+    monkeypatch.setattr(B, "_GATHER_PARALLEL_MIN", 1)
+    threaded = B._gather_geometry(sc, tri_dtype=np.int32)
+    for a, b in zip(serial, threaded):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+    assert threaded[1].dtype == np.int32 and len(threaded[1]) > 0
+
+
 def _cpu_gains(sc, case_golden):
     """A ChannelGains built on CPU tensors from the golden path table + gains."""
     from paper_2303_11103_b200.em import ChannelGains
