@@ -856,3 +856,39 @@ def test_coverage_footprint_edges_through_cell_centers(P, method):
     assert np.array_equal(cm.gains == 0.0, want == 0.0)
     nz = want > 0
     assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz])
+
+
+def _tilted_soup(n, seed, spread=8.0):
+    """Large randomly oriented triangles around a transmitter: reflection
+    footprints of arbitrary shape and orientation on the grid plane."""
+    from paper_2303_11103_b200.scene import AntennaArray, RadioDevice, RadioMaterial, Scene, SceneObject
+    rng = np.random.RandomState(seed)
+    centers = rng.uniform(-30, 30, (n, 3))
+    centers[:, 2] = rng.uniform(2, 25, n)
+    verts = np.repeat(centers, 3, axis=0) + rng.uniform(-spread, spread, (3 * n, 3))
+    tx = np.array([rng.uniform(-5, 5), rng.uniform(-5, 5), rng.uniform(8, 20)])
+    sc = Scene(3.5e9, [SceneObject("soup", "m", verts, np.arange(3 * n).reshape(-1, 3))],
+               {"m": RadioMaterial("m", "constant", eps_r=4.0, sigma=0.02)}, AntennaArray(), AntennaArray(),
+               [RadioDevice("tx", "tx", tx), RadioDevice("rx", "rx", tx + 1.0)])
+    sc.validate()
+    return sc
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+@pytest.mark.parametrize("height", [1.5, 12.0])
+def test_coverage_tilted_soup_matches_oracle(P, seed, height):
+    """Footprints of arbitrarily oriented triangles (the grid plane below or
+    cutting through the soup): every cell vs the oracle, depth 2 / 3 over the
+    exhaustive candidate set and depth 3 over Fibonacci candidates."""
+    import oracle as O
+    sc = _tilted_soup(24, seed)
+    b = _bvh(P, sc)
+    ob = O.Bvh(O.SceneArrays(sc))
+    grid = P.GridSpec((-47.0, -47.0), 2.0, 48, 48, height)
+    for depth, method in ((2, "exhaustive"), (3, "exhaustive"), (3, "fibonacci")):
+        want = O.coverage_map(sc, ob, grid.origin, grid.cell_size, grid.nx, grid.ny, grid.height, depth,
+                              method=method, num_rays=20_000)
+        cm = P.coverage_map(sc, b, grid, depth, method=method, num_rays=20_000)
+        assert np.array_equal(cm.gains == 0.0, want == 0.0), (depth, method)
+        nz = want > 0
+        assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz]), (depth, method)
