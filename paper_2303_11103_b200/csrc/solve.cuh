@@ -6,16 +6,19 @@
 // candidate-major pipeline:
 //   1. k_images      per candidate: the image chain I_1..I_K of the tx
 //                     (identical floats to solve_points' images).
-//   2. k_footprint   per candidate: conservative cell range on the grid plane:
-//                     a valid receiver lies in every cone from I_K through the
-//                     forward-mirrored interaction triangles; the bbox of their
-//                     projections (padded) bounds the cells worth solving.
-//   3. k_solve       per (candidate, cell in footprint) or (candidate, rx):
-//                     back-substitution + the geometric tests; survivors are
-//                     compacted (warp-aggregated atomics).
-//   4. k_validate    per survivor: occlusion of every segment (any-hit
-//                     traversals) then the field transfer; emits a record
+//   2. k_halfplanes + k_segments   per candidate: a valid receiver lies in
+//                     every cone from I_K through the forward-mirrored
+//                     interaction triangles (conservative half-planes on the
+//                     grid plane); per row, the x-interval of cell centers
+//                     inside all of them, one work item per cell.
+//   3. k_solve_validate  per work item (warp chunks of consecutive cells) or
+//                     per (candidate, rx): back-substitution + the geometric
+//                     tests, the candidate's receiver-side occluder hint, then
+//                     occlusion of every segment (any-hit traversals); thin
+//                     warps' open items go to
+//   4. k_validate    (deferred list, warm occluder cache); both emit records
 //                     keyed (receiver, order, candidate rank).
+//                     (RT_FUSED_SV=0: separate k_solve -> k_validate passes.)
 //   5. sort records (CUB) and merge coincident paths per receiver in the
 //      reference's greedy order, then accumulate / materialize.
 #pragma once
