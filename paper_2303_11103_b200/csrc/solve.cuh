@@ -295,9 +295,11 @@ __host__ __device__ inline long long shard_row(long long first, long long s, int
     return (bf + (t / RT_ROW_BLOCK + 1) * count) * RT_ROW_BLOCK + t % RT_ROW_BLOCK;
 }
 
-__global__ void k_halfplanes(Cands C, SceneDev S, const double* images, Receivers R,
-                             int shard_index, int shard_count, double* hps /*[n*HP_MAX*3]*/,
-                             int* nhp, int* row0, long long* seg_counts /*[n+1]*/) {
+// launched with 128-thread blocks: the shared clip lists are laid out [.][.][128]
+__global__ void __launch_bounds__(128) k_halfplanes(Cands C, SceneDev S, const double* images, Receivers R,
+                                                    int shard_index, int shard_count,
+                                                    double* hps /*[n*HP_MAX*3]*/, int* nhp, int* row0,
+                                                    long long* seg_counts /*[n+1]*/) {
     long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (c >= C.n) {
         if (c == C.n) seg_counts[c] = 0;
