@@ -48,7 +48,10 @@ constexpr int SAH_SMALL_LATENCY = 4;
 constexpr long long SAH_LATENCY_PRIMS = 65536;
 constexpr int SAH_BLOCK = 256;
 constexpr int SAH_BIG = RT_SAH_BIG;       // ranges above this: several CTAs (SAH_CHUNK prims each)
-constexpr int SAH_CHUNK = 2048;
+#ifndef RT_SAH_CHUNK
+#define RT_SAH_CHUNK 1024   // C3 build 2.02 -> 1.95 ms (2048: 98 CTAs per level for 201k prims, fewer than the SMs)
+#endif
+constexpr int SAH_CHUNK = RT_SAH_CHUNK;
 constexpr int SAH_NCAND = 3 * (SAH_BINS - 1);
 static_assert(SAH_BINS == 32, "k_sah_warp keeps one bin per lane");
 constexpr int SAH_NB = 3 * SAH_BINS * 7;   // bins per range: count + 6 ordered bounds, 3 axes
