@@ -892,3 +892,24 @@ def test_coverage_tilted_soup_matches_oracle(P, seed, height):
         assert np.array_equal(cm.gains == 0.0, want == 0.0), (depth, method)
         nz = want > 0
         assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz]), (depth, method)
+
+
+@pytest.mark.parametrize("nx,ny", [(1, 1), (7, 1), (1, 5), (3, 11)])
+def test_coverage_tiny_grids_match_oracle(P, nx, ny):
+    """Grids of a few cells: work lists far shorter than a warp chunk (256
+    items) and not multiples of 32, every cell vs the oracle."""
+    import oracle as O
+    from paper_2303_11103_b200 import scenes
+    sc = scenes.city(n_side=4, seed=5)
+    b = _bvh(P, sc)
+    ob = O.Bvh(O.SceneArrays(sc))
+    tx = sc.devices[0]
+    grid = P.GridSpec((float(tx.position[0]) - 13.0, float(tx.position[1]) - 21.0), 3.0, nx, ny, 1.5)
+    for depth, method in ((2, "exhaustive"), (4, "fibonacci")):
+        want = O.coverage_map(sc, ob, grid.origin, grid.cell_size, grid.nx, grid.ny, grid.height, depth,
+                              method=method, num_rays=30_000)
+        cm = P.coverage_map(sc, b, grid, depth, method=method, num_rays=30_000)
+        assert cm.gains.shape == (ny, nx)
+        assert np.array_equal(cm.gains == 0.0, want == 0.0), (depth, method)
+        nz = want > 0
+        assert np.all(np.abs(cm.gains[nz] - want[nz]) <= 1e-9 * want[nz]), (depth, method)
